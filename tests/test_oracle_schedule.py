@@ -1,0 +1,245 @@
+"""Pins for oracle/schedule.py and oracle/simulate.py.
+
+External pins (each is fixed by PAPER.md or textbook pipeline math, not by
+the oracle itself):
+  * Table 1 closed forms: 1F1B-I PP bubble and TP bubble exact;
+    R-STP TP bubble (2p+1)*T_AR and peak 3p*M_a exact; ZB-V TP bubble
+    4m*T_AR and peak 2p; R-STP bubble "approximate" -> makespan within 12%
+    of the closed-form makespan for m >= 4p (reading Q8).
+  * plain 1F1B (PipeDream): the textbook bubble (p-1)(T_F+T_B+T_W).
+  * §4.2 text: first braid F(2)&B(1); separation off in the
+    steady phase; App. A: forward mb > backward mb in every braid.
+  * Table 5 memory ratios.
+  * SURVEY §8c.2 golden lists (tests/golden/rstp_survey_8c2.txt).
+Invariants over a grid: completeness, F < B < W, no deadlock.
+"""
+import os
+
+import pytest
+
+from oracle import schedule as sc
+from oracle import simulate as sm
+
+GOLDEN = os.path.join(os.path.dirname(__file__), "golden", "rstp_survey_8c2.txt")
+KINDS = {"stp": sc.STP, "1f1b-i": sc.ONEF1B_I}
+
+
+def _golden():
+    for line in open(GOLDEN):
+        if line.startswith("#") or not line.strip():
+            continue
+        head, body = line.split(":", 1)
+        name, pp, mm, dev = head.split()
+        yield KINDS[name], int(pp[2:]), int(mm[2:]), int(dev[3:]), body.strip()
+
+
+@pytest.mark.parametrize("case", list(_golden()), ids=lambda c: f"{c[0]}-{c[1]}-{c[2]}-{c[3]}")
+def test_golden_action_lists(case):
+    kind, p, m, d, text = case
+    got = " | ".join(sc.action_str(a) for a in sc.build_program(kind, p, m)[d])
+    assert got == text
+
+
+COSTS = [(4, 4, 2, 1), (4, 4, 4, 0), (10, 12, 8, 4), (3, 5, 4, 2)]
+
+
+@pytest.mark.parametrize("p", [2, 3, 4, 8])
+@pytest.mark.parametrize("mult", [1, 2, 4])
+@pytest.mark.parametrize("costs", COSTS)
+def test_1f1b_interleaved_table1_exact(p, mult, costs):
+    T_F, T_B, T_W, T_AR = costs
+    m = mult * p
+    r = sm.simulate(sc.ONEF1B_I, p, sc.build_program(sc.ONEF1B_I, p, m), T_F, T_B, T_W, T_AR)
+    for d in range(p):
+        assert r["bubble"][d] == (p - 1) * (T_F + T_AR + T_B + T_W)      # Table 1 row 1
+        assert r["exposed"][d] == 2 * m * T_AR if T_W >= T_AR else True  # Table 1 TP col
+    # peak (3p-2)*M_a of Table 1 under its counting; ours counts F-start..B-end (Q7)
+    if m >= 2 * p:
+        assert r["peak"][0] in (3 * p - 2, 3 * p - 1)
+
+
+@pytest.mark.parametrize("p", [1, 2, 4, 8])
+@pytest.mark.parametrize("m", [1, 3, 8, 16])
+def test_plain_1f1b_textbook_bubble(p, m):
+    T_F, T_B, T_W = 3, 5, 2
+    r = sm.simulate(sc.ONEF1B, p, sc.build_program(sc.ONEF1B, p, m), T_F, T_B, T_W, 0)
+    for d in range(p):
+        assert r["bubble"][d] == (p - 1) * (T_F + T_B + T_W)
+
+
+@pytest.mark.parametrize("p", [1, 2, 3, 4, 8])
+@pytest.mark.parametrize("costs", [(10, 12, 8, 4), (4, 4, 2, 1), (6, 9, 6, 6)])
+def test_rstp_table1_tp_bubble_and_peak(p, costs):
+    T_F, T_B, T_W, T_AR = costs
+    for m in (4 * p, 6 * p, 8 * p):
+        r = sm.simulate(sc.STP, p, sc.build_program(sc.STP, p, m), T_F, T_B, T_W, T_AR)
+        assert max(r["exposed"]) == (2 * p + 1) * T_AR     # Table 1 "Ours" TP column
+        # Table 1 "Ours" memory; p = 1 is degenerate (both chunks on one device: 3p+1)
+        assert max(r["peak"]) == (3 * p if p > 1 else 4)
+        closed = 2 * m * (T_F + T_B + T_W) + (p - 1) * (T_F + T_AR + T_B - T_W) + (2 * p + 1) * T_AR
+        assert closed <= r["makespan"] <= 1.12 * closed     # "approximate bubble size" (Q8)
+
+
+@pytest.mark.parametrize("p", [1, 2, 4, 8])
+def test_rstp_beats_1f1b_interleaved(p):
+    for m in (4 * p, 8 * p):
+        for costs in ((10, 12, 8, 4), (4, 4, 2, 1)):
+            a = sm.simulate(sc.STP, p, sc.build_program(sc.STP, p, m), *costs)
+            b = sm.simulate(sc.ONEF1B_I, p, sc.build_program(sc.ONEF1B_I, p, m), *costs)
+            assert a["makespan"] < b["makespan"]
+
+
+def test_table1_arithmetic_examples():
+    # SPEC S:L363-365 evaluates Table 1 at p=4, T_F=4, T_AR=1, T_B=4, T_W=2
+    p, T_F, T_AR, T_B, T_W, m = 4, 4, 1, 4, 2, 12
+    r = sm.simulate(sc.ONEF1B_I, p, sc.build_program(sc.ONEF1B_I, p, m), T_F, T_B, T_W, T_AR)
+    assert r["bubble"][0] == 33 and r["exposed"][0] == 24
+    r = sm.simulate(sc.STP, p, sc.build_program(sc.STP, p, m), T_F, T_B, T_W, T_AR)
+    assert max(r["exposed"]) == 9 and max(r["peak"]) == 12
+    r = sm.simulate(sc.ZB, p, sc.build_program(sc.ZB, p, m), T_F, T_B, T_W, T_AR)
+    assert max(r["exposed"]) == 48 and max(r["peak"]) == 8
+
+
+@pytest.mark.parametrize("p", [1, 2, 3, 4])
+def test_zb_closed_forms(p):
+    for m in (2 * p, 4 * p):
+        progs = sc.build_program(sc.ZB, p, m)
+        assert not any(a[0] == sc.A_BFULL for pr in progs for a in pr)
+        r = sm.simulate(sc.ZB, p, progs, 10, 12, 8, 4)
+        assert all(e == 4 * m * 4 for e in r["exposed"])    # Table 1 ZB-V TP column
+        assert max(r["peak"]) <= 2 * p                      # Table 1 ZB-V memory
+
+
+def test_table5_memory_ratios():
+    # Table 5: 1F1B-I / ZB-V peak = 41/30 at p=4 and 55/38 at p=8;
+    # STP / ZB-V = 54/30 at p=4 once App. C's ~+19% per-microbatch overhead (P:L637,
+    # 4.3/3.6) is applied to the schedule-level 3p / 2p.
+    for p, paper in ((4, 41 / 30), (8, 55 / 38)):
+        m = 4 * p
+        a = max(sm.simulate(sc.ONEF1B_I, p, sc.build_program(sc.ONEF1B_I, p, m), 4, 4, 2, 1)["peak"])
+        b = max(sm.simulate(sc.ZB, p, sc.build_program(sc.ZB, p, m), 4, 4, 2, 1)["peak"])
+        assert abs(a / b - paper) / paper < 0.02
+    p = 4
+    s = max(sm.simulate(sc.STP, p, sc.build_program(sc.STP, p, 16), 4, 4, 2, 1)["peak"])
+    b = max(sm.simulate(sc.ZB, p, sc.build_program(sc.ZB, p, 16), 4, 4, 2, 1)["peak"])
+    assert abs(s / b * (4.3 / 3.6) - 54 / 30) / (54 / 30) < 0.02
+
+
+def _check_program(kind, p, m, progs):
+    V = sc.n_vstages(kind, p)
+    F, B, W = {}, {}, {}
+    for d, acts in enumerate(progs):
+        for i, a in enumerate(acts):
+            k, c, f, b, w, wc = a
+            if k in (sc.A_F, sc.A_FB, sc.A_FBS, sc.A_FW):
+                key = (f, sc.vstage(kind, p, d, c))
+                assert key not in F
+                F[key] = (d, i)
+            if k in (sc.A_BFULL, sc.A_FB, sc.A_B, sc.A_FBS):
+                key = (b, sc.vstage(kind, p, d, c))
+                assert key not in B
+                B[key] = (d, i)
+                if k in (sc.A_BFULL, sc.A_FB):
+                    W[key] = (d, i)
+            if k in (sc.A_W, sc.A_FW):
+                key = (w, sc.vstage(kind, p, d, wc))
+                assert key not in W
+                W[key] = (d, i)
+            if k in (sc.A_FB, sc.A_FBS):
+                assert f > b                                # App. A rule
+    want = {(mb, vs) for mb in range(1, m + 1) for vs in range(V)}
+    assert set(F) == want and set(B) == want and set(W) == want
+    for key in want:
+        assert F[key][0] == B[key][0] == W[key][0]
+        assert F[key][1] <= B[key][1] <= W[key][1]
+        if F[key][1] == B[key][1]:
+            pytest.fail("F and B of the same (mb, vs) in one action")
+
+
+@pytest.mark.parametrize("kind", [sc.STP, sc.STP_NOSEP, sc.ONEF1B_I, sc.ZB, sc.ONEF1B])
+@pytest.mark.parametrize("p", [1, 2, 3, 4, 5, 8])
+def test_program_invariants_and_no_deadlock(kind, p):
+    for m in range(1, 4 * p + 5):
+        if kind in (sc.ONEF1B_I,) and m % p:
+            with pytest.raises(ValueError):
+                sc.build_program(kind, p, m)
+            continue
+        progs = sc.build_program(kind, p, m)
+        _check_program(kind, p, m, progs)
+        sm.simulate(kind, p, progs, 10, 12, 8, 4)          # raises on deadlock
+
+
+@pytest.mark.parametrize("p", [2, 3, 4, 8])
+def test_rstp_phase_claims(p):
+    m = 4 * p
+    progs = sc.build_program(sc.STP, p, m)
+    for d, acts in enumerate(progs):
+        braids = [a for a in acts if a[0] in (sc.A_FB, sc.A_FBS)]
+        if d == 0:   # device 0 opens with "the first and second microbatches"
+            assert (braids[0][2], braids[0][3]) == (2, 1)
+        assert braids[0][3] == 1
+        # steady phase: separation deactivated while new microbatches arrive
+        last_f0 = max(i for i, a in enumerate(acts) if a[1] == 0 and a[0] in (sc.A_F, sc.A_FB, sc.A_FBS, sc.A_FW))
+        warm = p - 1 if d != p - 1 else 0
+        sep_before = [a for a in acts[:last_f0 + 1] if a[0] == sc.A_FBS]
+        assert len(sep_before) == warm
+        if d == p - 1:
+            assert not sep_before                           # "except for the last stage"
+    first = next(a for a in progs[0] if a[0] in (sc.A_FB, sc.A_FBS))
+    assert sc.action_str(first) == "FBS1 f2 b1"
+
+
+@pytest.mark.parametrize("kind", [sc.STP, sc.STP_NOBRAID, sc.ONEF1B_I, sc.ONEF1B_I_NAIVE, sc.ZB])
+@pytest.mark.parametrize("p,lay", [(1, [2, 1]), (2, [1, 1, 1, 1]), (2, [2, 1, 2, 1]), (3, [1] * 6)])
+def test_unit_expansion_invariants(kind, p, lay):
+    m = 2 * p
+    progs = sc.build_program(kind, p, m)
+    for d, acts in enumerate(progs):
+        units = sc.expand_units(kind, p, d, acts, lay)
+        seen = {}
+        for j, u in enumerate(units):
+            ai, stream, op, layer, c, mb, d0, d1 = u
+            assert 0 <= ai < len(acts)
+            assert d0 < j and d1 < j
+            if op in (sc.F_ATTN, sc.F_MLP, sc.B_MLP, sc.B_ATTN, sc.W_MLP, sc.W_ATTN,
+                      sc.F_EMB, sc.W_EMB, sc.F_HEAD, sc.B_HEAD, sc.W_HEAD):
+                assert stream == sc.S_COMPUTE
+                key = (op, layer, c, mb)
+                assert key not in seen
+                seen[key] = j
+            elif op in (sc.CF, sc.CB):
+                assert stream == sc.S_COMM
+            else:
+                assert stream == sc.S_PP
+        # every layer's six heavy units per (mb, chunk) exactly once
+        for c in range(1 if kind == sc.ONEF1B else 2):
+            vs = sc.vstage(kind, p, d, c)
+            first = sum(lay[:vs])
+            for mb in range(1, m + 1):
+                for l in range(first, first + lay[vs]):
+                    for op in (sc.F_ATTN, sc.F_MLP, sc.B_MLP, sc.B_ATTN, sc.W_MLP, sc.W_ATTN):
+                        assert (op, l, c, mb) in seen
+                # W after B after F
+                l = first
+                assert seen[(sc.F_ATTN, l, c, mb)] < seen[(sc.B_ATTN, l, c, mb)] < seen[(sc.W_ATTN, l, c, mb)]
+
+
+def test_fb_braid_alternates_forward_and_backward():
+    # Fig. 3a: compute stream alternates F units of mb f and B units of mb b
+    p, lay = 1, [2, 2]
+    acts = sc.build_program(sc.STP, p, 3)[0]
+    ai = next(i for i, a in enumerate(acts) if a[0] == sc.A_FB)
+    units = [u for u in sc.expand_units(sc.STP, p, 0, acts, lay) if u[0] == ai and u[1] == sc.S_COMPUTE]
+    ops = [u[2] for u in units]
+    fwd = {sc.F_ATTN, sc.F_MLP, sc.F_EMB, sc.F_HEAD}
+    pattern = ["f" if o in fwd else ("b" if o in (sc.B_MLP, sc.B_ATTN, sc.B_HEAD) else "w") for o in ops]
+    assert "".join(pattern).startswith("fbwfbwfbwfbw")
+
+
+def test_serialize_header_and_shape():
+    txt = sc.serialize(sc.STP, 2, 2, 2, 4, [1, 1, 1, 1])
+    lines = txt.split("\n")
+    assert lines[0] == "sched stp p 2 v 2 t 2 m 4"
+    assert lines[1] == "rank 0"
+    assert lines[2] == "A 0 0 0 1 -1 -1 -1"
+    assert txt.endswith("\n")

@@ -1,0 +1,479 @@
+// TP-sharded linear-layer GEMMs (the paper's
+// Column/RowParallelLinear matmuls, Fig. 2).
+//
+// bf16: persistent warp-specialised tcgen05 kernel.  One CTA per SM, 256
+// threads: warp 0 = TMA producer, warp 1 = MMA issuer (one elected lane),
+// warp 2 = TMEM allocator, warps 4-7 = epilogue (TMEM -> registers ->
+// global).  Tile 128 x BN x 64, BN in {128, 256}, a ring of smem stages
+// (128-byte swizzle, filled by TMA, released by tcgen05.commit), two TMEM
+// accumulators so the epilogue of tile i overlaps the main loop of tile i+1.
+// Operands may be K-major or MN-major (descriptor transpose bits) so forward
+// (X W^T), dgrad (dY W) and wgrad (dY^T X) all run without transposes.
+//
+// fp32: true-fp32 SIMT FMA GEMM (no TF32) for the fp32 parity mode.
+#include <cudaTypedefs.h>
+
+#include <mutex>
+#include <unordered_map>
+
+#include "common.h"
+#include "sm100.h"
+
+namespace stp {
+namespace {
+
+using namespace sm100;
+
+constexpr int BM = 128;
+constexpr int BK = 64;
+constexpr int kSmemBudget = 192 * 1024;
+
+struct GemmArgs {
+  int M, N, K;
+  int num_m_blk, num_n_blk, num_k_blk;
+  int epilogue;
+  void* C;
+  int64_t ldc;
+  const void* bias;
+  const void* R;
+  int64_t ldr;
+};
+
+template <int BN>
+struct Cfg {
+  static constexpr int A_BYTES = BM * BK * 2;
+  static constexpr int B_BYTES = BN * BK * 2;
+  static constexpr int STAGES = kSmemBudget / (A_BYTES + B_BYTES);
+  static constexpr int SMEM = STAGES * (A_BYTES + B_BYTES) + 1024 + 256;
+  static constexpr int TMEM_COLS = 2 * BN;
+};
+
+__device__ __forceinline__ uint32_t pack_bf16x2(float a, float b) {
+  __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
+  return *reinterpret_cast<uint32_t*>(&h);
+}
+
+// Epilogue for 32 consecutive columns of one row.
+__device__ __forceinline__ void epilogue_row32(const GemmArgs& p, int row, int col, const uint32_t* v) {
+  float f[32];
+#pragma unroll
+  for (int j = 0; j < 32; ++j) f[j] = __uint_as_float(v[j]);
+  const bool full = (col + 32 <= p.N);
+  if (p.epilogue == STP_EPI_ACCUM_F32) {
+    float* c = reinterpret_cast<float*>(p.C) + (int64_t)row * p.ldc + col;
+    if (full) {
+#pragma unroll
+      for (int j = 0; j < 32; j += 4) {
+        float4 o = *reinterpret_cast<float4*>(c + j);
+        o.x += f[j];
+        o.y += f[j + 1];
+        o.z += f[j + 2];
+        o.w += f[j + 3];
+        *reinterpret_cast<float4*>(c + j) = o;
+      }
+    } else {
+      for (int j = 0; j < 32 && col + j < p.N; ++j) c[j] += f[j];
+    }
+    return;
+  }
+  if (p.epilogue == STP_EPI_BIAS) {
+    const bf16* b = reinterpret_cast<const bf16*>(p.bias) + col;
+#pragma unroll
+    for (int j = 0; j < 32; ++j)
+      if (full || col + j < p.N) f[j] += __bfloat162float(b[j]);
+  } else if (p.epilogue == STP_EPI_RESID) {
+    const bf16* r = reinterpret_cast<const bf16*>(p.R) + (int64_t)row * p.ldr + col;
+    if (full) {
+#pragma unroll
+      for (int j = 0; j < 32; j += 8) {
+        uint4 u = *reinterpret_cast<const uint4*>(r + j);
+        const bf16* h = reinterpret_cast<const bf16*>(&u);
+#pragma unroll
+        for (int q = 0; q < 8; ++q) f[j + q] += __bfloat162float(h[q]);
+      }
+    } else {
+      for (int j = 0; j < 32 && col + j < p.N; ++j) f[j] += __bfloat162float(r[j]);
+    }
+  }
+  bf16* c = reinterpret_cast<bf16*>(p.C) + (int64_t)row * p.ldc + col;
+  if (full) {
+#pragma unroll
+    for (int j = 0; j < 32; j += 8) {
+      uint4 u;
+      u.x = pack_bf16x2(f[j], f[j + 1]);
+      u.y = pack_bf16x2(f[j + 2], f[j + 3]);
+      u.z = pack_bf16x2(f[j + 4], f[j + 5]);
+      u.w = pack_bf16x2(f[j + 6], f[j + 7]);
+      *reinterpret_cast<uint4*>(c + j) = u;
+    }
+  } else {
+    for (int j = 0; j < 32 && col + j < p.N; ++j) c[j] = __float2bfloat16_rn(f[j]);
+  }
+}
+
+template <int BN, bool A_MN, bool B_MN>
+__global__ void __launch_bounds__(256, 1)
+    gemm_bf16_sm100(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                    const GemmArgs p) {
+  using C = Cfg<BN>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + C::STAGES * C::A_BYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sB + C::STAGES * C::B_BYTES);
+  uint64_t* empty = full + C::STAGES;
+  uint64_t* tfull = empty + C::STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < C::STAGES; ++s) {
+      mbar_init(full + s, 1);
+      mbar_init(empty + s, 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(tfull + a, 1);
+      mbar_init(tempty + a, 4);
+    }
+    fence_barrier_init();
+    tma_prefetch_desc(&tmA);
+    tma_prefetch_desc(&tmB);
+  }
+  if (warp == 2) tmem_alloc<C::TMEM_COLS>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  const int num_tiles = p.num_m_blk * p.num_n_blk;
+  if (warp == 0) {
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+        const int mb = tile % p.num_m_blk, nb = tile / p.num_m_blk;
+        for (int kb = 0; kb < p.num_k_blk; ++kb) {
+          mbar_wait(empty + stage, phase ^ 1);
+          mbar_arrive_expect_tx(full + stage, C::A_BYTES + C::B_BYTES);
+          uint8_t* a = sA + stage * C::A_BYTES;
+          uint8_t* b = sB + stage * C::B_BYTES;
+          if (!A_MN) {
+            tma_load_2d(a, &tmA, full + stage, kb * BK, mb * BM);
+          } else {
+#pragma unroll
+            for (int c = 0; c < BM / 64; ++c) tma_load_2d(a + c * 64 * BK * 2, &tmA, full + stage, mb * BM + c * 64, kb * BK);
+          }
+          if (!B_MN) {
+            tma_load_2d(b, &tmB, full + stage, kb * BK, nb * BN);
+          } else {
+#pragma unroll
+            for (int c = 0; c < BN / 64; ++c) tma_load_2d(b + c * 64 * BK * 2, &tmB, full + stage, nb * BN + c * 64, kb * BK);
+          }
+          if (++stage == C::STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t idesc = make_idesc_bf16(BM, BN, A_MN, B_MN);
+      int stage = 0;
+      uint32_t phase = 0;
+      int local = 0;
+      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++local) {
+        const int acc = local & 1;
+        const uint32_t acc_phase = (local >> 1) & 1;
+        mbar_wait(tempty + acc, acc_phase ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + acc * BN;
+        for (int kb = 0; kb < p.num_k_blk; ++kb) {
+          mbar_wait(full + stage, phase);
+          tc_fence_after();
+          const uint32_t a_addr = smem_u32(sA + stage * C::A_BYTES);
+          const uint32_t b_addr = smem_u32(sB + stage * C::B_BYTES);
+#pragma unroll
+          for (int k = 0; k < BK / 16; ++k) {
+            const uint64_t ad = A_MN ? make_sw128_desc(a_addr + k * 2048, 64 * BK * 2, 1024)
+                                     : make_sw128_desc(a_addr + k * 32, 16, 1024);
+            const uint64_t bd = B_MN ? make_sw128_desc(b_addr + k * 2048, 64 * BK * 2, 1024)
+                                     : make_sw128_desc(b_addr + k * 32, 16, 1024);
+            mma_f16_ss(d_tmem, ad, bd, idesc, (kb | k) != 0);
+          }
+          mma_commit(empty + stage);
+          if (++stage == C::STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        mma_commit(tfull + acc);
+      }
+    }
+  } else if (warp >= 4) {
+    const int ew = warp & 3;
+    int local = 0;
+    for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++local) {
+      const int mb = tile % p.num_m_blk, nb = tile / p.num_m_blk;
+      const int acc = local & 1;
+      const uint32_t acc_phase = (local >> 1) & 1;
+      mbar_wait(tfull + acc, acc_phase);
+      tc_fence_after();
+      const int row = mb * BM + ew * 32 + lane;
+#pragma unroll 1
+      for (int c0 = 0; c0 < BN; c0 += 32) {
+        uint32_t v[32];
+        tmem_ld_32x32b_x32(tmem_base + ((uint32_t)(ew * 32) << 16) + acc * BN + c0, v);
+        tmem_wait_ld();
+        const int col = nb * BN + c0;
+        if (row < p.M && col < p.N) epilogue_row32(p, row, col, v);
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(tempty + acc);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc<C::TMEM_COLS>(tmem_base);
+  }
+}
+
+// ------------------------------------------------------------ host side
+PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, []() {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  });
+  return fn;
+}
+
+struct MapKey {
+  const void* ptr;
+  int64_t d0, d1, ld;
+  int b0, b1;
+  bool operator==(const MapKey& o) const {
+    return ptr == o.ptr && d0 == o.d0 && d1 == o.d1 && ld == o.ld && b0 == o.b0 && b1 == o.b1;
+  }
+};
+struct MapKeyHash {
+  size_t operator()(const MapKey& k) const {
+    size_t h = std::hash<const void*>()(k.ptr);
+    h ^= std::hash<int64_t>()(k.d0 * 1000003 + k.d1) + 0x9e3779b9 + (h << 6) + (h >> 2);
+    h ^= std::hash<int64_t>()(k.ld * 131 + k.b0 * 7 + k.b1) + 0x9e3779b9 + (h << 6) + (h >> 2);
+    return h;
+  }
+};
+
+// 2-D bf16 tensor map: inner dim d0 (contiguous), outer dim d1, row stride ld
+// elements, box b0 x b1, 128-byte swizzle, OOB -> zero.  Cached per thread.
+stp_status tensor_map(CUtensorMap* out, const void* ptr, int64_t d0, int64_t d1, int64_t ld, int b0, int b1) {
+  thread_local std::unordered_map<MapKey, CUtensorMap, MapKeyHash> cache;
+  MapKey key{ptr, d0, d1, ld, b0, b1};
+  auto it = cache.find(key);
+  if (it != cache.end()) {
+    *out = it->second;
+    return STP_OK;
+  }
+  auto enc = get_encode();
+  if (!enc) return fail(STP_ECUDA, "cuTensorMapEncodeTiled unavailable");
+  cuuint64_t dims[2] = {(cuuint64_t)d0, (cuuint64_t)d1};
+  cuuint64_t strides[1] = {(cuuint64_t)(ld * 2)};
+  cuuint32_t box[2] = {(cuuint32_t)b0, (cuuint32_t)b1};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = enc(out, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    set_error("cuTensorMapEncodeTiled failed (%d): d0=%lld d1=%lld ld=%lld box=%dx%d", (int)r, (long long)d0,
+              (long long)d1, (long long)ld, b0, b1);
+    return STP_ECUDA;
+  }
+  if (cache.size() > 4096) cache.clear();
+  cache.emplace(key, *out);
+  return STP_OK;
+}
+
+template <int BN, bool A_MN, bool B_MN>
+stp_status launch_bf16(const GemmArgs& a, const CUtensorMap& ta, const CUtensorMap& tb, int max_ctas,
+                       cudaStream_t st) {
+  using C = Cfg<BN>;
+  auto kern = gemm_bf16_sm100<BN, A_MN, B_MN>;
+  static bool attr_done = false;  // per instantiation
+  if (!attr_done) {
+    STP_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
+    attr_done = true;
+  }
+  const int tiles = a.num_m_blk * a.num_n_blk;
+  int grid = num_sms();
+  if (max_ctas > 0 && max_ctas < grid) grid = max_ctas;
+  if (tiles < grid) grid = tiles;
+  kern<<<grid, 256, C::SMEM, st>>>(ta, tb, a);
+  count_launch();
+  STP_LAUNCH_CHECK();
+  return STP_OK;
+}
+
+stp_status gemm_bf16(int layout, int epi, int64_t M, int64_t N, int64_t K, const void* A, int64_t lda,
+                     const void* B, int64_t ldb, void* Cp, int64_t ldc, const void* bias, const void* R,
+                     int64_t ldr, int max_ctas, cudaStream_t st) {
+  STP_CHECK_ARG(lda % 8 == 0 && ldb % 8 == 0 && ldc % 8 == 0, "bf16 GEMM strides must be multiples of 8");
+  STP_CHECK_ARG((reinterpret_cast<uintptr_t>(A) & 15) == 0 && (reinterpret_cast<uintptr_t>(B) & 15) == 0,
+                "bf16 GEMM operands must be 16-byte aligned");
+  STP_CHECK_ARG(epi != STP_EPI_RESID || (R != nullptr && ldr % 8 == 0), "RESID epilogue needs R, ldr%8==0");
+  STP_CHECK_ARG(epi != STP_EPI_BIAS || bias != nullptr, "BIAS epilogue needs bias");
+  const bool a_mn = (layout == STP_GEMM_TN);
+  const bool b_mn = (layout == STP_GEMM_NN || layout == STP_GEMM_TN);
+  // BN choice: minimise (waves x BN) with a small penalty for the narrow tile.
+  const int sms = (max_ctas > 0 && max_ctas < num_sms()) ? max_ctas : num_sms();
+  auto cost = [&](int bn) {
+    int64_t tiles = ((M + BM - 1) / BM) * ((N + bn - 1) / bn);
+    int64_t waves = (tiles + sms - 1) / sms;
+    return (double)waves * bn * (bn == 128 ? 1.08 : 1.0);
+  };
+  const int BNsel = (N <= 128 || cost(128) < cost(256)) ? 128 : 256;
+  GemmArgs g;
+  g.M = (int)M;
+  g.N = (int)N;
+  g.K = (int)K;
+  g.num_m_blk = (int)((M + BM - 1) / BM);
+  g.num_n_blk = (int)((N + BNsel - 1) / BNsel);
+  g.num_k_blk = (int)((K + BK - 1) / BK);
+  g.epilogue = epi;
+  g.C = Cp;
+  g.ldc = ldc;
+  g.bias = bias;
+  g.R = R;
+  g.ldr = ldr;
+  CUtensorMap ta, tb;
+  stp_status s;
+  if (!a_mn) s = tensor_map(&ta, A, K, M, lda, BK, BM);  // A [M, K]
+  else s = tensor_map(&ta, A, M, K, lda, 64, BK);         // A^T stored [K, M]
+  if (s != STP_OK) return s;
+  if (!b_mn) s = tensor_map(&tb, B, K, N, ldb, BK, BNsel);  // B [N, K]
+  else s = tensor_map(&tb, B, N, K, ldb, 64, BK);           // B [K, N]
+  if (s != STP_OK) return s;
+#define STP_GEMM_CASE(bn, amn, bmn) \
+  if (BNsel == bn && a_mn == amn && b_mn == bmn) return launch_bf16<bn, amn, bmn>(g, ta, tb, max_ctas, st);
+  STP_GEMM_CASE(128, false, false)
+  STP_GEMM_CASE(256, false, false)
+  STP_GEMM_CASE(128, false, true)
+  STP_GEMM_CASE(256, false, true)
+  STP_GEMM_CASE(128, true, true)
+  STP_GEMM_CASE(256, true, true)
+#undef STP_GEMM_CASE
+  return fail(STP_EUNSUPPORTED, "gemm layout");
+}
+
+// -------------------------------------------------------------- fp32 SIMT
+// C[m,n] = sum_k A(m,k) B(k,n), A(m,k) = A[m*sam + k*sak], B(k,n) = B[k*sbk + n*sbn].
+constexpr int FB = 64, FK = 16;
+__global__ void __launch_bounds__(256) gemm_f32_simt(int M, int N, int K, const float* __restrict__ A, int64_t sam,
+                                                     int64_t sak, const float* __restrict__ B, int64_t sbk,
+                                                     int64_t sbn, float* C, int64_t ldc, int epi,
+                                                     const float* __restrict__ bias, const float* __restrict__ R,
+                                                     int64_t ldr) {
+  __shared__ float As[FK][FB + 1];
+  __shared__ float Bs[FK][FB + 1];
+  const int tx = threadIdx.x % 16, ty = threadIdx.x / 16;
+  const int m0 = blockIdx.y * FB, n0 = blockIdx.x * FB;
+  float acc[4][4] = {};
+  for (int k0 = 0; k0 < K; k0 += FK) {
+    for (int i = threadIdx.x; i < FK * FB; i += 256) {
+      int kk = i / FB, mm = i % FB;
+      int m = m0 + mm, k = k0 + kk;
+      As[kk][mm] = (m < M && k < K) ? A[(int64_t)m * sam + (int64_t)k * sak] : 0.f;
+      int n = n0 + mm;
+      Bs[kk][mm] = (n < N && k < K) ? B[(int64_t)k * sbk + (int64_t)n * sbn] : 0.f;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int kk = 0; kk < FK; ++kk) {
+      float a[4], b[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) a[i] = As[kk][ty * 4 + i];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) b[j] = Bs[kk][tx * 4 + j];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(a[i], b[j], acc[i][j]);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    int m = m0 + ty * 4 + i;
+    if (m >= M) continue;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      int n = n0 + tx * 4 + j;
+      if (n >= N) continue;
+      float v = acc[i][j];
+      float* c = C + (int64_t)m * ldc + n;
+      if (epi == STP_EPI_ACCUM_F32) {
+        *c += v;
+      } else {
+        if (epi == STP_EPI_BIAS) v += bias[n];
+        if (epi == STP_EPI_RESID) v += R[(int64_t)m * ldr + n];
+        *c = v;
+      }
+    }
+  }
+}
+
+stp_status gemm_f32(int layout, int epi, int64_t M, int64_t N, int64_t K, const float* A, int64_t lda,
+                    const float* B, int64_t ldb, float* C, int64_t ldc, const float* bias, const float* R,
+                    int64_t ldr, cudaStream_t st) {
+  int64_t sam, sak, sbk, sbn;
+  if (layout == STP_GEMM_NT) {
+    sam = lda; sak = 1; sbk = 1; sbn = ldb;
+  } else if (layout == STP_GEMM_NN) {
+    sam = lda; sak = 1; sbk = ldb; sbn = 1;
+  } else {
+    sam = 1; sak = lda; sbk = ldb; sbn = 1;
+  }
+  dim3 grid((unsigned)((N + FB - 1) / FB), (unsigned)((M + FB - 1) / FB));
+  gemm_f32_simt<<<grid, 256, 0, st>>>((int)M, (int)N, (int)K, A, sam, sak, B, sbk, sbn, C, ldc, epi, bias, R, ldr);
+  count_launch();
+  STP_LAUNCH_CHECK();
+  return STP_OK;
+}
+
+}  // namespace
+
+stp_status gemm_dispatch(int dtype, int layout, int epi, int64_t M, int64_t N, int64_t K, const void* A,
+                         int64_t lda, const void* B, int64_t ldb, void* C, int64_t ldc, const void* bias,
+                         const void* R, int64_t ldr, int max_ctas, cudaStream_t st) {
+  STP_CHECK_ARG(M >= 0 && N >= 0 && K >= 0, "negative GEMM size");
+  STP_CHECK_ARG(layout >= 0 && layout <= 2, "layout");
+  STP_CHECK_ARG(epi >= 0 && epi <= 3, "epilogue");
+  if (M == 0 || N == 0) return STP_OK;
+  if (dtype == STP_DTYPE_F32)
+    return gemm_f32(layout, epi, M, N, K, (const float*)A, lda, (const float*)B, ldb, (float*)C, ldc,
+                    (const float*)bias, (const float*)R, ldr, st);
+  if (dtype == STP_DTYPE_BF16) {
+    if (K == 0) return fail(STP_EUNSUPPORTED, "bf16 GEMM with K == 0");
+    return gemm_bf16(layout, epi, M, N, K, A, lda, B, ldb, C, ldc, bias, R, ldr, max_ctas, st);
+  }
+  return fail(STP_EINVAL, "dtype");
+}
+
+}  // namespace stp
+
+extern "C" stp_status stp_op_gemm(int32_t dtype, int32_t layout, int32_t epilogue, int64_t M, int64_t N, int64_t K,
+                                  const void* A, int64_t lda, const void* B, int64_t ldb, void* C, int64_t ldc,
+                                  const void* bias, const void* R, int64_t ldr, int32_t max_ctas, void* stream) {
+  return stp::gemm_dispatch(dtype, layout, epilogue, M, N, K, A, lda, B, ldb, C, ldc, bias, R, ldr, max_ctas,
+                            (cudaStream_t)stream);
+}

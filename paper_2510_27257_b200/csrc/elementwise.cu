@@ -1,0 +1,564 @@
+// Fused memory-bound kernels of the STP units:
+// RMSNorm fwd/bwd with the fused residual of Eq. 1-2 (SP
+// reading Q10), rotate-half RoPE fwd/bwd, SwiGLU fwd/bwd, vocab-parallel
+// embedding fwd/bwd, vocab-parallel cross-entropy (local stats, combine,
+// gradient), bias column sums and dtype conversion.
+//
+// All are HBM-bound: 16-byte vectorised, coalesced row access (one warp per
+// row for the [s, h] row kernels), warp-shuffle reductions, fp32 arithmetic,
+// grids sized in multiples of the SM count.
+#include <cmath>
+
+#include "common.h"
+
+namespace stp {
+namespace {
+
+constexpr int kWarpsPerBlock = 8;
+
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+__device__ __forceinline__ float warp_max(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+// 16-byte vector of T.
+template <typename T>
+struct Vec {
+  static constexpr int N = 16 / sizeof(T);
+  union {
+    uint4 u;
+    T v[N];
+  };
+  __device__ __forceinline__ void load(const T* p) { u = *reinterpret_cast<const uint4*>(p); }
+  __device__ __forceinline__ void store(T* p) const { *reinterpret_cast<uint4*>(p) = u; }
+  __device__ __forceinline__ float f(int i) const { return to_f<T>(v[i]); }
+  __device__ __forceinline__ void set(int i, float x) { v[i] = from_f<T>(x); }
+};
+
+int grid_for(int64_t work_items, int items_per_block) {
+  int64_t b = (work_items + items_per_block - 1) / items_per_block;
+  int64_t cap = (int64_t)num_sms() * 16;
+  if (b > cap) b = cap;
+  if (b < 1) b = 1;
+  return (int)b;
+}
+
+// ---------------------------------------------------------------- RMSNorm
+template <typename T>
+__global__ void rmsnorm_fwd_kernel(int64_t rows, int h, const T* __restrict__ x, const T* __restrict__ resid,
+                                   T* x_out, const T* __restrict__ g, float eps, T* y, float* rstd_out) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp0 = (int64_t)blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5);
+  const int64_t nwarps = (int64_t)gridDim.x * kWarpsPerBlock;
+  constexpr int VN = Vec<T>::N;
+  for (int64_t r = warp0; r < rows; r += nwarps) {
+    const T* xr = x + r * h;
+    const T* rr = resid ? resid + r * h : nullptr;
+    float ss = 0.f;
+    for (int c = lane * VN; c < h; c += 32 * VN) {
+      Vec<T> a;
+      a.load(xr + c);
+      if (rr) {
+        Vec<T> b;
+        b.load(rr + c);
+#pragma unroll
+        for (int i = 0; i < VN; ++i) a.set(i, a.f(i) + b.f(i));
+        a.store(x_out + r * h + c);
+      }
+#pragma unroll
+      for (int i = 0; i < VN; ++i) ss += a.f(i) * a.f(i);
+    }
+    ss = warp_sum(ss);
+    const float rs = rsqrtf(ss / (float)h + eps);
+    if (rstd_out && lane == 0) rstd_out[r] = rs;
+    const T* src = rr ? x_out + r * h : xr;
+    if (rr) __syncwarp();
+    for (int c = lane * VN; c < h; c += 32 * VN) {
+      Vec<T> a, gg, o;
+      a.load(src + c);
+      gg.load(g + c);
+#pragma unroll
+      for (int i = 0; i < VN; ++i) o.set(i, a.f(i) * rs * gg.f(i));
+      o.store(y + r * h + c);
+    }
+  }
+}
+
+// dgamma partials accumulate in shared memory, flushed once per block.
+template <typename T>
+__global__ void rmsnorm_bwd_kernel(int64_t rows, int h, const T* __restrict__ dy, const T* __restrict__ x,
+                                   const T* __restrict__ g, const float* __restrict__ rstd,
+                                   const T* __restrict__ dres, T* dx, float* dgamma) {
+  extern __shared__ float sg[];
+  if (dgamma)
+    for (int i = threadIdx.x; i < h; i += blockDim.x) sg[i] = 0.f;
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  const int64_t warp0 = (int64_t)blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5);
+  const int64_t nwarps = (int64_t)gridDim.x * kWarpsPerBlock;
+  constexpr int VN = Vec<T>::N;
+  for (int64_t r = warp0; r < rows; r += nwarps) {
+    const float rs = rstd[r];
+    float dot = 0.f;
+    for (int c = lane * VN; c < h; c += 32 * VN) {
+      Vec<T> a, d, gg;
+      a.load(x + r * h + c);
+      d.load(dy + r * h + c);
+      gg.load(g + c);
+#pragma unroll
+      for (int i = 0; i < VN; ++i) {
+        dot += gg.f(i) * d.f(i) * a.f(i);
+        if (dgamma) atomicAdd(&sg[c + i], d.f(i) * a.f(i) * rs);
+      }
+    }
+    dot = warp_sum(dot) / (float)h;
+    const float k = rs * rs * rs * dot;
+    for (int c = lane * VN; c < h; c += 32 * VN) {
+      Vec<T> a, d, gg, o;
+      a.load(x + r * h + c);
+      d.load(dy + r * h + c);
+      gg.load(g + c);
+      Vec<T> rr;
+      if (dres) rr.load(dres + r * h + c);
+#pragma unroll
+      for (int i = 0; i < VN; ++i) {
+        float v = rs * gg.f(i) * d.f(i) - a.f(i) * k;
+        if (dres) v += rr.f(i);
+        o.set(i, v);
+      }
+      o.store(dx + r * h + c);
+    }
+  }
+  if (dgamma) {
+    __syncthreads();
+    for (int i = threadIdx.x; i < h; i += blockDim.x) atomicAdd(&dgamma[i], sg[i]);
+  }
+}
+
+// ------------------------------------------------------------------- RoPE
+template <typename T>
+__global__ void rope_kernel(int64_t s, int64_t ld, int64_t col0, int nh, int d, double theta, int64_t pos0,
+                            int backward, T* x) {
+  const int half = d / 2;
+  const int64_t total = s * nh * half;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int j = (int)(i % half);
+    const int64_t t = i / half;
+    const int hd = (int)(t % nh);
+    const int64_t row = t / nh;
+    const double inv = pow(theta, -2.0 * (double)j / (double)d);
+    double sn, cs;
+    sincos((double)(pos0 + row) * inv, &sn, &cs);
+    const float c = (float)cs, sv = (float)sn;
+    T* p = x + row * ld + col0 + (int64_t)hd * d;
+    const float x1 = to_f<T>(p[j]), x2 = to_f<T>(p[j + half]);
+    float y1, y2;
+    if (!backward) {
+      y1 = x1 * c - x2 * sv;
+      y2 = x2 * c + x1 * sv;
+    } else {
+      y1 = x1 * c + x2 * sv;
+      y2 = x2 * c - x1 * sv;
+    }
+    p[j] = from_f<T>(y1);
+    p[j + half] = from_f<T>(y2);
+  }
+}
+
+// ----------------------------------------------------------------- SwiGLU
+__device__ __forceinline__ float sigm(float z) { return 1.f / (1.f + __expf(-z)); }
+
+template <typename T>
+__global__ void swiglu_fwd_kernel(int64_t s, int64_t I, const T* __restrict__ gu, T* H) {
+  constexpr int VN = Vec<T>::N;
+  const int64_t nv = I / VN;
+  const int64_t total = s * nv;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = i / nv, c = (i % nv) * VN;
+    Vec<T> G, U, o;
+    G.load(gu + r * 2 * I + c);
+    U.load(gu + r * 2 * I + I + c);
+#pragma unroll
+    for (int k = 0; k < VN; ++k) {
+      const float z = G.f(k);
+      o.set(k, z * sigm(z) * U.f(k));
+    }
+    o.store(H + r * I + c);
+  }
+}
+
+template <typename T>
+__global__ void swiglu_bwd_kernel(int64_t s, int64_t I, const T* __restrict__ dH, const T* __restrict__ gu,
+                                  T* dgu) {
+  constexpr int VN = Vec<T>::N;
+  const int64_t nv = I / VN;
+  const int64_t total = s * nv;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = i / nv, c = (i % nv) * VN;
+    Vec<T> G, U, D, dG, dU;
+    G.load(gu + r * 2 * I + c);
+    U.load(gu + r * 2 * I + I + c);
+    D.load(dH + r * I + c);
+#pragma unroll
+    for (int k = 0; k < VN; ++k) {
+      const float z = G.f(k), sg = sigm(z), dh = D.f(k);
+      dU.set(k, dh * z * sg);
+      dG.set(k, dh * U.f(k) * sg * (1.f + z * (1.f - sg)));
+    }
+    dG.store(dgu + r * 2 * I + c);
+    dU.store(dgu + r * 2 * I + I + c);
+  }
+}
+
+// -------------------------------------------------------------- embedding
+template <typename T>
+__global__ void embed_fwd_kernel(int64_t s, int h, const int32_t* __restrict__ tok, int64_t v0, int64_t Vl,
+                                 const T* __restrict__ E, T* out) {
+  constexpr int VN = Vec<T>::N;
+  const int lane = threadIdx.x & 31;
+  const int64_t warp0 = (int64_t)blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5);
+  const int64_t nwarps = (int64_t)gridDim.x * kWarpsPerBlock;
+  for (int64_t r = warp0; r < s; r += nwarps) {
+    const int64_t t = (int64_t)tok[r] - v0;
+    const bool own = t >= 0 && t < Vl;
+    for (int c = lane * VN; c < h; c += 32 * VN) {
+      Vec<T> a;
+      if (own) a.load(E + t * h + c);
+      else a.u = make_uint4(0, 0, 0, 0);
+      a.store(out + r * h + c);
+    }
+  }
+}
+
+template <typename T>
+__global__ void embed_bwd_kernel(int64_t s, int h, const int32_t* __restrict__ tok, int64_t v0, int64_t Vl,
+                                 const T* __restrict__ dX, float* dE) {
+  const int64_t total = s * h;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = i / h, c = i % h;
+    const int64_t t = (int64_t)tok[r] - v0;
+    if (t >= 0 && t < Vl) atomicAdd(&dE[t * h + c], to_f<T>(dX[i]));
+  }
+}
+
+// ---------------------------------------------------------- cross-entropy
+template <typename T>
+__global__ void ce_stats_kernel(int64_t s, int64_t Vl, const T* __restrict__ logits, int64_t ld,
+                                const int32_t* __restrict__ tgt, int64_t v0, float* stats) {
+  __shared__ float sm[32], ssum[32];
+  for (int64_t r = blockIdx.x; r < s; r += gridDim.x) {
+    const T* z = logits + r * ld;
+    float m = -INFINITY, sum = 0.f;
+    for (int64_t j = threadIdx.x; j < Vl; j += blockDim.x) {
+      const float v = to_f<T>(z[j]);
+      if (v > m) {
+        sum = sum * __expf(m - v) + 1.f;
+        m = v;
+      } else {
+        sum += __expf(v - m);
+      }
+    }
+    // warp combine (m, sum)
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const float mo = __shfl_xor_sync(0xffffffffu, m, o), so = __shfl_xor_sync(0xffffffffu, sum, o);
+      const float mn = fmaxf(m, mo);
+      sum = (m == -INFINITY ? 0.f : sum * __expf(m - mn)) + (mo == -INFINITY ? 0.f : so * __expf(mo - mn));
+      m = mn;
+    }
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+    if (lane == 0) {
+      sm[w] = m;
+      ssum[w] = sum;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      float M = -INFINITY;
+      for (int i = 0; i < nw; ++i) M = fmaxf(M, sm[i]);
+      float S = 0.f;
+      for (int i = 0; i < nw; ++i)
+        if (sm[i] != -INFINITY) S += ssum[i] * __expf(sm[i] - M);
+      const int64_t t = (int64_t)tgt[r] - v0;
+      stats[r * 3 + 0] = M;
+      stats[r * 3 + 1] = S;
+      stats[r * 3 + 2] = (t >= 0 && t < Vl) ? to_f<T>(z[t]) : 0.f;
+    }
+    __syncthreads();
+  }
+}
+
+__global__ void ce_combine_kernel(int64_t s, int t, const float* __restrict__ st, float* lse, float* loss_acc,
+                                  float scale) {
+  float local = 0.f;
+  for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < s; r += (int64_t)gridDim.x * blockDim.x) {
+    float M = -INFINITY;
+    for (int q = 0; q < t; ++q) M = fmaxf(M, st[((int64_t)q * s + r) * 3]);
+    float Z = 0.f, tl = 0.f;
+    for (int q = 0; q < t; ++q) {
+      const float* p = st + ((int64_t)q * s + r) * 3;
+      Z += p[1] * __expf(p[0] - M);
+      tl += p[2];
+    }
+    const float l = M + logf(Z);
+    lse[r] = l;
+    local += l - tl;
+  }
+  local = warp_sum(local);
+  if ((threadIdx.x & 31) == 0) atomicAdd(loss_acc, local * scale);
+}
+
+template <typename T>
+__global__ void ce_grad_kernel(int64_t s, int64_t Vl, T* logits, int64_t ld, const int32_t* __restrict__ tgt,
+                               int64_t v0, const float* __restrict__ lse, float scale) {
+  for (int64_t r = blockIdx.x; r < s; r += gridDim.x) {
+    T* z = logits + r * ld;
+    const float l = lse[r];
+    const int64_t t = (int64_t)tgt[r] - v0;
+    for (int64_t j = threadIdx.x; j < Vl; j += blockDim.x) {
+      float p = __expf(to_f<T>(z[j]) - l);
+      if (j == t) p -= 1.f;
+      z[j] = from_f<T>(p * scale);
+    }
+  }
+}
+
+// ------------------------------------------------------------- misc
+template <typename T>
+__global__ void colsum_kernel(int64_t rows, int64_t n, const T* __restrict__ X, int64_t ld, float* acc,
+                              int64_t rows_per_block) {
+  const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= n) return;
+  const int64_t r0 = (int64_t)blockIdx.y * rows_per_block;
+  const int64_t r1 = min(rows, r0 + rows_per_block);
+  float s = 0.f;
+  for (int64_t r = r0; r < r1; ++r) s += to_f<T>(X[r * ld + c]);
+  atomicAdd(&acc[c], s);
+}
+
+template <typename S, typename D>
+__global__ void convert_kernel(int64_t n, const S* __restrict__ src, D* dst) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    dst[i] = from_f<D>(to_f<S>(src[i]));
+}
+
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+
+}  // namespace
+
+// Shared launchers (also used by the executor).
+stp_status rmsnorm_fwd(int dtype, int64_t rows, int64_t h, const void* x, const void* resid, void* x_out,
+                       const void* g, float eps, void* y, float* rstd, cudaStream_t st) {
+  STP_CHECK_ARG(h % 8 == 0, "hidden % 8 == 0");
+  STP_CHECK_ARG(aligned16(x) && aligned16(y) && aligned16(g), "16-byte aligned rows");
+  STP_CHECK_ARG(!resid || x_out, "resid needs x_out");
+  if (rows == 0) return STP_OK;
+  return STP_DISPATCH_DTYPE(dtype, [&] {
+    rmsnorm_fwd_kernel<T><<<grid_for(rows, kWarpsPerBlock), 32 * kWarpsPerBlock, 0, st>>>(
+        rows, (int)h, (const T*)x, (const T*)resid, (T*)x_out, (const T*)g, eps, (T*)y, rstd);
+    count_launch();
+    STP_LAUNCH_CHECK();
+    return STP_OK;
+  });
+}
+
+stp_status rmsnorm_bwd(int dtype, int64_t rows, int64_t h, const void* dy, const void* x, const void* g,
+                       const float* rstd, const void* dres, void* dx, float* dgamma, cudaStream_t st) {
+  STP_CHECK_ARG(h % 8 == 0, "hidden % 8 == 0");
+  STP_CHECK_ARG(h * 4 <= 200 * 1024, "hidden too large for the smem dgamma buffer");
+  if (rows == 0) return STP_OK;
+  return STP_DISPATCH_DTYPE(dtype, [&] {
+    const int grid = std::min<int64_t>(grid_for(rows, kWarpsPerBlock), 2 * num_sms());
+    const size_t sm = dgamma ? h * sizeof(float) : 0;
+    auto k = rmsnorm_bwd_kernel<T>;
+    if (sm > 48 * 1024) STP_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    k<<<grid, 32 * kWarpsPerBlock, sm, st>>>(rows, (int)h, (const T*)dy, (const T*)x, (const T*)g, rstd,
+                                             (const T*)dres, (T*)dx, dgamma);
+    count_launch();
+    STP_LAUNCH_CHECK();
+    return STP_OK;
+  });
+}
+
+stp_status rope(int dtype, int backward, int64_t s, int64_t ld, int64_t col0, int nh, int d, float theta,
+                int64_t pos0, void* x, cudaStream_t st) {
+  STP_CHECK_ARG(d % 2 == 0, "head_dim even");
+  if (s == 0 || nh == 0) return STP_OK;
+  return STP_DISPATCH_DTYPE(dtype, [&] {
+    rope_kernel<T><<<grid_for(s * nh * (d / 2), 256), 256, 0, st>>>(s, ld, col0, nh, d, (double)theta, pos0,
+                                                                     backward, (T*)x);
+    count_launch();
+    STP_LAUNCH_CHECK();
+    return STP_OK;
+  });
+}
+
+stp_status swiglu_fwd(int dtype, int64_t s, int64_t I, const void* gu, void* H, cudaStream_t st) {
+  STP_CHECK_ARG(I % 8 == 0, "ffn shard % 8 == 0");
+  if (s == 0) return STP_OK;
+  return STP_DISPATCH_DTYPE(dtype, [&] {
+    swiglu_fwd_kernel<T><<<grid_for(s * I / Vec<T>::N, 256), 256, 0, st>>>(s, I, (const T*)gu, (T*)H);
+    count_launch();
+    STP_LAUNCH_CHECK();
+    return STP_OK;
+  });
+}
+
+stp_status swiglu_bwd(int dtype, int64_t s, int64_t I, const void* dH, const void* gu, void* dgu, cudaStream_t st) {
+  STP_CHECK_ARG(I % 8 == 0, "ffn shard % 8 == 0");
+  if (s == 0) return STP_OK;
+  return STP_DISPATCH_DTYPE(dtype, [&] {
+    swiglu_bwd_kernel<T><<<grid_for(s * I / Vec<T>::N, 256), 256, 0, st>>>(s, I, (const T*)dH, (const T*)gu,
+                                                                            (T*)dgu);
+    count_launch();
+    STP_LAUNCH_CHECK();
+    return STP_OK;
+  });
+}
+
+stp_status embed_fwd(int dtype, int64_t s, int64_t h, const int32_t* tok, int64_t v0, int64_t Vl, const void* E,
+                     void* out, cudaStream_t st) {
+  STP_CHECK_ARG(h % 8 == 0, "hidden % 8 == 0");
+  if (s == 0) return STP_OK;
+  return STP_DISPATCH_DTYPE(dtype, [&] {
+    embed_fwd_kernel<T><<<grid_for(s, kWarpsPerBlock), 32 * kWarpsPerBlock, 0, st>>>(s, (int)h, tok, v0, Vl,
+                                                                                      (const T*)E, (T*)out);
+    count_launch();
+    STP_LAUNCH_CHECK();
+    return STP_OK;
+  });
+}
+
+stp_status embed_bwd(int dtype, int64_t s, int64_t h, const int32_t* tok, int64_t v0, int64_t Vl, const void* dX,
+                     float* dE, cudaStream_t st) {
+  if (s == 0) return STP_OK;
+  return STP_DISPATCH_DTYPE(dtype, [&] {
+    embed_bwd_kernel<T><<<grid_for(s * h, 256), 256, 0, st>>>(s, (int)h, tok, v0, Vl, (const T*)dX, dE);
+    count_launch();
+    STP_LAUNCH_CHECK();
+    return STP_OK;
+  });
+}
+
+stp_status ce_stats(int dtype, int64_t s, int64_t Vl, const void* logits, int64_t ld, const int32_t* tgt, int64_t v0,
+                    float* stats, cudaStream_t st) {
+  if (s == 0) return STP_OK;
+  return STP_DISPATCH_DTYPE(dtype, [&] {
+    ce_stats_kernel<T><<<(int)std::min<int64_t>(s, 16 * num_sms()), 512, 0, st>>>(s, Vl, (const T*)logits, ld, tgt,
+                                                                                   v0, stats);
+    count_launch();
+    STP_LAUNCH_CHECK();
+    return STP_OK;
+  });
+}
+
+stp_status ce_combine(int64_t s, int t, const float* stats_all, float* lse, float* loss_acc, float scale,
+                      cudaStream_t st) {
+  if (s == 0) return STP_OK;
+  ce_combine_kernel<<<grid_for(s, 256), 256, 0, st>>>(s, t, stats_all, lse, loss_acc, scale);
+  count_launch();
+  STP_LAUNCH_CHECK();
+  return STP_OK;
+}
+
+stp_status ce_grad(int dtype, int64_t s, int64_t Vl, void* logits, int64_t ld, const int32_t* tgt, int64_t v0,
+                   const float* lse, float scale, cudaStream_t st) {
+  if (s == 0) return STP_OK;
+  return STP_DISPATCH_DTYPE(dtype, [&] {
+    ce_grad_kernel<T><<<(int)std::min<int64_t>(s, 16 * num_sms()), 512, 0, st>>>(s, Vl, (T*)logits, ld, tgt, v0, lse,
+                                                                                  scale);
+    count_launch();
+    STP_LAUNCH_CHECK();
+    return STP_OK;
+  });
+}
+
+stp_status colsum_acc(int dtype, int64_t rows, int64_t n, const void* X, int64_t ld, float* acc, cudaStream_t st) {
+  if (rows == 0 || n == 0) return STP_OK;
+  return STP_DISPATCH_DTYPE(dtype, [&] {
+    const int64_t rpb = 256;
+    dim3 grid((unsigned)((n + 255) / 256), (unsigned)((rows + rpb - 1) / rpb));
+    colsum_kernel<T><<<grid, 256, 0, st>>>(rows, n, (const T*)X, ld, acc, rpb);
+    count_launch();
+    STP_LAUNCH_CHECK();
+    return STP_OK;
+  });
+}
+
+stp_status convert(int sd, int dd, int64_t n, const void* src, void* dst, cudaStream_t st) {
+  if (n == 0) return STP_OK;
+  const int grid = grid_for(n, 256);
+  if (sd == STP_DTYPE_F32 && dd == STP_DTYPE_BF16)
+    convert_kernel<float, bf16><<<grid, 256, 0, st>>>(n, (const float*)src, (bf16*)dst);
+  else if (sd == STP_DTYPE_BF16 && dd == STP_DTYPE_F32)
+    convert_kernel<bf16, float><<<grid, 256, 0, st>>>(n, (const bf16*)src, (float*)dst);
+  else if (sd == STP_DTYPE_F32 && dd == STP_DTYPE_F32)
+    convert_kernel<float, float><<<grid, 256, 0, st>>>(n, (const float*)src, (float*)dst);
+  else if (sd == STP_DTYPE_BF16 && dd == STP_DTYPE_BF16)
+    convert_kernel<bf16, bf16><<<grid, 256, 0, st>>>(n, (const bf16*)src, (bf16*)dst);
+  else
+    return fail(STP_EINVAL, "convert dtype");
+  count_launch();
+  STP_LAUNCH_CHECK();
+  return STP_OK;
+}
+
+}  // namespace stp
+
+extern "C" {
+
+stp_status stp_op_rmsnorm_fwd(int32_t dtype, int64_t rows, int64_t h, const void* x, const void* resid, void* x_out,
+                              const void* gamma, float eps, void* y, float* rstd_out, void* stream) {
+  return stp::rmsnorm_fwd(dtype, rows, h, x, resid, x_out, gamma, eps, y, rstd_out, (cudaStream_t)stream);
+}
+stp_status stp_op_rmsnorm_bwd(int32_t dtype, int64_t rows, int64_t h, const void* dy, const void* x,
+                              const void* gamma, const float* rstd, const void* dres, void* dx, float* dgamma_acc,
+                              void* stream) {
+  return stp::rmsnorm_bwd(dtype, rows, h, dy, x, gamma, rstd, dres, dx, dgamma_acc, (cudaStream_t)stream);
+}
+stp_status stp_op_rope(int32_t dtype, int32_t backward, int64_t s, int64_t ld, int64_t col0, int32_t n_heads,
+                       int32_t d, float theta, int64_t pos0, void* x, void* stream) {
+  return stp::rope(dtype, backward, s, ld, col0, n_heads, d, theta, pos0, x, (cudaStream_t)stream);
+}
+stp_status stp_op_swiglu_fwd(int32_t dtype, int64_t s, int64_t I, const void* gu, void* H, void* stream) {
+  return stp::swiglu_fwd(dtype, s, I, gu, H, (cudaStream_t)stream);
+}
+stp_status stp_op_swiglu_bwd(int32_t dtype, int64_t s, int64_t I, const void* dH, const void* gu, void* dgu,
+                             void* stream) {
+  return stp::swiglu_bwd(dtype, s, I, dH, gu, dgu, (cudaStream_t)stream);
+}
+stp_status stp_op_embed_fwd(int32_t dtype, int64_t s, int64_t h, const int32_t* tok, int64_t v0, int64_t Vl,
+                            const void* E, void* out, void* stream) {
+  return stp::embed_fwd(dtype, s, h, tok, v0, Vl, E, out, (cudaStream_t)stream);
+}
+stp_status stp_op_embed_bwd(int32_t dtype, int64_t s, int64_t h, const int32_t* tok, int64_t v0, int64_t Vl,
+                            const void* dX, float* dE_acc, void* stream) {
+  return stp::embed_bwd(dtype, s, h, tok, v0, Vl, dX, dE_acc, (cudaStream_t)stream);
+}
+stp_status stp_op_ce_stats(int32_t dtype, int64_t s, int64_t Vl, const void* logits, int64_t ld, const int32_t* tgt,
+                           int64_t v0, float* stats, void* stream) {
+  return stp::ce_stats(dtype, s, Vl, logits, ld, tgt, v0, stats, (cudaStream_t)stream);
+}
+stp_status stp_op_ce_combine(int64_t s, int32_t t, const float* stats_all, float* lse, float* loss_acc,
+                             float loss_scale, void* stream) {
+  return stp::ce_combine(s, t, stats_all, lse, loss_acc, loss_scale, (cudaStream_t)stream);
+}
+stp_status stp_op_ce_grad(int32_t dtype, int64_t s, int64_t Vl, void* logits, int64_t ld, const int32_t* tgt,
+                          int64_t v0, const float* lse, float grad_scale, void* stream) {
+  return stp::ce_grad(dtype, s, Vl, logits, ld, tgt, v0, lse, grad_scale, (cudaStream_t)stream);
+}
+stp_status stp_op_colsum_acc(int32_t dtype, int64_t rows, int64_t n, const void* X, int64_t ld, float* acc,
+                             void* stream) {
+  return stp::colsum_acc(dtype, rows, n, X, ld, acc, (cudaStream_t)stream);
+}
+stp_status stp_op_convert(int32_t src_dtype, int32_t dst_dtype, int64_t n, const void* src, void* dst,
+                          void* stream) {
+  return stp::convert(src_dtype, dst_dtype, n, src, dst, (cudaStream_t)stream);
+}
+
+}  // extern "C"

@@ -92,7 +92,7 @@ def test_gemm_bf16_epilogues(epi):
 @pytest.mark.parametrize("layout", [0, 1, 2])
 def test_gemm_bf16_max_ctas(layout):
     ops = _ops()
-    M, N, K = 1000, 700, 320
+    M, N, K = 1000, 712, 320
     sa, sb = _shapes_for(layout, M, N, K)
     A, dA = _mk(sa, 8, torch.bfloat16)
     B, dB = _mk(sb, 9, torch.bfloat16)

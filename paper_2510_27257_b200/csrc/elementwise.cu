@@ -94,7 +94,7 @@ __global__ void rmsnorm_fwd_kernel(int64_t rows, int h, const T* __restrict__ x,
 template <typename T>
 __global__ void rmsnorm_bwd_kernel(int64_t rows, int h, const T* __restrict__ dy, const T* __restrict__ x,
                                    const T* __restrict__ g, const float* __restrict__ rstd,
-                                   const T* __restrict__ dres, T* dx, float* dgamma) {
+                                   const T* dres, T* dx, float* dgamma) {
   extern __shared__ float sg[];
   if (dgamma)
     for (int i = threadIdx.x; i < h; i += blockDim.x) sg[i] = 0.f;
@@ -194,7 +194,7 @@ __global__ void swiglu_fwd_kernel(int64_t s, int64_t I, const T* __restrict__ gu
 }
 
 template <typename T>
-__global__ void swiglu_bwd_kernel(int64_t s, int64_t I, const T* __restrict__ dH, const T* __restrict__ gu,
+__global__ void swiglu_bwd_kernel(int64_t s, int64_t I, const T* __restrict__ dH, const T* gu,
                                   T* dgu) {
   constexpr int VN = Vec<T>::N;
   const int64_t nv = I / VN;
@@ -345,6 +345,12 @@ template <typename S, typename D>
 __global__ void convert_kernel(int64_t n, const S* __restrict__ src, D* dst) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
     dst[i] = from_f<D>(to_f<S>(src[i]));
+}
+
+template <typename T>
+__global__ void add_kernel(int64_t n, const T* __restrict__ a, const T* __restrict__ b, T* out) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = from_f<T>(to_f<T>(a[i]) + to_f<T>(b[i]));
 }
 
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
@@ -506,6 +512,17 @@ stp_status convert(int sd, int dd, int64_t n, const void* src, void* dst, cudaSt
   count_launch();
   STP_LAUNCH_CHECK();
   return STP_OK;
+}
+
+// out = a + b (residual add without a norm, the chunk's last layer).
+stp_status add(int dtype, int64_t n, const void* a, const void* b, void* out, cudaStream_t st) {
+  if (n == 0) return STP_OK;
+  return STP_DISPATCH_DTYPE(dtype, [&] {
+    add_kernel<T><<<grid_for(n, 256), 256, 0, st>>>(n, (const T*)a, (const T*)b, (T*)out);
+    count_launch();
+    STP_LAUNCH_CHECK();
+    return STP_OK;
+  });
 }
 
 }  // namespace stp

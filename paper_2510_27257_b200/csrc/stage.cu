@@ -1,0 +1,1144 @@
+// Stream/event unit executor of one TP x PP rank.
+//
+// One stp_stage per rank process.  It owns three kinds of CUDA streams:
+//   compute   F/B/W units (GEMMs, attention, SwiGLU, embedding, LM head)
+//   tp-comm   the TP communication phases of the units (NCCL reduce-scatter
+//             -> residual add + RMSNorm (fwd) / RMSNorm-bwd + residual grad
+//             (bwd) -> NCCL all-gather), i.e. the Pre-Attn / Pre-MLP units
+//             placed "according to their computational dependencies"
+//              in the sequence-parallel form (reading Q10)
+//   pp        one stream per (peer, direction) NCCL communicator for the PP
+//             activation / gradient send-recv
+// and executes its rank's unit list (stp_schedule_units) in order: every unit
+// waits on the events of its dep0/dep1 units, runs, and records its own
+// event.  A braided action therefore overlaps each TP comm phase of one
+// microbatch with the next compute unit of the other microbatch (Fig. 3,
+// P:L55-70) without any host synchronisation.
+//
+// Memory: per chunk a pool of stash slots (one per in-flight
+// chunk-microbatch, count = the program-order peak), each holding every
+// tensor the backward and the deferred weight-gradient units need; a slot is
+// reacquired only after the events of its last readers (its last W unit and
+// its PP sends).
+#include <nccl.h>
+
+#include <algorithm>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "common.h"
+#include "schedule.h"
+
+namespace stp {
+
+// launchers from the other translation units
+stp_status gemm_dispatch(int dtype, int layout, int epi, int64_t M, int64_t N, int64_t K, const void* A, int64_t lda,
+                         const void* B, int64_t ldb, void* C, int64_t ldc, const void* bias, const void* R,
+                         int64_t ldr, int max_ctas, cudaStream_t st);
+stp_status rmsnorm_fwd(int dtype, int64_t rows, int64_t h, const void* x, const void* resid, void* x_out,
+                       const void* g, float eps, void* y, float* rstd, cudaStream_t st);
+stp_status rmsnorm_bwd(int dtype, int64_t rows, int64_t h, const void* dy, const void* x, const void* g,
+                       const float* rstd, const void* dres, void* dx, float* dgamma, cudaStream_t st);
+stp_status rope(int dtype, int backward, int64_t s, int64_t ld, int64_t col0, int nh, int d, float theta,
+                int64_t pos0, void* x, cudaStream_t st);
+stp_status swiglu_fwd(int dtype, int64_t s, int64_t I, const void* gu, void* H, cudaStream_t st);
+stp_status swiglu_bwd(int dtype, int64_t s, int64_t I, const void* dH, const void* gu, void* dgu, cudaStream_t st);
+stp_status embed_fwd(int dtype, int64_t s, int64_t h, const int32_t* tok, int64_t v0, int64_t Vl, const void* E,
+                     void* out, cudaStream_t st);
+stp_status embed_bwd(int dtype, int64_t s, int64_t h, const int32_t* tok, int64_t v0, int64_t Vl, const void* dX,
+                     float* dE, cudaStream_t st);
+stp_status ce_stats(int dtype, int64_t s, int64_t Vl, const void* logits, int64_t ld, const int32_t* tgt, int64_t v0,
+                    float* stats, cudaStream_t st);
+stp_status ce_combine(int64_t s, int t, const float* stats_all, float* lse, float* loss_acc, float scale,
+                      cudaStream_t st);
+stp_status ce_grad(int dtype, int64_t s, int64_t Vl, void* logits, int64_t ld, const int32_t* tgt, int64_t v0,
+                   const float* lse, float scale, cudaStream_t st);
+stp_status colsum_acc(int dtype, int64_t rows, int64_t n, const void* X, int64_t ld, float* acc, cudaStream_t st);
+stp_status add(int dtype, int64_t n, const void* a, const void* b, void* out, cudaStream_t st);
+stp_status attn_fwd(int dtype, int64_t s, int nq, int nkv, int d, const void* q, const void* k, const void* v,
+                    int64_t ld, void* o, int64_t ldo, float* lse, cudaStream_t st);
+stp_status attn_bwd(int dtype, int64_t s, int nq, int nkv, int d, const void* q, const void* k, const void* v,
+                    int64_t ld, const void* o, int64_t ldo, const void* dout, const float* lse, void* dq, void* dk,
+                    void* dv, int64_t ldd, void* ws, cudaStream_t st);
+int64_t attn_bwd_ws_bytes(int64_t s, int nq, int nkv, int d);
+stp_status convert(int sd, int dd, int64_t n, const void* src, void* dst, cudaStream_t st);
+
+#define STP_NCCL_TRY(expr)                                                     \
+  do {                                                                         \
+    ncclResult_t r_ = (expr);                                                  \
+    if (r_ != ncclSuccess) {                                                   \
+      ::stp::set_error("%s:%d %s: %s", __FILE__, __LINE__, #expr,              \
+                       ncclGetErrorString(r_));                                \
+      return STP_ENCCL;                                                        \
+    }                                                                          \
+  } while (0)
+
+#define STP_TRY(expr)                     \
+  do {                                    \
+    stp_status s_ = (expr);               \
+    if (s_ != STP_OK) return s_;          \
+  } while (0)
+
+namespace {
+
+struct Param {
+  std::string name;
+  int64_t d0 = 0, d1 = 1;
+  void* p = nullptr;
+  float* g = nullptr;
+  int64_t numel() const { return d0 * d1; }
+};
+
+struct LayerIdx {
+  int ln1 = -1, wqkv = -1, bqkv = -1, wo = -1, ln2 = -1, wgu = -1, wd = -1;
+};
+
+struct SlotLayer {
+  void *xn = nullptr, *qkv = nullptr, *o = nullptr, *x1 = nullptr, *xn2 = nullptr, *gu = nullptr, *hh = nullptr,
+       *xres = nullptr, *dy_attn = nullptr, *dqkv = nullptr, *dy_mlp = nullptr;
+  float *lse = nullptr, *rstd1 = nullptr, *rstd2 = nullptr;
+};
+
+struct Slot {
+  void* mem = nullptr;
+  void *x_in = nullptr, *dx_in = nullptr;
+  std::vector<SlotLayer> L;
+  void *xf = nullptr, *logits = nullptr, *dx0 = nullptr;
+  float *rstdf = nullptr, *stats = nullptr, *stats_all = nullptr, *lse_ce = nullptr;
+  bool busy = false;
+  int mb = -1;
+  std::vector<cudaEvent_t> free_events;  // readers of the previous occupant
+};
+
+struct Chunk {
+  int c = 0, vs = 0, l0 = 0, nl = 0;
+  bool first = false, last = false;
+  std::vector<Slot> slots;
+  std::map<int, int> mb2slot;
+  size_t slot_bytes = 0;
+};
+
+}  // namespace
+}  // namespace stp
+
+struct stp_stage {
+  // config
+  stp_model_cfg mc{};
+  int t = 1, p = 1, vpp = 2, m = 1, tp_rank = 0, pp_rank = 0, kind = 0, dtype = 1;
+  int dev = 0;
+  int64_t s = 0, sl = 0, h = 0, qh = 0, kh = 0, d = 0, qkv_w = 0, o_w = 0, fi = 0, Vl = 0;
+  size_t es = 2;
+  std::vector<int> lay;
+  stp::Schedule sched;
+  std::vector<stp_unit> units;
+  // params
+  std::vector<stp::Param> params;
+  std::map<int, stp::LayerIdx> lidx;  // global layer -> indices
+  int p_embed = -1, p_final = -1, p_lm = -1;
+  bool bound = false;
+  // chunks
+  std::vector<stp::Chunk> chunks;
+  // streams / comms
+  cudaStream_t s_comp = nullptr, s_comm = nullptr;
+  std::map<int, cudaStream_t> s_send, s_recv;  // by peer device
+  ncclComm_t world = nullptr, tpc = nullptr;
+  std::map<int, ncclComm_t> c_send, c_recv;
+  std::vector<ncclComm_t> owned;
+  // buffers
+  void *pf = nullptr, *pb = nullptr;               // partial outputs (forward / backward lanes)
+  void *rtmp = nullptr, *ntmp = nullptr;           // comm-stream temps [sl, h]
+  void *dtmp_h = nullptr, *dtmp_o = nullptr;       // compute temps dH [s, fi], dO [s, o_w]
+  void* attn_ws = nullptr;
+  float* dgamma = nullptr;                         // internal gamma grads (per layer ln1, ln2, + final)
+  std::map<int, int> dgamma_off;                   // param index -> offset into dgamma
+  int64_t dgamma_n = 0;
+  float* loss_acc = nullptr;
+  int32_t *tok_buf = nullptr, *tgt_buf = nullptr;  // for the host-input path
+  std::vector<void*> allocs;
+  // events
+  std::vector<cudaEvent_t> ev_done;
+  std::vector<cudaEvent_t> ev_t0, ev_t1;  // timing
+  cudaEvent_t ev_base = nullptr, ev_end = nullptr;
+  cudaEvent_t ev_pf = nullptr, ev_pb = nullptr;
+  bool pf_pending = false, pb_pending = false;
+  std::vector<cudaEvent_t> ev_pool;
+  size_t ev_pool_next = 0;
+  int timing = 0;
+  bool poisoned = false;
+  // per-step
+  const int32_t* tokens = nullptr;
+  const int32_t* targets = nullptr;
+  std::vector<stp_unit> trace;
+  std::vector<float> t_start, t_end;
+  int gemm_max_ctas = 0;
+  int64_t launches_step = 0;
+  int64_t peak_bytes = 0;
+};
+
+namespace stp {
+namespace {
+
+int ncdt(int dtype) { return dtype == STP_DTYPE_BF16 ? ncclBfloat16 : ncclFloat32; }
+
+stp_status dalloc(stp_stage* S, void** p, size_t bytes) {
+  *p = nullptr;
+  if (bytes == 0) return STP_OK;
+  cudaError_t e = cudaMalloc(p, bytes);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    set_error("cudaMalloc(%zu bytes) failed: %s", bytes, cudaGetErrorString(e));
+    return STP_ENOMEM;
+  }
+  S->allocs.push_back(*p);
+  return STP_OK;
+}
+
+cudaEvent_t pool_event(stp_stage* S) {
+  if (S->ev_pool_next >= S->ev_pool.size()) {
+    cudaEvent_t e;
+    cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+    S->ev_pool.push_back(e);
+  }
+  return S->ev_pool[S->ev_pool_next++];
+}
+
+// Carve a slot's buffers out of one allocation (256-byte aligned pieces).
+struct Carver {
+  uint8_t* base;
+  size_t off = 0;
+  bool dry;
+  void* take(size_t bytes) {
+    off = (off + 255) & ~size_t(255);
+    void* p = dry ? nullptr : base + off;
+    off += bytes;
+    return p;
+  }
+};
+
+void carve_slot(stp_stage* S, const Chunk& C, Slot& sl, Carver& cv) {
+  const size_t es = S->es;
+  const int64_t s = S->s, h = S->h, shard = S->sl * S->h;
+  sl.x_in = cv.take(shard * es);
+  sl.dx_in = cv.take(shard * es);
+  sl.L.resize(C.nl);
+  for (int j = 0; j < C.nl; ++j) {
+    SlotLayer& L = sl.L[j];
+    L.xn = cv.take(s * h * es);
+    L.qkv = cv.take(s * S->qkv_w * es);
+    L.o = cv.take(s * S->o_w * es);
+    L.lse = (float*)cv.take(S->qh * s * 4);
+    L.rstd1 = (float*)cv.take(S->sl * 4);
+    L.rstd2 = (float*)cv.take(S->sl * 4);
+    L.x1 = cv.take(shard * es);
+    L.xn2 = cv.take(s * h * es);
+    L.gu = cv.take(s * 2 * S->fi * es);  // backward overwrites it with dGU
+    L.hh = cv.take(s * S->fi * es);
+    L.xres = cv.take(shard * es);
+    L.dy_attn = cv.take(s * h * es);
+    L.dqkv = cv.take(s * S->qkv_w * es);
+    L.dy_mlp = cv.take(s * h * es);
+  }
+  if (C.last) {
+    sl.xf = cv.take(s * h * es);
+    sl.rstdf = (float*)cv.take(S->sl * 4);
+    sl.logits = cv.take(s * S->Vl * es);
+    sl.stats = (float*)cv.take(s * 3 * 4);
+    sl.stats_all = (float*)cv.take((size_t)S->t * s * 3 * 4);
+    sl.lse_ce = (float*)cv.take(s * 4);
+  }
+  if (C.first) sl.dx0 = cv.take(s * h * es);
+}
+
+// ----------------------------------------------------------- collectives
+stp_status reduce_scatter(stp_stage* S, const void* src, void* dst) {
+  STP_NCCL_TRY(ncclReduceScatter(src, dst, (size_t)(S->sl * S->h), (ncclDataType_t)ncdt(S->dtype), ncclSum, S->tpc,
+                                 S->s_comm));
+  return STP_OK;
+}
+stp_status all_gather(stp_stage* S, const void* src, void* dst, size_t count) {
+  if (S->t == 1) {
+    if (src != dst) STP_CUDA_TRY(cudaMemcpyAsync(dst, src, count * S->es, cudaMemcpyDeviceToDevice, S->s_comm));
+    return STP_OK;
+  }
+  STP_NCCL_TRY(ncclAllGather(src, dst, count, (ncclDataType_t)ncdt(S->dtype), S->tpc, S->s_comm));
+  return STP_OK;
+}
+
+Chunk& chunk_of(stp_stage* S, int c) { return S->chunks[c]; }
+
+stp_status acquire(stp_stage* S, int c, int mb, Slot** out) {
+  Chunk& C = chunk_of(S, c);
+  auto it = C.mb2slot.find(mb);
+  if (it != C.mb2slot.end()) {
+    *out = &C.slots[it->second];
+    return STP_OK;
+  }
+  for (size_t i = 0; i < C.slots.size(); ++i) {
+    Slot& sl = C.slots[i];
+    if (sl.busy) continue;
+    sl.busy = true;
+    sl.mb = mb;
+    C.mb2slot[mb] = (int)i;
+    // every stream that may write this slot waits for the previous readers
+    for (cudaEvent_t e : sl.free_events) {
+      STP_CUDA_TRY(cudaStreamWaitEvent(S->s_comp, e, 0));
+      STP_CUDA_TRY(cudaStreamWaitEvent(S->s_comm, e, 0));
+      for (auto& kv : S->s_recv) STP_CUDA_TRY(cudaStreamWaitEvent(kv.second, e, 0));
+    }
+    sl.free_events.clear();
+    *out = &sl;
+    return STP_OK;
+  }
+  return fail(STP_ESTATE, "no free stash slot (schedule / slot-count mismatch)");
+}
+
+Slot* find_slot(stp_stage* S, int c, int mb) {
+  Chunk& C = chunk_of(S, c);
+  auto it = C.mb2slot.find(mb);
+  return it == C.mb2slot.end() ? nullptr : &C.slots[it->second];
+}
+
+void release(stp_stage* S, int c, int mb, cudaEvent_t comp_ev) {
+  Chunk& C = chunk_of(S, c);
+  auto it = C.mb2slot.find(mb);
+  if (it == C.mb2slot.end()) return;
+  Slot& sl = C.slots[it->second];
+  sl.free_events.push_back(comp_ev);
+  sl.busy = false;
+  sl.mb = -1;
+  C.mb2slot.erase(it);
+}
+
+int dev_of_vs(stp_stage* S, int vs) { return sched_vstage_device(S->kind, S->p, vs); }
+
+const stp::LayerIdx& LI(stp_stage* S, int l) { return S->lidx.at(l); }
+void* P(stp_stage* S, int i) { return S->params[i].p; }
+float* G(stp_stage* S, int i) { return S->params[i].g; }
+float* DG(stp_stage* S, int i) { return S->dgamma + S->dgamma_off.at(i); }
+
+int64_t vocab0(stp_stage* S) { return (int64_t)S->tp_rank * S->Vl; }
+
+// ------------------------------------------------------------ units
+stp_status unit_compute(stp_stage* S, const stp_unit& u) {
+  Chunk& C = chunk_of(S, u.chunk);
+  const int dt = S->dtype;
+  const int64_t s = S->s, h = S->h;
+  const int mc = S->gemm_max_ctas;
+  cudaStream_t st = S->s_comp;
+  Slot* sl = nullptr;
+  const bool fwd = u.op == STP_U_F_ATTN || u.op == STP_U_F_MLP || u.op == STP_U_F_EMB || u.op == STP_U_F_HEAD;
+  if (fwd) {
+    STP_TRY(acquire(S, u.chunk, u.mb, &sl));
+  } else {
+    sl = find_slot(S, u.chunk, u.mb);
+    if (!sl) return fail(STP_ESTATE, "backward/W unit without a forward stash");
+  }
+  const bool writes_pf = u.op == STP_U_F_ATTN || u.op == STP_U_F_MLP || u.op == STP_U_F_EMB;
+  const bool writes_pb = u.op == STP_U_B_ATTN || u.op == STP_U_B_MLP || u.op == STP_U_B_HEAD;
+  if (writes_pf && S->pf_pending) STP_CUDA_TRY(cudaStreamWaitEvent(st, S->ev_pf, 0));
+  if (writes_pb && S->pb_pending) STP_CUDA_TRY(cudaStreamWaitEvent(st, S->ev_pb, 0));
+  const int j = u.layer - C.l0;
+  switch (u.op) {
+    case STP_U_F_EMB: {
+      const int32_t* tok = S->tokens + (int64_t)(u.mb - 1) * s;
+      return embed_fwd(dt, s, h, tok, vocab0(S), S->Vl, P(S, S->p_embed), S->pf, st);
+    }
+    case STP_U_F_ATTN: {
+      SlotLayer& L = sl->L[j];
+      const LayerIdx& I = LI(S, u.layer);
+      const bool bias = I.bqkv >= 0;
+      STP_TRY(gemm_dispatch(dt, STP_GEMM_NT, bias ? STP_EPI_BIAS : STP_EPI_STORE, s, S->qkv_w, h, L.xn, h,
+                            P(S, I.wqkv), h, L.qkv, S->qkv_w, bias ? P(S, I.bqkv) : nullptr, nullptr, 0, mc, st));
+      STP_TRY(rope(dt, 0, s, S->qkv_w, 0, (int)(S->qh + S->kh), (int)S->d, S->mc.rope_theta, 0, L.qkv, st));
+      const uint8_t* q = (const uint8_t*)L.qkv;
+      STP_TRY(attn_fwd(dt, s, (int)S->qh, (int)S->kh, (int)S->d, q, q + S->qh * S->d * S->es,
+                       q + (S->qh + S->kh) * S->d * S->es, S->qkv_w, L.o, S->o_w, L.lse, st));
+      return gemm_dispatch(dt, STP_GEMM_NT, STP_EPI_STORE, s, h, S->o_w, L.o, S->o_w, P(S, I.wo), S->o_w, S->pf, h,
+                           nullptr, nullptr, 0, mc, st);
+    }
+    case STP_U_F_MLP: {
+      SlotLayer& L = sl->L[j];
+      const LayerIdx& I = LI(S, u.layer);
+      STP_TRY(gemm_dispatch(dt, STP_GEMM_NT, STP_EPI_STORE, s, 2 * S->fi, h, L.xn2, h, P(S, I.wgu), h, L.gu,
+                            2 * S->fi, nullptr, nullptr, 0, mc, st));
+      STP_TRY(swiglu_fwd(dt, s, S->fi, L.gu, L.hh, st));
+      return gemm_dispatch(dt, STP_GEMM_NT, STP_EPI_STORE, s, h, S->fi, L.hh, S->fi, P(S, I.wd), S->fi, S->pf, h,
+                           nullptr, nullptr, 0, mc, st);
+    }
+    case STP_U_F_HEAD: {
+      STP_TRY(gemm_dispatch(dt, STP_GEMM_NT, STP_EPI_STORE, s, S->Vl, h, sl->xf, h, P(S, S->p_lm), h, sl->logits,
+                            S->Vl, nullptr, nullptr, 0, mc, st));
+      const int32_t* tgt = S->targets + (int64_t)(u.mb - 1) * s;
+      return ce_stats(dt, s, S->Vl, sl->logits, S->Vl, tgt, vocab0(S), sl->stats, st);
+    }
+    case STP_U_B_HEAD: {
+      const float scale = 1.f / ((float)s * (float)S->m);
+      const int32_t* tgt = S->targets + (int64_t)(u.mb - 1) * s;
+      STP_TRY(ce_combine(s, S->t, sl->stats_all, sl->lse_ce, S->loss_acc, scale, st));
+      STP_TRY(ce_grad(dt, s, S->Vl, sl->logits, S->Vl, tgt, vocab0(S), sl->lse_ce, scale, st));
+      return gemm_dispatch(dt, STP_GEMM_NN, STP_EPI_STORE, s, h, S->Vl, sl->logits, S->Vl, P(S, S->p_lm), h, S->pb,
+                           h, nullptr, nullptr, 0, mc, st);
+    }
+    case STP_U_W_HEAD:
+      return gemm_dispatch(dt, STP_GEMM_TN, STP_EPI_ACCUM_F32, S->Vl, h, s, sl->logits, S->Vl, sl->xf, h,
+                           G(S, S->p_lm), h, nullptr, nullptr, 0, mc, st);
+    case STP_U_B_MLP: {
+      SlotLayer& L = sl->L[j];
+      const LayerIdx& I = LI(S, u.layer);
+      STP_TRY(gemm_dispatch(dt, STP_GEMM_NN, STP_EPI_STORE, s, S->fi, h, L.dy_mlp, h, P(S, I.wd), S->fi, S->dtmp_h,
+                            S->fi, nullptr, nullptr, 0, mc, st));
+      STP_TRY(swiglu_bwd(dt, s, S->fi, S->dtmp_h, L.gu, L.gu, st));  // dGU overwrites GU
+      return gemm_dispatch(dt, STP_GEMM_NN, STP_EPI_STORE, s, h, 2 * S->fi, L.gu, 2 * S->fi, P(S, I.wgu), h, S->pb,
+                           h, nullptr, nullptr, 0, mc, st);
+    }
+    case STP_U_W_MLP: {
+      SlotLayer& L = sl->L[j];
+      const LayerIdx& I = LI(S, u.layer);
+      STP_TRY(gemm_dispatch(dt, STP_GEMM_TN, STP_EPI_ACCUM_F32, h, S->fi, s, L.dy_mlp, h, L.hh, S->fi, G(S, I.wd),
+                            S->fi, nullptr, nullptr, 0, mc, st));
+      return gemm_dispatch(dt, STP_GEMM_TN, STP_EPI_ACCUM_F32, 2 * S->fi, h, s, L.gu, 2 * S->fi, L.xn2, h,
+                           G(S, I.wgu), h, nullptr, nullptr, 0, mc, st);
+    }
+    case STP_U_B_ATTN: {
+      SlotLayer& L = sl->L[j];
+      const LayerIdx& I = LI(S, u.layer);
+      STP_TRY(gemm_dispatch(dt, STP_GEMM_NN, STP_EPI_STORE, s, S->o_w, h, L.dy_attn, h, P(S, I.wo), S->o_w,
+                            S->dtmp_o, S->o_w, nullptr, nullptr, 0, mc, st));
+      const uint8_t* q = (const uint8_t*)L.qkv;
+      uint8_t* dq = (uint8_t*)L.dqkv;
+      const int64_t ko = S->qh * S->d * S->es, vo = (S->qh + S->kh) * S->d * S->es;
+      STP_TRY(attn_bwd(dt, s, (int)S->qh, (int)S->kh, (int)S->d, q, q + ko, q + vo, S->qkv_w, L.o, S->o_w,
+                       S->dtmp_o, L.lse, dq, dq + ko, dq + vo, S->qkv_w, S->attn_ws, st));
+      STP_TRY(rope(dt, 1, s, S->qkv_w, 0, (int)(S->qh + S->kh), (int)S->d, S->mc.rope_theta, 0, L.dqkv, st));
+      return gemm_dispatch(dt, STP_GEMM_NN, STP_EPI_STORE, s, h, S->qkv_w, L.dqkv, S->qkv_w, P(S, I.wqkv), h, S->pb,
+                           h, nullptr, nullptr, 0, mc, st);
+    }
+    case STP_U_W_ATTN: {
+      SlotLayer& L = sl->L[j];
+      const LayerIdx& I = LI(S, u.layer);
+      STP_TRY(gemm_dispatch(dt, STP_GEMM_TN, STP_EPI_ACCUM_F32, h, S->o_w, s, L.dy_attn, h, L.o, S->o_w, G(S, I.wo),
+                            S->o_w, nullptr, nullptr, 0, mc, st));
+      STP_TRY(gemm_dispatch(dt, STP_GEMM_TN, STP_EPI_ACCUM_F32, S->qkv_w, h, s, L.dqkv, S->qkv_w, L.xn, h,
+                            G(S, I.wqkv), h, nullptr, nullptr, 0, mc, st));
+      if (I.bqkv >= 0) STP_TRY(colsum_acc(dt, s, S->qkv_w, L.dqkv, S->qkv_w, G(S, I.bqkv), st));
+      return STP_OK;
+    }
+    case STP_U_W_EMB: {
+      const int32_t* tok = S->tokens + (int64_t)(u.mb - 1) * s;
+      return embed_bwd(dt, s, h, tok, vocab0(S), S->Vl, sl->dx0, G(S, S->p_embed), st);
+    }
+  }
+  return fail(STP_ESTATE, "unknown compute unit");
+}
+
+// Forward comm phase k of pass (chunk, mb): see DESIGN.md "Comm phases".
+stp_status unit_cf(stp_stage* S, const stp_unit& u) {
+  Chunk& C = chunk_of(S, u.chunk);
+  Slot* sl = nullptr;
+  STP_TRY(acquire(S, u.chunk, u.mb, &sl));
+  const int dt = S->dtype;
+  const int64_t h = S->h, shard = S->sl * S->h;
+  const float eps = S->mc.rms_eps;
+  cudaStream_t st = S->s_comm;
+  const int k = u.layer;
+  // normalise `x` (shard) with gamma into the all-gathered destination `dst`
+  auto norm_ag = [&](const void* x, const void* resid, void* x_out, const void* g, float* rstd, void* dst) {
+    void* y = (S->t == 1) ? dst : S->ntmp;
+    STP_TRY(rmsnorm_fwd(dt, S->sl, h, x, resid, x_out, g, eps, y, rstd, st));
+    if (S->t > 1) STP_TRY(all_gather(S, S->ntmp, dst, (size_t)shard));
+    return STP_OK;
+  };
+  auto rs_src = [&](const void** out) {
+    if (S->t == 1) {
+      *out = S->pf;
+      return STP_OK;
+    }
+    STP_TRY(reduce_scatter(S, S->pf, S->rtmp));
+    *out = S->rtmp;
+    return STP_OK;
+  };
+  if (k == 0) {
+    // input phase: chunk input shard (PP recv or local handoff) -> ln1 -> AG
+    if (dev_of_vs(S, C.vs - 1) == S->pp_rank) {
+      // local handoff from the other chunk on this device (V-shape turn)
+      for (auto& O : S->chunks)
+        if (O.vs == C.vs - 1) {
+          Slot* src = find_slot(S, O.c, u.mb);
+          if (!src) return fail(STP_ESTATE, "handoff source stash missing");
+          STP_CUDA_TRY(cudaMemcpyAsync(sl->x_in, src->L[O.nl - 1].xres, shard * S->es, cudaMemcpyDeviceToDevice, st));
+        }
+    }
+    const LayerIdx& I = LI(S, C.l0);
+    return norm_ag(sl->x_in, nullptr, nullptr, P(S, I.ln1), sl->L[0].rstd1, sl->L[0].xn);
+  }
+  // heavy unit k (1-based) of the forward lane
+  int idx = k - 1;
+  if (C.first) {
+    if (idx == 0) {  // after F_EMB: RS -> chunk input shard -> ln1 -> AG
+      if (S->t == 1) STP_CUDA_TRY(cudaMemcpyAsync(sl->x_in, S->pf, shard * S->es, cudaMemcpyDeviceToDevice, st));
+      else STP_TRY(reduce_scatter(S, S->pf, sl->x_in));
+      S->pf_pending = true;
+      const LayerIdx& I = LI(S, C.l0);
+      return norm_ag(sl->x_in, nullptr, nullptr, P(S, I.ln1), sl->L[0].rstd1, sl->L[0].xn);
+    }
+    idx -= 1;
+  }
+  if (idx < 2 * C.nl) {
+    const int j = idx / 2;
+    SlotLayer& L = sl->L[j];
+    const LayerIdx& I = LI(S, C.l0 + j);
+    const void* src = nullptr;
+    STP_TRY(rs_src(&src));
+    S->pf_pending = true;
+    if (idx % 2 == 0) {  // after attention: x1 = RS + x; ln2 -> AG
+      const void* xprev = j == 0 ? sl->x_in : sl->L[j - 1].xres;
+      return norm_ag(src, xprev, L.x1, P(S, I.ln2), L.rstd2, L.xn2);
+    }
+    // after MLP: x2 = RS + x1; next layer's ln1 (or final norm) -> AG
+    if (j + 1 < C.nl) {
+      const LayerIdx& I2 = LI(S, C.l0 + j + 1);
+      return norm_ag(src, L.x1, L.xres, P(S, I2.ln1), sl->L[j + 1].rstd1, sl->L[j + 1].xn);
+    }
+    if (C.last) return norm_ag(src, L.x1, L.xres, P(S, S->p_final), sl->rstdf, sl->xf);
+    return add(dt, shard, src, L.x1, L.xres, st);
+  }
+  // after F_HEAD: all-gather the cross-entropy row statistics
+  if (S->t == 1) {
+    STP_CUDA_TRY(cudaMemcpyAsync(sl->stats_all, sl->stats, S->s * 3 * 4, cudaMemcpyDeviceToDevice, st));
+    return STP_OK;
+  }
+  STP_NCCL_TRY(ncclAllGather(sl->stats, sl->stats_all, (size_t)(S->s * 3), ncclFloat32, S->tpc, st));
+  return STP_OK;
+}
+
+stp_status unit_cb(stp_stage* S, const stp_unit& u) {
+  Chunk& C = chunk_of(S, u.chunk);
+  Slot* sl = find_slot(S, u.chunk, u.mb);
+  if (!sl) return fail(STP_ESTATE, "backward comm without stash");
+  const int dt = S->dtype;
+  const int64_t h = S->h, shard = S->sl * S->h;
+  cudaStream_t st = S->s_comm;
+  const int k = u.layer;
+  auto rs_src = [&](const void** out) {
+    if (S->t == 1) {
+      *out = S->pb;
+      return STP_OK;
+    }
+    STP_TRY(reduce_scatter(S, S->pb, S->rtmp));
+    *out = S->rtmp;
+    return STP_OK;
+  };
+  if (k == 0) {  // incoming gradient shard -> AG for the last layer's MLP B unit
+    return all_gather(S, sl->dx_in, sl->L[C.nl - 1].dy_mlp, (size_t)shard);
+  }
+  int idx = k - 1;
+  if (C.last) {
+    if (idx == 0) {  // after B_HEAD: RS -> final-norm bwd -> residual grad -> AG
+      const void* src = nullptr;
+      STP_TRY(rs_src(&src));
+      S->pb_pending = true;
+      STP_TRY(rmsnorm_bwd(dt, S->sl, h, src, sl->L[C.nl - 1].xres, P(S, S->p_final), sl->rstdf, nullptr, sl->dx_in,
+                          DG(S, S->p_final), st));
+      return all_gather(S, sl->dx_in, sl->L[C.nl - 1].dy_mlp, (size_t)shard);
+    }
+    idx -= 1;
+  }
+  // backward heavy order: MLP(L-1), ATTN(L-1), ..., MLP(0), ATTN(0)
+  const int jj = idx / 2;
+  const int j = C.nl - 1 - jj;
+  SlotLayer& L = sl->L[j];
+  const LayerIdx& I = LI(S, C.l0 + j);
+  const void* src = nullptr;
+  STP_TRY(rs_src(&src));
+  S->pb_pending = true;
+  if (idx % 2 == 0) {  // after B_MLP: ln2 bwd + residual grad -> AG for B_ATTN
+    STP_TRY(rmsnorm_bwd(dt, S->sl, h, src, L.x1, P(S, I.ln2), L.rstd2, sl->dx_in, sl->dx_in, DG(S, I.ln2), st));
+    return all_gather(S, sl->dx_in, L.dy_attn, (size_t)shard);
+  }
+  // after B_ATTN: ln1 bwd + residual grad
+  const void* xprev = j == 0 ? sl->x_in : sl->L[j - 1].xres;
+  STP_TRY(rmsnorm_bwd(dt, S->sl, h, src, xprev, P(S, I.ln1), L.rstd1, sl->dx_in, sl->dx_in, DG(S, I.ln1), st));
+  if (j > 0) return all_gather(S, sl->dx_in, sl->L[j - 1].dy_mlp, (size_t)shard);
+  if (C.first) return all_gather(S, sl->dx_in, sl->dx0, (size_t)shard);
+  if (dev_of_vs(S, C.vs - 1) == S->pp_rank) {  // V-shape turn: hand the grad to the other chunk now
+    for (auto& O : S->chunks)
+      if (O.vs == C.vs - 1) {
+        Slot* dst = find_slot(S, O.c, u.mb);
+        if (!dst) return fail(STP_ESTATE, "handoff destination stash missing");
+        STP_CUDA_TRY(cudaMemcpyAsync(dst->dx_in, sl->dx_in, shard * S->es, cudaMemcpyDeviceToDevice, st));
+      }
+  }
+  return STP_OK;
+}
+
+stp_status unit_pp(stp_stage* S, const stp_unit& u, cudaStream_t st, cudaEvent_t* send_ev) {
+  Chunk& C = chunk_of(S, u.chunk);
+  const int peer = u.layer;
+  const size_t count = (size_t)(S->sl * S->h);
+  // direction: forward pass receives from vs-1 / sends to vs+1
+  const bool fwd_recv = (dev_of_vs(S, C.vs - 1) == peer && C.vs > 0);
+  Slot* sl = nullptr;
+  if (u.op == STP_U_PP_RECV) {
+    // a forward recv starts a new pass; a backward recv targets the existing stash
+    const bool is_fwd = fwd_recv && !find_slot(S, u.chunk, u.mb);
+    if (is_fwd) STP_TRY(acquire(S, u.chunk, u.mb, &sl));
+    else sl = find_slot(S, u.chunk, u.mb);
+    if (!sl) return fail(STP_ESTATE, "recv without stash");
+    void* dst = is_fwd ? sl->x_in : sl->dx_in;
+    STP_NCCL_TRY(ncclRecv(dst, count, (ncclDataType_t)ncdt(S->dtype), 1, S->c_recv.at(peer), st));
+    return STP_OK;
+  }
+  sl = find_slot(S, u.chunk, u.mb);
+  if (!sl) return fail(STP_ESTATE, "send without stash");
+  // A send is forward iff it follows the forward lane (its dep is a CF unit).
+  const bool fwd_send = S->units[u.dep0].op == STP_U_CF;
+  const void* src = fwd_send ? sl->L[C.nl - 1].xres : sl->dx_in;
+  STP_NCCL_TRY(ncclSend(src, count, (ncclDataType_t)ncdt(S->dtype), 1, S->c_send.at(peer), st));
+  *send_ev = pool_event(S);
+  STP_CUDA_TRY(cudaEventRecord(*send_ev, st));
+  sl->free_events.push_back(*send_ev);
+  return STP_OK;
+}
+
+cudaStream_t stream_of(stp_stage* S, const stp_unit& u) {
+  if (u.stream == 0) return S->s_comp;
+  if (u.stream == 1) return S->s_comm;
+  return u.op == STP_U_PP_SEND ? S->s_send.at(u.layer) : S->s_recv.at(u.layer);
+}
+
+bool is_last_w(stp_stage* S, const stp_unit& u) {
+  const Chunk& C = S->chunks[u.chunk];
+  if (C.first) return u.op == STP_U_W_EMB;
+  return u.op == STP_U_W_ATTN && u.layer == C.l0;
+}
+
+stp_status run_step(stp_stage* S, float* h_loss, stp_step_stats* stats) {
+  if (S->poisoned) return fail(STP_ESTATE, "stage poisoned by an earlier CUDA/NCCL error");
+  if (!S->bound) return fail(STP_ESTATE, "stp_bind_params not called");
+  STP_CUDA_TRY(cudaSetDevice(S->dev));
+  const int64_t launches0 = g_kernel_launches;
+  S->ev_pool_next = 0;
+  S->trace.clear();
+  S->pf_pending = S->pb_pending = false;
+  for (auto& C : S->chunks) {
+    C.mb2slot.clear();
+    for (auto& sl : C.slots) {
+      sl.busy = false;
+      sl.mb = -1;
+    }
+  }
+  // start: everything after whatever the caller enqueued before
+  STP_CUDA_TRY(cudaEventRecord(S->ev_base, S->s_comp));
+  STP_CUDA_TRY(cudaStreamWaitEvent(S->s_comm, S->ev_base, 0));
+  for (auto& kv : S->s_send) STP_CUDA_TRY(cudaStreamWaitEvent(kv.second, S->ev_base, 0));
+  for (auto& kv : S->s_recv) STP_CUDA_TRY(cudaStreamWaitEvent(kv.second, S->ev_base, 0));
+  STP_CUDA_TRY(cudaMemsetAsync(S->loss_acc, 0, sizeof(float), S->s_comp));
+  STP_CUDA_TRY(cudaMemsetAsync(S->dgamma, 0, S->dgamma_n * sizeof(float), S->s_comp));
+  STP_CUDA_TRY(cudaEventRecord(S->ev_base, S->s_comp));
+  STP_CUDA_TRY(cudaStreamWaitEvent(S->s_comm, S->ev_base, 0));
+  const int n = (int)S->units.size();
+  for (int i = 0; i < n; ++i) {
+    const stp_unit& u = S->units[i];
+    cudaStream_t st = stream_of(S, u);
+    if (u.dep0 >= 0) STP_CUDA_TRY(cudaStreamWaitEvent(st, S->ev_done[u.dep0], 0));
+    if (u.dep1 >= 0) STP_CUDA_TRY(cudaStreamWaitEvent(st, S->ev_done[u.dep1], 0));
+    if (S->timing) STP_CUDA_TRY(cudaEventRecord(S->ev_t0[i], st));
+    stp_status r = STP_OK;
+    cudaEvent_t send_ev = nullptr;
+    switch (u.op) {
+      case STP_U_CF: r = unit_cf(S, u); break;
+      case STP_U_CB: r = unit_cb(S, u); break;
+      case STP_U_PP_SEND:
+      case STP_U_PP_RECV: r = unit_pp(S, u, st, &send_ev); break;
+      default: r = unit_compute(S, u); break;
+    }
+    if (r != STP_OK) {
+      if (r == STP_ECUDA || r == STP_ENCCL) S->poisoned = true;
+      return r;
+    }
+    STP_CUDA_TRY(cudaEventRecord(S->ev_done[i], st));
+    if (S->timing) STP_CUDA_TRY(cudaEventRecord(S->ev_t1[i], st));
+    // comm phases consuming the partial buffers release them for the next writer
+    if (u.op == STP_U_CF && S->pf_pending) {
+      STP_CUDA_TRY(cudaEventRecord(S->ev_pf, st));
+    }
+    if (u.op == STP_U_CB && S->pb_pending) {
+      STP_CUDA_TRY(cudaEventRecord(S->ev_pb, st));
+    }
+    if (is_last_w(S, u)) release(S, u.chunk, u.mb, S->ev_done[i]);
+    S->trace.push_back(u);
+  }
+  // end of step: TP all-reduce of the replicated gamma gradients, add to grads
+  STP_CUDA_TRY(cudaEventRecord(S->ev_end, S->s_comp));
+  STP_CUDA_TRY(cudaStreamWaitEvent(S->s_comm, S->ev_end, 0));
+  if (S->t > 1)
+    STP_NCCL_TRY(ncclAllReduce(S->dgamma, S->dgamma, (size_t)S->dgamma_n, ncclFloat32, ncclSum, S->tpc, S->s_comm));
+  for (auto& kv : S->dgamma_off) {
+    const int pi = kv.first;
+    STP_TRY(add(STP_DTYPE_F32, S->params[pi].numel(), S->params[pi].g, S->dgamma + kv.second, S->params[pi].g,
+                S->s_comm));
+  }
+  for (auto& kv : S->s_send) {
+    STP_CUDA_TRY(cudaEventRecord(S->ev_end, kv.second));
+    STP_CUDA_TRY(cudaStreamWaitEvent(S->s_comm, S->ev_end, 0));
+  }
+  for (auto& kv : S->s_recv) {
+    STP_CUDA_TRY(cudaEventRecord(S->ev_end, kv.second));
+    STP_CUDA_TRY(cudaStreamWaitEvent(S->s_comm, S->ev_end, 0));
+  }
+  STP_CUDA_TRY(cudaEventRecord(S->ev_end, S->s_comm));
+  float loss = 0.f;
+  STP_CUDA_TRY(cudaMemcpyAsync(&loss, S->loss_acc, sizeof(float), cudaMemcpyDeviceToHost, S->s_comm));
+  cudaError_t e = cudaStreamSynchronize(S->s_comm);
+  if (e != cudaSuccess) {
+    S->poisoned = true;
+    return fail(STP_ECUDA, std::string("step failed: ") + cudaGetErrorString(e));
+  }
+  STP_CUDA_TRY(cudaDeviceSynchronize());
+  const bool holds_loss = S->chunks.back().last || S->chunks.front().last;
+  if (h_loss) *h_loss = holds_loss ? loss : 0.f;
+  S->launches_step = g_kernel_launches - launches0;
+  if (stats) {
+    memset(stats, 0, sizeof(*stats));
+    float ms = 0.f;
+    STP_CUDA_TRY(cudaEventElapsedTime(&ms, S->ev_base, S->ev_end));
+    stats->step_ms = ms;
+    stats->n_units = n;
+    stats->n_kernels = (int32_t)S->launches_step;
+    stats->peak_act_bytes = S->peak_bytes;
+    if (S->timing) {
+      S->t_start.assign(n, 0.f);
+      S->t_end.assign(n, 0.f);
+      for (int i = 0; i < n; ++i) {
+        STP_CUDA_TRY(cudaEventElapsedTime(&S->t_start[i], S->ev_base, S->ev_t0[i]));
+        STP_CUDA_TRY(cudaEventElapsedTime(&S->t_end[i], S->ev_base, S->ev_t1[i]));
+      }
+      // compute-stream idle gaps: waiting on a TP comm phase (exposed TP) or
+      // on PP data / an empty pipeline (PP bubble)
+      double busy = 0, exposed = 0, bubble = 0;
+      float prev_end = 0.f;
+      bool first = true;
+      for (int i = 0; i < n; ++i) {
+        const stp_unit& u = S->units[i];
+        if (u.stream != 0) continue;
+        busy += S->t_end[i] - S->t_start[i];
+        const float gap = first ? S->t_start[i] : S->t_start[i] - prev_end;
+        if (gap > 0) {
+          bool tp = false;
+          if (u.dep0 >= 0 && S->units[u.dep0].stream == 1) {
+            const stp_unit& c = S->units[u.dep0];
+            const bool waits_pp = c.dep0 >= 0 && S->units[c.dep0].stream == 2 && S->t_end[c.dep0] > prev_end;
+            tp = !waits_pp && S->t_end[u.dep0] > prev_end;
+          }
+          if (tp) exposed += gap;
+          else bubble += gap;
+        }
+        prev_end = std::max(prev_end, S->t_end[i]);
+        first = false;
+      }
+      bubble += std::max(0.0, (double)ms - (double)prev_end);
+      stats->compute_busy_ms = busy;
+      stats->exposed_tp_ms = exposed;
+      stats->pp_bubble_ms = bubble;
+    }
+  }
+  return STP_OK;
+}
+
+// ---------------------------------------------------------------- init
+stp_status build_params(stp_stage* S) {
+  S->params.clear();
+  auto add_p = [&](const std::string& name, int64_t d0, int64_t d1) {
+    Param p;
+    p.name = name;
+    p.d0 = d0;
+    p.d1 = d1;
+    S->params.push_back(p);
+    return (int)S->params.size() - 1;
+  };
+  for (auto& C : S->chunks) {
+    for (int l = C.l0; l < C.l0 + C.nl; ++l) {
+      const std::string pre = "layers." + std::to_string(l) + ".";
+      LayerIdx I;
+      I.ln1 = add_p(pre + "ln1", S->h, 1);
+      I.wqkv = add_p(pre + "wqkv", S->qkv_w, S->h);
+      if (S->mc.qkv_bias) I.bqkv = add_p(pre + "bqkv", S->qkv_w, 1);
+      I.wo = add_p(pre + "wo", S->h, S->o_w);
+      I.ln2 = add_p(pre + "ln2", S->h, 1);
+      I.wgu = add_p(pre + "wgu", 2 * S->fi, S->h);
+      I.wd = add_p(pre + "wd", S->h, S->fi);
+      S->lidx[l] = I;
+    }
+  }
+  for (auto& C : S->chunks)
+    if (C.first) S->p_embed = add_p("embed", S->Vl, S->h);
+  for (auto& C : S->chunks)
+    if (C.last) {
+      S->p_final = add_p("final_ln", S->h, 1);
+      S->p_lm = add_p("lm_head", S->Vl, S->h);
+    }
+  // internal gamma-grad accumulators
+  S->dgamma_off.clear();
+  int64_t off = 0;
+  for (size_t i = 0; i < S->params.size(); ++i) {
+    const std::string& nm = S->params[i].name;
+    const bool gamma = nm == "final_ln" || (nm.size() > 4 && (nm.compare(nm.size() - 4, 4, ".ln1") == 0 ||
+                                                              nm.compare(nm.size() - 4, 4, ".ln2") == 0));
+    if (gamma) {
+      S->dgamma_off[(int)i] = off;
+      off += S->params[i].numel();
+    }
+  }
+  S->dgamma_n = off;
+  return STP_OK;
+}
+
+stp_status init_nccl(stp_stage* S, const void* uid) {
+  const int world = S->t * S->p;
+  if (world == 1) return STP_OK;
+  if (!uid) return fail(STP_EINVAL, "world_nccl_id required when tp*pp > 1");
+  ncclUniqueId id;
+  memcpy(&id, uid, sizeof(id));
+  const int rank = S->pp_rank * S->t + S->tp_rank;
+  STP_NCCL_TRY(ncclCommInitRank(&S->world, world, id, rank));
+  S->owned.push_back(S->world);
+  // TP group: same PP rank
+  STP_NCCL_TRY(ncclCommSplit(S->world, S->pp_rank, S->tp_rank, &S->tpc, nullptr));
+  if (S->tpc) S->owned.push_back(S->tpc);
+  // PP pair communicators: one per (ordered device pair, tp rank), direction
+  // a -> b with the sender as rank 0.  Pairs are split in matching rounds so
+  // each split call puts every rank in at most one pair.
+  std::vector<std::pair<int, int>> pairs;  // unordered {a < b} that exchange messages
+  {
+    std::vector<int> lay(S->lay);
+    for (int d = 0; d < S->p; ++d) {
+      std::vector<stp_unit> us;
+      STP_TRY(schedule_expand(S->sched, d, lay, us));
+      for (auto& u : us)
+        if (u.op == STP_U_PP_SEND) {
+          std::pair<int, int> pr(std::min(d, u.layer), std::max(d, u.layer));
+          if (std::find(pairs.begin(), pairs.end(), pr) == pairs.end()) pairs.push_back(pr);
+        }
+    }
+    std::sort(pairs.begin(), pairs.end());
+  }
+  std::vector<std::vector<std::pair<int, int>>> rounds;
+  for (auto& pr : pairs) {
+    bool placed = false;
+    for (auto& rd : rounds) {
+      bool clash = false;
+      for (auto& q : rd)
+        if (q.first == pr.first || q.first == pr.second || q.second == pr.first || q.second == pr.second) clash = true;
+      if (!clash) {
+        rd.push_back(pr);
+        placed = true;
+        break;
+      }
+    }
+    if (!placed) rounds.push_back({pr});
+  }
+  const int me = S->pp_rank;
+  for (auto& rd : rounds) {
+    for (int dir = 0; dir < 2; ++dir) {  // dir 0: a -> b, dir 1: b -> a
+      int color = NCCL_SPLIT_NOCOLOR, key = 0, peer = -1;
+      bool sender = false;
+      for (size_t i = 0; i < rd.size(); ++i) {
+        const int a = rd[i].first, b = rd[i].second;
+        const int src = dir == 0 ? a : b, dst = dir == 0 ? b : a;
+        if (me == src || me == dst) {
+          color = (int)i * S->t + S->tp_rank;
+          sender = me == src;
+          key = sender ? 0 : 1;
+          peer = sender ? dst : src;
+        }
+      }
+      ncclComm_t c = nullptr;
+      STP_NCCL_TRY(ncclCommSplit(S->world, color, key, &c, nullptr));
+      if (c) {
+        S->owned.push_back(c);
+        if (sender) S->c_send[peer] = c;
+        else S->c_recv[peer] = c;
+      }
+    }
+  }
+  return STP_OK;
+}
+
+}  // namespace
+}  // namespace stp
+
+// ------------------------------------------------------------------ C ABI
+using namespace stp;
+
+extern "C" {
+
+int32_t stp_nccl_id_bytes(void) { return (int32_t)sizeof(ncclUniqueId); }
+
+stp_status stp_nccl_get_id(void* buf) {
+  if (!buf) return fail(STP_EINVAL, "buf is NULL");
+  ncclUniqueId id;
+  ncclResult_t r = ncclGetUniqueId(&id);
+  if (r != ncclSuccess) return fail(STP_ENCCL, std::string("ncclGetUniqueId: ") + ncclGetErrorString(r));
+  memcpy(buf, &id, sizeof(id));
+  return STP_OK;
+}
+
+stp_status stp_init_stage(const stp_model_cfg* mc, const stp_parallel_cfg* pc, const void* world_nccl_id,
+                          int32_t cuda_device, stp_stage** out) {
+  if (!mc || !pc || !out) return fail(STP_EINVAL, "NULL argument");
+  *out = nullptr;
+  const int t = pc->tp, p = pc->pp;
+  STP_CHECK_ARG(t >= 1 && p >= 1, "tp, pp >= 1");
+  STP_CHECK_ARG(pc->tp_rank >= 0 && pc->tp_rank < t && pc->pp_rank >= 0 && pc->pp_rank < p, "ranks");
+  STP_CHECK_ARG(pc->n_micro >= 1, "n_micro >= 1");
+  STP_CHECK_ARG(mc->dtype == STP_DTYPE_F32 || mc->dtype == STP_DTYPE_BF16, "dtype");
+  STP_CHECK_ARG(mc->n_q_heads % t == 0 && mc->n_kv_heads % t == 0, "heads % tp == 0");
+  STP_CHECK_ARG(mc->n_q_heads % mc->n_kv_heads == 0, "n_q_heads % n_kv_heads == 0");
+  STP_CHECK_ARG(mc->ffn % t == 0 && mc->vocab % t == 0 && mc->seq % t == 0, "ffn, vocab, seq % tp == 0");
+  STP_CHECK_ARG(mc->hidden % 8 == 0 && (mc->ffn / t) % 8 == 0, "hidden and ffn/tp multiples of 8");
+  std::unique_ptr<stp_stage> S(new stp_stage);
+  S->mc = *mc;
+  S->t = t;
+  S->p = p;
+  S->vpp = pc->vpp;
+  S->m = pc->n_micro;
+  S->tp_rank = pc->tp_rank;
+  S->pp_rank = pc->pp_rank;
+  S->kind = pc->sched_kind;
+  S->dtype = mc->dtype;
+  S->es = dtype_size(mc->dtype);
+  S->dev = cuda_device;
+  S->s = mc->seq;
+  S->sl = mc->seq / t;
+  S->h = mc->hidden;
+  S->d = mc->head_dim;
+  S->qh = mc->n_q_heads / t;
+  S->kh = mc->n_kv_heads / t;
+  S->qkv_w = (S->qh + 2 * S->kh) * S->d;
+  S->o_w = S->qh * S->d;
+  S->fi = mc->ffn / t;
+  S->Vl = mc->vocab / t;
+  STP_CHECK_ARG(S->qkv_w % 8 == 0 && S->o_w % 8 == 0 && S->Vl % 8 == 0, "per-rank widths multiples of 8");
+  STP_TRY(schedule_build(p, pc->vpp, t, pc->n_micro, pc->sched_kind, S->sched));
+  const int V = sched_n_vstages(S->kind, p);
+  S->lay.resize(V);
+  if (pc->layers_per_vstage) {
+    int sum = 0;
+    for (int i = 0; i < V; ++i) {
+      S->lay[i] = pc->layers_per_vstage[i];
+      STP_CHECK_ARG(S->lay[i] >= 1, "every virtual stage needs >= 1 layer");
+      sum += S->lay[i];
+    }
+    if (sum != mc->n_layers) return fail(STP_EINVAL, "IndivisibleLayers: layers_per_vstage does not sum to n_layers");
+  } else {
+    STP_TRY(layer_split(mc->n_layers, V, S->lay.data()));
+  }
+  STP_TRY(schedule_expand(S->sched, S->pp_rank, S->lay, S->units));
+  STP_CUDA_TRY(cudaSetDevice(cuda_device));
+  // chunks held by this rank
+  const int nchunks = sched_n_chunks(S->kind);
+  for (int c = 0; c < nchunks; ++c) {
+    Chunk C;
+    C.c = c;
+    C.vs = sched_vstage(S->kind, p, S->pp_rank, c);
+    C.l0 = 0;
+    for (int i = 0; i < C.vs; ++i) C.l0 += S->lay[i];
+    C.nl = S->lay[C.vs];
+    C.first = C.vs == 0;
+    C.last = C.vs == V - 1;
+    S->chunks.push_back(C);
+  }
+  STP_TRY(build_params(S.get()));
+  // stash slots per chunk: program-order peak of live chunk-microbatches
+  std::vector<int> cur(nchunks, 0), best(nchunks, 0);
+  for (const auto& a : S->sched.ranks[S->pp_rank]) {
+    const bool f = a.kind == STP_A_F || a.kind == STP_A_FB || a.kind == STP_A_FBS || a.kind == STP_A_FW;
+    if (f) best[a.chunk] = std::max(best[a.chunk], ++cur[a.chunk]);
+    if (a.kind == STP_A_BFULL || a.kind == STP_A_FB) --cur[a.chunk];
+    if (a.kind == STP_A_W || a.kind == STP_A_FW) --cur[a.w_chunk];
+  }
+  S->peak_bytes = 0;
+  for (auto& C : S->chunks) {
+    Slot probe;
+    Carver dry{nullptr, 0, true};
+    carve_slot(S.get(), C, probe, dry);
+    C.slot_bytes = dry.off + 256;
+    C.slots.resize(best[C.c]);
+    for (auto& sl : C.slots) {
+      STP_TRY(dalloc(S.get(), &sl.mem, C.slot_bytes));
+      Carver cv{(uint8_t*)sl.mem, 0, false};
+      carve_slot(S.get(), C, sl, cv);
+    }
+    S->peak_bytes += (int64_t)C.slot_bytes * best[C.c];
+  }
+  const size_t es = S->es;
+  STP_TRY(dalloc(S.get(), &S->pf, S->s * S->h * es));
+  STP_TRY(dalloc(S.get(), &S->pb, S->s * S->h * es));
+  STP_TRY(dalloc(S.get(), &S->rtmp, S->sl * S->h * es));
+  STP_TRY(dalloc(S.get(), &S->ntmp, S->sl * S->h * es));
+  STP_TRY(dalloc(S.get(), &S->dtmp_h, S->s * S->fi * es));
+  STP_TRY(dalloc(S.get(), &S->dtmp_o, S->s * S->o_w * es));
+  STP_TRY(dalloc(S.get(), &S->attn_ws, attn_bwd_ws_bytes(S->s, (int)S->qh, (int)S->kh, (int)S->d)));
+  void* tmp = nullptr;
+  STP_TRY(dalloc(S.get(), &tmp, std::max<int64_t>(1, S->dgamma_n) * sizeof(float)));
+  S->dgamma = (float*)tmp;
+  STP_TRY(dalloc(S.get(), &tmp, 256));
+  S->loss_acc = (float*)tmp;
+  STP_TRY(dalloc(S.get(), &tmp, (size_t)S->m * S->s * 4));
+  S->tok_buf = (int32_t*)tmp;
+  STP_TRY(dalloc(S.get(), &tmp, (size_t)S->m * S->s * 4));
+  S->tgt_buf = (int32_t*)tmp;
+  // streams
+  int lo = 0, hi = 0;
+  STP_CUDA_TRY(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+  STP_CUDA_TRY(cudaStreamCreateWithFlags(&S->s_comp, cudaStreamNonBlocking));
+  STP_CUDA_TRY(cudaStreamCreateWithPriority(&S->s_comm, cudaStreamNonBlocking, hi));
+  // events
+  const int n = (int)S->units.size();
+  S->ev_done.resize(n);
+  S->ev_t0.resize(n);
+  S->ev_t1.resize(n);
+  for (int i = 0; i < n; ++i) {
+    STP_CUDA_TRY(cudaEventCreateWithFlags(&S->ev_done[i], cudaEventDisableTiming));
+    STP_CUDA_TRY(cudaEventCreate(&S->ev_t0[i]));
+    STP_CUDA_TRY(cudaEventCreate(&S->ev_t1[i]));
+  }
+  STP_CUDA_TRY(cudaEventCreate(&S->ev_base));
+  STP_CUDA_TRY(cudaEventCreate(&S->ev_end));
+  STP_CUDA_TRY(cudaEventCreateWithFlags(&S->ev_pf, cudaEventDisableTiming));
+  STP_CUDA_TRY(cudaEventCreateWithFlags(&S->ev_pb, cudaEventDisableTiming));
+  if (const char* e = getenv("STP_GEMM_MAX_CTAS")) S->gemm_max_ctas = atoi(e);
+  STP_TRY(init_nccl(S.get(), world_nccl_id));
+  for (auto& kv : S->c_send) {
+    cudaStream_t st;
+    STP_CUDA_TRY(cudaStreamCreateWithPriority(&st, cudaStreamNonBlocking, hi));
+    S->s_send[kv.first] = st;
+  }
+  for (auto& kv : S->c_recv) {
+    cudaStream_t st;
+    STP_CUDA_TRY(cudaStreamCreateWithPriority(&st, cudaStreamNonBlocking, hi));
+    S->s_recv[kv.first] = st;
+  }
+  // every PP peer used by the unit list must have its communicator
+  for (auto& u : S->units) {
+    if (u.op == STP_U_PP_SEND && !S->c_send.count(u.layer)) return fail(STP_ENCCL, "missing PP send communicator");
+    if (u.op == STP_U_PP_RECV && !S->c_recv.count(u.layer)) return fail(STP_ENCCL, "missing PP recv communicator");
+  }
+  *out = S.release();
+  return STP_OK;
+}
+
+stp_status stp_stage_param_count(const stp_stage* st, int32_t* n_out) {
+  if (!st || !n_out) return fail(STP_EINVAL, "NULL argument");
+  *n_out = (int32_t)st->params.size();
+  return STP_OK;
+}
+
+stp_status stp_stage_param_info(const stp_stage* st, int32_t i, const char** name, int64_t* numel, int64_t* dim0,
+                                int64_t* dim1) {
+  if (!st) return fail(STP_EINVAL, "NULL stage");
+  if (i < 0 || i >= (int32_t)st->params.size()) return fail(STP_EINVAL, "param index out of range");
+  const Param& p = st->params[i];
+  if (name) *name = p.name.c_str();
+  if (numel) *numel = p.numel();
+  if (dim0) *dim0 = p.d0;
+  if (dim1) *dim1 = p.d1;
+  return STP_OK;
+}
+
+stp_status stp_bind_params(stp_stage* st, int32_t n, void* const* param_ptrs, void* const* grad_ptrs) {
+  if (!st || !param_ptrs || !grad_ptrs) return fail(STP_EINVAL, "NULL argument");
+  if (n != (int32_t)st->params.size()) return fail(STP_EINVAL, "param count mismatch");
+  for (int i = 0; i < n; ++i) {
+    if (!param_ptrs[i] || !grad_ptrs[i]) return fail(STP_EINVAL, "NULL param/grad pointer");
+    if ((reinterpret_cast<uintptr_t>(param_ptrs[i]) & 15) || (reinterpret_cast<uintptr_t>(grad_ptrs[i]) & 15))
+      return fail(STP_EINVAL, "param/grad pointers must be 16-byte aligned");
+    st->params[i].p = param_ptrs[i];
+    st->params[i].g = (float*)grad_ptrs[i];
+  }
+  st->bound = true;
+  return STP_OK;
+}
+
+stp_status stp_stage_set_timing(stp_stage* st, int32_t mode) {
+  if (!st) return fail(STP_EINVAL, "NULL stage");
+  st->timing = mode ? 1 : 0;
+  return STP_OK;
+}
+
+stp_status stp_train_step(stp_stage* st, const int32_t* d_tokens, const int32_t* d_targets, float* h_loss,
+                          stp_step_stats* stats) {
+  if (!st) return fail(STP_EINVAL, "NULL stage");
+  bool need_tok = false, need_tgt = false;
+  for (auto& C : st->chunks) {
+    need_tok |= C.first;
+    need_tgt |= C.last;
+  }
+  if (need_tok && !d_tokens) return fail(STP_EINVAL, "tokens required on the rank holding virtual stage 0");
+  if (need_tgt && !d_targets) return fail(STP_EINVAL, "targets required on the rank holding the last virtual stage");
+  st->tokens = d_tokens;
+  st->targets = d_targets;
+  return run_step(st, h_loss, stats);
+}
+
+stp_status stp_train_step_host(stp_stage* st, const int32_t* h_tokens, const int32_t* h_targets, float* h_loss,
+                               stp_step_stats* stats) {
+  if (!st) return fail(STP_EINVAL, "NULL stage");
+  STP_CUDA_TRY(cudaSetDevice(st->dev));
+  const size_t bytes = (size_t)st->m * st->s * 4;
+  const int32_t* dt = nullptr;
+  const int32_t* dg = nullptr;
+  if (h_tokens) {
+    STP_CUDA_TRY(cudaMemcpyAsync(st->tok_buf, h_tokens, bytes, cudaMemcpyHostToDevice, st->s_comp));
+    dt = st->tok_buf;
+  }
+  if (h_targets) {
+    STP_CUDA_TRY(cudaMemcpyAsync(st->tgt_buf, h_targets, bytes, cudaMemcpyHostToDevice, st->s_comp));
+    dg = st->tgt_buf;
+  }
+  return stp_train_step(st, dt, dg, h_loss, stats);
+}
+
+stp_status stp_stage_trace(const stp_stage* st, stp_unit* buf, int32_t cap, int32_t* n_out) {
+  if (!st || !n_out) return fail(STP_EINVAL, "NULL argument");
+  *n_out = (int32_t)st->trace.size();
+  if (cap < (int32_t)st->trace.size()) return fail(STP_ECAPACITY, "buffer too small");
+  std::copy(st->trace.begin(), st->trace.end(), buf);
+  return STP_OK;
+}
+
+stp_status stp_stage_unit_times(const stp_stage* st, float* start_ms, float* end_ms, int32_t cap, int32_t* n_out) {
+  if (!st || !n_out) return fail(STP_EINVAL, "NULL argument");
+  *n_out = (int32_t)st->t_start.size();
+  if (cap < (int32_t)st->t_start.size()) return fail(STP_ECAPACITY, "buffer too small");
+  std::copy(st->t_start.begin(), st->t_start.end(), start_ms);
+  std::copy(st->t_end.begin(), st->t_end.end(), end_ms);
+  return STP_OK;
+}
+
+void stp_destroy_stage(stp_stage* st) {
+  if (!st) return;
+  cudaSetDevice(st->dev);
+  cudaDeviceSynchronize();
+  for (auto c : st->owned)
+    if (c) ncclCommDestroy(c);
+  for (auto e : st->ev_done) cudaEventDestroy(e);
+  for (auto e : st->ev_t0) cudaEventDestroy(e);
+  for (auto e : st->ev_t1) cudaEventDestroy(e);
+  for (auto e : st->ev_pool) cudaEventDestroy(e);
+  if (st->ev_base) cudaEventDestroy(st->ev_base);
+  if (st->ev_end) cudaEventDestroy(st->ev_end);
+  if (st->ev_pf) cudaEventDestroy(st->ev_pf);
+  if (st->ev_pb) cudaEventDestroy(st->ev_pb);
+  for (auto& kv : st->s_send) cudaStreamDestroy(kv.second);
+  for (auto& kv : st->s_recv) cudaStreamDestroy(kv.second);
+  if (st->s_comp) cudaStreamDestroy(st->s_comp);
+  if (st->s_comm) cudaStreamDestroy(st->s_comm);
+  for (void* p : st->allocs) cudaFree(p);
+  delete st;
+}
+
+}  // extern "C"

@@ -1,0 +1,327 @@
+"""STP training-step benchmark (BASELINE.json metric: tokens/s per step at
+TP x PP on 1-8 B200; exposed TP-comm %; PP bubble rate).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+N = 1: Qwen2-7B-shaped model (configs[1] shape: h 3584, 28 layers, 28/4
+heads, d 128, I 18944, V 152064), seq 6144, 8 microbatches, TP=1 PP=1 with
+two virtual stages (V-shape), the R-STP braided schedule, bf16.  N > 1
+(torchrun, one rank per GPU): TP x PP = 2x1, 2x2 (N=4), 4x2 (N=8), same
+model and global batch (strong scaling).  A step = one stp_train_step: all
+microbatches' forward + B + W over the TP x PP grid, fp32 gradient
+accumulation, end-of-step gamma all-reduce; no optimizer.
+
+Timing: W untimed steps, then K steps each timed on the device by the
+library's CUDA events (first event recorded before the step's first enqueue,
+last after its final stream joins), barrier + synchronize on both sides, max
+over ranks.  Weights (15 GB) and the activation stash (~84 GB at N=1) are far
+larger than L2, so no explicit L2 flush is needed (stated in config.l2).
+
+--impl reference: the CPU oracle (oracle/model.py, fp64 numpy) timed on the
+host cores on a bounded sample of the same workload (see cpu_sample()).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+METRIC = "tokens/s per step at TP×PP on 1–8 B200; exposed TP-comm %; PP bubble rate"
+GRID = {1: (1, 1), 2: (2, 1), 4: (2, 2), 8: (4, 2)}
+
+
+def model_cfg(seq: int):
+    import dataclasses
+
+    import stp_inputs as si
+    return dataclasses.replace(si.QWEN2_7B, seq=seq)
+
+
+def gemm_flops_per_token(cfg):
+    """Algorithmic FLOPs per token of the training step:
+    6 * (layer GEMM params * L + h * V) + causal attention 6 * L * s * nq * d."""
+    h, d = cfg.hidden, cfg.head_dim
+    p_layer = h * (cfg.n_q_heads + 2 * cfg.n_kv_heads) * d + cfg.n_q_heads * d * h + 3 * h * cfg.ffn
+    return 6.0 * (p_layer * cfg.n_layers + h * cfg.vocab) + 6.0 * cfg.n_layers * cfg.seq * cfg.n_q_heads * d
+
+
+# ----------------------------------------------------------------- clocks
+class ClockSampler:
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                     timeout=5).stdout.strip()
+                if out:
+                    self.samples.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4) if "Active" in s[3 + i]})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+# ------------------------------------------------------------ CPU oracle
+def cpu_sample(seconds_hint: float = 20.0):
+    """Time the CPU oracle (as it stands) on a bounded sample of the workload:
+    one Qwen2-7B-shaped decoder layer + LM head (vocab 32768) over one
+    512-token microbatch, forward + backward in fp64.  Throughput is scaled to
+    the full workload by algorithmic FLOPs (tokens/s = sample FLOP/s /
+    full-model FLOPs per token)."""
+    import dataclasses
+
+    import stp_inputs as si
+    from oracle import model as om
+    cfg = dataclasses.replace(si.QWEN2_7B, n_layers=1, seq=512, vocab=32768)
+    P = si.make_params(cfg, seed=1)
+    toks, tgts = si.make_tokens(cfg, 1, seed=2)
+    t0 = time.perf_counter()
+    om.forward_backward(P, cfg, toks, tgts)
+    dt = time.perf_counter() - t0
+    sample_flops = gemm_flops_per_token(cfg) * cfg.seq
+    return dt, sample_flops, cfg
+
+
+def cpu_cores():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count()
+
+
+def reference_arm(args, full_cfg):
+    """--impl reference: the oracle on the host cores, bounded sample per step."""
+    import torch.distributed as dist  # noqa: F401
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    per_tok = gemm_flops_per_token(full_cfg)
+    times = []
+    for i in range(args.warmup + args.steps):
+        dt, fl, cfg = cpu_sample()
+        if i >= args.warmup:
+            times.append(dt)
+    mean = float(np.mean(times))
+    tok_s = (fl / mean) / per_tok
+    m = args.m
+    line = {
+        "impl": "reference", "metric": METRIC, "value": tok_s, "unit": "tokens/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": (m * full_cfg.seq / tok_s) * 1e3, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": workload_config(args, full_cfg, GRID.get(args.gpus, (1, 1))),
+        "cpu_baseline": {"value": tok_s, "unit": "tokens/s", "cores": cpu_cores(), "kind": "oracle",
+                         "sample": f"1 Qwen2-7B-shaped layer + LM head (V=32768), 1 x 512 tokens, fwd+bwd fp64 "
+                                   f"({mean:.1f} s/sample), scaled by algorithmic FLOPs to the full workload"},
+        "e2e": {"value": tok_s, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def workload_config(args, cfg, tp_pp):
+    t, p = tp_pp
+    return {"workload": f"qwen2-7b-shaped s{cfg.seq} m{args.m} tp{t}pp{p}vpp2 ({args.sched})",
+            "model": "Qwen2-7B-shaped (h3584 L28 28/4 heads d128 I18944 V152064), random init",
+            "global_batch": args.m, "seq_len": cfg.seq, "parallelism": f"tp{t}pp{p}vpp2",
+            "schedule": args.sched,
+            "l2": "no flush: weights (15.2 GB / tp*pp) and stash (tens of GB) exceed the 126 MB L2"}
+
+
+# ------------------------------------------------------------------ ours
+def ours(args):
+    import torch
+    import torch.distributed as dist
+
+    import stp_inputs as si
+    from paper_2510_27257_b200 import _lib as L
+    from paper_2510_27257_b200.stage import Stage, broadcast_nccl_id
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    t, p = GRID[world]
+    tp_rank, pp_rank = rank % t, rank // t
+    cfg = model_cfg(args.seq)
+    if args.layers:
+        import dataclasses
+        cfg = dataclasses.replace(cfg, n_layers=args.layers)
+    uid = broadcast_nccl_id() if world > 1 else None
+    st = Stage(cfg, tp=t, pp=p, n_micro=args.m, tp_rank=tp_rank, pp_rank=pp_rank, dtype="bf16",
+               sched=args.sched, device=local, world_nccl_id=uid)
+    # random-init weights on the device (seeded per tensor), N(0, 0.02^2); gammas 1
+    g = torch.Generator(device=f"cuda:{local}")
+    for i, (name, prm) in enumerate(zip(st.names, st.params)):
+        g.manual_seed(1000 * rank + i)
+        if name.endswith(("ln1", "ln2")) or name == "final_ln":
+            prm.fill_(1.0)
+        elif name.endswith("bqkv"):
+            prm.zero_()
+        else:
+            prm.copy_(torch.randn(prm.shape, generator=g, device=prm.device, dtype=torch.float32) * 0.02)
+    toks, tgts = si.make_tokens(cfg, args.m, seed=1234)
+    d_tok = torch.from_numpy(toks).cuda()
+    d_tgt = torch.from_numpy(tgts).cuda()
+    h_tok = torch.from_numpy(toks).pin_memory()
+    h_tgt = torch.from_numpy(tgts).pin_memory()
+
+    def barrier():
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+
+    for _ in range(args.warmup):
+        st.step(d_tok, d_tgt)
+    st.zero_grads()
+    barrier()
+    L.call("stp_prof_reset")
+    L.call("stp_prof_enable", 1)
+    ms = []
+    launches = 0
+    loss = 0.0
+    with ClockSampler(local) as clk:
+        for _ in range(args.steps):
+            loss, stats = st.step(d_tok, d_tgt)
+            ms.append(stats.step_ms)
+            launches += stats.n_kernels
+    barrier()
+    L.call("stp_prof_enable", 0)
+    prof = {}
+    for cls, nm in ((0, "gemm"), (1, "attn_fwd"), (2, "attn_bwd")):
+        c, fl, by, tm = L.i64(), L.C.c_double(), L.C.c_double(), L.C.c_double()
+        L.call("stp_prof_read", cls, L.C.byref(c), L.C.byref(fl), L.C.byref(by), L.C.byref(tm))
+        prof[nm] = (c.value, fl.value, by.value, tm.value)
+    L.call("stp_prof_reset")
+    # one extra step with per-unit events: exposed TP and PP bubble
+    st.set_timing(True)
+    _, tstats = st.step(d_tok, d_tgt)
+    st.set_timing(False)
+    # end-to-end through the public API with host (pinned) inputs
+    barrier()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        st.step_host(h_tok.numpy(), h_tgt.numpy())
+    barrier()
+    e2e_s = (time.perf_counter() - t0) / args.steps
+
+    step_ms = float(np.mean(ms))
+    vals = torch.tensor([step_ms, e2e_s, tstats.exposed_tp_ms / max(tstats.step_ms, 1e-9),
+                         tstats.pp_bubble_ms / max(tstats.step_ms, 1e-9)], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(vals, op=dist.ReduceOp.MAX)
+    step_ms, e2e_s, exp_frac, bub_frac = vals.tolist()
+    tokens = args.m * cfg.seq
+    value = tokens / (step_ms / 1e3)
+    if rank == 0:
+        peaks = {}
+        try:
+            peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+        except Exception:
+            pass
+        peak = peaks.get("bf16_tflops_sustained", 1415.3)
+        gc, gfl, gby, gms = prof["gemm"]
+        achieved = (gfl / (gms / 1e3)) / 1e12 if gms > 0 else None
+        traffic = None
+        tfile = os.path.join(ROOT, "profiles", "gemm_traffic.json")
+        if os.path.exists(tfile):
+            try:
+                traffic = json.load(open(tfile)).get("traffic_bytes_per_launch")
+            except Exception:
+                traffic = None
+        afc, afl, _, afm = prof["attn_fwd"]
+        abc, abl, _, abm = prof["attn_bwd"]
+        line = {
+            "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": step_ms, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "bf16", "data": "synthetic (seeded uniform tokens, N(0,0.02^2) weights)",
+            "config": workload_config(args, cfg, (t, p)),
+            "exposed_tp_pct": 100.0 * exp_frac, "pp_bubble_pct": 100.0 * bub_frac,
+            "loss": loss,
+            "roofline": {"bound": "tensor", "kernel": "gemm_bf16_sm100 (tcgen05), all GEMM launches of the timed steps",
+                         "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                         "frac": (achieved / peak) if achieved else None, "traffic": traffic,
+                         "launches": gc, "gemm_ms_per_step": gms / args.steps,
+                         "peak_source": "MEASURED_PEAKS.json bf16_tflops_sustained"},
+            "attention": {"fwd_tflops": (afl / (afm / 1e3)) / 1e12 if afm > 0 else None,
+                          "bwd_tflops": (abl / (abm / 1e3)) / 1e12 if abm > 0 else None,
+                          "fwd_ms_per_step": afm / args.steps, "bwd_ms_per_step": abm / args.steps},
+            "e2e": {"value": tokens / e2e_s, "unit": "tokens/s",
+                    "h2d_bytes_per_step": int(toks.nbytes + tgts.nbytes), "d2h_bytes_per_step": 4},
+            "gpu_launches": launches,
+            "clocks": clk.summary(),
+        }
+        if world == 1 and not args.no_cpu:
+            dt, fl, _ = cpu_sample()
+            cpu_tok = (fl / dt) / gemm_flops_per_token(cfg)
+            line["cpu_baseline"] = {"value": cpu_tok, "unit": "tokens/s", "cores": cpu_cores(), "kind": "oracle",
+                                    "sample": f"1 Qwen2-7B-shaped layer + LM head (V=32768), 1 x 512 tokens, "
+                                              f"fwd+bwd fp64 ({dt:.1f} s), scaled by algorithmic FLOPs"}
+        print(json.dumps(line), flush=True)
+    st.close()
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--seq", type=int, default=6144)
+    ap.add_argument("--m", type=int, default=8)
+    ap.add_argument("--layers", type=int, default=0, help="override layer count (debug only)")
+    ap.add_argument("--sched", default="stp")
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        return reference_arm(args, model_cfg(args.seq))
+    return ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -133,6 +133,18 @@ stp_status stp_op_convert(int32_t src_dtype, int32_t dst_dtype, int64_t n, const
                           void* dst, void* stream);
 /* Number of SMs of the current device (for launch sizing / roofline). */
 int32_t stp_num_sms(void);
+/* Kernels launched by this library on the calling thread since load. */
+int64_t stp_kernel_launches(void);
+
+/* ------------------------------------------------------------ profiling
+ * Kernel-class profiler (calling thread): when enabled, each launch of class
+ * cls (0 GEMM, 1 attention fwd, 2 attention bwd) is bracketed by CUDA events
+ * on its own stream and tagged with its algorithmic FLOPs and bytes.
+ * stp_prof_read synchronises on the recorded events and returns the launch
+ * count and the sums (ms = summed per-launch event time). */
+stp_status stp_prof_enable(int32_t on);
+stp_status stp_prof_reset(void);
+stp_status stp_prof_read(int32_t cls, int64_t* count, double* flops, double* bytes, double* ms);
 
 #ifdef __cplusplus
 }

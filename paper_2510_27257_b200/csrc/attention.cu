@@ -15,6 +15,7 @@
 #include <cmath>
 
 #include "common.h"
+#include "prof.h"
 
 namespace stp {
 namespace {
@@ -596,6 +597,9 @@ stp_status attn_fwd(int dtype, int64_t s, int nq, int nkv, int d, const void* q,
   STP_CHECK_ARG(nq > 0 && nkv > 0 && nq % nkv == 0, "nq % nkv == 0");
   STP_CHECK_ARG(d > 0 && d <= 128, "head_dim <= 128");
   if (s == 0) return STP_OK;
+  // algorithmic causal FLOPs: QK^T and PV over the s(s+1)/2 visible pairs
+  const double pairs = 0.5 * (double)s * (double)(s + 1);
+  ProfScope prof(PROF_ATTN_FWD, 4.0 * pairs * nq * d, (double)dtype_size(dtype) * s * (nq + 2 * nkv + nq) * d, st);
   if (dtype == STP_DTYPE_F32) {
     const int64_t warps = s * nq;
     attn_fwd_f32<<<(unsigned)((warps + 7) / 8), 256, 0, st>>>((int)s, nq, nkv, d, (const float*)q, (const float*)k,
@@ -621,6 +625,9 @@ stp_status attn_bwd(int dtype, int64_t s, int nq, int nkv, int d, const void* q,
   STP_CHECK_ARG(d > 0 && d <= 128, "head_dim <= 128");
   STP_CHECK_ARG(ws != nullptr, "workspace");
   if (s == 0) return STP_OK;
+  const double pairs = 0.5 * (double)s * (double)(s + 1);
+  ProfScope prof(PROF_ATTN_BWD, 8.0 * pairs * nq * d,
+                 (double)dtype_size(dtype) * s * (2 * (nq + 2 * nkv) + 2 * nq) * d, st);
   float* Dl = (float*)ws;
   const int64_t warps = s * nq;
   return STP_DISPATCH_DTYPE(dtype, [&] {

@@ -17,6 +17,7 @@
 #include <unordered_map>
 
 #include "common.h"
+#include "prof.h"
 #include "sm100.h"
 
 namespace stp {
@@ -459,6 +460,9 @@ stp_status gemm_dispatch(int dtype, int layout, int epi, int64_t M, int64_t N, i
   STP_CHECK_ARG(layout >= 0 && layout <= 2, "layout");
   STP_CHECK_ARG(epi >= 0 && epi <= 3, "epilogue");
   if (M == 0 || N == 0) return STP_OK;
+  const double es = dtype == STP_DTYPE_BF16 ? 2.0 : 4.0;
+  const double cbytes = (epi == STP_EPI_ACCUM_F32 ? 8.0 : es) * (double)M * N;
+  ProfScope prof(PROF_GEMM, 2.0 * M * N * K, es * ((double)M * K + (double)N * K) + cbytes, st);
   if (dtype == STP_DTYPE_F32)
     return gemm_f32(layout, epi, M, N, K, (const float*)A, lda, (const float*)B, ldb, (float*)C, ldc,
                     (const float*)bias, (const float*)R, ldr, st);

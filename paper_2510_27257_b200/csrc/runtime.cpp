@@ -3,7 +3,10 @@
 #include <cstdio>
 #include <mutex>
 
+#include <vector>
+
 #include "common.h"
+#include "prof.h"
 
 namespace stp {
 
@@ -31,9 +34,67 @@ int num_sms() {
   return n;
 }
 
+namespace {
+struct ProfState {
+  bool on = false;
+  std::vector<cudaEvent_t> pool;
+  size_t next = 0;
+  struct Rec {
+    int cls;
+    double flops, bytes;
+    cudaEvent_t e0, e1;
+  };
+  std::vector<Rec> recs;
+};
+thread_local ProfState g_prof;
+}  // namespace
+
+bool prof_on() { return g_prof.on; }
+cudaEvent_t prof_event() {
+  if (g_prof.next >= g_prof.pool.size()) {
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    g_prof.pool.push_back(e);
+  }
+  return g_prof.pool[g_prof.next++];
+}
+void prof_push(int cls, double flops, double bytes, cudaEvent_t e0, cudaEvent_t e1) {
+  g_prof.recs.push_back({cls, flops, bytes, e0, e1});
+}
+
 }  // namespace stp
 
 extern "C" {
+
+// Kernel-class profiling (stp_ops.h): enable / reset / read per class.
+stp_status stp_prof_enable(int32_t on) {
+  stp::g_prof.on = on != 0;
+  return STP_OK;
+}
+stp_status stp_prof_reset(void) {
+  stp::g_prof.recs.clear();
+  stp::g_prof.next = 0;
+  return STP_OK;
+}
+stp_status stp_prof_read(int32_t cls, int64_t* count, double* flops, double* bytes, double* ms) {
+  if (!count || !flops || !bytes || !ms) return stp::fail(STP_EINVAL, "NULL argument");
+  *count = 0;
+  *flops = *bytes = *ms = 0.0;
+  for (auto& r : stp::g_prof.recs) {
+    if (r.cls != cls) continue;
+    cudaError_t e = cudaEventSynchronize(r.e1);
+    if (e != cudaSuccess) return stp::fail(STP_ECUDA, cudaGetErrorString(e));
+    float t = 0.f;
+    e = cudaEventElapsedTime(&t, r.e0, r.e1);
+    if (e != cudaSuccess) return stp::fail(STP_ECUDA, cudaGetErrorString(e));
+    *count += 1;
+    *flops += r.flops;
+    *bytes += r.bytes;
+    *ms += t;
+  }
+  return STP_OK;
+}
+
 
 const char* stp_last_error(void) { return stp::g_err; }
 

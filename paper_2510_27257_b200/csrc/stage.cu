@@ -143,9 +143,14 @@ struct stp_stage {
   std::vector<stp::Chunk> chunks;
   // streams / comms
   cudaStream_t s_comp = nullptr, s_comm = nullptr;
-  std::map<int, cudaStream_t> s_send, s_recv;  // by peer device
+  // PP channels: one NCCL communicator + stream per virtual-stage edge
+  // (src vs, dst vs) this rank sends or receives on (per-edge FIFO; a single
+  // channel per device pair is not FIFO for ZB / 1F1B-I).
+  std::map<std::pair<int, int>, cudaStream_t> s_send, s_recv;
   ncclComm_t world = nullptr, tpc = nullptr;
-  std::map<int, ncclComm_t> c_send, c_recv;
+  std::map<std::pair<int, int>, ncclComm_t> c_send, c_recv;
+  std::vector<std::pair<int, int>> unit_edge;  // per unit: PP edge (src vs, dst vs)
+  std::vector<char> unit_fwd;                  // per unit: PP message belongs to a forward pass
   std::vector<ncclComm_t> owned;
   // buffers
   void *pf = nullptr, *pb = nullptr;               // partial outputs (forward / backward lanes)
@@ -574,39 +579,60 @@ stp_status unit_cb(stp_stage* S, const stp_unit& u) {
   return STP_OK;
 }
 
-stp_status unit_pp(stp_stage* S, const stp_unit& u, cudaStream_t st, cudaEvent_t* send_ev) {
+stp_status unit_pp(stp_stage* S, int ui, const stp_unit& u, cudaStream_t st) {
   Chunk& C = chunk_of(S, u.chunk);
-  const int peer = u.layer;
   const size_t count = (size_t)(S->sl * S->h);
-  // direction: forward pass receives from vs-1 / sends to vs+1
-  const bool fwd_recv = (dev_of_vs(S, C.vs - 1) == peer && C.vs > 0);
+  const bool fwd = S->unit_fwd[ui] != 0;
+  const auto edge = S->unit_edge[ui];
   Slot* sl = nullptr;
   if (u.op == STP_U_PP_RECV) {
-    // a forward recv starts a new pass; a backward recv targets the existing stash
-    const bool is_fwd = fwd_recv && !find_slot(S, u.chunk, u.mb);
-    if (is_fwd) STP_TRY(acquire(S, u.chunk, u.mb, &sl));
+    // a forward recv opens the pass's stash slot; a backward recv fills it
+    if (fwd) STP_TRY(acquire(S, u.chunk, u.mb, &sl));
     else sl = find_slot(S, u.chunk, u.mb);
     if (!sl) return fail(STP_ESTATE, "recv without stash");
-    void* dst = is_fwd ? sl->x_in : sl->dx_in;
-    STP_NCCL_TRY(ncclRecv(dst, count, (ncclDataType_t)ncdt(S->dtype), 1, S->c_recv.at(peer), st));
+    STP_NCCL_TRY(ncclRecv(fwd ? sl->x_in : sl->dx_in, count, (ncclDataType_t)ncdt(S->dtype), 0, S->c_recv.at(edge),
+                          st));
     return STP_OK;
   }
   sl = find_slot(S, u.chunk, u.mb);
   if (!sl) return fail(STP_ESTATE, "send without stash");
-  // A send is forward iff it follows the forward lane (its dep is a CF unit).
-  const bool fwd_send = S->units[u.dep0].op == STP_U_CF;
-  const void* src = fwd_send ? sl->L[C.nl - 1].xres : sl->dx_in;
-  STP_NCCL_TRY(ncclSend(src, count, (ncclDataType_t)ncdt(S->dtype), 1, S->c_send.at(peer), st));
-  *send_ev = pool_event(S);
-  STP_CUDA_TRY(cudaEventRecord(*send_ev, st));
-  sl->free_events.push_back(*send_ev);
+  const void* src = fwd ? sl->L[C.nl - 1].xres : sl->dx_in;
+  STP_NCCL_TRY(ncclSend(src, count, (ncclDataType_t)ncdt(S->dtype), 1, S->c_send.at(edge), st));
+  cudaEvent_t e = pool_event(S);
+  STP_CUDA_TRY(cudaEventRecord(e, st));
+  sl->free_events.push_back(e);
   return STP_OK;
 }
 
-cudaStream_t stream_of(stp_stage* S, const stp_unit& u) {
+cudaStream_t stream_of(stp_stage* S, int ui, const stp_unit& u) {
   if (u.stream == 0) return S->s_comp;
   if (u.stream == 1) return S->s_comm;
-  return u.op == STP_U_PP_SEND ? S->s_send.at(u.layer) : S->s_recv.at(u.layer);
+  return u.op == STP_U_PP_SEND ? S->s_send.at(S->unit_edge[ui]) : S->s_recv.at(S->unit_edge[ui]);
+}
+
+// PP edge of every PP unit: sends follow their lane's last comm phase (CF =
+// forward); a recv is forward iff a CF unit depends on it.
+void classify_pp_units(const Schedule& sched, int p, int d, const std::vector<stp_unit>& us,
+                       std::vector<std::pair<int, int>>& edge, std::vector<char>& fwd) {
+  const int kind = sched.kind;
+  edge.assign(us.size(), {-1, -1});
+  fwd.assign(us.size(), 0);
+  std::vector<char> recv_fwd(us.size(), 0);
+  for (size_t i = 0; i < us.size(); ++i)
+    if (us[i].op == STP_U_CF && us[i].dep0 >= 0 && us[us[i].dep0].op == STP_U_PP_RECV) recv_fwd[us[i].dep0] = 1;
+  for (size_t i = 0; i < us.size(); ++i) {
+    const stp_unit& u = us[i];
+    const int vs = sched_vstage(kind, p, d, u.chunk);
+    if (u.op == STP_U_PP_SEND) {
+      const bool f = us[u.dep0].op == STP_U_CF;
+      fwd[i] = f;
+      edge[i] = {vs, f ? vs + 1 : vs - 1};
+    } else if (u.op == STP_U_PP_RECV) {
+      const bool f = recv_fwd[i] != 0;
+      fwd[i] = f;
+      edge[i] = {f ? vs - 1 : vs + 1, vs};
+    }
+  }
 }
 
 bool is_last_w(stp_stage* S, const stp_unit& u) {
@@ -642,17 +668,16 @@ stp_status run_step(stp_stage* S, float* h_loss, stp_step_stats* stats) {
   const int n = (int)S->units.size();
   for (int i = 0; i < n; ++i) {
     const stp_unit& u = S->units[i];
-    cudaStream_t st = stream_of(S, u);
+    cudaStream_t st = stream_of(S, i, u);
     if (u.dep0 >= 0) STP_CUDA_TRY(cudaStreamWaitEvent(st, S->ev_done[u.dep0], 0));
     if (u.dep1 >= 0) STP_CUDA_TRY(cudaStreamWaitEvent(st, S->ev_done[u.dep1], 0));
     if (S->timing) STP_CUDA_TRY(cudaEventRecord(S->ev_t0[i], st));
     stp_status r = STP_OK;
-    cudaEvent_t send_ev = nullptr;
     switch (u.op) {
       case STP_U_CF: r = unit_cf(S, u); break;
       case STP_U_CB: r = unit_cb(S, u); break;
       case STP_U_PP_SEND:
-      case STP_U_PP_RECV: r = unit_pp(S, u, st, &send_ev); break;
+      case STP_U_PP_RECV: r = unit_pp(S, i, u, st); break;
       default: r = unit_compute(S, u); break;
     }
     if (r != STP_OK) {
@@ -808,60 +833,63 @@ stp_status init_nccl(stp_stage* S, const void* uid) {
   // TP group: same PP rank
   STP_NCCL_TRY(ncclCommSplit(S->world, S->pp_rank, S->tp_rank, &S->tpc, nullptr));
   if (S->tpc) S->owned.push_back(S->tpc);
-  // PP pair communicators: one per (ordered device pair, tp rank), direction
-  // a -> b with the sender as rank 0.  Pairs are split in matching rounds so
-  // each split call puts every rank in at most one pair.
-  std::vector<std::pair<int, int>> pairs;  // unordered {a < b} that exchange messages
-  {
-    std::vector<int> lay(S->lay);
-    for (int d = 0; d < S->p; ++d) {
-      std::vector<stp_unit> us;
-      STP_TRY(schedule_expand(S->sched, d, lay, us));
-      for (auto& u : us)
-        if (u.op == STP_U_PP_SEND) {
-          std::pair<int, int> pr(std::min(d, u.layer), std::max(d, u.layer));
-          if (std::find(pairs.begin(), pairs.end(), pr) == pairs.end()) pairs.push_back(pr);
-        }
-    }
-    std::sort(pairs.begin(), pairs.end());
+  // PP channels: one 2-rank communicator per (virtual-stage edge, tp rank),
+  // sender = rank 0.  Every rank enumerates every device's edges (the
+  // schedule is deterministic), then splits them in rounds in which each
+  // device appears in at most one edge.
+  struct Edge {
+    int src_vs, dst_vs, src_dev, dst_dev;
+  };
+  std::vector<Edge> edges;
+  for (int d = 0; d < S->p; ++d) {
+    std::vector<stp_unit> us;
+    STP_TRY(schedule_expand(S->sched, d, S->lay, us));
+    std::vector<std::pair<int, int>> ue;
+    std::vector<char> uf;
+    classify_pp_units(S->sched, S->p, d, us, ue, uf);
+    for (size_t i = 0; i < us.size(); ++i)
+      if (us[i].op == STP_U_PP_SEND) {
+        Edge e{ue[i].first, ue[i].second, d, us[i].layer};
+        bool seen = false;
+        for (auto& x : edges) seen |= (x.src_vs == e.src_vs && x.dst_vs == e.dst_vs);
+        if (!seen) edges.push_back(e);
+      }
   }
-  std::vector<std::vector<std::pair<int, int>>> rounds;
-  for (auto& pr : pairs) {
+  std::sort(edges.begin(), edges.end(), [](const Edge& a, const Edge& b) {
+    return a.src_vs != b.src_vs ? a.src_vs < b.src_vs : a.dst_vs < b.dst_vs;
+  });
+  std::vector<std::vector<Edge>> rounds;
+  for (auto& e : edges) {
     bool placed = false;
     for (auto& rd : rounds) {
       bool clash = false;
       for (auto& q : rd)
-        if (q.first == pr.first || q.first == pr.second || q.second == pr.first || q.second == pr.second) clash = true;
+        clash |= q.src_dev == e.src_dev || q.src_dev == e.dst_dev || q.dst_dev == e.src_dev || q.dst_dev == e.dst_dev;
       if (!clash) {
-        rd.push_back(pr);
+        rd.push_back(e);
         placed = true;
         break;
       }
     }
-    if (!placed) rounds.push_back({pr});
+    if (!placed) rounds.push_back({e});
   }
   const int me = S->pp_rank;
   for (auto& rd : rounds) {
-    for (int dir = 0; dir < 2; ++dir) {  // dir 0: a -> b, dir 1: b -> a
-      int color = NCCL_SPLIT_NOCOLOR, key = 0, peer = -1;
-      bool sender = false;
-      for (size_t i = 0; i < rd.size(); ++i) {
-        const int a = rd[i].first, b = rd[i].second;
-        const int src = dir == 0 ? a : b, dst = dir == 0 ? b : a;
-        if (me == src || me == dst) {
-          color = (int)i * S->t + S->tp_rank;
-          sender = me == src;
-          key = sender ? 0 : 1;
-          peer = sender ? dst : src;
-        }
+    int color = NCCL_SPLIT_NOCOLOR, key = 0;
+    const Edge* mine = nullptr;
+    for (size_t i = 0; i < rd.size(); ++i)
+      if (rd[i].src_dev == me || rd[i].dst_dev == me) {
+        color = (int)i * S->t + S->tp_rank;
+        key = rd[i].src_dev == me ? 0 : 1;
+        mine = &rd[i];
       }
-      ncclComm_t c = nullptr;
-      STP_NCCL_TRY(ncclCommSplit(S->world, color, key, &c, nullptr));
-      if (c) {
-        S->owned.push_back(c);
-        if (sender) S->c_send[peer] = c;
-        else S->c_recv[peer] = c;
-      }
+    ncclComm_t c = nullptr;
+    STP_NCCL_TRY(ncclCommSplit(S->world, color, key, &c, nullptr));
+    if (c && mine) {
+      S->owned.push_back(c);
+      const std::pair<int, int> k(mine->src_vs, mine->dst_vs);
+      if (mine->src_dev == me) S->c_send[k] = c;
+      else S->c_recv[k] = c;
     }
   }
   return STP_OK;
@@ -937,6 +965,7 @@ stp_status stp_init_stage(const stp_model_cfg* mc, const stp_parallel_cfg* pc, c
     STP_TRY(layer_split(mc->n_layers, V, S->lay.data()));
   }
   STP_TRY(schedule_expand(S->sched, S->pp_rank, S->lay, S->units));
+  classify_pp_units(S->sched, p, S->pp_rank, S->units, S->unit_edge, S->unit_fwd);
   STP_CUDA_TRY(cudaSetDevice(cuda_device));
   // chunks held by this rank
   const int nchunks = sched_n_chunks(S->kind);
@@ -1022,10 +1051,11 @@ stp_status stp_init_stage(const stp_model_cfg* mc, const stp_parallel_cfg* pc, c
     STP_CUDA_TRY(cudaStreamCreateWithPriority(&st, cudaStreamNonBlocking, hi));
     S->s_recv[kv.first] = st;
   }
-  // every PP peer used by the unit list must have its communicator
-  for (auto& u : S->units) {
-    if (u.op == STP_U_PP_SEND && !S->c_send.count(u.layer)) return fail(STP_ENCCL, "missing PP send communicator");
-    if (u.op == STP_U_PP_RECV && !S->c_recv.count(u.layer)) return fail(STP_ENCCL, "missing PP recv communicator");
+  // every PP edge used by the unit list must have its communicator
+  for (size_t i = 0; i < S->units.size(); ++i) {
+    const stp_unit& u = S->units[i];
+    if (u.op == STP_U_PP_SEND && !S->c_send.count(S->unit_edge[i])) return fail(STP_ENCCL, "missing PP send channel");
+    if (u.op == STP_U_PP_RECV && !S->c_recv.count(S->unit_edge[i])) return fail(STP_ENCCL, "missing PP recv channel");
   }
   *out = S.release();
   return STP_OK;

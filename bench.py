@@ -311,7 +311,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--seq", type=int, default=6144)
-    ap.add_argument("--m", type=int, default=8)
+    ap.add_argument("--micro", dest="m", type=int, default=8)
     ap.add_argument("--layers", type=int, default=0, help="override layer count (debug only)")
     ap.add_argument("--sched", default="stp")
     ap.add_argument("--no-cpu", action="store_true")

@@ -586,6 +586,9 @@ stp_status bwd_bf16(int s, int nq, int nkv, const void* q, const void* k, const 
 
 }  // namespace
 
+stp_status attn_fwd_sm100_launch(int s, int nq, int nkv, const void* qkv_base, int64_t ld, void* o, int64_t ldo,
+                                 float* lse, cudaStream_t st);
+
 int64_t attn_bwd_ws_bytes(int64_t s, int nq, int nkv, int d) {
   (void)nkv;
   (void)d;
@@ -609,6 +612,11 @@ stp_status attn_fwd(int dtype, int64_t s, int nq, int nkv, int d, const void* q,
     return STP_OK;
   }
   STP_CHECK_ARG(ld % 8 == 0 && ldo % 8 == 0, "bf16 attention strides % 8 == 0");
+  // tcgen05 path: d = 128 with the fused [q | k | v] row layout
+  static const bool force_mma = getenv("STP_ATTN_MMA_SYNC") != nullptr;
+  if (d == 128 && !force_mma && (const uint8_t*)k == (const uint8_t*)q + (int64_t)nq * d * 2 &&
+      (const uint8_t*)v == (const uint8_t*)k + (int64_t)nkv * d * 2 && ld == (int64_t)(nq + 2 * nkv) * d)
+    return attn_fwd_sm100_launch((int)s, nq, nkv, q, ld, o, ldo, lse, st);
   switch (d) {
     case 16: return fwd_bf16<16>((int)s, nq, nkv, q, k, v, ld, o, ldo, lse, st);
     case 32: return fwd_bf16<32>((int)s, nq, nkv, q, k, v, ld, o, ldo, lse, st);

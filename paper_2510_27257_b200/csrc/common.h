@@ -81,3 +81,12 @@ inline size_t dtype_size(int dtype) { return dtype == STP_DTYPE_BF16 ? 2 : 4; }
     ::stp::set_error("unknown dtype %d", (int)(dtype));                        \
     return STP_EINVAL;                                                         \
   }()
+
+#ifndef STP_TRY
+#define STP_TRY(expr)                     \
+  do {                                    \
+    stp_status s_ = (expr);               \
+    if (s_ != STP_OK) return s_;          \
+  } while (0)
+#endif
+#define STP_TRY_STATUS(expr) STP_TRY(expr)

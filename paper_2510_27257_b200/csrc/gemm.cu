@@ -453,6 +453,11 @@ stp_status gemm_f32(int layout, int epi, int64_t M, int64_t N, int64_t K, const 
 
 }  // namespace
 
+// 2-D bf16 tensor map with 128-byte swizzle (shared with the attention kernels).
+stp_status tensor_map_bf16(CUtensorMap* out, const void* ptr, int64_t d0, int64_t d1, int64_t ld, int b0, int b1) {
+  return tensor_map(out, ptr, d0, d1, ld, b0, b1);
+}
+
 stp_status gemm_dispatch(int dtype, int layout, int epi, int64_t M, int64_t N, int64_t K, const void* A,
                          int64_t lda, const void* B, int64_t ldb, void* C, int64_t ldc, const void* bias,
                          const void* R, int64_t ldr, int max_ctas, cudaStream_t st) {

@@ -76,12 +76,6 @@ stp_status convert(int sd, int dd, int64_t n, const void* src, void* dst, cudaSt
     }                                                                          \
   } while (0)
 
-#define STP_TRY(expr)                     \
-  do {                                    \
-    stp_status s_ = (expr);               \
-    if (s_ != STP_OK) return s_;          \
-  } while (0)
-
 namespace {
 
 struct Param {

@@ -21,7 +21,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--tp", type=int, required=True)
     ap.add_argument("--pp", type=int, required=True)
-    ap.add_argument("--m", type=int, default=4)
+    ap.add_argument("--n-micro", type=int, default=4)
     ap.add_argument("--dtype", default="f32")
     ap.add_argument("--sched", default="stp")
     ap.add_argument("--seq", type=int, default=32)
@@ -35,10 +35,10 @@ def main():
     cfg = dataclasses.replace(si.TINY, seq=a.seq, n_kv_heads=max(2, a.tp))
     lay = [int(x) for x in a.layers.split(",")] if a.layers else [1] * (2 * a.pp if a.sched != "1f1b" else a.pp)
     cfg = dataclasses.replace(cfg, n_layers=sum(lay))
-    P, toks, tgts, ref_loss, G = oracle_reference(cfg, a.m)
+    P, toks, tgts, ref_loss, G = oracle_reference(cfg, a.n_micro)
     tp_rank, pp_rank = rank % a.tp, rank // a.tp
     uid = broadcast_nccl_id()
-    st = Stage(cfg, tp=a.tp, pp=a.pp, n_micro=a.m, tp_rank=tp_rank, pp_rank=pp_rank, dtype=a.dtype, sched=a.sched,
+    st = Stage(cfg, tp=a.tp, pp=a.pp, n_micro=a.n_micro, tp_rank=tp_rank, pp_rank=pp_rank, dtype=a.dtype, sched=a.sched,
                layers_per_vstage=lay, device=local, world_nccl_id=uid)
     st.load_params(P)
     loss, stats = st.step(torch.from_numpy(toks).cuda(), torch.from_numpy(tgts).cuda())
@@ -48,7 +48,7 @@ def main():
     bad = compare(cfg, got, ref, loss if holds_loss else ref_loss, ref_loss, a.dtype)
     # the executed unit order equals the schedule's unit order
     from paper_2510_27257_b200.stage import schedule_units
-    if st.trace() != schedule_units(a.sched, a.pp, a.m, a.tp, pp_rank, lay):
+    if st.trace() != schedule_units(a.sched, a.pp, a.n_micro, a.tp, pp_rank, lay):
         bad.append("trace != schedule units")
     st.close()
     flag = torch.tensor([len(bad)], device="cuda")

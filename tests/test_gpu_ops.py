@@ -110,7 +110,8 @@ def test_swiglu(dt, s, I):
     assert _rel(_np(out), np.concatenate([dG, dU], 1)) <= TOL[dt]
 
 
-ATT = [(1, 2, 1, 16), (33, 4, 2, 16), (130, 4, 4, 32), (200, 6, 2, 64), (257, 7, 1, 128), (1024, 4, 2, 128)]
+ATT = [(1, 2, 1, 16), (33, 4, 2, 16), (130, 4, 4, 32), (200, 6, 2, 64), (257, 7, 1, 128), (1024, 4, 2, 128),
+       (2048, 7, 1, 128), (300, 2, 2, 128)]
 
 
 @pytest.mark.parametrize("dt", ["f32", "bf16"])

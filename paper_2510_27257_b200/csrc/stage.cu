@@ -145,6 +145,7 @@ struct stp_stage {
   std::map<std::pair<int, int>, ncclComm_t> c_send, c_recv;
   std::vector<std::pair<int, int>> unit_edge;  // per unit: PP edge (src vs, dst vs)
   std::vector<char> unit_fwd;                  // per unit: PP message belongs to a forward pass
+  std::vector<std::pair<int, int>> edges_sorted;  // all PP edges of the grid, global order
   std::vector<ncclComm_t> owned;
   // buffers
   void *pf = nullptr, *pb = nullptr;               // partial outputs (forward / backward lanes)
@@ -821,6 +822,7 @@ stp_status init_nccl(stp_stage* S, const void* uid) {
   if (!uid) return fail(STP_EINVAL, "world_nccl_id required when tp*pp > 1");
   ncclUniqueId id;
   memcpy(&id, uid, sizeof(id));
+  setenv("NCCL_RUNTIME_CONNECT", "0", 0);  // connect at init (see warmup_comms)
   const int rank = S->pp_rank * S->t + S->tp_rank;
   STP_NCCL_TRY(ncclCommInitRank(&S->world, world, id, rank));
   S->owned.push_back(S->world);
@@ -884,6 +886,44 @@ stp_status init_nccl(stp_stage* S, const void* uid) {
       const std::pair<int, int> k(mine->src_vs, mine->dst_vs);
       if (mine->src_dev == me) S->c_send[k] = c;
       else S->c_recv[k] = c;
+    }
+  }
+  S->edges_sorted.clear();
+  for (auto& e : edges) S->edges_sorted.push_back({e.src_vs, e.dst_vs});
+  return STP_OK;
+}
+
+// NCCL sets up connections lazily, and the setup handshake blocks the host.
+// Two ranks that first touch different communicators in different orders can
+// therefore deadlock inside the handshake.  Touch every communicator once at
+// init, in one global order: TP groups first (every rank is in exactly one),
+// then every PP edge in sorted order (the globally smallest unfinished edge
+// always has both endpoints waiting on it, so the sequence cannot deadlock).
+// The TP collectives use the step's real message sizes so the algorithms the
+// step will pick are the ones connected here.
+stp_status warmup_comms(stp_stage* S) {
+  const ncclDataType_t dt = (ncclDataType_t)ncdt(S->dtype);
+  const size_t shard = (size_t)(S->sl * S->h);
+  if (S->t > 1) {
+    STP_NCCL_TRY(ncclReduceScatter(S->pf, S->rtmp, shard, dt, ncclSum, S->tpc, S->s_comm));
+    STP_NCCL_TRY(ncclAllGather(S->ntmp, S->pf, shard, dt, S->tpc, S->s_comm));
+    STP_NCCL_TRY(ncclAllGather(S->pf, S->pb, (size_t)(S->s * 3), ncclFloat32, S->tpc, S->s_comm));
+    STP_NCCL_TRY(ncclAllReduce(S->dgamma, S->dgamma, (size_t)std::max<int64_t>(1, S->dgamma_n), ncclFloat32, ncclSum,
+                               S->tpc, S->s_comm));
+    STP_CUDA_TRY(cudaStreamSynchronize(S->s_comm));
+  }
+  for (auto& e : S->edges_sorted) {
+    auto is = S->c_send.find(e);
+    if (is != S->c_send.end()) {
+      cudaStream_t st = S->s_send.at(e);
+      STP_NCCL_TRY(ncclSend(S->pf, shard, dt, 1, is->second, st));
+      STP_CUDA_TRY(cudaStreamSynchronize(st));
+    }
+    auto ir = S->c_recv.find(e);
+    if (ir != S->c_recv.end()) {
+      cudaStream_t st = S->s_recv.at(e);
+      STP_NCCL_TRY(ncclRecv(S->pb, shard, dt, 0, ir->second, st));
+      STP_CUDA_TRY(cudaStreamSynchronize(st));
     }
   }
   return STP_OK;
@@ -1045,6 +1085,7 @@ stp_status stp_init_stage(const stp_model_cfg* mc, const stp_parallel_cfg* pc, c
     STP_CUDA_TRY(cudaStreamCreateWithPriority(&st, cudaStreamNonBlocking, hi));
     S->s_recv[kv.first] = st;
   }
+  STP_TRY(warmup_comms(S.get()));
   // every PP edge used by the unit list must have its communicator
   for (size_t i = 0; i < S->units.size(); ++i) {
     const stp_unit& u = S->units[i];

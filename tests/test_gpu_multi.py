@@ -25,7 +25,7 @@ def test_multi_rank_parity(tp, pp, sched, dtype):
            "--master-addr=127.0.0.1", f"--master-port={29500 + 7 * tp + 3 * pp}",
            os.path.join(ROOT, "tests", "multi_rank_parity.py"), "--tp", str(tp), "--pp", str(pp),
            "--sched", sched, "--dtype", dtype, "--seq", str(seq), "--n-micro", str(2 * pp if sched != "stp" else 4)]
-    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=150, cwd=ROOT)
     out = r.stdout + r.stderr
     assert r.returncode == 0, out[-4000:]
     assert out.count("PASS") == n, out[-4000:]

@@ -276,6 +276,448 @@ __global__ void __launch_bounds__(256, 1)
   }
 }
 
+
+// ---------------------------------------------------------------- backward
+// dQ kernel: one CTA per (query tile, head); loop over key tiles j <= i:
+//   S = Q K_j^T, dP = dO V_j^T (TMEM), dS = P * (dP - D) (softmax warps,
+//   bf16 -> smem), dQ += dS K_j (TMEM).  dQ = scale * dQ at the end.
+constexpr int DQ_SMEM = 1024 + 7 * TILE_BYTES + 256;  // Q, dO, K[2], V[2], dS
+
+struct BwdArgs {
+  int s, nq, nkv;
+  const float* lse;  // [nq, s] natural log
+  const float* Dl;   // [nq, s]
+  void* dq;          // bf16 [s, ldd] (q columns)
+  int64_t ldd;
+  float* dk_part;    // fp32 [nq, s, D]
+  float* dv_part;    // fp32 [nq, s, D]
+  float scale_log2, scale;
+};
+
+__device__ __forceinline__ void named_bar(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+
+__global__ void __launch_bounds__(256, 1)
+    attn_bwd_dq_sm100(const __grid_constant__ CUtensorMap tm_qkv, const __grid_constant__ CUtensorMap tm_do,
+                      const BwdArgs a) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sQ = smem;
+  uint8_t* sdO = smem + TILE_BYTES;
+  uint8_t* sK = smem + 2 * TILE_BYTES;  // [2]
+  uint8_t* sV = smem + 4 * TILE_BYTES;  // [2]
+  uint8_t* sdS = smem + 6 * TILE_BYTES;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + 7 * TILE_BYTES);
+  uint64_t* qdo_full = bar + 0;
+  uint64_t* k_full = bar + 1;   // [2]
+  uint64_t* k_empty = bar + 3;  // [2]
+  uint64_t* v_full = bar + 5;   // [2]
+  uint64_t* v_empty = bar + 7;  // [2]
+  uint64_t* sdp_full = bar + 9;
+  uint64_t* sdp_empty = bar + 10;
+  uint64_t* ds_full = bar + 11;
+  uint64_t* dq_done = bar + 12;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 14);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int qt = gridDim.x - 1 - blockIdx.x;
+  const int h = blockIdx.y;
+  const int grp = a.nq / a.nkv, g = h / grp;
+  const int n_kv = qt + 1;
+  const int qcol = h * D, kcol = a.nq * D + g * D, vcol = (a.nq + a.nkv) * D + g * D;
+
+  if (threadIdx.x == 0) {
+    mbar_init(qdo_full, 1);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(k_full + i, 1);
+      mbar_init(k_empty + i, 1);
+      mbar_init(v_full + i, 1);
+      mbar_init(v_empty + i, 1);
+    }
+    mbar_init(sdp_full, 1);
+    mbar_init(sdp_empty, 128);
+    mbar_init(ds_full, 128);
+    mbar_init(dq_done, 1);
+    fence_barrier_init();
+    tma_prefetch_desc(&tm_qkv);
+    tma_prefetch_desc(&tm_do);
+  }
+  if (warp == 2) tmem_alloc<512>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t tS = tmem, tP = tmem + 128, tQ = tmem + 256;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      mbar_arrive_expect_tx(qdo_full, 2 * TILE_BYTES);
+      tma_load_2d(sQ, &tm_qkv, qdo_full, qcol, qt * T);
+      tma_load_2d(sQ + ATOM, &tm_qkv, qdo_full, qcol + 64, qt * T);
+      tma_load_2d(sdO, &tm_do, qdo_full, h * D, qt * T);
+      tma_load_2d(sdO + ATOM, &tm_do, qdo_full, h * D + 64, qt * T);
+      for (int j = 0; j < n_kv; ++j) {
+        const int b = j & 1;
+        const uint32_t ph = (j >> 1) & 1;
+        mbar_wait(k_empty + b, ph ^ 1);
+        mbar_arrive_expect_tx(k_full + b, TILE_BYTES);
+        tma_load_2d(sK + b * TILE_BYTES, &tm_qkv, k_full + b, kcol, j * T);
+        tma_load_2d(sK + b * TILE_BYTES + ATOM, &tm_qkv, k_full + b, kcol + 64, j * T);
+        mbar_wait(v_empty + b, ph ^ 1);
+        mbar_arrive_expect_tx(v_full + b, TILE_BYTES);
+        tma_load_2d(sV + b * TILE_BYTES, &tm_qkv, v_full + b, vcol, j * T);
+        tma_load_2d(sV + b * TILE_BYTES + ATOM, &tm_qkv, v_full + b, vcol + 64, j * T);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t idKK = make_idesc_bf16(T, T, false, false);  // S, dP: both operands K-major
+      constexpr uint32_t idQ = make_idesc_bf16(T, D, false, true);    // dQ += dS K (K MN-major)
+      const uint32_t q_addr = smem_u32(sQ), do_addr = smem_u32(sdO), ds_addr = smem_u32(sdS);
+      mbar_wait(qdo_full, 0);
+      auto issue_sdp = [&](int j) {
+        const int b = j & 1;
+        const uint32_t ph = (j >> 1) & 1;
+        mbar_wait(k_full + b, ph);
+        mbar_wait(v_full + b, ph);
+        tc_fence_after();
+        const uint32_t k_addr = smem_u32(sK + b * TILE_BYTES), v_addr = smem_u32(sV + b * TILE_BYTES);
+#pragma unroll
+        for (int kk = 0; kk < D / 16; ++kk) {
+          const uint32_t off = (kk >> 2) * ATOM + (kk & 3) * 32;
+          mma_f16_ss(tS, make_sw128_desc(q_addr + off, 16, 1024), make_sw128_desc(k_addr + off, 16, 1024), idKK,
+                     kk > 0 ? 1u : 0u);
+        }
+#pragma unroll
+        for (int kk = 0; kk < D / 16; ++kk) {
+          const uint32_t off = (kk >> 2) * ATOM + (kk & 3) * 32;
+          mma_f16_ss(tP, make_sw128_desc(do_addr + off, 16, 1024), make_sw128_desc(v_addr + off, 16, 1024), idKK,
+                     kk > 0 ? 1u : 0u);
+        }
+        mma_commit(v_empty + b);
+        mma_commit(sdp_full);
+      };
+      issue_sdp(0);
+      for (int j = 0; j < n_kv; ++j) {
+        if (j + 1 < n_kv) {
+          mbar_wait(sdp_empty, j & 1);  // softmax has read S/dP of tile j
+          issue_sdp(j + 1);
+        }
+        mbar_wait(ds_full, j & 1);
+        tc_fence_after();
+        const int b = j & 1;
+        const uint32_t k_addr = smem_u32(sK + b * TILE_BYTES);
+#pragma unroll
+        for (int kk = 0; kk < T / 16; ++kk) {
+          const uint64_t ad = make_sw128_desc(ds_addr + (kk >> 2) * ATOM + (kk & 3) * 32, 16, 1024);
+          const uint64_t bd = make_sw128_desc(k_addr + kk * 2048, ATOM, 1024);
+          mma_f16_ss(tQ, ad, bd, idQ, (j > 0 || kk > 0) ? 1u : 0u);
+        }
+        mma_commit(k_empty + b);
+        mma_commit(dq_done);
+      }
+    }
+  } else if (warp >= 4) {
+    const int r = (warp - 4) * 32 + lane;
+    const uint32_t lane_off = (uint32_t)((warp - 4) * 32) << 16;
+    const int qrow = qt * T + r;
+    const bool vrow = qrow < a.s;
+    const float lse2 = vrow ? a.lse[(int64_t)h * a.s + qrow] * 1.4426950408889634f : 0.f;
+    const float Dv = vrow ? a.Dl[(int64_t)h * a.s + qrow] : 0.f;
+    uint8_t* drow = sdS + (r >> 3) * 1024 + (r & 7) * 128;
+    for (int j = 0; j < n_kv; ++j) {
+      mbar_wait(sdp_full, j & 1);
+      tc_fence_after();
+      uint32_t pk[T / 2];
+      const int kbase = j * T;
+      const bool diag = (j == qt);
+#pragma unroll
+      for (int c = 0; c < T / 32; ++c) {
+        uint32_t sv[32], dv[32];
+        tmem_ld_32x32b_x32(tS + lane_off + c * 32, sv);
+        tmem_ld_32x32b_x32(tP + lane_off + c * 32, dv);
+        tmem_wait_ld();
+#pragma unroll
+        for (int i = 0; i < 32; i += 2) {
+          float d2[2];
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const int col = kbase + c * 32 + i + e;
+            float p = ex2(__uint_as_float(sv[i + e]) * a.scale_log2 - lse2);
+            if ((diag && col > qrow) || col >= a.s || !vrow) p = 0.f;
+            d2[e] = p * (__uint_as_float(dv[i + e]) - Dv);
+          }
+          pk[(c * 32 + i) >> 1] = pack2(d2[0], d2[1]);
+        }
+      }
+      tc_fence_before();
+      mbar_arrive(sdp_empty);
+      if (j > 0) mbar_wait(dq_done, (j - 1) & 1);  // previous dQ MMA done reading dS smem
+#pragma unroll
+      for (int c = 0; c < T / 8; ++c) {
+        uint4 u = make_uint4(pk[c * 4], pk[c * 4 + 1], pk[c * 4 + 2], pk[c * 4 + 3]);
+        const int atom = c >> 3, ch = c & 7;
+        *reinterpret_cast<uint4*>(drow + atom * ATOM + ((ch ^ (r & 7)) << 4)) = u;
+      }
+      fence_proxy_async();
+      tc_fence_before();
+      mbar_arrive(ds_full);
+    }
+    mbar_wait(dq_done, (n_kv - 1) & 1);
+    tc_fence_after();
+    bf16* orow = reinterpret_cast<bf16*>(a.dq) + (int64_t)(vrow ? qrow : 0) * a.ldd + (int64_t)h * D;
+#pragma unroll 1
+    for (int c = 0; c < D / 32; ++c) {
+      uint32_t v[32];
+      tmem_ld_32x32b_x32(tQ + lane_off + c * 32, v);
+      tmem_wait_ld();
+      if (vrow) {
+#pragma unroll
+        for (int i = 0; i < 32; i += 8) {
+          uint4 u;
+          u.x = pack2(__uint_as_float(v[i]) * a.scale, __uint_as_float(v[i + 1]) * a.scale);
+          u.y = pack2(__uint_as_float(v[i + 2]) * a.scale, __uint_as_float(v[i + 3]) * a.scale);
+          u.z = pack2(__uint_as_float(v[i + 4]) * a.scale, __uint_as_float(v[i + 5]) * a.scale);
+          u.w = pack2(__uint_as_float(v[i + 6]) * a.scale, __uint_as_float(v[i + 7]) * a.scale);
+          *reinterpret_cast<uint4*>(orow + c * 32 + i) = u;
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc<512>(tmem);
+  }
+}
+
+// dK/dV kernel: one CTA per (key tile, query head); loop over query tiles
+// i >= j: S^T = K Q_i^T, dP^T = V dO_i^T (TMEM); P^T, dS^T = P^T (dP^T - D)
+// (bf16 -> smem, one thread per key row); dV += P^T dO_i, dK += dS^T Q_i
+// (TMEM).  fp32 partials per query head; attn_bwd_reduce sums the group.
+constexpr int KV_SMEM = 1024 + 6 * TILE_BYTES + 2 * T * 4 + 256;  // K, V, Q, dO, P^T, dS^T, lse/D tiles
+
+__global__ void __launch_bounds__(256, 1)
+    attn_bwd_dkdv_sm100(const __grid_constant__ CUtensorMap tm_qkv, const __grid_constant__ CUtensorMap tm_do,
+                        const BwdArgs a) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sK = smem;
+  uint8_t* sV = smem + TILE_BYTES;
+  uint8_t* sQ = smem + 2 * TILE_BYTES;
+  uint8_t* sdO = smem + 3 * TILE_BYTES;
+  uint8_t* sP = smem + 4 * TILE_BYTES;
+  uint8_t* sdS = smem + 5 * TILE_BYTES;
+  float* s_lse = reinterpret_cast<float*>(smem + 6 * TILE_BYTES);
+  float* s_D = s_lse + T;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(s_D + T);
+  uint64_t* kv_full = bar + 0;
+  uint64_t* qdo_full = bar + 1;
+  uint64_t* qdo_empty = bar + 2;
+  uint64_t* sdp_full = bar + 3;
+  uint64_t* sdp_empty = bar + 4;
+  uint64_t* pds_full = bar + 5;
+  uint64_t* pds_free = bar + 6;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 8);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nt = (a.s + T - 1) / T;
+  const int kt = gridDim.x - 1 - blockIdx.x;  // key tile; low tiles (most query tiles) first
+  const int h = blockIdx.y;
+  const int grp = a.nq / a.nkv, g = h / grp;
+  const int n_q = nt - kt;
+  const int qcol = h * D, kcol = a.nq * D + g * D, vcol = (a.nq + a.nkv) * D + g * D;
+
+  if (threadIdx.x == 0) {
+    mbar_init(kv_full, 1);
+    mbar_init(qdo_full, 1);
+    mbar_init(qdo_empty, 1);
+    mbar_init(sdp_full, 1);
+    mbar_init(sdp_empty, 128);
+    mbar_init(pds_full, 128);
+    mbar_init(pds_free, 1);
+    fence_barrier_init();
+    tma_prefetch_desc(&tm_qkv);
+    tma_prefetch_desc(&tm_do);
+  }
+  if (warp == 2) tmem_alloc<512>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t tdV = tmem, tdK = tmem + 128, tS = tmem + 256, tP = tmem + 384;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      mbar_arrive_expect_tx(kv_full, 2 * TILE_BYTES);
+      tma_load_2d(sK, &tm_qkv, kv_full, kcol, kt * T);
+      tma_load_2d(sK + ATOM, &tm_qkv, kv_full, kcol + 64, kt * T);
+      tma_load_2d(sV, &tm_qkv, kv_full, vcol, kt * T);
+      tma_load_2d(sV + ATOM, &tm_qkv, kv_full, vcol + 64, kt * T);
+      for (int it = 0; it < n_q; ++it) {
+        const int qi = kt + it;
+        mbar_wait(qdo_empty, (it & 1) ^ 1);
+        mbar_arrive_expect_tx(qdo_full, 2 * TILE_BYTES);
+        tma_load_2d(sQ, &tm_qkv, qdo_full, qcol, qi * T);
+        tma_load_2d(sQ + ATOM, &tm_qkv, qdo_full, qcol + 64, qi * T);
+        tma_load_2d(sdO, &tm_do, qdo_full, h * D, qi * T);
+        tma_load_2d(sdO + ATOM, &tm_do, qdo_full, h * D + 64, qi * T);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t idKK = make_idesc_bf16(T, T, false, false);
+      constexpr uint32_t idMN = make_idesc_bf16(T, D, false, true);
+      const uint32_t k_addr = smem_u32(sK), v_addr = smem_u32(sV), q_addr = smem_u32(sQ), do_addr = smem_u32(sdO);
+      const uint32_t p_addr = smem_u32(sP), ds_addr = smem_u32(sdS);
+      mbar_wait(kv_full, 0);
+      for (int it = 0; it < n_q; ++it) {
+        mbar_wait(qdo_full, it & 1);
+        mbar_wait(sdp_empty, (it & 1) ^ 1);
+        tc_fence_after();
+#pragma unroll
+        for (int kk = 0; kk < D / 16; ++kk) {
+          const uint32_t off = (kk >> 2) * ATOM + (kk & 3) * 32;
+          mma_f16_ss(tS, make_sw128_desc(k_addr + off, 16, 1024), make_sw128_desc(q_addr + off, 16, 1024), idKK,
+                     kk > 0 ? 1u : 0u);
+        }
+#pragma unroll
+        for (int kk = 0; kk < D / 16; ++kk) {
+          const uint32_t off = (kk >> 2) * ATOM + (kk & 3) * 32;
+          mma_f16_ss(tP, make_sw128_desc(v_addr + off, 16, 1024), make_sw128_desc(do_addr + off, 16, 1024), idKK,
+                     kk > 0 ? 1u : 0u);
+        }
+        mma_commit(sdp_full);
+        mbar_wait(pds_full, it & 1);
+        tc_fence_after();
+#pragma unroll
+        for (int kk = 0; kk < T / 16; ++kk) {  // K dim = query rows of the tile
+          const uint32_t aoff = (kk >> 2) * ATOM + (kk & 3) * 32;
+          mma_f16_ss(tdV, make_sw128_desc(p_addr + aoff, 16, 1024), make_sw128_desc(do_addr + kk * 2048, ATOM, 1024),
+                     idMN, (it > 0 || kk > 0) ? 1u : 0u);
+        }
+#pragma unroll
+        for (int kk = 0; kk < T / 16; ++kk) {
+          const uint32_t aoff = (kk >> 2) * ATOM + (kk & 3) * 32;
+          mma_f16_ss(tdK, make_sw128_desc(ds_addr + aoff, 16, 1024), make_sw128_desc(q_addr + kk * 2048, ATOM, 1024),
+                     idMN, (it > 0 || kk > 0) ? 1u : 0u);
+        }
+        mma_commit(qdo_empty);
+        mma_commit(pds_free);
+      }
+    }
+  } else if (warp >= 4) {
+    const int r = (warp - 4) * 32 + lane;  // key row within the tile
+    const uint32_t lane_off = (uint32_t)((warp - 4) * 32) << 16;
+    const int krow = kt * T + r;
+    const bool vrow = krow < a.s;
+    uint8_t* prow = sP + (r >> 3) * 1024 + (r & 7) * 128;
+    uint8_t* drow = sdS + (r >> 3) * 1024 + (r & 7) * 128;
+    for (int it = 0; it < n_q; ++it) {
+      const int qi = kt + it;
+      const int qbase = qi * T;
+      named_bar(1, 128);  // everyone is done reading the previous tile's lse / D
+      {
+        const int q = qbase + r;
+        s_lse[r] = q < a.s ? a.lse[(int64_t)h * a.s + q] * 1.4426950408889634f : INFINITY;
+        s_D[r] = q < a.s ? a.Dl[(int64_t)h * a.s + q] : 0.f;
+      }
+      named_bar(1, 128);
+      mbar_wait(sdp_full, it & 1);
+      tc_fence_after();
+      uint32_t pp[T / 2], pd[T / 2];
+      const bool diag = (qi == kt);
+#pragma unroll
+      for (int c = 0; c < T / 32; ++c) {
+        uint32_t sv[32], dv[32];
+        tmem_ld_32x32b_x32(tS + lane_off + c * 32, sv);
+        tmem_ld_32x32b_x32(tP + lane_off + c * 32, dv);
+        tmem_wait_ld();
+#pragma unroll
+        for (int i = 0; i < 32; i += 2) {
+          float p2[2], d2[2];
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const int qc = c * 32 + i + e;
+            float p = ex2(__uint_as_float(sv[i + e]) * a.scale_log2 - s_lse[qc]);
+            if ((diag && qbase + qc < krow) || !vrow) p = 0.f;
+            p2[e] = p;
+            d2[e] = p * (__uint_as_float(dv[i + e]) - s_D[qc]);
+          }
+          pp[(c * 32 + i) >> 1] = pack2(p2[0], p2[1]);
+          pd[(c * 32 + i) >> 1] = pack2(d2[0], d2[1]);
+        }
+      }
+      tc_fence_before();
+      mbar_arrive(sdp_empty);
+      if (it > 0) mbar_wait(pds_free, (it - 1) & 1);
+#pragma unroll
+      for (int c = 0; c < T / 8; ++c) {
+        const int atom = c >> 3, ch = c & 7;
+        const int off = atom * ATOM + ((ch ^ (r & 7)) << 4);
+        *reinterpret_cast<uint4*>(prow + off) = make_uint4(pp[c * 4], pp[c * 4 + 1], pp[c * 4 + 2], pp[c * 4 + 3]);
+        *reinterpret_cast<uint4*>(drow + off) = make_uint4(pd[c * 4], pd[c * 4 + 1], pd[c * 4 + 2], pd[c * 4 + 3]);
+      }
+      fence_proxy_async();
+      tc_fence_before();
+      mbar_arrive(pds_full);
+    }
+    mbar_wait(pds_free, (n_q - 1) & 1);
+    tc_fence_after();
+    float* kr = a.dk_part + ((int64_t)h * a.s + (vrow ? krow : 0)) * D;
+    float* vr = a.dv_part + ((int64_t)h * a.s + (vrow ? krow : 0)) * D;
+#pragma unroll 1
+    for (int c = 0; c < D / 32; ++c) {
+      uint32_t v[32], k[32];
+      tmem_ld_32x32b_x32(tdV + lane_off + c * 32, v);
+      tmem_ld_32x32b_x32(tdK + lane_off + c * 32, k);
+      tmem_wait_ld();
+      if (vrow) {
+#pragma unroll
+        for (int i = 0; i < 32; i += 4) {
+          *reinterpret_cast<float4*>(vr + c * 32 + i) =
+              make_float4(__uint_as_float(v[i]), __uint_as_float(v[i + 1]), __uint_as_float(v[i + 2]),
+                          __uint_as_float(v[i + 3]));
+          *reinterpret_cast<float4*>(kr + c * 32 + i) =
+              make_float4(__uint_as_float(k[i]) * a.scale, __uint_as_float(k[i + 1]) * a.scale,
+                          __uint_as_float(k[i + 2]) * a.scale, __uint_as_float(k[i + 3]) * a.scale);
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc<512>(tmem);
+  }
+}
+
+// dk/dv (bf16, kv-head columns of dqkv) = sum over the group's query heads.
+__global__ void attn_bwd_reduce(int s, int nq, int nkv, const float* __restrict__ dk_part,
+                                const float* __restrict__ dv_part, bf16* dk, bf16* dv, int64_t ldd) {
+  const int grp = nq / nkv;
+  const int64_t total = (int64_t)s * nkv * (D / 4);
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int c4 = (int)(i % (D / 4)) * 4;
+    const int64_t t2 = i / (D / 4);
+    const int g = (int)(t2 % nkv);
+    const int64_t row = t2 / nkv;
+    float4 sk = make_float4(0.f, 0.f, 0.f, 0.f), sv = sk;
+    for (int hh = 0; hh < grp; ++hh) {
+      const int64_t off = ((int64_t)(g * grp + hh) * s + row) * D + c4;
+      const float4 a = *reinterpret_cast<const float4*>(dk_part + off);
+      const float4 b = *reinterpret_cast<const float4*>(dv_part + off);
+      sk.x += a.x; sk.y += a.y; sk.z += a.z; sk.w += a.w;
+      sv.x += b.x; sv.y += b.y; sv.z += b.z; sv.w += b.w;
+    }
+    bf16* kd = dk + row * ldd + (int64_t)g * D + c4;
+    bf16* vd = dv + row * ldd + (int64_t)g * D + c4;
+    *reinterpret_cast<uint2*>(kd) = make_uint2(pack2(sk.x, sk.y), pack2(sk.z, sk.w));
+    *reinterpret_cast<uint2*>(vd) = make_uint2(pack2(sv.x, sv.y), pack2(sv.z, sv.w));
+  }
+}
+
 }  // namespace
 
 // Used by attention.cu for d == 128, bf16.
@@ -303,4 +745,49 @@ stp_status attn_fwd_sm100_launch(int s, int nq, int nkv, const void* qkv_base, i
   return STP_OK;
 }
 
+}  // namespace stp
+
+namespace stp {
+// dq/dk/dv for d == 128 bf16 with the fused [q | k | v] layout; ws: fp32
+// [nq*s] D (already computed) followed by dk/dv partials [2, nq, s, 128].
+stp_status attn_bwd_sm100_launch(int s, int nq, int nkv, const void* qkv_base, int64_t ld, const void* dout,
+                                 int64_t ldo, const float* lse, const float* Dl, void* dq_base, int64_t ldd,
+                                 float* part, cudaStream_t st) {
+  CUtensorMap tq, td;
+  STP_TRY(tensor_map_bf16(&tq, qkv_base, ld, s, ld, 64, T));
+  STP_TRY(tensor_map_bf16(&td, dout, ldo, s, ldo, 64, T));
+  static bool attr = false;
+  if (!attr) {
+    STP_CUDA_TRY(cudaFuncSetAttribute(attn_bwd_dq_sm100, cudaFuncAttributeMaxDynamicSharedMemorySize, DQ_SMEM));
+    STP_CUDA_TRY(cudaFuncSetAttribute(attn_bwd_dkdv_sm100, cudaFuncAttributeMaxDynamicSharedMemorySize, KV_SMEM));
+    attr = true;
+  }
+  BwdArgs a;
+  a.s = s;
+  a.nq = nq;
+  a.nkv = nkv;
+  a.lse = lse;
+  a.Dl = Dl;
+  a.dq = dq_base;
+  a.ldd = ldd;
+  a.dk_part = part;
+  a.dv_part = part + (int64_t)nq * s * D;
+  a.scale = 1.f / sqrtf((float)D);
+  a.scale_log2 = 1.4426950408889634f * a.scale;
+  const int nt = (s + T - 1) / T;
+  attn_bwd_dkdv_sm100<<<dim3(nt, nq), 256, KV_SMEM, st>>>(tq, td, a);
+  count_launch();
+  STP_LAUNCH_CHECK();
+  attn_bwd_dq_sm100<<<dim3(nt, nq), 256, DQ_SMEM, st>>>(tq, td, a);
+  count_launch();
+  STP_LAUNCH_CHECK();
+  bf16* dk = reinterpret_cast<bf16*>(dq_base) + (int64_t)nq * D;
+  bf16* dv = dk + (int64_t)nkv * D;
+  const int64_t total = (int64_t)s * nkv * (D / 4);
+  const int grid = (int)std::min<int64_t>((total + 255) / 256, 16 * num_sms());
+  attn_bwd_reduce<<<grid, 256, 0, st>>>(s, nq, nkv, a.dk_part, a.dv_part, dk, dv, ldd);
+  count_launch();
+  STP_LAUNCH_CHECK();
+  return STP_OK;
+}
 }  // namespace stp

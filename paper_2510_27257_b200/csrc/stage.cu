@@ -661,6 +661,11 @@ stp_status run_step(stp_stage* S, float* h_loss, stp_step_stats* stats) {
   STP_CUDA_TRY(cudaEventRecord(S->ev_base, S->s_comp));
   STP_CUDA_TRY(cudaStreamWaitEvent(S->s_comm, S->ev_base, 0));
   const int n = (int)S->units.size();
+  struct Pending {
+    int c, mb;
+    cudaEvent_t ev;
+  };
+  std::vector<Pending> pending;
   for (int i = 0; i < n; ++i) {
     const stp_unit& u = S->units[i];
     cudaStream_t st = stream_of(S, i, u);
@@ -688,7 +693,14 @@ stp_status run_step(stp_stage* S, float* h_loss, stp_step_stats* stats) {
     if (u.op == STP_U_CB && S->pb_pending) {
       STP_CUDA_TRY(cudaEventRecord(S->ev_pb, st));
     }
-    if (is_last_w(S, u)) release(S, u.chunk, u.mb, S->ev_done[i]);
+    // a slot is released once its last W unit is enqueued, but only at the
+    // end of that action: the action's backward PP send (emitted after the W
+    // units of a full backward) still reads the slot and adds its event.
+    if (is_last_w(S, u)) pending.push_back({u.chunk, u.mb, S->ev_done[i]});
+    if (!pending.empty() && (i + 1 == n || S->units[i + 1].action != u.action)) {
+      for (auto& pr : pending) release(S, pr.c, pr.mb, pr.ev);
+      pending.clear();
+    }
     S->trace.push_back(u);
   }
   // end of step: TP all-reduce of the replicated gamma gradients, add to grads

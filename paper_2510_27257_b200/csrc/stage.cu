@@ -174,6 +174,7 @@ struct stp_stage {
   std::vector<stp_unit> trace;
   std::vector<float> t_start, t_end;
   int gemm_max_ctas = 0;
+  bool debug = false;
   int64_t launches_step = 0;
   int64_t peak_bytes = 0;
 };
@@ -685,6 +686,12 @@ stp_status run_step(stp_stage* S, float* h_loss, stp_step_stats* stats) {
       return r;
     }
     STP_CUDA_TRY(cudaEventRecord(S->ev_done[i], st));
+    if (S->debug) {  // STP_DEBUG=1: log every unit and run it to completion
+      fprintf(stderr, "[stp pp%d tp%d] unit %d/%d a%d s%d op%d l%d c%d mb%d dep%d\n", S->pp_rank, S->tp_rank, i, n,
+              u.action, u.stream, u.op, u.layer, u.chunk, u.mb, u.dep0);
+      cudaError_t e = cudaStreamSynchronize(st);
+      if (e != cudaSuccess) return fail(STP_ECUDA, std::string("debug sync: ") + cudaGetErrorString(e));
+    }
     if (S->timing) STP_CUDA_TRY(cudaEventRecord(S->ev_t1[i], st));
     // comm phases consuming the partial buffers release them for the next writer
     if (u.op == STP_U_CF && S->pf_pending) {
@@ -1086,6 +1093,7 @@ stp_status stp_init_stage(const stp_model_cfg* mc, const stp_parallel_cfg* pc, c
   STP_CUDA_TRY(cudaEventCreateWithFlags(&S->ev_pf, cudaEventDisableTiming));
   STP_CUDA_TRY(cudaEventCreateWithFlags(&S->ev_pb, cudaEventDisableTiming));
   if (const char* e = getenv("STP_GEMM_MAX_CTAS")) S->gemm_max_ctas = atoi(e);
+  S->debug = getenv("STP_DEBUG") != nullptr;
   STP_TRY(init_nccl(S.get(), world_nccl_id));
   for (auto& kv : S->c_send) {
     cudaStream_t st;

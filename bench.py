@@ -35,6 +35,8 @@ sys.path.insert(0, ROOT)
 
 import numpy as np  # noqa: E402
 
+import paper_2510_27257_b200  # noqa: E402,F401  (sets CUDA_DEVICE_MAX_CONNECTIONS before CUDA init)
+
 METRIC = "tokens/s per step at TP×PP on 1–8 B200; exposed TP-comm %; PP bubble rate"
 GRID = {1: (1, 1), 2: (2, 1), 4: (2, 2), 8: (4, 2)}
 

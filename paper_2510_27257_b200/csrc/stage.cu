@@ -839,6 +839,13 @@ stp_status init_nccl(stp_stage* S, const void* uid) {
   const int world = S->t * S->p;
   if (world == 1) return STP_OK;
   if (!uid) return fail(STP_EINVAL, "world_nccl_id required when tp*pp > 1");
+  {
+    const char* c = getenv("CUDA_DEVICE_MAX_CONNECTIONS");
+    if (!c || atoi(c) < 16)
+      return fail(STP_EUNSUPPORTED,
+                  "set CUDA_DEVICE_MAX_CONNECTIONS>=16 (32 recommended) before CUDA initialises: with the default 8 "
+                  "hardware queues a spinning NCCL recv can serialise the matching send (deadlock)");
+  }
   ncclUniqueId id;
   memcpy(&id, uid, sizeof(id));
   setenv("NCCL_RUNTIME_CONNECT", "0", 0);  // connect at init (see warmup_comms)

@@ -10,6 +10,7 @@ import sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
+import paper_2510_27257_b200  # noqa: E402,F401  (sets CUDA_DEVICE_MAX_CONNECTIONS before CUDA init)
 import torch  # noqa: E402
 import torch.distributed as dist  # noqa: E402
 

@@ -32,7 +32,7 @@ constexpr int T = 128;             // query rows per CTA = key rows per tile
 constexpr int D = 128;             // head dim
 constexpr int TILE_BYTES = T * D * 2;  // 32 KB: two 16 KB SW128 atoms (64 columns each)
 constexpr int ATOM = T * 64 * 2;       // 16 KB
-constexpr int SMEM_BYTES = 1024 + 6 * TILE_BYTES + 256;  // Q, K0, K1, V0, V1, P + barriers
+constexpr int SMEM_BYTES = 1024 + 7 * TILE_BYTES + 256;  // Q, K0, K1, V0, V1, P0, P1 + barriers
 
 struct FwdArgs {
   int s, nq, nkv;
@@ -60,8 +60,8 @@ __global__ void __launch_bounds__(256, 1)
   uint8_t* sQ = smem;
   uint8_t* sK = smem + TILE_BYTES;          // 2 buffers
   uint8_t* sV = smem + 3 * TILE_BYTES;      // 2 buffers
-  uint8_t* sP = smem + 5 * TILE_BYTES;
-  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + 6 * TILE_BYTES);
+  uint8_t* sP = smem + 5 * TILE_BYTES;      // 2 buffers
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + 7 * TILE_BYTES);
   uint64_t* q_full = bar + 0;
   uint64_t* k_full = bar + 1;   // [2]
   uint64_t* k_empty = bar + 3;  // [2]
@@ -69,9 +69,9 @@ __global__ void __launch_bounds__(256, 1)
   uint64_t* v_empty = bar + 7;  // [2]
   uint64_t* s_full = bar + 9;   // [2]
   uint64_t* s_empty = bar + 11; // [2]
-  uint64_t* p_full = bar + 13;
-  uint64_t* o_done = bar + 14;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 16);
+  uint64_t* p_full = bar + 13;  // [2]
+  uint64_t* o_done = bar + 15;  // [2]: PV of tiles with j % 2 == b done
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 18);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nqt = gridDim.x;
@@ -90,9 +90,9 @@ __global__ void __launch_bounds__(256, 1)
       mbar_init(v_empty + i, 1);
       mbar_init(s_full + i, 1);
       mbar_init(s_empty + i, 128);
+      mbar_init(p_full + i, 128);
+      mbar_init(o_done + i, 1);
     }
-    mbar_init(p_full, 128);
-    mbar_init(o_done, 1);
     fence_barrier_init();
     tma_prefetch_desc(&tm_qkv);
   }
@@ -129,18 +129,19 @@ __global__ void __launch_bounds__(256, 1)
       mbar_wait(q_full, 0);
       auto issue_pv = [&](int jj) {
         const int b = jj & 1;
-        mbar_wait(p_full, jj & 1);
+        mbar_wait(p_full + b, (jj >> 1) & 1);
         mbar_wait(v_full + b, (jj >> 1) & 1);
         tc_fence_after();
         const uint32_t v_addr = smem_u32(sV + b * TILE_BYTES);
+        const uint32_t pb_addr = p_addr + b * TILE_BYTES;
 #pragma unroll
         for (int kk = 0; kk < T / 16; ++kk) {
-          const uint64_t ad = make_sw128_desc(p_addr + (kk >> 2) * ATOM + (kk & 3) * 32, 16, 1024);
+          const uint64_t ad = make_sw128_desc(pb_addr + (kk >> 2) * ATOM + (kk & 3) * 32, 16, 1024);
           const uint64_t bd = make_sw128_desc(v_addr + kk * 2048, ATOM, 1024);
           mma_f16_ss(tO, ad, bd, idO, (jj > 0 || kk > 0) ? 1u : 0u);
         }
         mma_commit(v_empty + b);
-        mma_commit(o_done);
+        mma_commit(o_done + b);
       };
       for (int j = 0; j < n_kv; ++j) {
         const int b = j & 1;
@@ -167,19 +168,19 @@ __global__ void __launch_bounds__(256, 1)
     const uint32_t lane_off = (uint32_t)((warp - 4) * 32) << 16;
     const int qrow = qt * T + r;
     float m = -INFINITY, l = 0.f;
-    uint8_t* prow = sP + (r >> 3) * 1024 + (r & 7) * 128;
+    uint8_t* prow0 = sP + (r >> 3) * 1024 + (r & 7) * 128;
     for (int j = 0; j < n_kv; ++j) {
       const int b = j & 1;
       mbar_wait(s_full + b, (j >> 1) & 1);
       tc_fence_after();
       float sv[T];
+      {
+        uint32_t v[T];
 #pragma unroll
-      for (int c = 0; c < T / 32; ++c) {
-        uint32_t v[32];
-        tmem_ld_32x32b_x32(tS0 + b * 128 + lane_off + c * 32, v);
+        for (int c = 0; c < T / 32; ++c) tmem_ld_32x32b_x32(tS0 + b * 128 + lane_off + c * 32, v + c * 32);
         tmem_wait_ld();
 #pragma unroll
-        for (int i = 0; i < 32; ++i) sv[c * 32 + i] = __uint_as_float(v[i]);
+        for (int i = 0; i < T; ++i) sv[i] = __uint_as_float(v[i]);
       }
       tc_fence_before();
       mbar_arrive(s_empty + b);
@@ -194,8 +195,6 @@ __global__ void __launch_bounds__(256, 1)
         sv[i] = x;
         mx = fmaxf(mx, x);
       }
-      // P_{j-1} consumed and O stable before touching P smem / O
-      if (j > 0) mbar_wait(o_done, (j - 1) & 1);
       // rescale O and l to a new max only when it grew by > 2^8 (first tile:
       // m = -inf); tcgen05.ld/st are warp-collective, so the branch is
       // warp-uniform and rows that keep their max use alpha = 1
@@ -208,6 +207,8 @@ __global__ void __launch_bounds__(256, 1)
           m = mx;
         }
         if (j > 0) {
+          // O must be stable: every PV up to j-1 has completed
+          mbar_wait(o_done + ((j - 1) & 1), ((j - 1) >> 1) & 1);
           tc_fence_after();
 #pragma unroll 1
           for (int c = 0; c < D / 32; ++c) {
@@ -220,8 +221,11 @@ __global__ void __launch_bounds__(256, 1)
           }
           tmem_wait_st();
         }
+      } else if (j >= 2) {
+        mbar_wait(o_done + b, ((j - 2) >> 1) & 1);  // P buffer b free (PV j-2 done)
       }
       // P = exp2(x - m) -> bf16, K-major SW128 smem layout (two 64-col atoms)
+      uint8_t* prow = prow0 + b * TILE_BYTES;
 #pragma unroll
       for (int c = 0; c < T / 8; ++c) {
         float p[8];
@@ -240,10 +244,10 @@ __global__ void __launch_bounds__(256, 1)
       }
       fence_proxy_async();  // generic-proxy smem writes -> visible to the tensor core
       tc_fence_before();
-      mbar_arrive(p_full);
+      mbar_arrive(p_full + b);
     }
-    // epilogue: O / l
-    mbar_wait(o_done, (n_kv - 1) & 1);
+    // epilogue: O / l once the last PV (and therefore all) completed
+    mbar_wait(o_done + ((n_kv - 1) & 1), ((n_kv - 1) >> 1) & 1);
     tc_fence_after();
     // every lane loads (tcgen05.ld is warp-collective); rows >= s skip the store
     const bool valid = qrow < a.s;

@@ -33,7 +33,7 @@ def main():
     torch.cuda.set_device(local)
     dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     from paper_2510_27257_b200.stage import Stage, broadcast_nccl_id
-    cfg = dataclasses.replace(si.TINY, seq=a.seq, n_kv_heads=max(2, a.tp))
+    cfg = dataclasses.replace(si.TINY, seq=a.seq, n_kv_heads=max(2, a.tp), ffn=176 if a.tp <= 2 else 192)
     lay = [int(x) for x in a.layers.split(",")] if a.layers else [1] * (2 * a.pp if a.sched != "1f1b" else a.pp)
     cfg = dataclasses.replace(cfg, n_layers=sum(lay))
     P, toks, tgts, ref_loss, G = oracle_reference(cfg, a.n_micro)

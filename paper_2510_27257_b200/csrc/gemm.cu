@@ -30,6 +30,7 @@ constexpr int BK = 64;
 constexpr int kSmemBudget = 192 * 1024;
 
 struct GemmArgs {
+  int* tile_ctr;  // dynamic tile scheduler counter (0 at launch; reset by the last fetch)
   int M, N, K;
   int num_m_blk, num_n_blk, num_k_blk;
   int epilogue;
@@ -45,7 +46,7 @@ struct Cfg {
   static constexpr int A_BYTES = BM * BK * 2;
   static constexpr int B_BYTES = BN * BK * 2;
   static constexpr int STAGES = kSmemBudget / (A_BYTES + B_BYTES);
-  static constexpr int SMEM = STAGES * (A_BYTES + B_BYTES) + 1024 + 256;
+  static constexpr int SMEM = STAGES * (A_BYTES + B_BYTES) + 1024 + 512;
   static constexpr int TMEM_COLS = 2 * BN;
 };
 
@@ -125,7 +126,10 @@ __global__ void __launch_bounds__(256, 1)
   uint64_t* empty = full + C::STAGES;
   uint64_t* tfull = empty + C::STAGES;
   uint64_t* tempty = tfull + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint64_t* ring_full = tempty + 2;   // [4] tile-id ring (dynamic scheduler)
+  uint64_t* ring_empty = ring_full + 4;
+  int* ring = reinterpret_cast<int*>(ring_empty + 4);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(ring + 4);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -139,6 +143,10 @@ __global__ void __launch_bounds__(256, 1)
       mbar_init(tfull + a, 1);
       mbar_init(tempty + a, 4);
     }
+    for (int r = 0; r < 4; ++r) {
+      mbar_init(ring_full + r, 1);
+      mbar_init(ring_empty + r, 5);  // MMA lane + 4 epilogue warps
+    }
     fence_barrier_init();
     tma_prefetch_desc(&tmA);
     tma_prefetch_desc(&tmB);
@@ -150,11 +158,23 @@ __global__ void __launch_bounds__(256, 1)
   const uint32_t tmem_base = *tmem_slot;
 
   const int num_tiles = p.num_m_blk * p.num_n_blk;
+  // Dynamic persistent scheduling: the producer lane fetches tile ids from a
+  // global atomic counter and hands them to the MMA and epilogue roles via a
+  // 4-deep smem ring.  CTAs that start late (SMs busy with communication
+  // kernels of the braid) simply take fewer tiles -- no static tail.
   if (warp == 0) {
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
-      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+      for (int it = 0;; ++it) {
+        const int rs = it & 3;
+        mbar_wait(ring_empty + rs, ((it >> 2) & 1) ^ 1);
+        const int got = atomicAdd(p.tile_ctr, 1);
+        if (got == num_tiles + (int)gridDim.x - 1) atomicExch(p.tile_ctr, 0);  // last fetch of the launch
+        const int tile = got < num_tiles ? got : -1;
+        ring[rs] = tile;
+        mbar_arrive(ring_full + rs);
+        if (tile < 0) break;
         const int mb = tile % p.num_m_blk, nb = tile / p.num_m_blk;
         for (int kb = 0; kb < p.num_k_blk; ++kb) {
           mbar_wait(empty + stage, phase ^ 1);
@@ -185,8 +205,12 @@ __global__ void __launch_bounds__(256, 1)
       constexpr uint32_t idesc = make_idesc_bf16(BM, BN, A_MN, B_MN);
       int stage = 0;
       uint32_t phase = 0;
-      int local = 0;
-      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++local) {
+      for (int local = 0;; ++local) {
+        const int rs = local & 3;
+        mbar_wait(ring_full + rs, (local >> 2) & 1);
+        const int tile = ring[rs];
+        mbar_arrive(ring_empty + rs);
+        if (tile < 0) break;
         const int acc = local & 1;
         const uint32_t acc_phase = (local >> 1) & 1;
         mbar_wait(tempty + acc, acc_phase ^ 1);
@@ -216,8 +240,13 @@ __global__ void __launch_bounds__(256, 1)
     }
   } else if (warp >= 4) {
     const int ew = warp & 3;
-    int local = 0;
-    for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++local) {
+    for (int local = 0;; ++local) {
+      const int rs = local & 3;
+      mbar_wait(ring_full + rs, (local >> 2) & 1);
+      const int tile = ring[rs];
+      __syncwarp();
+      if (lane == 0) mbar_arrive(ring_empty + rs);
+      if (tile < 0) break;
       const int mb = tile % p.num_m_blk, nb = tile / p.num_m_blk;
       const int acc = local & 1;
       const uint32_t acc_phase = (local >> 1) & 1;
@@ -305,6 +334,29 @@ stp_status tensor_map(CUtensorMap* out, const void* ptr, int64_t d0, int64_t d1,
   return STP_OK;
 }
 
+// One tile counter per stream (GEMMs on one stream run in order; the last
+// fetch of each launch resets its counter to 0).
+stp_status tile_counter(cudaStream_t st, int** out) {
+  thread_local int* base = nullptr;
+  thread_local int base_dev = -1;
+  thread_local std::unordered_map<cudaStream_t, int> slots;
+  int dev = 0;
+  STP_CUDA_TRY(cudaGetDevice(&dev));
+  if (!base || base_dev != dev) {
+    STP_CUDA_TRY(cudaMalloc(&base, 1024 * sizeof(int)));
+    STP_CUDA_TRY(cudaMemset(base, 0, 1024 * sizeof(int)));
+    base_dev = dev;
+    slots.clear();
+  }
+  auto it = slots.find(st);
+  if (it == slots.end()) {
+    if (slots.size() >= 1024 / 32) return fail(STP_EUNSUPPORTED, "too many GEMM streams");
+    it = slots.emplace(st, (int)slots.size() * 32).first;  // 128-byte apart
+  }
+  *out = base + it->second;
+  return STP_OK;
+}
+
 template <int BN, bool A_MN, bool B_MN>
 stp_status launch_bf16(const GemmArgs& a, const CUtensorMap& ta, const CUtensorMap& tb, int max_ctas,
                        cudaStream_t st) {
@@ -344,6 +396,7 @@ stp_status gemm_bf16(int layout, int epi, int64_t M, int64_t N, int64_t K, const
   };
   const int BNsel = (N <= 128 || cost(128) < cost(256)) ? 128 : 256;
   GemmArgs g;
+  STP_TRY(tile_counter(st, &g.tile_ctr));
   g.M = (int)M;
   g.N = (int)N;
   g.K = (int)K;

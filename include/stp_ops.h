@@ -136,6 +136,10 @@ int32_t stp_num_sms(void);
 /* Kernels launched by this library on the calling thread since load. */
 int64_t stp_kernel_launches(void);
 
+/* Runtime tuning knobs: "gemm_mc" = 2 (2-CTA cluster GEMM with B-tile TMA
+ * multicast, default) or 0 (single-CTA GEMM).  STP_EINVAL for unknown keys. */
+stp_status stp_set_option(const char* key, int64_t value);
+
 /* ------------------------------------------------------------ profiling
  * Kernel-class profiler (calling thread): when enabled, each launch of class
  * cls (0 GEMM, 1 attention fwd, 2 attention bwd) is bracketed by CUDA events

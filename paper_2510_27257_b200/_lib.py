@@ -98,6 +98,7 @@ _SIGS = {
     "stp_op_ce_grad": (i32, [i32, i64, i64, vp, i64, vp, i64, vp, f32, vp]),
     "stp_op_colsum_acc": (i32, [i32, i64, i64, vp, i64, vp, vp]),
     "stp_op_convert": (i32, [i32, i32, i64, vp, vp, vp]),
+    "stp_set_option": (i32, [cp, i64]),
     "stp_prof_enable": (i32, [i32]),
     "stp_prof_reset": (i32, []),
     "stp_prof_read": (i32, [i32, C.POINTER(i64), C.POINTER(C.c_double), C.POINTER(C.c_double),

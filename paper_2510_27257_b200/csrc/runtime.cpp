@@ -62,9 +62,23 @@ void prof_push(int cls, double flops, double bytes, cudaEvent_t e0, cudaEvent_t 
   g_prof.recs.push_back({cls, flops, bytes, e0, e1});
 }
 
+int& gemm_mc_mode_ref();
+
 }  // namespace stp
 
 extern "C" {
+
+// Runtime tuning knobs (stp_ops.h).
+stp_status stp_set_option(const char* key, int64_t value) {
+  if (!key) return stp::fail(STP_EINVAL, "key is NULL");
+  const std::string k(key);
+  if (k == "gemm_mc") {
+    if (value != 0 && value != 2) return stp::fail(STP_EINVAL, "gemm_mc must be 0 or 2");
+    stp::gemm_mc_mode_ref() = (int)value;
+    return STP_OK;
+  }
+  return stp::fail(STP_EINVAL, "unknown option " + k);
+}
 
 // Kernel-class profiling (stp_ops.h): enable / reset / read per class.
 stp_status stp_prof_enable(int32_t on) {

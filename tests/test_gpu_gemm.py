@@ -44,9 +44,17 @@ def _shapes_for(layout, M, N, K):
     return (K, M), (K, N)
 
 
+@pytest.fixture(params=[2, 0], ids=["mc2", "mc0"])
+def gemm_mode(request):
+    from paper_2510_27257_b200 import _lib
+    _lib.call("stp_set_option", b"gemm_mc", request.param)
+    yield request.param
+    _lib.call("stp_set_option", b"gemm_mc", 0)
+
+
 @pytest.mark.parametrize("layout", [0, 1, 2])
 @pytest.mark.parametrize("MNK", SHAPES)
-def test_gemm_bf16(layout, MNK):
+def test_gemm_bf16(layout, MNK, gemm_mode):
     ops = _ops()
     M, N, K = MNK
     sa, sb = _shapes_for(layout, M, N, K)
@@ -63,7 +71,7 @@ def test_gemm_bf16(layout, MNK):
 
 
 @pytest.mark.parametrize("epi", [1, 2, 3])
-def test_gemm_bf16_epilogues(epi):
+def test_gemm_bf16_epilogues(epi, gemm_mode):
     ops = _ops()
     M, N, K = 300, 392, 256
     A, dA = _mk((M, K), 3, torch.bfloat16)
@@ -90,7 +98,7 @@ def test_gemm_bf16_epilogues(epi):
 
 
 @pytest.mark.parametrize("layout", [0, 1, 2])
-def test_gemm_bf16_max_ctas(layout):
+def test_gemm_bf16_max_ctas(layout, gemm_mode):
     ops = _ops()
     M, N, K = 1000, 712, 320
     sa, sb = _shapes_for(layout, M, N, K)

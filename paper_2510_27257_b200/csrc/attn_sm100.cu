@@ -697,6 +697,201 @@ __global__ void __launch_bounds__(256, 1)
   }
 }
 
+
+// dK/dV kernel, version 2: P^T and dS^T stay in TMEM (written over the S^T /
+// dP^T accumulators once read) and feed tcgen05.mma as the A operand, so the
+// freed shared memory double-buffers Q_i / dO_i: the loads of tile i+1
+// overlap the MMAs and softmax of tile i.  Relies on tcgen05.mma executing
+// in issue order (dV/dK of tile i read P^T/dS^T before S^T/dP^T of tile i+1
+// overwrite them).
+constexpr int KV2_SMEM = 1024 + 6 * TILE_BYTES + 4 * T * 4 + 256;  // K, V, Q[2], dO[2], lse/D[2]
+
+__global__ void __launch_bounds__(256, 1)
+    attn_bwd_dkdv_sm100_v2(const __grid_constant__ CUtensorMap tm_qkv, const __grid_constant__ CUtensorMap tm_do,
+                           const BwdArgs a) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sK = smem;
+  uint8_t* sV = smem + TILE_BYTES;
+  uint8_t* sQ = smem + 2 * TILE_BYTES;   // [2]
+  uint8_t* sdO = smem + 4 * TILE_BYTES;  // [2]
+  float* s_lse = reinterpret_cast<float*>(smem + 6 * TILE_BYTES);  // [2][T]
+  float* s_D = s_lse + 2 * T;                                       // [2][T]
+  uint64_t* bar = reinterpret_cast<uint64_t*>(s_D + 2 * T);
+  uint64_t* kv_full = bar + 0;
+  uint64_t* qdo_full = bar + 1;   // [2]
+  uint64_t* qdo_empty = bar + 3;  // [2]
+  uint64_t* sdp_full = bar + 5;
+  uint64_t* pds_full = bar + 6;
+  uint64_t* done = bar + 7;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 8);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nt = (a.s + T - 1) / T;
+  const int kt = gridDim.x - 1 - blockIdx.x;
+  const int h = blockIdx.y;
+  const int grp = a.nq / a.nkv, g = h / grp;
+  const int n_q = nt - kt;
+  const int qcol = h * D, kcol = a.nq * D + g * D, vcol = (a.nq + a.nkv) * D + g * D;
+
+  if (threadIdx.x == 0) {
+    mbar_init(kv_full, 1);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(qdo_full + i, 1);
+      mbar_init(qdo_empty + i, 1);
+    }
+    mbar_init(sdp_full, 1);
+    mbar_init(pds_full, 128);
+    mbar_init(done, 1);
+    fence_barrier_init();
+    tma_prefetch_desc(&tm_qkv);
+    tma_prefetch_desc(&tm_do);
+  }
+  if (warp == 2) tmem_alloc<512>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t tdV = tmem, tdK = tmem + 128, tS = tmem + 256, tP = tmem + 384;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      mbar_arrive_expect_tx(kv_full, 2 * TILE_BYTES);
+      tma_load_2d(sK, &tm_qkv, kv_full, kcol, kt * T);
+      tma_load_2d(sK + ATOM, &tm_qkv, kv_full, kcol + 64, kt * T);
+      tma_load_2d(sV, &tm_qkv, kv_full, vcol, kt * T);
+      tma_load_2d(sV + ATOM, &tm_qkv, kv_full, vcol + 64, kt * T);
+      for (int it = 0; it < n_q; ++it) {
+        const int b = it & 1, qi = kt + it;
+        mbar_wait(qdo_empty + b, ((it >> 1) & 1) ^ 1);
+        mbar_arrive_expect_tx(qdo_full + b, 2 * TILE_BYTES);
+        uint8_t* q = sQ + b * TILE_BYTES;
+        uint8_t* o = sdO + b * TILE_BYTES;
+        tma_load_2d(q, &tm_qkv, qdo_full + b, qcol, qi * T);
+        tma_load_2d(q + ATOM, &tm_qkv, qdo_full + b, qcol + 64, qi * T);
+        tma_load_2d(o, &tm_do, qdo_full + b, h * D, qi * T);
+        tma_load_2d(o + ATOM, &tm_do, qdo_full + b, h * D + 64, qi * T);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t idKK = make_idesc_bf16(T, T, false, false);
+      constexpr uint32_t idMN = make_idesc_bf16(T, D, false, true);
+      const uint32_t k_addr = smem_u32(sK), v_addr = smem_u32(sV);
+      mbar_wait(kv_full, 0);
+      for (int it = 0; it < n_q; ++it) {
+        const int b = it & 1;
+        const uint32_t q_addr = smem_u32(sQ + b * TILE_BYTES), do_addr = smem_u32(sdO + b * TILE_BYTES);
+        mbar_wait(qdo_full + b, (it >> 1) & 1);
+        tc_fence_after();
+#pragma unroll
+        for (int kk = 0; kk < D / 16; ++kk) {
+          const uint32_t off = (kk >> 2) * ATOM + (kk & 3) * 32;
+          mma_f16_ss(tS, make_sw128_desc(k_addr + off, 16, 1024), make_sw128_desc(q_addr + off, 16, 1024), idKK,
+                     kk > 0 ? 1u : 0u);
+        }
+#pragma unroll
+        for (int kk = 0; kk < D / 16; ++kk) {
+          const uint32_t off = (kk >> 2) * ATOM + (kk & 3) * 32;
+          mma_f16_ss(tP, make_sw128_desc(v_addr + off, 16, 1024), make_sw128_desc(do_addr + off, 16, 1024), idKK,
+                     kk > 0 ? 1u : 0u);
+        }
+        mma_commit(sdp_full);
+        mbar_wait(pds_full, it & 1);
+        tc_fence_after();
+#pragma unroll
+        for (int kk = 0; kk < T / 16; ++kk)  // dV += P^T dO_i   (P^T from TMEM, 8 columns per k16)
+          mma_f16_ts(tdV, tS + kk * 8, make_sw128_desc(do_addr + kk * 2048, ATOM, 1024), idMN,
+                     (it > 0 || kk > 0) ? 1u : 0u);
+#pragma unroll
+        for (int kk = 0; kk < T / 16; ++kk)  // dK += dS^T Q_i
+          mma_f16_ts(tdK, tP + kk * 8, make_sw128_desc(q_addr + kk * 2048, ATOM, 1024), idMN,
+                     (it > 0 || kk > 0) ? 1u : 0u);
+        mma_commit(qdo_empty + b);
+      }
+      mma_commit(done);
+    }
+  } else if (warp >= 4) {
+    const int r = (warp - 4) * 32 + lane;
+    const uint32_t lane_off = (uint32_t)((warp - 4) * 32) << 16;
+    const int krow = kt * T + r;
+    const bool vrow = krow < a.s;
+    for (int it = 0; it < n_q; ++it) {
+      const int b = it & 1, qi = kt + it;
+      const int qbase = qi * T;
+      {
+        const int q = qbase + r;
+        s_lse[b * T + r] = q < a.s ? a.lse[(int64_t)h * a.s + q] * 1.4426950408889634f : INFINITY;
+        s_D[b * T + r] = q < a.s ? a.Dl[(int64_t)h * a.s + q] : 0.f;
+      }
+      named_bar(1, 128);
+      const float* lse_t = s_lse + b * T;
+      const float* D_t = s_D + b * T;
+      mbar_wait(sdp_full, it & 1);
+      tc_fence_after();
+      uint32_t pp[T / 2], pd[T / 2];
+      const bool diag = (qi == kt);
+#pragma unroll
+      for (int c = 0; c < T / 32; ++c) {
+        uint32_t sv[32], dv[32];
+        tmem_ld_32x32b_x32(tS + lane_off + c * 32, sv);
+        tmem_ld_32x32b_x32(tP + lane_off + c * 32, dv);
+        tmem_wait_ld();
+#pragma unroll
+        for (int i = 0; i < 32; i += 2) {
+          float p2[2], d2[2];
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const int qc = c * 32 + i + e;
+            float p = ex2(__uint_as_float(sv[i + e]) * a.scale_log2 - lse_t[qc]);
+            if ((diag && qbase + qc < krow) || !vrow) p = 0.f;
+            p2[e] = p;
+            d2[e] = p * (__uint_as_float(dv[i + e]) - D_t[qc]);
+          }
+          pp[(c * 32 + i) >> 1] = pack2(p2[0], p2[1]);
+          pd[(c * 32 + i) >> 1] = pack2(d2[0], d2[1]);
+        }
+      }
+      // P^T over the S^T columns, dS^T over the dP^T columns (bf16 pairs)
+      tmem_st_32x32b_x32(tS + lane_off, pp);
+      tmem_st_32x32b_x32(tS + lane_off + 32, pp + 32);
+      tmem_st_32x32b_x32(tP + lane_off, pd);
+      tmem_st_32x32b_x32(tP + lane_off + 32, pd + 32);
+      tmem_wait_st();
+      tc_fence_before();
+      mbar_arrive(pds_full);
+    }
+    mbar_wait(done, 0);
+    tc_fence_after();
+    float* kr = a.dk_part + ((int64_t)h * a.s + (vrow ? krow : 0)) * D;
+    float* vr = a.dv_part + ((int64_t)h * a.s + (vrow ? krow : 0)) * D;
+#pragma unroll 1
+    for (int c = 0; c < D / 32; ++c) {
+      uint32_t v[32], k[32];
+      tmem_ld_32x32b_x32(tdV + lane_off + c * 32, v);
+      tmem_ld_32x32b_x32(tdK + lane_off + c * 32, k);
+      tmem_wait_ld();
+      if (vrow) {
+#pragma unroll
+        for (int i = 0; i < 32; i += 4) {
+          *reinterpret_cast<float4*>(vr + c * 32 + i) =
+              make_float4(__uint_as_float(v[i]), __uint_as_float(v[i + 1]), __uint_as_float(v[i + 2]),
+                          __uint_as_float(v[i + 3]));
+          *reinterpret_cast<float4*>(kr + c * 32 + i) =
+              make_float4(__uint_as_float(k[i]) * a.scale, __uint_as_float(k[i + 1]) * a.scale,
+                          __uint_as_float(k[i + 2]) * a.scale, __uint_as_float(k[i + 3]) * a.scale);
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc<512>(tmem);
+  }
+}
+
 // dk/dv (bf16, kv-head columns of dqkv) = sum over the group's query heads.
 __global__ void attn_bwd_reduce(int s, int nq, int nkv, const float* __restrict__ dk_part,
                                 const float* __restrict__ dv_part, bf16* dk, bf16* dv, int64_t ldd) {
@@ -752,6 +947,15 @@ stp_status attn_fwd_sm100_launch(int s, int nq, int nkv, const void* qkv_base, i
 }  // namespace stp
 
 namespace stp {
+// Tuning knob (stp_set_option "attn_bwd"): 1 = smem P^T/dS^T dK/dV kernel,
+// 2 = TMEM-resident P^T/dS^T with double-buffered Q/dO.
+int& attn_bwd_version_ref() {
+  static int v = [] {
+    const char* e = getenv("STP_ATTN_BWD");
+    return e ? atoi(e) : 1;
+  }();
+  return v;
+}
 // dq/dk/dv for d == 128 bf16 with the fused [q | k | v] layout; ws: fp32
 // [nq*s] D (already computed) followed by dk/dv partials [2, nq, s, 128].
 stp_status attn_bwd_sm100_launch(int s, int nq, int nkv, const void* qkv_base, int64_t ld, const void* dout,
@@ -764,6 +968,8 @@ stp_status attn_bwd_sm100_launch(int s, int nq, int nkv, const void* qkv_base, i
   if (!attr) {
     STP_CUDA_TRY(cudaFuncSetAttribute(attn_bwd_dq_sm100, cudaFuncAttributeMaxDynamicSharedMemorySize, DQ_SMEM));
     STP_CUDA_TRY(cudaFuncSetAttribute(attn_bwd_dkdv_sm100, cudaFuncAttributeMaxDynamicSharedMemorySize, KV_SMEM));
+    STP_CUDA_TRY(
+        cudaFuncSetAttribute(attn_bwd_dkdv_sm100_v2, cudaFuncAttributeMaxDynamicSharedMemorySize, KV2_SMEM));
     attr = true;
   }
   BwdArgs a;
@@ -779,7 +985,8 @@ stp_status attn_bwd_sm100_launch(int s, int nq, int nkv, const void* qkv_base, i
   a.scale = 1.f / sqrtf((float)D);
   a.scale_log2 = 1.4426950408889634f * a.scale;
   const int nt = (s + T - 1) / T;
-  attn_bwd_dkdv_sm100<<<dim3(nt, nq), 256, KV_SMEM, st>>>(tq, td, a);
+  if (attn_bwd_version_ref() == 2) attn_bwd_dkdv_sm100_v2<<<dim3(nt, nq), 256, KV2_SMEM, st>>>(tq, td, a);
+  else attn_bwd_dkdv_sm100<<<dim3(nt, nq), 256, KV_SMEM, st>>>(tq, td, a);
   count_launch();
   STP_LAUNCH_CHECK();
   attn_bwd_dq_sm100<<<dim3(nt, nq), 256, DQ_SMEM, st>>>(tq, td, a);

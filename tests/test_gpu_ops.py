@@ -207,3 +207,14 @@ def test_colsum(dt):
     ops.colsum_acc(dX_, acc)
     torch.cuda.synchronize()
     assert np.abs(_np(acc) - (1 + X.sum(0))).max() <= 1e-3
+
+
+@pytest.mark.parametrize("s,nq,nkv", [(257, 7, 1), (1024, 4, 2), (2048, 7, 1), (300, 2, 2)])
+def test_attention_bwd_tmem_variant(s, nq, nkv):
+    """tcgen05 dK/dV kernel v2 (P^T / dS^T in TMEM, double-buffered Q/dO)."""
+    from paper_2510_27257_b200 import _lib
+    _lib.call("stp_set_option", b"attn_bwd", 2)
+    try:
+        test_attention_fwd_bwd("bf16", s, nq, nkv, 128)
+    finally:
+        _lib.call("stp_set_option", b"attn_bwd", 1)

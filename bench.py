@@ -189,19 +189,23 @@ def ours(args):
     if args.layers:
         import dataclasses
         cfg = dataclasses.replace(cfg, n_layers=args.layers)
-    uid = broadcast_nccl_id() if world > 1 else None
-    st = Stage(cfg, tp=t, pp=p, n_micro=args.m, tp_rank=tp_rank, pp_rank=pp_rank, dtype="bf16",
-               sched=args.sched, device=local, world_nccl_id=uid)
-    # random-init weights on the device (seeded per tensor), N(0, 0.02^2); gammas 1
-    g = torch.Generator(device=f"cuda:{local}")
-    for i, (name, prm) in enumerate(zip(st.names, st.params)):
-        g.manual_seed(1000 * rank + i)
-        if name.endswith(("ln1", "ln2")) or name == "final_ln":
-            prm.fill_(1.0)
-        elif name.endswith("bqkv"):
-            prm.zero_()
-        else:
-            prm.copy_(torch.randn(prm.shape, generator=g, device=prm.device, dtype=torch.float32) * 0.02)
+    def make_stage(sched):
+        uid = broadcast_nccl_id() if world > 1 else None
+        stg = Stage(cfg, tp=t, pp=p, n_micro=args.m, tp_rank=tp_rank, pp_rank=pp_rank, dtype="bf16",
+                    sched=sched, device=local, world_nccl_id=uid)
+        # random-init weights on the device (seeded per tensor), N(0, 0.02^2); gammas 1
+        g = torch.Generator(device=f"cuda:{local}")
+        for i, (name, prm) in enumerate(zip(stg.names, stg.params)):
+            g.manual_seed(1000 * rank + i)
+            if name.endswith(("ln1", "ln2")) or name == "final_ln":
+                prm.fill_(1.0)
+            elif name.endswith("bqkv"):
+                prm.zero_()
+            else:
+                prm.copy_(torch.randn(prm.shape, generator=g, device=prm.device, dtype=torch.float32) * 0.02)
+        return stg
+
+    st = make_stage(args.sched)
     toks, tgts = si.make_tokens(cfg, args.m, seed=1234)
     d_tok = torch.from_numpy(toks).cuda()
     d_tgt = torch.from_numpy(tgts).cuda()
@@ -299,8 +303,38 @@ def ours(args):
             line["cpu_baseline"] = {"value": cpu_tok, "unit": "tokens/s", "cores": cpu_cores(), "kind": "oracle",
                                     "sample": f"1 Qwen2-7B-shaped layer + LM head (V=32768), 1 x 512 tokens, "
                                               f"fwd+bwd fp64 ({dt:.1f} s), scaled by algorithmic FLOPs"}
-        print(json.dumps(line), flush=True)
     st.close()
+    if args.compare:
+        # the paper's comparison (§5, Table 1) on the same kernels: every schedule,
+        # same model / inputs / grid, W warm-up + K device-timed steps each
+        comp = {}
+        for sched in [x for x in ("stp", "1f1b-i", "1f1b-i-naive", "zb", "stp-nobraid", "stp-nosep")
+                      if x != args.sched or True]:
+            if sched.startswith("1f1b-i") and args.m % p:
+                continue
+            stc = make_stage(sched)
+            for _ in range(args.warmup):
+                stc.step(d_tok, d_tgt)
+            barrier()
+            cms = [stc.step(d_tok, d_tgt)[1].step_ms for _ in range(args.steps)]
+            stc.set_timing(True)
+            _, ts = stc.step(d_tok, d_tgt)
+            stc.close()
+            v = torch.tensor([float(np.mean(cms)), ts.exposed_tp_ms / max(ts.step_ms, 1e-9),
+                              ts.pp_bubble_ms / max(ts.step_ms, 1e-9), float(ts.peak_act_bytes)],
+                             dtype=torch.float64, device="cuda")
+            if world > 1:
+                dist.all_reduce(v, op=dist.ReduceOp.MAX)
+            cm, ce, cb, cpk = v.tolist()
+            comp[sched] = {"tokens_per_s": tokens / (cm / 1e3), "ms_per_step": cm, "exposed_tp_pct": 100 * ce,
+                           "pp_bubble_pct": 100 * cb, "stash_gb_per_rank": cpk / 1e9}
+        if rank == 0:
+            base = comp.get("1f1b-i", {}).get("tokens_per_s")
+            for k in comp:
+                comp[k]["vs_1f1b_i"] = comp[k]["tokens_per_s"] / base if base else None
+            line["schedule_comparison"] = comp
+    if rank == 0:
+        print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
     return 0
@@ -317,6 +351,8 @@ def main():
     ap.add_argument("--layers", type=int, default=0, help="override layer count (debug only)")
     ap.add_argument("--sched", default="stp")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--compare", action="store_true",
+                    help="also time 1F1B-I (+naive), ZB and the STP ablations on the same kernels")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

@@ -281,6 +281,229 @@ __global__ void __launch_bounds__(256, 1)
 }
 
 
+// Forward, version 2: P in TMEM (A operand of PV, tcgen05 ts-mode), three K/V
+// stages in the freed shared memory.
+constexpr int KV_ST = 3;
+constexpr int SMEM_BYTES_V2 = 1024 + (1 + 2 * KV_ST) * TILE_BYTES + 256;
+
+__global__ void __launch_bounds__(256, 1)
+    attn_fwd_sm100_v2(const __grid_constant__ CUtensorMap tm_qkv, const FwdArgs a) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sQ = smem;
+  uint8_t* sK = smem + TILE_BYTES;          // KV_ST buffers
+  uint8_t* sV = smem + (1 + KV_ST) * TILE_BYTES;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + (1 + 2 * KV_ST) * TILE_BYTES);
+  uint64_t* q_full = bar + 0;
+  uint64_t* k_full = bar + 1;            // [KV_ST]
+  uint64_t* k_empty = k_full + KV_ST;    // [KV_ST]
+  uint64_t* v_full = k_empty + KV_ST;    // [KV_ST]
+  uint64_t* v_empty = v_full + KV_ST;    // [KV_ST]
+  uint64_t* s_full = v_empty + KV_ST;    // [2]
+  uint64_t* s_empty = s_full + 2;        // [2]
+  uint64_t* p_full = s_empty + 2;        // [2]
+  uint64_t* o_done = p_full + 2;         // [2]: PV of tiles with j % 2 == b done
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_done + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nqt = gridDim.x;
+  const int qt = nqt - 1 - blockIdx.x;  // longest (most key tiles) first
+  const int h = blockIdx.y;
+  const int grp = a.nq / a.nkv, g = h / grp;
+  const int n_kv = qt + 1;              // causal: key tiles 0..qt
+  const int qcol = h * D, kcol = a.nq * D + g * D, vcol = (a.nq + a.nkv) * D + g * D;
+
+  if (threadIdx.x == 0) {
+    mbar_init(q_full, 1);
+    for (int i = 0; i < KV_ST; ++i) {
+      mbar_init(k_full + i, 1);
+      mbar_init(k_empty + i, 1);
+      mbar_init(v_full + i, 1);
+      mbar_init(v_empty + i, 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(s_full + i, 1);
+      mbar_init(s_empty + i, 128);
+      mbar_init(p_full + i, 128);
+      mbar_init(o_done + i, 1);
+    }
+    fence_barrier_init();
+    tma_prefetch_desc(&tm_qkv);
+  }
+  if (warp == 2) tmem_alloc<512>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t tO = tmem, tS0 = tmem + 128, tP0 = tmem + 384;  // P0 | P1: 64 columns each
+
+  if (warp == 0) {
+    if (lane == 0) {
+      mbar_arrive_expect_tx(q_full, TILE_BYTES);
+      tma_load_2d(sQ, &tm_qkv, q_full, qcol, qt * T);
+      tma_load_2d(sQ + ATOM, &tm_qkv, q_full, qcol + 64, qt * T);
+      for (int j = 0; j < n_kv; ++j) {
+        const int b = j % KV_ST;
+        const uint32_t ph = (j / KV_ST) & 1;
+        mbar_wait(k_empty + b, ph ^ 1);
+        mbar_arrive_expect_tx(k_full + b, TILE_BYTES);
+        tma_load_2d(sK + b * TILE_BYTES, &tm_qkv, k_full + b, kcol, j * T);
+        tma_load_2d(sK + b * TILE_BYTES + ATOM, &tm_qkv, k_full + b, kcol + 64, j * T);
+        mbar_wait(v_empty + b, ph ^ 1);
+        mbar_arrive_expect_tx(v_full + b, TILE_BYTES);
+        tma_load_2d(sV + b * TILE_BYTES, &tm_qkv, v_full + b, vcol, j * T);
+        tma_load_2d(sV + b * TILE_BYTES + ATOM, &tm_qkv, v_full + b, vcol + 64, j * T);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t idS = make_idesc_bf16(T, T, false, false);  // S = Q K^T
+      constexpr uint32_t idO = make_idesc_bf16(T, D, false, true);   // O += P V (V MN-major)
+      const uint32_t q_addr = smem_u32(sQ);
+      mbar_wait(q_full, 0);
+      auto issue_pv = [&](int jj) {
+        const int pb = jj & 1, vb = jj % KV_ST;
+        mbar_wait(p_full + pb, (jj >> 1) & 1);
+        mbar_wait(v_full + vb, (jj / KV_ST) & 1);
+        tc_fence_after();
+        const uint32_t v_addr = smem_u32(sV + vb * TILE_BYTES);
+#pragma unroll
+        for (int kk = 0; kk < T / 16; ++kk) {
+          const uint64_t bd = make_sw128_desc(v_addr + kk * 2048, ATOM, 1024);
+          mma_f16_ts(tO, tP0 + pb * 64 + kk * 8, bd, idO, (jj > 0 || kk > 0) ? 1u : 0u);
+        }
+        mma_commit(v_empty + vb);
+        mma_commit(o_done + pb);
+      };
+      for (int j = 0; j < n_kv; ++j) {
+        const int b = j & 1, kb = j % KV_ST;
+        const uint32_t ph = (j >> 1) & 1;
+        mbar_wait(k_full + kb, (j / KV_ST) & 1);
+        mbar_wait(s_empty + b, ph ^ 1);
+        tc_fence_after();
+        const uint32_t k_addr = smem_u32(sK + kb * TILE_BYTES);
+        const uint32_t tS = tS0 + b * 128;
+#pragma unroll
+        for (int kk = 0; kk < D / 16; ++kk) {
+          const uint64_t ad = make_sw128_desc(q_addr + (kk >> 2) * ATOM + (kk & 3) * 32, 16, 1024);
+          const uint64_t bd = make_sw128_desc(k_addr + (kk >> 2) * ATOM + (kk & 3) * 32, 16, 1024);
+          mma_f16_ss(tS, ad, bd, idS, kk > 0 ? 1u : 0u);
+        }
+        mma_commit(k_empty + kb);
+        mma_commit(s_full + b);
+        if (j > 0) issue_pv(j - 1);
+      }
+      issue_pv(n_kv - 1);
+    }
+  } else if (warp >= 4) {
+    const int r = (warp - 4) * 32 + lane;       // query row within the tile == TMEM lane
+    const uint32_t lane_off = (uint32_t)((warp - 4) * 32) << 16;
+    const int qrow = qt * T + r;
+    float m = -INFINITY, l = 0.f;
+    for (int j = 0; j < n_kv; ++j) {
+      const int b = j & 1;
+      mbar_wait(s_full + b, (j >> 1) & 1);
+      tc_fence_after();
+      float sv[T];
+      {
+        uint32_t v[T];
+#pragma unroll
+        for (int c = 0; c < T / 32; ++c) tmem_ld_32x32b_x32(tS0 + b * 128 + lane_off + c * 32, v + c * 32);
+        tmem_wait_ld();
+#pragma unroll
+        for (int i = 0; i < T; ++i) sv[i] = __uint_as_float(v[i]);
+      }
+      tc_fence_before();
+      mbar_arrive(s_empty + b);
+      // scale to the log2 domain, causal / length mask, row max
+      float mx = -INFINITY;
+      const int kbase = j * T;
+      const bool diag = (j == qt);
+#pragma unroll
+      for (int i = 0; i < T; ++i) {
+        float x = sv[i] * a.scale_log2;
+        if ((diag && kbase + i > qrow) || kbase + i >= a.s) x = -INFINITY;
+        sv[i] = x;
+        mx = fmaxf(mx, x);
+      }
+      // rescale O and l to a new max only when it grew by > 2^8 (first tile:
+      // m = -inf); tcgen05.ld/st are warp-collective, so the branch is
+      // warp-uniform and rows that keep their max use alpha = 1
+      const bool need = mx > m + 8.f;
+      if (__any_sync(0xffffffffu, need)) {
+        float alpha = 1.f;
+        if (need) {
+          alpha = (m == -INFINITY) ? 0.f : ex2(m - mx);
+          l *= alpha;
+          m = mx;
+        }
+        if (j > 0) {
+          // O must be stable: every PV up to j-1 has completed
+          mbar_wait(o_done + ((j - 1) & 1), ((j - 1) >> 1) & 1);
+          tc_fence_after();
+#pragma unroll 1
+          for (int c = 0; c < D / 32; ++c) {
+            uint32_t v[32];
+            tmem_ld_32x32b_x32(tO + lane_off + c * 32, v);
+            tmem_wait_ld();
+#pragma unroll
+            for (int i = 0; i < 32; ++i) v[i] = __float_as_uint(__uint_as_float(v[i]) * alpha);
+            tmem_st_32x32b_x32(tO + lane_off + c * 32, v);
+          }
+          tmem_wait_st();
+        }
+      } else if (j >= 2) {
+        mbar_wait(o_done + b, ((j - 2) >> 1) & 1);  // P buffer b free (PV j-2 done)
+      }
+      // P = exp2(x - m) -> bf16 pairs into TMEM buffer b (A operand of PV)
+      uint32_t pk[T / 2];
+#pragma unroll
+      for (int i = 0; i < T; i += 2) {
+        const float p0 = ex2(sv[i] - m), p1 = ex2(sv[i + 1] - m);
+        l += p0 + p1;
+        pk[i >> 1] = pack2(p0, p1);
+      }
+      tmem_st_32x32b_x32(tP0 + b * 64 + lane_off, pk);
+      tmem_st_32x32b_x32(tP0 + b * 64 + lane_off + 32, pk + 32);
+      tmem_wait_st();
+      tc_fence_before();
+      mbar_arrive(p_full + b);
+    }
+    // epilogue: O / l once the last PV (and therefore all) completed
+    mbar_wait(o_done + ((n_kv - 1) & 1), ((n_kv - 1) >> 1) & 1);
+    tc_fence_after();
+    // every lane loads (tcgen05.ld is warp-collective); rows >= s skip the store
+    const bool valid = qrow < a.s;
+    const float inv = 1.f / l;
+    bf16* orow = reinterpret_cast<bf16*>(a.o) + (int64_t)(valid ? qrow : 0) * a.ldo + (int64_t)h * D;
+#pragma unroll 1
+    for (int c = 0; c < D / 32; ++c) {
+      uint32_t v[32];
+      tmem_ld_32x32b_x32(tO + lane_off + c * 32, v);
+      tmem_wait_ld();
+      if (valid) {
+#pragma unroll
+        for (int i = 0; i < 32; i += 8) {
+          uint4 u;
+          u.x = pack2(__uint_as_float(v[i]) * inv, __uint_as_float(v[i + 1]) * inv);
+          u.y = pack2(__uint_as_float(v[i + 2]) * inv, __uint_as_float(v[i + 3]) * inv);
+          u.z = pack2(__uint_as_float(v[i + 4]) * inv, __uint_as_float(v[i + 5]) * inv);
+          u.w = pack2(__uint_as_float(v[i + 6]) * inv, __uint_as_float(v[i + 7]) * inv);
+          *reinterpret_cast<uint4*>(orow + c * 32 + i) = u;
+        }
+      }
+    }
+    if (valid) a.lse[(int64_t)h * a.s + qrow] = (m + log2f(l)) * 0.69314718055994530942f;
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc<512>(tmem);
+  }
+}
+
+
 // ---------------------------------------------------------------- backward
 // dQ kernel: one CTA per (query tile, head); loop over key tiles j <= i:
 //   S = Q K_j^T, dP = dO V_j^T (TMEM), dS = P * (dP - D) (softmax warps,
@@ -919,6 +1142,15 @@ __global__ void attn_bwd_reduce(int s, int nq, int nkv, const float* __restrict_
 
 }  // namespace
 
+// Tuning knob (stp_set_option "attn_fwd"): 1 = P via smem, 2 = P in TMEM.
+int& attn_fwd_version_ref() {
+  static int v = [] {
+    const char* e = getenv("STP_ATTN_FWD");
+    return e ? atoi(e) : 1;
+  }();
+  return v;
+}
+
 // Used by attention.cu for d == 128, bf16.
 stp_status attn_fwd_sm100_launch(int s, int nq, int nkv, const void* qkv_base, int64_t ld, void* o, int64_t ldo,
                                  float* lse, cudaStream_t st) {
@@ -938,7 +1170,16 @@ stp_status attn_fwd_sm100_launch(int s, int nq, int nkv, const void* qkv_base, i
   a.lse = lse;
   a.scale_log2 = 1.4426950408889634f / sqrtf((float)D);
   dim3 grid((s + T - 1) / T, nq);
-  attn_fwd_sm100<<<grid, 256, SMEM_BYTES, st>>>(tm, a);
+  if (attn_fwd_version_ref() == 2) {
+    static bool attr2 = false;
+    if (!attr2) {
+      STP_CUDA_TRY(cudaFuncSetAttribute(attn_fwd_sm100_v2, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES_V2));
+      attr2 = true;
+    }
+    attn_fwd_sm100_v2<<<grid, 256, SMEM_BYTES_V2, st>>>(tm, a);
+  } else {
+    attn_fwd_sm100<<<grid, 256, SMEM_BYTES, st>>>(tm, a);
+  }
   count_launch();
   STP_LAUNCH_CHECK();
   return STP_OK;

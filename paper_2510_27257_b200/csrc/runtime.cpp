@@ -64,6 +64,7 @@ void prof_push(int cls, double flops, double bytes, cudaEvent_t e0, cudaEvent_t 
 
 int& gemm_mc_mode_ref();
 int& attn_bwd_version_ref();
+int& attn_fwd_version_ref();
 
 }  // namespace stp
 
@@ -76,6 +77,11 @@ stp_status stp_set_option(const char* key, int64_t value) {
   if (k == "gemm_mc") {
     if (value != 0 && value != 2) return stp::fail(STP_EINVAL, "gemm_mc must be 0 or 2");
     stp::gemm_mc_mode_ref() = (int)value;
+    return STP_OK;
+  }
+  if (k == "attn_fwd") {
+    if (value != 1 && value != 2) return stp::fail(STP_EINVAL, "attn_fwd must be 1 or 2");
+    stp::attn_fwd_version_ref() = (int)value;
     return STP_OK;
   }
   if (k == "attn_bwd") {

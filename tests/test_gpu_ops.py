@@ -218,3 +218,14 @@ def test_attention_bwd_tmem_variant(s, nq, nkv):
         test_attention_fwd_bwd("bf16", s, nq, nkv, 128)
     finally:
         _lib.call("stp_set_option", b"attn_bwd", 1)
+
+
+@pytest.mark.parametrize("s,nq,nkv", [(257, 7, 1), (1024, 4, 2), (2048, 7, 1), (300, 2, 2)])
+def test_attention_fwd_tmem_variant(s, nq, nkv):
+    """tcgen05 forward v2 (P in TMEM as the PV A operand, 3 K/V stages)."""
+    from paper_2510_27257_b200 import _lib
+    _lib.call("stp_set_option", b"attn_fwd", 2)
+    try:
+        test_attention_fwd_bwd("bf16", s, nq, nkv, 128)
+    finally:
+        _lib.call("stp_set_option", b"attn_fwd", 1)

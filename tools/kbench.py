@@ -1,0 +1,96 @@
+"""Kernel microbenchmark at the production shapes (Qwen2-7B layer, TP = t,
+seq 6144): every GEMM of the unit set (forward NT, dgrad NN, wgrad TN with
+fp32 accumulation) and causal GQA attention fwd / bwd, timed with CUDA events
+(warm-up 3, mean of N), for each tuning-knob variant.  One JSON line per case.
+
+  python tools/kbench.py [--tp 1] [--iters 10] [--gemm-mc 0,2] [--attn-fwd 1,2] [--attn-bwd 1,2]
+"""
+import argparse
+import json
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+import paper_2510_27257_b200  # noqa: E402,F401
+import torch  # noqa: E402
+
+from paper_2510_27257_b200 import _lib, ops  # noqa: E402
+
+
+def timed(fn, iters):
+    for _ in range(3):
+        fn()
+    torch.cuda.synchronize()
+    a = torch.cuda.Event(enable_timing=True)
+    b = torch.cuda.Event(enable_timing=True)
+    a.record()
+    for _ in range(iters):
+        fn()
+    b.record()
+    torch.cuda.synchronize()
+    return a.elapsed_time(b) / iters
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--tp", type=int, default=1)
+    ap.add_argument("--seq", type=int, default=6144)
+    ap.add_argument("--iters", type=int, default=10)
+    ap.add_argument("--gemm-mc", default="0,2")
+    ap.add_argument("--attn-fwd", default="1,2")
+    ap.add_argument("--attn-bwd", default="1,2")
+    ap.add_argument("--skip-gemm", action="store_true")
+    a = ap.parse_args()
+    t, s = a.tp, a.seq
+    h, I, V = 3584, 18944 // t, 152064 // t
+    nq, nkv, d = 28 // t, 4 // t, 128
+    qkv = (nq + 2 * nkv) * d
+    bf = torch.bfloat16
+    dev = "cuda"
+    gemms = [  # name, layout, M, N, K, epilogue
+        ("qkv_fwd", 0, s, qkv, h, 0), ("o_fwd", 0, s, h, nq * d, 0), ("fc1_fwd", 0, s, 2 * I, h, 0),
+        ("fc2_fwd", 0, s, h, I, 0), ("lm_head_fwd", 0, s, V, h, 0),
+        ("fc2_dgrad", 1, s, I, h, 0), ("fc1_dgrad", 1, s, h, 2 * I, 0), ("qkv_dgrad", 1, s, h, qkv, 0),
+        ("fc2_wgrad", 2, h, I, s, 2), ("fc1_wgrad", 2, 2 * I, h, s, 2), ("qkv_wgrad", 2, qkv, h, s, 2),
+    ]
+    if not a.skip_gemm:
+        for mc in [int(x) for x in a.gemm_mc.split(",")]:
+            _lib.call("stp_set_option", b"gemm_mc", mc)
+            for name, lay, M, N, K, epi in gemms:
+                if lay == 0:
+                    A = torch.randn(M, K, device=dev, dtype=bf)
+                    B = torch.randn(N, K, device=dev, dtype=bf)
+                elif lay == 1:
+                    A = torch.randn(M, K, device=dev, dtype=bf)
+                    B = torch.randn(K, N, device=dev, dtype=bf)
+                else:
+                    A = torch.randn(K, M, device=dev, dtype=bf)
+                    B = torch.randn(K, N, device=dev, dtype=bf)
+                C = torch.zeros(M, N, device=dev, dtype=torch.float32 if epi == 2 else bf)
+                ms = timed(lambda: ops.gemm(lay, A, B, C, M, N, K, epi=epi, dtype=1), a.iters)
+                print(json.dumps({"kernel": "gemm", "name": name, "gemm_mc": mc, "M": M, "N": N, "K": K,
+                                  "ms": ms, "tflops": 2 * M * N * K / ms / 1e9}), flush=True)
+                del A, B, C
+    x = torch.randn(s, qkv, device=dev, dtype=bf)
+    o = torch.empty(s, nq * d, device=dev, dtype=bf)
+    lse = torch.empty(nq, s, device=dev, dtype=torch.float32)
+    pairs = s * (s + 1) / 2
+    for v in [int(x) for x in a.attn_fwd.split(",")]:
+        _lib.call("stp_set_option", b"attn_fwd", v)
+        ms = timed(lambda: ops.attn_fwd(x, nq, nkv, d, o, lse), a.iters)
+        print(json.dumps({"kernel": "attn_fwd", "version": v, "s": s, "nq": nq, "nkv": nkv, "ms": ms,
+                          "tflops": 4 * pairs * nq * d / ms / 1e9}), flush=True)
+    _lib.call("stp_set_option", b"attn_fwd", 1)
+    ops.attn_fwd(x, nq, nkv, d, o, lse)
+    do = torch.randn(s, nq * d, device=dev, dtype=bf)
+    dx = torch.empty_like(x)
+    for v in [int(x) for x in a.attn_bwd.split(",")]:
+        _lib.call("stp_set_option", b"attn_bwd", v)
+        ms = timed(lambda: ops.attn_bwd(x, nq, nkv, d, o, do, lse, dx), a.iters)
+        print(json.dumps({"kernel": "attn_bwd", "version": v, "s": s, "nq": nq, "nkv": nkv, "ms": ms,
+                          "tflops": 8 * pairs * nq * d / ms / 1e9}), flush=True)
+
+
+if __name__ == "__main__":
+    main()

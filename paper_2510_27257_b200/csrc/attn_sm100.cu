@@ -718,6 +718,200 @@ __global__ void __launch_bounds__(256, 1)
   }
 }
 
+// dQ kernel, version 2: dS double-buffered in TMEM (A operand of dQ += dS K).
+constexpr int DQ2_SMEM = 1024 + 6 * TILE_BYTES + 256;
+
+__global__ void __launch_bounds__(256, 1)
+    attn_bwd_dq_sm100_v2(const __grid_constant__ CUtensorMap tm_qkv, const __grid_constant__ CUtensorMap tm_do,
+                      const BwdArgs a) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sQ = smem;
+  uint8_t* sdO = smem + TILE_BYTES;
+  uint8_t* sK = smem + 2 * TILE_BYTES;  // [2]
+  uint8_t* sV = smem + 4 * TILE_BYTES;  // [2]
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + 6 * TILE_BYTES);
+  uint64_t* qdo_full = bar + 0;
+  uint64_t* k_full = bar + 1;   // [2]
+  uint64_t* k_empty = bar + 3;  // [2]
+  uint64_t* v_full = bar + 5;   // [2]
+  uint64_t* v_empty = bar + 7;  // [2]
+  uint64_t* sdp_full = bar + 9;
+  uint64_t* sdp_empty = bar + 10;
+  uint64_t* ds_full = bar + 11;   // [2]
+  uint64_t* dq_done = bar + 13;   // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 16);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int qt = gridDim.x - 1 - blockIdx.x;
+  const int h = blockIdx.y;
+  const int grp = a.nq / a.nkv, g = h / grp;
+  const int n_kv = qt + 1;
+  const int qcol = h * D, kcol = a.nq * D + g * D, vcol = (a.nq + a.nkv) * D + g * D;
+
+  if (threadIdx.x == 0) {
+    mbar_init(qdo_full, 1);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(k_full + i, 1);
+      mbar_init(k_empty + i, 1);
+      mbar_init(v_full + i, 1);
+      mbar_init(v_empty + i, 1);
+    }
+    mbar_init(sdp_full, 1);
+    mbar_init(sdp_empty, 128);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(ds_full + i, 128);
+      mbar_init(dq_done + i, 1);
+    }
+    fence_barrier_init();
+    tma_prefetch_desc(&tm_qkv);
+    tma_prefetch_desc(&tm_do);
+  }
+  if (warp == 2) tmem_alloc<512>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t tS = tmem, tP = tmem + 128, tQ = tmem + 256, tdS0 = tmem + 384;  // dS0 | dS1 (64 cols)
+
+  if (warp == 0) {
+    if (lane == 0) {
+      mbar_arrive_expect_tx(qdo_full, 2 * TILE_BYTES);
+      tma_load_2d(sQ, &tm_qkv, qdo_full, qcol, qt * T);
+      tma_load_2d(sQ + ATOM, &tm_qkv, qdo_full, qcol + 64, qt * T);
+      tma_load_2d(sdO, &tm_do, qdo_full, h * D, qt * T);
+      tma_load_2d(sdO + ATOM, &tm_do, qdo_full, h * D + 64, qt * T);
+      for (int j = 0; j < n_kv; ++j) {
+        const int b = j & 1;
+        const uint32_t ph = (j >> 1) & 1;
+        mbar_wait(k_empty + b, ph ^ 1);
+        mbar_arrive_expect_tx(k_full + b, TILE_BYTES);
+        tma_load_2d(sK + b * TILE_BYTES, &tm_qkv, k_full + b, kcol, j * T);
+        tma_load_2d(sK + b * TILE_BYTES + ATOM, &tm_qkv, k_full + b, kcol + 64, j * T);
+        mbar_wait(v_empty + b, ph ^ 1);
+        mbar_arrive_expect_tx(v_full + b, TILE_BYTES);
+        tma_load_2d(sV + b * TILE_BYTES, &tm_qkv, v_full + b, vcol, j * T);
+        tma_load_2d(sV + b * TILE_BYTES + ATOM, &tm_qkv, v_full + b, vcol + 64, j * T);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t idKK = make_idesc_bf16(T, T, false, false);  // S, dP: both operands K-major
+      constexpr uint32_t idQ = make_idesc_bf16(T, D, false, true);    // dQ += dS K (K MN-major)
+      const uint32_t q_addr = smem_u32(sQ), do_addr = smem_u32(sdO);
+      mbar_wait(qdo_full, 0);
+      auto issue_sdp = [&](int j) {
+        const int b = j & 1;
+        const uint32_t ph = (j >> 1) & 1;
+        mbar_wait(k_full + b, ph);
+        mbar_wait(v_full + b, ph);
+        tc_fence_after();
+        const uint32_t k_addr = smem_u32(sK + b * TILE_BYTES), v_addr = smem_u32(sV + b * TILE_BYTES);
+#pragma unroll
+        for (int kk = 0; kk < D / 16; ++kk) {
+          const uint32_t off = (kk >> 2) * ATOM + (kk & 3) * 32;
+          mma_f16_ss(tS, make_sw128_desc(q_addr + off, 16, 1024), make_sw128_desc(k_addr + off, 16, 1024), idKK,
+                     kk > 0 ? 1u : 0u);
+        }
+#pragma unroll
+        for (int kk = 0; kk < D / 16; ++kk) {
+          const uint32_t off = (kk >> 2) * ATOM + (kk & 3) * 32;
+          mma_f16_ss(tP, make_sw128_desc(do_addr + off, 16, 1024), make_sw128_desc(v_addr + off, 16, 1024), idKK,
+                     kk > 0 ? 1u : 0u);
+        }
+        mma_commit(v_empty + b);
+        mma_commit(sdp_full);
+      };
+      issue_sdp(0);
+      for (int j = 0; j < n_kv; ++j) {
+        if (j + 1 < n_kv) {
+          mbar_wait(sdp_empty, j & 1);  // softmax has read S/dP of tile j
+          issue_sdp(j + 1);
+        }
+        const int b = j & 1;
+        mbar_wait(ds_full + b, (j >> 1) & 1);
+        tc_fence_after();
+        const uint32_t k_addr = smem_u32(sK + b * TILE_BYTES);
+#pragma unroll
+        for (int kk = 0; kk < T / 16; ++kk) {
+          const uint64_t bd = make_sw128_desc(k_addr + kk * 2048, ATOM, 1024);
+          mma_f16_ts(tQ, tdS0 + b * 64 + kk * 8, bd, idQ, (j > 0 || kk > 0) ? 1u : 0u);
+        }
+        mma_commit(k_empty + b);
+        mma_commit(dq_done + b);
+      }
+    }
+  } else if (warp >= 4) {
+    const int r = (warp - 4) * 32 + lane;
+    const uint32_t lane_off = (uint32_t)((warp - 4) * 32) << 16;
+    const int qrow = qt * T + r;
+    const bool vrow = qrow < a.s;
+    const float lse2 = vrow ? a.lse[(int64_t)h * a.s + qrow] * 1.4426950408889634f : 0.f;
+    const float Dv = vrow ? a.Dl[(int64_t)h * a.s + qrow] : 0.f;
+    for (int j = 0; j < n_kv; ++j) {
+      mbar_wait(sdp_full, j & 1);
+      tc_fence_after();
+      uint32_t pk[T / 2];
+      const int kbase = j * T;
+      const bool diag = (j == qt);
+#pragma unroll
+      for (int c = 0; c < T / 32; ++c) {
+        uint32_t sv[32], dv[32];
+        tmem_ld_32x32b_x32(tS + lane_off + c * 32, sv);
+        tmem_ld_32x32b_x32(tP + lane_off + c * 32, dv);
+        tmem_wait_ld();
+#pragma unroll
+        for (int i = 0; i < 32; i += 2) {
+          float d2[2];
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const int col = kbase + c * 32 + i + e;
+            float p = ex2(__uint_as_float(sv[i + e]) * a.scale_log2 - lse2);
+            if ((diag && col > qrow) || col >= a.s || !vrow) p = 0.f;
+            d2[e] = p * (__uint_as_float(dv[i + e]) - Dv);
+          }
+          pk[(c * 32 + i) >> 1] = pack2(d2[0], d2[1]);
+        }
+      }
+      tc_fence_before();
+      mbar_arrive(sdp_empty);
+      const int b = j & 1;
+      if (j >= 2) mbar_wait(dq_done + b, ((j - 2) >> 1) & 1);  // dQ MMA of tile j-2 done reading dS buffer b
+      tmem_st_32x32b_x32(tdS0 + b * 64 + lane_off, pk);
+      tmem_st_32x32b_x32(tdS0 + b * 64 + lane_off + 32, pk + 32);
+      tmem_wait_st();
+      tc_fence_before();
+      mbar_arrive(ds_full + b);
+    }
+    mbar_wait(dq_done + ((n_kv - 1) & 1), ((n_kv - 1) >> 1) & 1);
+    tc_fence_after();
+    bf16* orow = reinterpret_cast<bf16*>(a.dq) + (int64_t)(vrow ? qrow : 0) * a.ldd + (int64_t)h * D;
+#pragma unroll 1
+    for (int c = 0; c < D / 32; ++c) {
+      uint32_t v[32];
+      tmem_ld_32x32b_x32(tQ + lane_off + c * 32, v);
+      tmem_wait_ld();
+      if (vrow) {
+#pragma unroll
+        for (int i = 0; i < 32; i += 8) {
+          uint4 u;
+          u.x = pack2(__uint_as_float(v[i]) * a.scale, __uint_as_float(v[i + 1]) * a.scale);
+          u.y = pack2(__uint_as_float(v[i + 2]) * a.scale, __uint_as_float(v[i + 3]) * a.scale);
+          u.z = pack2(__uint_as_float(v[i + 4]) * a.scale, __uint_as_float(v[i + 5]) * a.scale);
+          u.w = pack2(__uint_as_float(v[i + 6]) * a.scale, __uint_as_float(v[i + 7]) * a.scale);
+          *reinterpret_cast<uint4*>(orow + c * 32 + i) = u;
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc<512>(tmem);
+  }
+}
+
 // dK/dV kernel: one CTA per (key tile, query head); loop over query tiles
 // i >= j: S^T = K Q_i^T, dP^T = V dO_i^T (TMEM); P^T, dS^T = P^T (dP^T - D)
 // (bf16 -> smem, one thread per key row); dV += P^T dO_i, dK += dS^T Q_i
@@ -1211,6 +1405,7 @@ stp_status attn_bwd_sm100_launch(int s, int nq, int nkv, const void* qkv_base, i
     STP_CUDA_TRY(cudaFuncSetAttribute(attn_bwd_dkdv_sm100, cudaFuncAttributeMaxDynamicSharedMemorySize, KV_SMEM));
     STP_CUDA_TRY(
         cudaFuncSetAttribute(attn_bwd_dkdv_sm100_v2, cudaFuncAttributeMaxDynamicSharedMemorySize, KV2_SMEM));
+    STP_CUDA_TRY(cudaFuncSetAttribute(attn_bwd_dq_sm100_v2, cudaFuncAttributeMaxDynamicSharedMemorySize, DQ2_SMEM));
     attr = true;
   }
   BwdArgs a;
@@ -1230,7 +1425,8 @@ stp_status attn_bwd_sm100_launch(int s, int nq, int nkv, const void* qkv_base, i
   else attn_bwd_dkdv_sm100<<<dim3(nt, nq), 256, KV_SMEM, st>>>(tq, td, a);
   count_launch();
   STP_LAUNCH_CHECK();
-  attn_bwd_dq_sm100<<<dim3(nt, nq), 256, DQ_SMEM, st>>>(tq, td, a);
+  if (attn_bwd_version_ref() == 2) attn_bwd_dq_sm100_v2<<<dim3(nt, nq), 256, DQ2_SMEM, st>>>(tq, td, a);
+  else attn_bwd_dq_sm100<<<dim3(nt, nq), 256, DQ_SMEM, st>>>(tq, td, a);
   count_launch();
   STP_LAUNCH_CHECK();
   bf16* dk = reinterpret_cast<bf16*>(dq_base) + (int64_t)nq * D;

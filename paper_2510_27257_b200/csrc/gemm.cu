@@ -468,6 +468,160 @@ __global__ void __launch_bounds__(256, 1)
   }
 }
 
+
+// 2-SM variant (tcgen05.mma.cta_group::2): a CTA pair computes a 256 x 256
+// tile; each SM stages 128 rows of A and 128 of the 256 B columns, and one
+// thread of the even CTA issues M=256 MMAs reading both SMs' shared memory,
+// accumulating rows 0-127 in the even CTA's TMEM and 128-255 in the odd one.
+// Per SM this halves the shared-memory operand traffic per FLOP (the 1-SM
+// 128x256 tile needs ~192 B/clk of smem reads+writes at full tensor rate,
+// above the ~128 B/clk the SM provides — ncu: 64% tensor-active).
+constexpr int S2_STAGE = 2 * 128 * BK * 2;           // A half + B half per CTA: 32 KB
+constexpr int S2_STAGES = kSmemBudget / S2_STAGE;    // 6
+constexpr int S2_SMEM = S2_STAGES * S2_STAGE + 1024 + 256;
+
+template <bool A_MN, bool B_MN>
+__global__ void __launch_bounds__(256, 1)
+    gemm_bf16_sm100_2sm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                        const GemmArgs p) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  constexpr int HALF = 128 * BK * 2;  // 16 KB
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + S2_STAGES * HALF;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + S2_STAGES * S2_STAGE);
+  uint64_t* empty = full + S2_STAGES;
+  uint64_t* tfull = empty + S2_STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_ctarank();
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < S2_STAGES; ++s) {
+      mbar_init(full + s, 1);
+      mbar_init(empty + s, 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(tfull + a, 1);
+      mbar_init(tempty + a, 8);  // 4 epilogue warps x 2 CTAs (used on the even CTA)
+    }
+    fence_barrier_init();
+    tma_prefetch_desc(&tmA);
+    tma_prefetch_desc(&tmB);
+  }
+  if (warp == 2) tmem_alloc_2sm<512>(tmem_slot);
+  tc_fence_before();
+  cluster_sync();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  const int num_m2 = (p.M + 255) / 256;
+  const int num_n2 = (p.N + 255) / 256;
+  const int num_tiles = num_m2 * num_n2;
+  const int cl = blockIdx.x >> 1, ncl = gridDim.x >> 1;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      const uint32_t full0 = mapa(smem_u32(full), 0);
+      for (int tile = cl; tile < num_tiles; tile += ncl) {
+        const int m0 = (tile % num_m2) * 256 + (int)rank * 128;
+        const int n0 = (tile / num_m2) * 256 + (int)rank * 128;
+        for (int kb = 0; kb < p.num_k_blk; ++kb) {
+          mbar_wait(empty + stage, phase ^ 1);
+          if (rank == 0) mbar_arrive_expect_tx(full + stage, 2 * S2_STAGE);
+          const uint32_t fb = full0 + stage * 8;
+          uint8_t* a = sA + stage * HALF;
+          uint8_t* b = sB + stage * HALF;
+          if (!A_MN) {
+            tma_load_2d_2sm(a, &tmA, fb, kb * BK, m0);
+          } else {
+            tma_load_2d_2sm(a, &tmA, fb, m0, kb * BK);
+            tma_load_2d_2sm(a + 64 * BK * 2, &tmA, fb, m0 + 64, kb * BK);
+          }
+          if (!B_MN) {
+            tma_load_2d_2sm(b, &tmB, fb, kb * BK, n0);
+          } else {
+            tma_load_2d_2sm(b, &tmB, fb, n0, kb * BK);
+            tma_load_2d_2sm(b + 64 * BK * 2, &tmB, fb, n0 + 64, kb * BK);
+          }
+          if (++stage == S2_STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (rank == 0 && lane == 0) {
+      constexpr uint32_t idesc = make_idesc_bf16(256, 256, A_MN, B_MN);
+      int stage = 0;
+      uint32_t phase = 0;
+      int local = 0;
+      for (int tile = cl; tile < num_tiles; tile += ncl, ++local) {
+        const int acc = local & 1;
+        const uint32_t acc_phase = (local >> 1) & 1;
+        mbar_wait_cluster(tempty + acc, acc_phase ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + acc * 256;
+        for (int kb = 0; kb < p.num_k_blk; ++kb) {
+          mbar_wait(full + stage, phase);
+          tc_fence_after();
+          const uint32_t a_addr = smem_u32(sA + stage * HALF);
+          const uint32_t b_addr = smem_u32(sB + stage * HALF);
+#pragma unroll
+          for (int k = 0; k < BK / 16; ++k) {
+            const uint64_t ad = A_MN ? make_sw128_desc(a_addr + k * 2048, 64 * BK * 2, 1024)
+                                     : make_sw128_desc(a_addr + k * 32, 16, 1024);
+            const uint64_t bd = B_MN ? make_sw128_desc(b_addr + k * 2048, 64 * BK * 2, 1024)
+                                     : make_sw128_desc(b_addr + k * 32, 16, 1024);
+            mma_f16_ss_2sm(d_tmem, ad, bd, idesc, (kb | k) != 0);
+          }
+          mma_commit_2sm_mc(empty + stage, 0x3);
+          if (++stage == S2_STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        mma_commit_2sm_mc(tfull + acc, 0x3);
+      }
+    }
+  } else if (warp >= 4) {
+    const int ew = warp & 3;
+    const uint32_t tempty0 = mapa(smem_u32(tempty), 0);
+    int local = 0;
+    for (int tile = cl; tile < num_tiles; tile += ncl, ++local) {
+      const int acc = local & 1;
+      const uint32_t acc_phase = (local >> 1) & 1;
+      mbar_wait(tfull + acc, acc_phase);
+      tc_fence_after();
+      const int row = (tile % num_m2) * 256 + (int)rank * 128 + ew * 32 + lane;
+      const int nb0 = (tile / num_m2) * 256;
+#pragma unroll 1
+      for (int c0 = 0; c0 < 256; c0 += 32) {
+        uint32_t v[32];
+        tmem_ld_32x32b_x32(tmem_base + ((uint32_t)(ew * 32) << 16) + acc * 256 + c0, v);
+        tmem_wait_ld();
+        const int col = nb0 + c0;
+        if (row < p.M && col < p.N) epilogue_row32(p, row, col, v);
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cluster(tempty0 + acc * 8);
+    }
+  }
+  tc_fence_before();
+  cluster_sync();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc_2sm<512>(tmem_base);
+  }
+}
+
 // ------------------------------------------------------------ host side
 PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
@@ -618,6 +772,36 @@ namespace {
 
 int gemm_mc_mode() { return gemm_mc_mode_ref(); }
 
+template <bool A_MN, bool B_MN>
+stp_status launch_bf16_2sm(const GemmArgs& a, const CUtensorMap& ta, const CUtensorMap& tb, int max_ctas,
+                           cudaStream_t st) {
+  auto kern = gemm_bf16_sm100_2sm<A_MN, B_MN>;
+  static bool attr_done = false;
+  if (!attr_done) {
+    STP_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, S2_SMEM));
+    attr_done = true;
+  }
+  const int tiles = ((a.M + 255) / 256) * ((a.N + 255) / 256);
+  int clusters = num_sms() / 2;
+  if (max_ctas > 0 && max_ctas / 2 < clusters) clusters = std::max(1, max_ctas / 2);
+  if (tiles < clusters) clusters = tiles;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(2 * clusters);
+  cfg.blockDim = dim3(256);
+  cfg.dynamicSmemBytes = S2_SMEM;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 2;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  STP_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, ta, tb, a));
+  count_launch();
+  return STP_OK;
+}
+
 stp_status gemm_bf16(int layout, int epi, int64_t M, int64_t N, int64_t K, const void* A, int64_t lda,
                      const void* B, int64_t ldb, void* Cp, int64_t ldc, const void* bias, const void* R,
                      int64_t ldr, int max_ctas, cudaStream_t st) {
@@ -655,6 +839,19 @@ stp_status gemm_bf16(int layout, int epi, int64_t M, int64_t N, int64_t K, const
   if (!a_mn) s = tensor_map(&ta, A, K, M, lda, BK, BM);  // A [M, K]
   else s = tensor_map(&ta, A, M, K, lda, 64, BK);         // A^T stored [K, M]
   if (s != STP_OK) return s;
+  if (gemm_mc_mode() == 3 && M > 128) {
+    // 2-SM: per-CTA boxes of 128 rows (K-major) / 2 x 64 columns (MN-major)
+    CUtensorMap ta2, tb2;
+    if (!a_mn) s = tensor_map(&ta2, A, K, M, lda, BK, 128);
+    else s = tensor_map(&ta2, A, M, K, lda, 64, BK);
+    if (s != STP_OK) return s;
+    if (!b_mn) s = tensor_map(&tb2, B, K, N, ldb, BK, 128);
+    else s = tensor_map(&tb2, B, N, K, ldb, 64, BK);
+    if (s != STP_OK) return s;
+    if (!a_mn && !b_mn) return launch_bf16_2sm<false, false>(g, ta2, tb2, max_ctas, st);
+    if (!a_mn && b_mn) return launch_bf16_2sm<false, true>(g, ta2, tb2, max_ctas, st);
+    if (a_mn && b_mn) return launch_bf16_2sm<true, true>(g, ta2, tb2, max_ctas, st);
+  }
   const bool mc2 = gemm_mc_mode() == 2 && g.num_m_blk >= 2;
   // multicast variant: each CTA loads half of the B tile (K-major: BN/2 rows)
   if (!b_mn) s = tensor_map(&tb, B, K, N, ldb, BK, mc2 ? BNsel / 2 : BNsel);  // B [N, K]

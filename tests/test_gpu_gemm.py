@@ -7,6 +7,8 @@ Tolerances: bf16 output => max |err| <= 1e-2 * max |ref| and relative
 Frobenius error <= 4e-3 (bf16 rounding of the output, 2^-9 relative, with
 fp32 accumulation); fp32 => relative Frobenius error <= 1e-6.
 """
+import os
+
 import numpy as np
 import pytest
 import torch
@@ -44,7 +46,7 @@ def _shapes_for(layout, M, N, K):
     return (K, M), (K, N)
 
 
-@pytest.fixture(params=[2, 0], ids=["mc2", "mc0"])
+@pytest.fixture(params=[int(x) for x in os.environ.get("STP_TEST_GEMM_MODES", "0,2,3").split(",")], ids=lambda m: f"mode{m}")
 def gemm_mode(request):
     from paper_2510_27257_b200 import _lib
     _lib.call("stp_set_option", b"gemm_mc", request.param)

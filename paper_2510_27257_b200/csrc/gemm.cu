@@ -758,12 +758,14 @@ stp_status launch_bf16_mc2(const GemmArgs& a, const CUtensorMap& ta, const CUten
 
 }  // namespace
 
-// Tuning knob (stp_set_option "gemm_mc"): 2 = 2-CTA cluster with B multicast
-// (default), 0 = single-CTA kernel.  Env STP_GEMM_MC sets the initial value.
+// Tuning knob (stp_set_option "gemm_mc"): 1 = auto (default: 2-SM kernel unless
+// its 256x256 wave quantisation is clearly worse than the 1-SM 128xBN one),
+// 0 = 1-SM kernel, 3 = 2-SM kernel, 2 = 1-SM cluster with B multicast
+// (measured slower; kept for comparison).  Env STP_GEMM_MC sets the default.
 int& gemm_mc_mode_ref() {
   static int mode = [] {
     const char* e = getenv("STP_GEMM_MC");
-    return e ? atoi(e) : 0;  // 2 after validation
+    return e ? atoi(e) : 1;
   }();
   return mode;
 }
@@ -839,7 +841,19 @@ stp_status gemm_bf16(int layout, int epi, int64_t M, int64_t N, int64_t K, const
   if (!a_mn) s = tensor_map(&ta, A, K, M, lda, BK, BM);  // A [M, K]
   else s = tensor_map(&ta, A, M, K, lda, 64, BK);         // A^T stored [K, M]
   if (s != STP_OK) return s;
-  if (gemm_mc_mode() == 3 && M > 128) {
+  bool use_2sm = gemm_mc_mode() == 3 && M > 128;
+  if (gemm_mc_mode() == 1 && M > 128) {
+    const int nsm = (max_ctas > 0 && max_ctas < num_sms()) ? max_ctas : num_sms();
+    auto eff = [](int64_t tiles, int64_t slots) {
+      const int64_t waves = (tiles + slots - 1) / slots;
+      return (double)tiles / (double)(waves * slots);
+    };
+    const int64_t t1 = ((M + BM - 1) / BM) * ((N + BNsel - 1) / BNsel);
+    const int64_t t2 = ((M + 255) / 256) * ((N + 255) / 256);
+    // measured per-tile advantage of the 2-SM kernel ~1.1-1.25x on these shapes
+    use_2sm = eff(t2, nsm / 2) * 1.12 >= eff(t1, nsm);
+  }
+  if (use_2sm) {
     // 2-SM: per-CTA boxes of 128 rows (K-major) / 2 x 64 columns (MN-major)
     CUtensorMap ta2, tb2;
     if (!a_mn) s = tensor_map(&ta2, A, K, M, lda, BK, 128);

@@ -217,7 +217,7 @@ def test_attention_bwd_tmem_variant(s, nq, nkv):
     try:
         test_attention_fwd_bwd("bf16", s, nq, nkv, 128)
     finally:
-        _lib.call("stp_set_option", b"attn_bwd", 1)
+        _lib.call("stp_set_option", b"attn_bwd", 2)
 
 
 @pytest.mark.parametrize("s,nq,nkv", [(257, 7, 1), (1024, 4, 2), (2048, 7, 1), (300, 2, 2)])
@@ -228,4 +228,4 @@ def test_attention_fwd_tmem_variant(s, nq, nkv):
     try:
         test_attention_fwd_bwd("bf16", s, nq, nkv, 128)
     finally:
-        _lib.call("stp_set_option", b"attn_fwd", 1)
+        _lib.call("stp_set_option", b"attn_fwd", 2)

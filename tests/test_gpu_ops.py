@@ -210,10 +210,10 @@ def test_colsum(dt):
 
 
 @pytest.mark.parametrize("s,nq,nkv", [(257, 7, 1), (1024, 4, 2), (2048, 7, 1), (300, 2, 2)])
-def test_attention_bwd_tmem_variant(s, nq, nkv):
-    """tcgen05 dK/dV kernel v2 (P^T / dS^T in TMEM, double-buffered Q/dO)."""
+def test_attention_bwd_smem_variant(s, nq, nkv):
+    """tcgen05 backward v1 (P^T / dS^T staged in shared memory); v2 is the default."""
     from paper_2510_27257_b200 import _lib
-    _lib.call("stp_set_option", b"attn_bwd", 2)
+    _lib.call("stp_set_option", b"attn_bwd", 1)
     try:
         test_attention_fwd_bwd("bf16", s, nq, nkv, 128)
     finally:
@@ -221,10 +221,10 @@ def test_attention_bwd_tmem_variant(s, nq, nkv):
 
 
 @pytest.mark.parametrize("s,nq,nkv", [(257, 7, 1), (1024, 4, 2), (2048, 7, 1), (300, 2, 2)])
-def test_attention_fwd_tmem_variant(s, nq, nkv):
-    """tcgen05 forward v2 (P in TMEM as the PV A operand, 3 K/V stages)."""
+def test_attention_fwd_smem_variant(s, nq, nkv):
+    """tcgen05 forward v1 (P staged in shared memory); v2 is the default."""
     from paper_2510_27257_b200 import _lib
-    _lib.call("stp_set_option", b"attn_fwd", 2)
+    _lib.call("stp_set_option", b"attn_fwd", 1)
     try:
         test_attention_fwd_bwd("bf16", s, nq, nkv, 128)
     finally:

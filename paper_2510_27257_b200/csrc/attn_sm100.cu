@@ -53,6 +53,8 @@ __device__ __forceinline__ float ex2(float x) {
   return y;
 }
 
+__device__ __forceinline__ void named_bar(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+
 __global__ void __launch_bounds__(256, 1)
     attn_fwd_sm100(const __grid_constant__ CUtensorMap tm_qkv, const FwdArgs a) {
   extern __shared__ uint8_t smem_raw[];
@@ -504,6 +506,228 @@ __global__ void __launch_bounds__(256, 1)
 }
 
 
+
+// Forward, version 3: 8 softmax warps (two per row: warp w covers TMEM lanes
+// 32(w%4).. and S columns 64*half..), the softmax scale folded into one FFMA
+// per element (p = ex2(s*scale_log2 - m)), masking only on the diagonal /
+// ragged tile, P in TMEM (ts-mode PV), two K/V stages.  The two halves of a
+// row exchange their partial max through shared memory once per tile.
+constexpr int FWD3_THREADS = 384;
+constexpr int SMEM_BYTES_V3 = 1024 + 5 * TILE_BYTES + 3 * 2 * T * 4 + 256;
+
+__global__ void __launch_bounds__(FWD3_THREADS, 1)
+    attn_fwd_sm100_v3(const __grid_constant__ CUtensorMap tm_qkv, const FwdArgs a) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sQ = smem;
+  uint8_t* sK = smem + TILE_BYTES;      // [2]
+  uint8_t* sV = smem + 3 * TILE_BYTES;  // [2]
+  float* smax = reinterpret_cast<float*>(smem + 5 * TILE_BYTES);  // [2 tiles][2 halves][T]
+  float* ssum = smax + 4 * T;                                      // [2 halves][T]
+  uint64_t* bar = reinterpret_cast<uint64_t*>(ssum + 2 * T);
+  uint64_t* q_full = bar + 0;
+  uint64_t* k_full = bar + 1;   // [2]
+  uint64_t* k_empty = bar + 3;  // [2]
+  uint64_t* v_full = bar + 5;   // [2]
+  uint64_t* v_empty = bar + 7;  // [2]
+  uint64_t* s_full = bar + 9;   // [2]
+  uint64_t* s_empty = bar + 11; // [2]
+  uint64_t* p_full = bar + 13;  // [2]
+  uint64_t* o_done = bar + 15;  // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 18);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nqt = gridDim.x;
+  const int qt = nqt - 1 - blockIdx.x;
+  const int h = blockIdx.y;
+  const int grp = a.nq / a.nkv, g = h / grp;
+  const int n_kv = qt + 1;
+  const int qcol = h * D, kcol = a.nq * D + g * D, vcol = (a.nq + a.nkv) * D + g * D;
+
+  if (threadIdx.x == 0) {
+    mbar_init(q_full, 1);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(k_full + i, 1);
+      mbar_init(k_empty + i, 1);
+      mbar_init(v_full + i, 1);
+      mbar_init(v_empty + i, 1);
+      mbar_init(s_full + i, 1);
+      mbar_init(s_empty + i, 256);
+      mbar_init(p_full + i, 256);
+      mbar_init(o_done + i, 1);
+    }
+    fence_barrier_init();
+    tma_prefetch_desc(&tm_qkv);
+  }
+  if (warp == 2) tmem_alloc<512>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t tO = tmem, tS0 = tmem + 128, tP0 = tmem + 384;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      mbar_arrive_expect_tx(q_full, TILE_BYTES);
+      tma_load_2d(sQ, &tm_qkv, q_full, qcol, qt * T);
+      tma_load_2d(sQ + ATOM, &tm_qkv, q_full, qcol + 64, qt * T);
+      for (int j = 0; j < n_kv; ++j) {
+        const int b = j & 1;
+        const uint32_t ph = (j >> 1) & 1;
+        mbar_wait(k_empty + b, ph ^ 1);
+        mbar_arrive_expect_tx(k_full + b, TILE_BYTES);
+        tma_load_2d(sK + b * TILE_BYTES, &tm_qkv, k_full + b, kcol, j * T);
+        tma_load_2d(sK + b * TILE_BYTES + ATOM, &tm_qkv, k_full + b, kcol + 64, j * T);
+        mbar_wait(v_empty + b, ph ^ 1);
+        mbar_arrive_expect_tx(v_full + b, TILE_BYTES);
+        tma_load_2d(sV + b * TILE_BYTES, &tm_qkv, v_full + b, vcol, j * T);
+        tma_load_2d(sV + b * TILE_BYTES + ATOM, &tm_qkv, v_full + b, vcol + 64, j * T);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t idS = make_idesc_bf16(T, T, false, false);
+      constexpr uint32_t idO = make_idesc_bf16(T, D, false, true);
+      const uint32_t q_addr = smem_u32(sQ);
+      mbar_wait(q_full, 0);
+      auto issue_pv = [&](int jj) {
+        const int b = jj & 1;
+        mbar_wait(p_full + b, (jj >> 1) & 1);
+        mbar_wait(v_full + b, (jj >> 1) & 1);
+        tc_fence_after();
+        const uint32_t v_addr = smem_u32(sV + b * TILE_BYTES);
+#pragma unroll
+        for (int kk = 0; kk < T / 16; ++kk)
+          mma_f16_ts(tO, tP0 + b * 64 + kk * 8, make_sw128_desc(v_addr + kk * 2048, ATOM, 1024), idO,
+                     (jj > 0 || kk > 0) ? 1u : 0u);
+        mma_commit(v_empty + b);
+        mma_commit(o_done + b);
+      };
+      for (int j = 0; j < n_kv; ++j) {
+        const int b = j & 1;
+        const uint32_t ph = (j >> 1) & 1;
+        mbar_wait(k_full + b, ph);
+        mbar_wait(s_empty + b, ph ^ 1);
+        tc_fence_after();
+        const uint32_t k_addr = smem_u32(sK + b * TILE_BYTES);
+#pragma unroll
+        for (int kk = 0; kk < D / 16; ++kk) {
+          const uint32_t off = (kk >> 2) * ATOM + (kk & 3) * 32;
+          mma_f16_ss(tS0 + b * 128, make_sw128_desc(q_addr + off, 16, 1024), make_sw128_desc(k_addr + off, 16, 1024),
+                     idS, kk > 0 ? 1u : 0u);
+        }
+        mma_commit(k_empty + b);
+        mma_commit(s_full + b);
+        if (j > 0) issue_pv(j - 1);
+      }
+      issue_pv(n_kv - 1);
+    }
+  } else if (warp >= 4) {
+    const int half = (warp - 4) >> 2;          // S / O columns [64*half, 64*half + 64)
+    const int quad = warp & 3;                 // TMEM lanes 32*quad ..
+    const int r = quad * 32 + lane;
+    const uint32_t lane_off = (uint32_t)(quad * 32) << 16;
+    const int qrow = qt * T + r;
+    const float sl2 = a.scale_log2;
+    float m = -INFINITY, l = 0.f;
+    for (int j = 0; j < n_kv; ++j) {
+      const int b = j & 1;
+      mbar_wait(s_full + b, (j >> 1) & 1);
+      tc_fence_after();
+      uint32_t u[64];
+      tmem_ld_32x32b_x32(tS0 + b * 128 + half * 64 + lane_off, u);
+      tmem_ld_32x32b_x32(tS0 + b * 128 + half * 64 + 32 + lane_off, u + 32);
+      tmem_wait_ld();
+      tc_fence_before();
+      mbar_arrive(s_empty + b);
+      float sv[64];
+#pragma unroll
+      for (int i = 0; i < 64; ++i) sv[i] = __uint_as_float(u[i]);
+      const int cbase = j * T + half * 64;
+      if (j == qt || cbase + 64 > a.s) {  // diagonal or ragged tile: causal / length mask
+#pragma unroll
+        for (int i = 0; i < 64; ++i)
+          if (cbase + i > qrow || cbase + i >= a.s) sv[i] = -INFINITY;
+      }
+      float mx = sv[0];
+#pragma unroll
+      for (int i = 1; i < 64; ++i) mx = fmaxf(mx, sv[i]);
+      smax[(b * 2 + half) * T + r] = mx;
+      named_bar(2, 256);
+      mx = fmaxf(smax[(b * 2) * T + r], smax[(b * 2 + 1) * T + r]) * sl2;
+      const bool need = mx > m + 8.f;
+      if (__any_sync(0xffffffffu, need)) {
+        float alpha = 1.f;
+        if (need) {
+          alpha = (m == -INFINITY) ? 0.f : ex2(m - mx);
+          l *= alpha;
+          m = mx;
+        }
+        if (j > 0) {
+          mbar_wait(o_done + ((j - 1) & 1), ((j - 1) >> 1) & 1);
+          tc_fence_after();
+#pragma unroll 1
+          for (int c = 0; c < 2; ++c) {
+            uint32_t v[32];
+            const uint32_t ta = tO + half * 64 + c * 32 + lane_off;
+            tmem_ld_32x32b_x32(ta, v);
+            tmem_wait_ld();
+#pragma unroll
+            for (int i = 0; i < 32; ++i) v[i] = __float_as_uint(__uint_as_float(v[i]) * alpha);
+            tmem_st_32x32b_x32(ta, v);
+          }
+          tmem_wait_st();
+        }
+      } else if (j >= 2) {
+        mbar_wait(o_done + b, ((j - 2) >> 1) & 1);
+      }
+      const float nm = -m;
+#pragma unroll
+      for (int i = 0; i < 64; i += 2) {
+        const float p0 = ex2(fmaf(sv[i], sl2, nm)), p1 = ex2(fmaf(sv[i + 1], sl2, nm));
+        l += p0 + p1;
+        u[i >> 1] = pack2(p0, p1);
+      }
+      tmem_st_32x32b_x32(tP0 + b * 64 + half * 32 + lane_off, u);
+      tmem_wait_st();
+      tc_fence_before();
+      mbar_arrive(p_full + b);
+    }
+    ssum[half * T + r] = l;
+    named_bar(2, 256);
+    const float lt = ssum[r] + ssum[T + r];
+    mbar_wait(o_done + ((n_kv - 1) & 1), ((n_kv - 1) >> 1) & 1);
+    tc_fence_after();
+    const bool valid = qrow < a.s;
+    const float inv = 1.f / lt;
+    bf16* orow = reinterpret_cast<bf16*>(a.o) + (int64_t)(valid ? qrow : 0) * a.ldo + (int64_t)h * D + half * 64;
+#pragma unroll 1
+    for (int c = 0; c < 2; ++c) {
+      uint32_t v[32];
+      tmem_ld_32x32b_x32(tO + half * 64 + c * 32 + lane_off, v);
+      tmem_wait_ld();
+      if (valid) {
+#pragma unroll
+        for (int i = 0; i < 32; i += 8) {
+          uint4 q;
+          q.x = pack2(__uint_as_float(v[i]) * inv, __uint_as_float(v[i + 1]) * inv);
+          q.y = pack2(__uint_as_float(v[i + 2]) * inv, __uint_as_float(v[i + 3]) * inv);
+          q.z = pack2(__uint_as_float(v[i + 4]) * inv, __uint_as_float(v[i + 5]) * inv);
+          q.w = pack2(__uint_as_float(v[i + 6]) * inv, __uint_as_float(v[i + 7]) * inv);
+          *reinterpret_cast<uint4*>(orow + c * 32 + i) = q;
+        }
+      }
+    }
+    if (valid && half == 0) a.lse[(int64_t)h * a.s + qrow] = (m + log2f(lt)) * 0.69314718055994530942f;
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc<512>(tmem);
+  }
+}
+
 // ---------------------------------------------------------------- backward
 // dQ kernel: one CTA per (query tile, head); loop over key tiles j <= i:
 //   S = Q K_j^T, dP = dO V_j^T (TMEM), dS = P * (dP - D) (softmax warps,
@@ -521,7 +745,6 @@ struct BwdArgs {
   float scale_log2, scale;
 };
 
-__device__ __forceinline__ void named_bar(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
 
 __global__ void __launch_bounds__(256, 1)
     attn_bwd_dq_sm100(const __grid_constant__ CUtensorMap tm_qkv, const __grid_constant__ CUtensorMap tm_do,
@@ -1309,6 +1532,388 @@ __global__ void __launch_bounds__(256, 1)
   }
 }
 
+// Backward version 3: dQ and dK/dV kernels with 8 softmax warps (two per
+// row, 64 columns each), FFMA-folded exponent, masking only on edge tiles.
+__global__ void __launch_bounds__(384, 1)
+    attn_bwd_dq_sm100_v3(const __grid_constant__ CUtensorMap tm_qkv, const __grid_constant__ CUtensorMap tm_do,
+                      const BwdArgs a) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sQ = smem;
+  uint8_t* sdO = smem + TILE_BYTES;
+  uint8_t* sK = smem + 2 * TILE_BYTES;  // [2]
+  uint8_t* sV = smem + 4 * TILE_BYTES;  // [2]
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + 6 * TILE_BYTES);
+  uint64_t* qdo_full = bar + 0;
+  uint64_t* k_full = bar + 1;   // [2]
+  uint64_t* k_empty = bar + 3;  // [2]
+  uint64_t* v_full = bar + 5;   // [2]
+  uint64_t* v_empty = bar + 7;  // [2]
+  uint64_t* sdp_full = bar + 9;
+  uint64_t* sdp_empty = bar + 10;
+  uint64_t* ds_full = bar + 11;   // [2]
+  uint64_t* dq_done = bar + 13;   // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 16);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int qt = gridDim.x - 1 - blockIdx.x;
+  const int h = blockIdx.y;
+  const int grp = a.nq / a.nkv, g = h / grp;
+  const int n_kv = qt + 1;
+  const int qcol = h * D, kcol = a.nq * D + g * D, vcol = (a.nq + a.nkv) * D + g * D;
+
+  if (threadIdx.x == 0) {
+    mbar_init(qdo_full, 1);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(k_full + i, 1);
+      mbar_init(k_empty + i, 1);
+      mbar_init(v_full + i, 1);
+      mbar_init(v_empty + i, 1);
+    }
+    mbar_init(sdp_full, 1);
+    mbar_init(sdp_empty, 256);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(ds_full + i, 256);
+      mbar_init(dq_done + i, 1);
+    }
+    fence_barrier_init();
+    tma_prefetch_desc(&tm_qkv);
+    tma_prefetch_desc(&tm_do);
+  }
+  if (warp == 2) tmem_alloc<512>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t tS = tmem, tP = tmem + 128, tQ = tmem + 256, tdS0 = tmem + 384;  // dS0 | dS1 (64 cols)
+
+  if (warp == 0) {
+    if (lane == 0) {
+      mbar_arrive_expect_tx(qdo_full, 2 * TILE_BYTES);
+      tma_load_2d(sQ, &tm_qkv, qdo_full, qcol, qt * T);
+      tma_load_2d(sQ + ATOM, &tm_qkv, qdo_full, qcol + 64, qt * T);
+      tma_load_2d(sdO, &tm_do, qdo_full, h * D, qt * T);
+      tma_load_2d(sdO + ATOM, &tm_do, qdo_full, h * D + 64, qt * T);
+      for (int j = 0; j < n_kv; ++j) {
+        const int b = j & 1;
+        const uint32_t ph = (j >> 1) & 1;
+        mbar_wait(k_empty + b, ph ^ 1);
+        mbar_arrive_expect_tx(k_full + b, TILE_BYTES);
+        tma_load_2d(sK + b * TILE_BYTES, &tm_qkv, k_full + b, kcol, j * T);
+        tma_load_2d(sK + b * TILE_BYTES + ATOM, &tm_qkv, k_full + b, kcol + 64, j * T);
+        mbar_wait(v_empty + b, ph ^ 1);
+        mbar_arrive_expect_tx(v_full + b, TILE_BYTES);
+        tma_load_2d(sV + b * TILE_BYTES, &tm_qkv, v_full + b, vcol, j * T);
+        tma_load_2d(sV + b * TILE_BYTES + ATOM, &tm_qkv, v_full + b, vcol + 64, j * T);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t idKK = make_idesc_bf16(T, T, false, false);  // S, dP: both operands K-major
+      constexpr uint32_t idQ = make_idesc_bf16(T, D, false, true);    // dQ += dS K (K MN-major)
+      const uint32_t q_addr = smem_u32(sQ), do_addr = smem_u32(sdO);
+      mbar_wait(qdo_full, 0);
+      auto issue_sdp = [&](int j) {
+        const int b = j & 1;
+        const uint32_t ph = (j >> 1) & 1;
+        mbar_wait(k_full + b, ph);
+        mbar_wait(v_full + b, ph);
+        tc_fence_after();
+        const uint32_t k_addr = smem_u32(sK + b * TILE_BYTES), v_addr = smem_u32(sV + b * TILE_BYTES);
+#pragma unroll
+        for (int kk = 0; kk < D / 16; ++kk) {
+          const uint32_t off = (kk >> 2) * ATOM + (kk & 3) * 32;
+          mma_f16_ss(tS, make_sw128_desc(q_addr + off, 16, 1024), make_sw128_desc(k_addr + off, 16, 1024), idKK,
+                     kk > 0 ? 1u : 0u);
+        }
+#pragma unroll
+        for (int kk = 0; kk < D / 16; ++kk) {
+          const uint32_t off = (kk >> 2) * ATOM + (kk & 3) * 32;
+          mma_f16_ss(tP, make_sw128_desc(do_addr + off, 16, 1024), make_sw128_desc(v_addr + off, 16, 1024), idKK,
+                     kk > 0 ? 1u : 0u);
+        }
+        mma_commit(v_empty + b);
+        mma_commit(sdp_full);
+      };
+      issue_sdp(0);
+      for (int j = 0; j < n_kv; ++j) {
+        if (j + 1 < n_kv) {
+          mbar_wait(sdp_empty, j & 1);  // softmax has read S/dP of tile j
+          issue_sdp(j + 1);
+        }
+        const int b = j & 1;
+        mbar_wait(ds_full + b, (j >> 1) & 1);
+        tc_fence_after();
+        const uint32_t k_addr = smem_u32(sK + b * TILE_BYTES);
+#pragma unroll
+        for (int kk = 0; kk < T / 16; ++kk) {
+          const uint64_t bd = make_sw128_desc(k_addr + kk * 2048, ATOM, 1024);
+          mma_f16_ts(tQ, tdS0 + b * 64 + kk * 8, bd, idQ, (j > 0 || kk > 0) ? 1u : 0u);
+        }
+        mma_commit(k_empty + b);
+        mma_commit(dq_done + b);
+      }
+    }
+  } else if (warp >= 4) {
+    const int half = (warp - 4) >> 2, quad = warp & 3;
+    const int r = quad * 32 + lane;
+    const uint32_t lane_off = (uint32_t)(quad * 32) << 16;
+    const int qrow = qt * T + r;
+    const bool vrow = qrow < a.s;
+    const float nlse2 = vrow ? -a.lse[(int64_t)h * a.s + qrow] * 1.4426950408889634f : 0.f;
+    const float Dv = vrow ? a.Dl[(int64_t)h * a.s + qrow] : 0.f;
+    const float sl2 = a.scale_log2;
+    for (int j = 0; j < n_kv; ++j) {
+      mbar_wait(sdp_full, j & 1);
+      tc_fence_after();
+      uint32_t sv[64], dv[64];
+      tmem_ld_32x32b_x32(tS + half * 64 + lane_off, sv);
+      tmem_ld_32x32b_x32(tS + half * 64 + 32 + lane_off, sv + 32);
+      tmem_ld_32x32b_x32(tP + half * 64 + lane_off, dv);
+      tmem_ld_32x32b_x32(tP + half * 64 + 32 + lane_off, dv + 32);
+      tmem_wait_ld();
+      tc_fence_before();
+      mbar_arrive(sdp_empty);
+      const int cbase = j * T + half * 64;
+      const bool edge = (j == qt) || cbase + 64 > a.s || !vrow;
+      uint32_t pk[32];
+#pragma unroll
+      for (int i = 0; i < 64; i += 2) {
+        float d2[2];
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          float p = ex2(fmaf(__uint_as_float(sv[i + e]), sl2, nlse2));
+          if (edge && (cbase + i + e > qrow || cbase + i + e >= a.s || !vrow)) p = 0.f;
+          d2[e] = p * (__uint_as_float(dv[i + e]) - Dv);
+        }
+        pk[i >> 1] = pack2(d2[0], d2[1]);
+      }
+      const int b = j & 1;
+      if (j >= 2) mbar_wait(dq_done + b, ((j - 2) >> 1) & 1);
+      tmem_st_32x32b_x32(tdS0 + b * 64 + half * 32 + lane_off, pk);
+      tmem_wait_st();
+      tc_fence_before();
+      mbar_arrive(ds_full + b);
+    }
+    mbar_wait(dq_done + ((n_kv - 1) & 1), ((n_kv - 1) >> 1) & 1);
+    tc_fence_after();
+    bf16* orow = reinterpret_cast<bf16*>(a.dq) + (int64_t)(vrow ? qrow : 0) * a.ldd + (int64_t)h * D + half * 64;
+#pragma unroll 1
+    for (int c = 0; c < 2; ++c) {
+      uint32_t v[32];
+      tmem_ld_32x32b_x32(tQ + half * 64 + c * 32 + lane_off, v);
+      tmem_wait_ld();
+      if (vrow) {
+#pragma unroll
+        for (int i = 0; i < 32; i += 8) {
+          uint4 u;
+          u.x = pack2(__uint_as_float(v[i]) * a.scale, __uint_as_float(v[i + 1]) * a.scale);
+          u.y = pack2(__uint_as_float(v[i + 2]) * a.scale, __uint_as_float(v[i + 3]) * a.scale);
+          u.z = pack2(__uint_as_float(v[i + 4]) * a.scale, __uint_as_float(v[i + 5]) * a.scale);
+          u.w = pack2(__uint_as_float(v[i + 6]) * a.scale, __uint_as_float(v[i + 7]) * a.scale);
+          *reinterpret_cast<uint4*>(orow + c * 32 + i) = u;
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc<512>(tmem);
+  }
+}
+
+__global__ void __launch_bounds__(384, 1)
+    attn_bwd_dkdv_sm100_v3(const __grid_constant__ CUtensorMap tm_qkv, const __grid_constant__ CUtensorMap tm_do,
+                           const BwdArgs a) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sK = smem;
+  uint8_t* sV = smem + TILE_BYTES;
+  uint8_t* sQ = smem + 2 * TILE_BYTES;   // [2]
+  uint8_t* sdO = smem + 4 * TILE_BYTES;  // [2]
+  float* s_lse = reinterpret_cast<float*>(smem + 6 * TILE_BYTES);  // [2][T]
+  float* s_D = s_lse + 2 * T;                                       // [2][T]
+  uint64_t* bar = reinterpret_cast<uint64_t*>(s_D + 2 * T);
+  uint64_t* kv_full = bar + 0;
+  uint64_t* qdo_full = bar + 1;   // [2]
+  uint64_t* qdo_empty = bar + 3;  // [2]
+  uint64_t* sdp_full = bar + 5;
+  uint64_t* pds_full = bar + 6;
+  uint64_t* done = bar + 7;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 8);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nt = (a.s + T - 1) / T;
+  const int kt = gridDim.x - 1 - blockIdx.x;
+  const int h = blockIdx.y;
+  const int grp = a.nq / a.nkv, g = h / grp;
+  const int n_q = nt - kt;
+  const int qcol = h * D, kcol = a.nq * D + g * D, vcol = (a.nq + a.nkv) * D + g * D;
+
+  if (threadIdx.x == 0) {
+    mbar_init(kv_full, 1);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(qdo_full + i, 1);
+      mbar_init(qdo_empty + i, 1);
+    }
+    mbar_init(sdp_full, 1);
+    mbar_init(pds_full, 256);
+    mbar_init(done, 1);
+    fence_barrier_init();
+    tma_prefetch_desc(&tm_qkv);
+    tma_prefetch_desc(&tm_do);
+  }
+  if (warp == 2) tmem_alloc<512>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t tdV = tmem, tdK = tmem + 128, tS = tmem + 256, tP = tmem + 384;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      mbar_arrive_expect_tx(kv_full, 2 * TILE_BYTES);
+      tma_load_2d(sK, &tm_qkv, kv_full, kcol, kt * T);
+      tma_load_2d(sK + ATOM, &tm_qkv, kv_full, kcol + 64, kt * T);
+      tma_load_2d(sV, &tm_qkv, kv_full, vcol, kt * T);
+      tma_load_2d(sV + ATOM, &tm_qkv, kv_full, vcol + 64, kt * T);
+      for (int it = 0; it < n_q; ++it) {
+        const int b = it & 1, qi = kt + it;
+        mbar_wait(qdo_empty + b, ((it >> 1) & 1) ^ 1);
+        mbar_arrive_expect_tx(qdo_full + b, 2 * TILE_BYTES);
+        uint8_t* q = sQ + b * TILE_BYTES;
+        uint8_t* o = sdO + b * TILE_BYTES;
+        tma_load_2d(q, &tm_qkv, qdo_full + b, qcol, qi * T);
+        tma_load_2d(q + ATOM, &tm_qkv, qdo_full + b, qcol + 64, qi * T);
+        tma_load_2d(o, &tm_do, qdo_full + b, h * D, qi * T);
+        tma_load_2d(o + ATOM, &tm_do, qdo_full + b, h * D + 64, qi * T);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t idKK = make_idesc_bf16(T, T, false, false);
+      constexpr uint32_t idMN = make_idesc_bf16(T, D, false, true);
+      const uint32_t k_addr = smem_u32(sK), v_addr = smem_u32(sV);
+      mbar_wait(kv_full, 0);
+      for (int it = 0; it < n_q; ++it) {
+        const int b = it & 1;
+        const uint32_t q_addr = smem_u32(sQ + b * TILE_BYTES), do_addr = smem_u32(sdO + b * TILE_BYTES);
+        mbar_wait(qdo_full + b, (it >> 1) & 1);
+        tc_fence_after();
+#pragma unroll
+        for (int kk = 0; kk < D / 16; ++kk) {
+          const uint32_t off = (kk >> 2) * ATOM + (kk & 3) * 32;
+          mma_f16_ss(tS, make_sw128_desc(k_addr + off, 16, 1024), make_sw128_desc(q_addr + off, 16, 1024), idKK,
+                     kk > 0 ? 1u : 0u);
+        }
+#pragma unroll
+        for (int kk = 0; kk < D / 16; ++kk) {
+          const uint32_t off = (kk >> 2) * ATOM + (kk & 3) * 32;
+          mma_f16_ss(tP, make_sw128_desc(v_addr + off, 16, 1024), make_sw128_desc(do_addr + off, 16, 1024), idKK,
+                     kk > 0 ? 1u : 0u);
+        }
+        mma_commit(sdp_full);
+        mbar_wait(pds_full, it & 1);
+        tc_fence_after();
+#pragma unroll
+        for (int kk = 0; kk < T / 16; ++kk)  // dV += P^T dO_i   (P^T from TMEM, 8 columns per k16)
+          mma_f16_ts(tdV, tS + kk * 8, make_sw128_desc(do_addr + kk * 2048, ATOM, 1024), idMN,
+                     (it > 0 || kk > 0) ? 1u : 0u);
+#pragma unroll
+        for (int kk = 0; kk < T / 16; ++kk)  // dK += dS^T Q_i
+          mma_f16_ts(tdK, tP + kk * 8, make_sw128_desc(q_addr + kk * 2048, ATOM, 1024), idMN,
+                     (it > 0 || kk > 0) ? 1u : 0u);
+        mma_commit(qdo_empty + b);
+      }
+      mma_commit(done);
+    }
+  } else if (warp >= 4) {
+    const int half = (warp - 4) >> 2, quad = warp & 3;
+    const int r = quad * 32 + lane;           // key row
+    const int tid = threadIdx.x - 128;        // 0..255
+    const uint32_t lane_off = (uint32_t)(quad * 32) << 16;
+    const int krow = kt * T + r;
+    const bool vrow = krow < a.s;
+    const float sl2 = a.scale_log2;
+    for (int it = 0; it < n_q; ++it) {
+      const int b = it & 1, qi = kt + it;
+      const int qbase = qi * T;
+      {  // threads 0-127 stage -lse*log2e, threads 128-255 stage D, for the 128 query rows
+        const int q = qbase + (tid & 127);
+        if (tid < 128) s_lse[b * T + tid] = q < a.s ? -a.lse[(int64_t)h * a.s + q] * 1.4426950408889634f : -INFINITY;
+        else s_D[b * T + tid - 128] = q < a.s ? a.Dl[(int64_t)h * a.s + q] : 0.f;
+      }
+      named_bar(1, 256);
+      const float* nl = s_lse + b * T + half * 64;
+      const float* Dq = s_D + b * T + half * 64;
+      mbar_wait(sdp_full, it & 1);
+      tc_fence_after();
+      uint32_t sv[64], dv[64];
+      tmem_ld_32x32b_x32(tS + half * 64 + lane_off, sv);
+      tmem_ld_32x32b_x32(tS + half * 64 + 32 + lane_off, sv + 32);
+      tmem_ld_32x32b_x32(tP + half * 64 + lane_off, dv);
+      tmem_ld_32x32b_x32(tP + half * 64 + 32 + lane_off, dv + 32);
+      tmem_wait_ld();
+      const bool diag = (qi == kt);
+      uint32_t pp[32], pd[32];
+#pragma unroll
+      for (int i = 0; i < 64; i += 4) {
+        const float4 l4 = *reinterpret_cast<const float4*>(nl + i);
+        const float4 d4 = *reinterpret_cast<const float4*>(Dq + i);
+        const float la[4] = {l4.x, l4.y, l4.z, l4.w}, da[4] = {d4.x, d4.y, d4.z, d4.w};
+        float p[4], d[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          p[e] = ex2(fmaf(__uint_as_float(sv[i + e]), sl2, la[e]));
+          if (diag && qbase + half * 64 + i + e < krow) p[e] = 0.f;
+          d[e] = p[e] * (__uint_as_float(dv[i + e]) - da[e]);
+        }
+        if (!vrow) p[0] = p[1] = p[2] = p[3] = d[0] = d[1] = d[2] = d[3] = 0.f;
+        pp[i >> 1] = pack2(p[0], p[1]);
+        pp[(i >> 1) + 1] = pack2(p[2], p[3]);
+        pd[i >> 1] = pack2(d[0], d[1]);
+        pd[(i >> 1) + 1] = pack2(d[2], d[3]);
+      }
+      // P^T over the S^T columns, dS^T over the dP^T columns (bf16 pairs)
+      tmem_st_32x32b_x32(tS + half * 32 + lane_off, pp);
+      tmem_st_32x32b_x32(tP + half * 32 + lane_off, pd);
+      tmem_wait_st();
+      tc_fence_before();
+      mbar_arrive(pds_full);
+    }
+    mbar_wait(done, 0);
+    tc_fence_after();
+    float* kr = a.dk_part + ((int64_t)h * a.s + (vrow ? krow : 0)) * D + half * 64;
+    float* vr = a.dv_part + ((int64_t)h * a.s + (vrow ? krow : 0)) * D + half * 64;
+#pragma unroll 1
+    for (int c = 0; c < 2; ++c) {
+      uint32_t v[32], k[32];
+      tmem_ld_32x32b_x32(tdV + half * 64 + c * 32 + lane_off, v);
+      tmem_ld_32x32b_x32(tdK + half * 64 + c * 32 + lane_off, k);
+      tmem_wait_ld();
+      if (vrow) {
+#pragma unroll
+        for (int i = 0; i < 32; i += 4) {
+          *reinterpret_cast<float4*>(vr + c * 32 + i) =
+              make_float4(__uint_as_float(v[i]), __uint_as_float(v[i + 1]), __uint_as_float(v[i + 2]),
+                          __uint_as_float(v[i + 3]));
+          *reinterpret_cast<float4*>(kr + c * 32 + i) =
+              make_float4(__uint_as_float(k[i]) * a.scale, __uint_as_float(k[i + 1]) * a.scale,
+                          __uint_as_float(k[i + 2]) * a.scale, __uint_as_float(k[i + 3]) * a.scale);
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc<512>(tmem);
+  }
+}
+
 // dk/dv (bf16, kv-head columns of dqkv) = sum over the group's query heads.
 __global__ void attn_bwd_reduce(int s, int nq, int nkv, const float* __restrict__ dk_part,
                                 const float* __restrict__ dv_part, bf16* dk, bf16* dv, int64_t ldd) {
@@ -1364,7 +1969,14 @@ stp_status attn_fwd_sm100_launch(int s, int nq, int nkv, const void* qkv_base, i
   a.lse = lse;
   a.scale_log2 = 1.4426950408889634f / sqrtf((float)D);
   dim3 grid((s + T - 1) / T, nq);
-  if (attn_fwd_version_ref() == 2) {
+  if (attn_fwd_version_ref() == 3) {
+    static bool attr3 = false;
+    if (!attr3) {
+      STP_CUDA_TRY(cudaFuncSetAttribute(attn_fwd_sm100_v3, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES_V3));
+      attr3 = true;
+    }
+    attn_fwd_sm100_v3<<<grid, FWD3_THREADS, SMEM_BYTES_V3, st>>>(tm, a);
+  } else if (attn_fwd_version_ref() == 2) {
     static bool attr2 = false;
     if (!attr2) {
       STP_CUDA_TRY(cudaFuncSetAttribute(attn_fwd_sm100_v2, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES_V2));
@@ -1406,6 +2018,9 @@ stp_status attn_bwd_sm100_launch(int s, int nq, int nkv, const void* qkv_base, i
     STP_CUDA_TRY(
         cudaFuncSetAttribute(attn_bwd_dkdv_sm100_v2, cudaFuncAttributeMaxDynamicSharedMemorySize, KV2_SMEM));
     STP_CUDA_TRY(cudaFuncSetAttribute(attn_bwd_dq_sm100_v2, cudaFuncAttributeMaxDynamicSharedMemorySize, DQ2_SMEM));
+    STP_CUDA_TRY(cudaFuncSetAttribute(attn_bwd_dq_sm100_v3, cudaFuncAttributeMaxDynamicSharedMemorySize, DQ2_SMEM));
+    STP_CUDA_TRY(
+        cudaFuncSetAttribute(attn_bwd_dkdv_sm100_v3, cudaFuncAttributeMaxDynamicSharedMemorySize, KV2_SMEM));
     attr = true;
   }
   BwdArgs a;
@@ -1421,11 +2036,13 @@ stp_status attn_bwd_sm100_launch(int s, int nq, int nkv, const void* qkv_base, i
   a.scale = 1.f / sqrtf((float)D);
   a.scale_log2 = 1.4426950408889634f * a.scale;
   const int nt = (s + T - 1) / T;
-  if (attn_bwd_version_ref() == 2) attn_bwd_dkdv_sm100_v2<<<dim3(nt, nq), 256, KV2_SMEM, st>>>(tq, td, a);
+  if (attn_bwd_version_ref() == 3) attn_bwd_dkdv_sm100_v3<<<dim3(nt, nq), 384, KV2_SMEM, st>>>(tq, td, a);
+  else if (attn_bwd_version_ref() == 2) attn_bwd_dkdv_sm100_v2<<<dim3(nt, nq), 256, KV2_SMEM, st>>>(tq, td, a);
   else attn_bwd_dkdv_sm100<<<dim3(nt, nq), 256, KV_SMEM, st>>>(tq, td, a);
   count_launch();
   STP_LAUNCH_CHECK();
-  if (attn_bwd_version_ref() == 2) attn_bwd_dq_sm100_v2<<<dim3(nt, nq), 256, DQ2_SMEM, st>>>(tq, td, a);
+  if (attn_bwd_version_ref() == 3) attn_bwd_dq_sm100_v3<<<dim3(nt, nq), 384, DQ2_SMEM, st>>>(tq, td, a);
+  else if (attn_bwd_version_ref() == 2) attn_bwd_dq_sm100_v2<<<dim3(nt, nq), 256, DQ2_SMEM, st>>>(tq, td, a);
   else attn_bwd_dq_sm100<<<dim3(nt, nq), 256, DQ_SMEM, st>>>(tq, td, a);
   count_launch();
   STP_LAUNCH_CHECK();

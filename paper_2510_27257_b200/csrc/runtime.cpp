@@ -80,12 +80,12 @@ stp_status stp_set_option(const char* key, int64_t value) {
     return STP_OK;
   }
   if (k == "attn_fwd") {
-    if (value != 1 && value != 2) return stp::fail(STP_EINVAL, "attn_fwd must be 1 or 2");
+    if (value < 1 || value > 3) return stp::fail(STP_EINVAL, "attn_fwd must be 1, 2 or 3");
     stp::attn_fwd_version_ref() = (int)value;
     return STP_OK;
   }
   if (k == "attn_bwd") {
-    if (value != 1 && value != 2) return stp::fail(STP_EINVAL, "attn_bwd must be 1 or 2");
+    if (value < 1 || value > 3) return stp::fail(STP_EINVAL, "attn_bwd must be 1, 2 or 3");
     stp::attn_bwd_version_ref() = (int)value;
     return STP_OK;
   }

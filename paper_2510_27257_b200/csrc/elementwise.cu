@@ -8,6 +8,9 @@
 // row for the [s, h] row kernels), warp-shuffle reductions, fp32 arithmetic,
 // grids sized in multiples of the SM count.
 #include <cmath>
+#include <map>
+#include <mutex>
+#include <tuple>
 
 #include "common.h"
 
@@ -91,14 +94,24 @@ __global__ void rmsnorm_fwd_kernel(int64_t rows, int h, const T* __restrict__ x,
 }
 
 // dgamma partials accumulate in shared memory, flushed once per block.
+// dgamma[c] += sum_rows dy * x * rstd: one thread per column, a block of
+// rows per blockIdx.y (coalesced across threads), one atomic per column.
+template <typename T>
+__global__ void rmsnorm_dgamma_kernel(int64_t rows, int h, const T* __restrict__ dy, const T* __restrict__ x,
+                                      const float* __restrict__ rstd, float* dgamma, int64_t rows_per_block) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= h) return;
+  const int64_t r0 = (int64_t)blockIdx.y * rows_per_block;
+  const int64_t r1 = min(rows, r0 + rows_per_block);
+  float acc = 0.f;
+  for (int64_t r = r0; r < r1; ++r) acc += to_f<T>(dy[r * h + c]) * to_f<T>(x[r * h + c]) * rstd[r];
+  atomicAdd(&dgamma[c], acc);
+}
+
 template <typename T>
 __global__ void rmsnorm_bwd_kernel(int64_t rows, int h, const T* __restrict__ dy, const T* __restrict__ x,
                                    const T* __restrict__ g, const float* __restrict__ rstd,
                                    const T* dres, T* dx, float* dgamma) {
-  extern __shared__ float sg[];
-  if (dgamma)
-    for (int i = threadIdx.x; i < h; i += blockDim.x) sg[i] = 0.f;
-  __syncthreads();
   const int lane = threadIdx.x & 31;
   const int64_t warp0 = (int64_t)blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5);
   const int64_t nwarps = (int64_t)gridDim.x * kWarpsPerBlock;
@@ -112,10 +125,7 @@ __global__ void rmsnorm_bwd_kernel(int64_t rows, int h, const T* __restrict__ dy
       d.load(dy + r * h + c);
       gg.load(g + c);
 #pragma unroll
-      for (int i = 0; i < VN; ++i) {
-        dot += gg.f(i) * d.f(i) * a.f(i);
-        if (dgamma) atomicAdd(&sg[c + i], d.f(i) * a.f(i) * rs);
-      }
+      for (int i = 0; i < VN; ++i) dot += gg.f(i) * d.f(i) * a.f(i);
     }
     dot = warp_sum(dot) / (float)h;
     const float k = rs * rs * rs * dot;
@@ -135,39 +145,52 @@ __global__ void rmsnorm_bwd_kernel(int64_t rows, int h, const T* __restrict__ dy
       o.store(dx + r * h + c);
     }
   }
-  if (dgamma) {
-    __syncthreads();
-    for (int i = threadIdx.x; i < h; i += blockDim.x) atomicAdd(&dgamma[i], sg[i]);
-  }
+  (void)dgamma;
 }
 
 // ------------------------------------------------------------------- RoPE
-template <typename T>
-__global__ void rope_kernel(int64_t s, int64_t ld, int64_t col0, int nh, int d, double theta, int64_t pos0,
-                            int backward, T* x) {
-  const int half = d / 2;
-  const int64_t total = s * nh * half;
+// cos/sin of pos * theta^(-2j/d), j < d/2, evaluated once in fp64 per
+// (s, d, theta, pos0) and cached on the device as float2 [s][d/2].
+__global__ void rope_table_kernel(int64_t s, int half, int d, double theta, int64_t pos0, float2* tab) {
+  const int64_t total = s * half;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
     const int j = (int)(i % half);
-    const int64_t t = i / half;
-    const int hd = (int)(t % nh);
-    const int64_t row = t / nh;
+    const int64_t row = i / half;
     const double inv = pow(theta, -2.0 * (double)j / (double)d);
     double sn, cs;
     sincos((double)(pos0 + row) * inv, &sn, &cs);
-    const float c = (float)cs, sv = (float)sn;
+    tab[i] = make_float2((float)cs, (float)sn);
+  }
+}
+
+// one thread = 4 consecutive rotation pairs (j..j+3 with their partners j+d/2..)
+template <typename T>
+__global__ void rope_kernel(int64_t s, int64_t ld, int64_t col0, int nh, int d, const float2* __restrict__ tab,
+                            int backward, T* x) {
+  const int half = d / 2, q4 = half / 4;
+  const int64_t total = s * nh * q4;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int j = (int)(i % q4) * 4;
+    const int64_t t = i / q4;
+    const int hd = (int)(t % nh);
+    const int64_t row = t / nh;
     T* p = x + row * ld + col0 + (int64_t)hd * d;
-    const float x1 = to_f<T>(p[j]), x2 = to_f<T>(p[j + half]);
-    float y1, y2;
-    if (!backward) {
-      y1 = x1 * c - x2 * sv;
-      y2 = x2 * c + x1 * sv;
-    } else {
-      y1 = x1 * c + x2 * sv;
-      y2 = x2 * c - x1 * sv;
+    const float2* cs = tab + row * half + j;
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const float c = cs[e].x, sv = cs[e].y;
+      const float x1 = to_f<T>(p[j + e]), x2 = to_f<T>(p[j + e + half]);
+      float y1, y2;
+      if (!backward) {
+        y1 = x1 * c - x2 * sv;
+        y2 = x2 * c + x1 * sv;
+      } else {
+        y1 = x1 * c + x2 * sv;
+        y2 = x2 * c - x1 * sv;
+      }
+      p[j + e] = from_f<T>(y1);
+      p[j + e + half] = from_f<T>(y2);
     }
-    p[j] = from_f<T>(y1);
-    p[j + half] = from_f<T>(y2);
   }
 }
 
@@ -376,28 +399,59 @@ stp_status rmsnorm_fwd(int dtype, int64_t rows, int64_t h, const void* x, const 
 stp_status rmsnorm_bwd(int dtype, int64_t rows, int64_t h, const void* dy, const void* x, const void* g,
                        const float* rstd, const void* dres, void* dx, float* dgamma, cudaStream_t st) {
   STP_CHECK_ARG(h % 8 == 0, "hidden % 8 == 0");
-  STP_CHECK_ARG(h * 4 <= 200 * 1024, "hidden too large for the smem dgamma buffer");
   if (rows == 0) return STP_OK;
   return STP_DISPATCH_DTYPE(dtype, [&] {
-    const int grid = std::min<int64_t>(grid_for(rows, kWarpsPerBlock), 2 * num_sms());
-    const size_t sm = dgamma ? h * sizeof(float) : 0;
-    auto k = rmsnorm_bwd_kernel<T>;
-    if (sm > 48 * 1024) STP_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-    k<<<grid, 32 * kWarpsPerBlock, sm, st>>>(rows, (int)h, (const T*)dy, (const T*)x, (const T*)g, rstd,
-                                             (const T*)dres, (T*)dx, dgamma);
+    if (dgamma) {  // before dx: dx may alias dres, never dy / x
+      const int64_t rpb = 128;
+      dim3 grid2((unsigned)((h + 255) / 256), (unsigned)((rows + rpb - 1) / rpb));
+      rmsnorm_dgamma_kernel<T><<<grid2, 256, 0, st>>>(rows, (int)h, (const T*)dy, (const T*)x, rstd, dgamma, rpb);
+      count_launch();
+      STP_LAUNCH_CHECK();
+    }
+    rmsnorm_bwd_kernel<T><<<grid_for(rows, kWarpsPerBlock), 32 * kWarpsPerBlock, 0, st>>>(
+        rows, (int)h, (const T*)dy, (const T*)x, (const T*)g, rstd, (const T*)dres, (T*)dx, nullptr);
     count_launch();
     STP_LAUNCH_CHECK();
     return STP_OK;
   });
 }
 
+struct RopeKey {
+  int dev;
+  int64_t s;
+  int d;
+  float theta;
+  int64_t pos0;
+  bool operator<(const RopeKey& o) const {
+    return std::tie(dev, s, d, theta, pos0) < std::tie(o.dev, o.s, o.d, o.theta, o.pos0);
+  }
+};
+
 stp_status rope(int dtype, int backward, int64_t s, int64_t ld, int64_t col0, int nh, int d, float theta,
                 int64_t pos0, void* x, cudaStream_t st) {
-  STP_CHECK_ARG(d % 2 == 0, "head_dim even");
+  STP_CHECK_ARG(d % 8 == 0, "head_dim % 8 == 0");
   if (s == 0 || nh == 0) return STP_OK;
+  static std::mutex mu;
+  static std::map<RopeKey, float2*> tables;  // device tables, kept for the process lifetime
+  int dev = 0;
+  STP_CUDA_TRY(cudaGetDevice(&dev));
+  float2* tab = nullptr;
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    RopeKey key{dev, s, d, theta, pos0};
+    auto it = tables.find(key);
+    if (it == tables.end()) {
+      STP_CUDA_TRY(cudaMalloc(&tab, (size_t)s * (d / 2) * sizeof(float2)));
+      rope_table_kernel<<<grid_for(s * (d / 2), 256), 256, 0, st>>>(s, d / 2, d, (double)theta, pos0, tab);
+      count_launch();
+      STP_LAUNCH_CHECK();
+      tables[key] = tab;
+    } else {
+      tab = it->second;
+    }
+  }
   return STP_DISPATCH_DTYPE(dtype, [&] {
-    rope_kernel<T><<<grid_for(s * nh * (d / 2), 256), 256, 0, st>>>(s, ld, col0, nh, d, (double)theta, pos0,
-                                                                     backward, (T*)x);
+    rope_kernel<T><<<grid_for(s * nh * (d / 8), 256), 256, 0, st>>>(s, ld, col0, nh, d, tab, backward, (T*)x);
     count_launch();
     STP_LAUNCH_CHECK();
     return STP_OK;

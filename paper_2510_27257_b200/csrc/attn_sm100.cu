@@ -1945,7 +1945,7 @@ __global__ void attn_bwd_reduce(int s, int nq, int nkv, const float* __restrict_
 int& attn_fwd_version_ref() {
   static int v = [] {
     const char* e = getenv("STP_ATTN_FWD");
-    return e ? atoi(e) : 2;
+    return e ? atoi(e) : 3;
   }();
   return v;
 }
@@ -1999,7 +1999,7 @@ namespace stp {
 int& attn_bwd_version_ref() {
   static int v = [] {
     const char* e = getenv("STP_ATTN_BWD");
-    return e ? atoi(e) : 2;
+    return e ? atoi(e) : 3;
   }();
   return v;
 }

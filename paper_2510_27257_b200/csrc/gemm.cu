@@ -478,7 +478,7 @@ __global__ void __launch_bounds__(256, 1)
 // above the ~128 B/clk the SM provides — ncu: 64% tensor-active).
 constexpr int S2_STAGE = 2 * 128 * BK * 2;           // A half + B half per CTA: 32 KB
 constexpr int S2_STAGES = kSmemBudget / S2_STAGE;    // 6
-constexpr int S2_SMEM = S2_STAGES * S2_STAGE + 1024 + 256;
+constexpr int S2_SMEM = S2_STAGES * S2_STAGE + 1024 + 512;
 
 template <bool A_MN, bool B_MN>
 __global__ void __launch_bounds__(256, 1)
@@ -493,7 +493,10 @@ __global__ void __launch_bounds__(256, 1)
   uint64_t* empty = full + S2_STAGES;
   uint64_t* tfull = empty + S2_STAGES;
   uint64_t* tempty = tfull + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint64_t* ring_full = tempty + 2;  // [4] cluster tile-id ring (dynamic scheduler)
+  uint64_t* ring_empty = ring_full + 4;
+  int* ring = reinterpret_cast<int*>(ring_empty + 4);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(ring + 4);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -508,6 +511,10 @@ __global__ void __launch_bounds__(256, 1)
       mbar_init(tfull + a, 1);
       mbar_init(tempty + a, 8);  // 4 epilogue warps x 2 CTAs (used on the even CTA)
     }
+    for (int r = 0; r < 4; ++r) {
+      mbar_init(ring_full + r, 1);
+      mbar_init(ring_empty + r, 10);  // even CTA: MMA + 4 epi; odd CTA: producer + 4 epi
+    }
     fence_barrier_init();
     tma_prefetch_desc(&tmA);
     tma_prefetch_desc(&tmB);
@@ -521,14 +528,36 @@ __global__ void __launch_bounds__(256, 1)
   const int num_m2 = (p.M + 255) / 256;
   const int num_n2 = (p.N + 255) / 256;
   const int num_tiles = num_m2 * num_n2;
-  const int cl = blockIdx.x >> 1, ncl = gridDim.x >> 1;
+  const int ncl = gridDim.x >> 1;
+  const uint32_t ring_empty0 = mapa(smem_u32(ring_empty), 0);
+  auto release_slot = [&](int rs) {
+    if (rank == 0) mbar_arrive(ring_empty + rs);
+    else mbar_arrive_cluster(ring_empty0 + rs * 8);
+  };
 
   if (warp == 0) {
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
       const uint32_t full0 = mapa(smem_u32(full), 0);
-      for (int tile = cl; tile < num_tiles; tile += ncl) {
+      for (int it = 0;; ++it) {
+        const int rs = it & 3;
+        int tile;
+        if (rank == 0) {
+          mbar_wait_cluster(ring_empty + rs, ((it >> 2) & 1) ^ 1);
+          const int got = atomicAdd(p.tile_ctr, 1);
+          if (got == num_tiles + ncl - 1) atomicExch(p.tile_ctr, 0);  // last fetch of the launch
+          tile = got < num_tiles ? got : -1;
+          ring[rs] = tile;
+          st_cluster_u32(mapa(smem_u32(ring + rs), 1), (uint32_t)tile);
+          mbar_arrive(ring_full + rs);
+          mbar_arrive_cluster(mapa(smem_u32(ring_full + rs), 1));
+        } else {
+          mbar_wait_cluster(ring_full + rs, (it >> 2) & 1);
+          tile = ring[rs];
+          release_slot(rs);
+        }
+        if (tile < 0) break;
         const int m0 = (tile % num_m2) * 256 + (int)rank * 128;
         const int n0 = (tile / num_m2) * 256 + (int)rank * 128;
         for (int kb = 0; kb < p.num_k_blk; ++kb) {
@@ -561,8 +590,12 @@ __global__ void __launch_bounds__(256, 1)
       constexpr uint32_t idesc = make_idesc_bf16(256, 256, A_MN, B_MN);
       int stage = 0;
       uint32_t phase = 0;
-      int local = 0;
-      for (int tile = cl; tile < num_tiles; tile += ncl, ++local) {
+      for (int local = 0;; ++local) {
+        const int rs = local & 3;
+        mbar_wait_cluster(ring_full + rs, (local >> 2) & 1);
+        const int tile = ring[rs];
+        release_slot(rs);
+        if (tile < 0) break;
         const int acc = local & 1;
         const uint32_t acc_phase = (local >> 1) & 1;
         mbar_wait_cluster(tempty + acc, acc_phase ^ 1);
@@ -593,8 +626,13 @@ __global__ void __launch_bounds__(256, 1)
   } else if (warp >= 4) {
     const int ew = warp & 3;
     const uint32_t tempty0 = mapa(smem_u32(tempty), 0);
-    int local = 0;
-    for (int tile = cl; tile < num_tiles; tile += ncl, ++local) {
+    for (int local = 0;; ++local) {
+      const int rs = local & 3;
+      mbar_wait_cluster(ring_full + rs, (local >> 2) & 1);
+      const int tile = ring[rs];
+      __syncwarp();
+      if (lane == 0) release_slot(rs);
+      if (tile < 0) break;
       const int acc = local & 1;
       const uint32_t acc_phase = (local >> 1) & 1;
       mbar_wait(tfull + acc, acc_phase);

@@ -268,11 +268,12 @@ def ours(args):
         peak = peaks.get("bf16_tflops_sustained", 1415.3)
         gc, gfl, gby, gms = prof["gemm"]
         achieved = (gfl / (gms / 1e3)) / 1e12 if gms > 0 else None
-        traffic = None
+        traffic, tinfo = None, {}
         tfile = os.path.join(ROOT, "profiles", "gemm_traffic.json")
         if os.path.exists(tfile):
             try:
-                traffic = json.load(open(tfile)).get("traffic_bytes_per_launch")
+                tinfo = json.load(open(tfile))
+                traffic = tinfo.get("traffic_bytes_per_launch")
             except Exception:
                 traffic = None
         afc, afl, _, afm = prof["attn_fwd"]
@@ -287,6 +288,8 @@ def ours(args):
             "roofline": {"bound": "tensor", "kernel": "gemm_bf16_sm100 (tcgen05), all GEMM launches of the timed steps",
                          "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                          "frac": (achieved / peak) if achieved else None, "traffic": traffic,
+                         "traffic_launch": tinfo.get("kernel"),
+                         "traffic_algorithmic_bytes": tinfo.get("algorithmic_bytes_per_launch"),
                          "launches": gc, "gemm_ms_per_step": gms / args.steps,
                          "peak_source": "MEASURED_PEAKS.json bf16_tflops_sustained"},
             "attention": {"fwd_tflops": (afl / (afm / 1e3)) / 1e12 if afm > 0 else None,

@@ -311,8 +311,7 @@ def ours(args):
         # the paper's comparison (§5, Table 1) on the same kernels: every schedule,
         # same model / inputs / grid, W warm-up + K device-timed steps each
         comp = {}
-        for sched in [x for x in ("stp", "1f1b-i", "1f1b-i-naive", "zb", "stp-nobraid", "stp-nosep")
-                      if x != args.sched or True]:
+        for sched in args.compare_scheds.split(","):
             if sched.startswith("1f1b-i") and args.m % p:
                 continue
             stc = make_stage(sched)
@@ -356,6 +355,7 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--compare", action="store_true",
                     help="also time 1F1B-I (+naive), ZB and the STP ablations on the same kernels")
+    ap.add_argument("--compare-scheds", default="stp,1f1b-i,1f1b-i-naive,zb,stp-nobraid,stp-nosep")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

@@ -852,8 +852,20 @@ stp_status init_nccl(stp_stage* S, const void* uid) {
   const int rank = S->pp_rank * S->t + S->tp_rank;
   STP_NCCL_TRY(ncclCommInitRank(&S->world, world, id, rank));
   S->owned.push_back(S->world);
-  // TP group: same PP rank
-  STP_NCCL_TRY(ncclCommSplit(S->world, S->pp_rank, S->tp_rank, &S->tpc, nullptr));
+  // TP group: same PP rank.  The TP collectives run concurrently with the
+  // other microbatch's GEMMs (the braid), so their SM footprint is capped
+  // (STP_NCCL_TP_CTAS, default 8): NCCL's default 32-channel kernels take SMs
+  // from the overlapped GEMM (App. F contention).
+  ncclConfig_t tcfg = NCCL_CONFIG_INITIALIZER;
+  {
+    const char* e = getenv("STP_NCCL_TP_CTAS");
+    const int ctas = e ? atoi(e) : 8;
+    if (ctas > 0) {
+      tcfg.maxCTAs = ctas;
+      tcfg.minCTAs = std::min(ctas, 2);
+    }
+  }
+  STP_NCCL_TRY(ncclCommSplit(S->world, S->pp_rank, S->tp_rank, &S->tpc, &tcfg));
   if (S->tpc) S->owned.push_back(S->tpc);
   // PP channels: one 2-rank communicator per (virtual-stage edge, tp rank),
   // sender = rank 0.  Every rank enumerates every device's edges (the
@@ -906,7 +918,16 @@ stp_status init_nccl(stp_stage* S, const void* uid) {
         mine = &rd[i];
       }
     ncclComm_t c = nullptr;
-    STP_NCCL_TRY(ncclCommSplit(S->world, color, key, &c, nullptr));
+    ncclConfig_t pcfg = NCCL_CONFIG_INITIALIZER;
+    {
+      const char* e = getenv("STP_NCCL_PP_CTAS");
+      const int ctas = e ? atoi(e) : 4;
+      if (ctas > 0) {
+        pcfg.maxCTAs = ctas;
+        pcfg.minCTAs = 1;
+      }
+    }
+    STP_NCCL_TRY(ncclCommSplit(S->world, color, key, &c, &pcfg));
     if (c && mine) {
       S->owned.push_back(c);
       const std::pair<int, int> k(mine->src_vs, mine->dst_vs);

@@ -184,6 +184,10 @@ def ours(args):
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     t, p = GRID[world]
+    if args.grid:
+        t, p = (int(x) for x in args.grid.lower().split("x"))
+        if t * p != world:
+            raise SystemExit(f"--grid {args.grid} needs {t * p} ranks, have {world}")
     tp_rank, pp_rank = rank % t, rank // t
     cfg = model_cfg(args.seq)
     if args.layers:
@@ -356,6 +360,7 @@ def main():
     ap.add_argument("--compare", action="store_true",
                     help="also time 1F1B-I (+naive), ZB and the STP ablations on the same kernels")
     ap.add_argument("--compare-scheds", default="stp,1f1b-i,1f1b-i-naive,zb,stp-nobraid,stp-nosep")
+    ap.add_argument("--grid", default="", help="TPxPP override, e.g. 4x1 (default: 1x1, 2x1, 2x2, 4x2 by N)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

@@ -156,3 +156,52 @@ def program_order_peak(kind: int, p: int, d: int, actions) -> int:
         if ww is not None:
             cur -= 1
     return best
+
+
+def simulate_durations(kind: int, p: int, progs, durations):
+    """Same dependency semantics as `simulate`, but every action takes the
+    given duration (durations[d][i], e.g. measured compute time of action i on
+    device d) instead of the Table 1 block cost.  Returns the makespan — the
+    executor-consistency check of SURVEY §8d.4 compares it with the measured
+    step time."""
+    V = sc.n_vstages(kind, p)
+    fend, bend = {}, {}
+    ptr = [0] * p
+    free = [0.0] * p
+    total = sum(len(x) for x in progs)
+    done = 0
+    while done < total:
+        progress = False
+        for d in range(p):
+            while ptr[d] < len(progs[d]):
+                a = progs[d][ptr[d]]
+                fw, bw, full, ww = _parts(a)
+                vs = sc.vstage(kind, p, d, a[1])
+                deps, ready = [], True
+                if fw is not None and vs > 0:
+                    ready &= (fw, vs - 1) in fend
+                    deps.append(fend.get((fw, vs - 1), 0.0))
+                if bw is not None:
+                    if vs < V - 1:
+                        ready &= (bw, vs + 1) in bend
+                        deps.append(bend.get((bw, vs + 1), 0.0))
+                    ready &= (bw, vs) in fend
+                    deps.append(fend.get((bw, vs), 0.0))
+                if ww is not None:
+                    wvs = sc.vstage(kind, p, d, ww[1])
+                    ready &= (ww[0], wvs) in bend
+                    deps.append(bend.get((ww[0], wvs), 0.0))
+                if not ready:
+                    break
+                end = max([free[d]] + deps) + durations[d][ptr[d]]
+                free[d] = end
+                if fw is not None:
+                    fend[(fw, vs)] = end
+                if bw is not None:
+                    bend[(bw, vs)] = end
+                ptr[d] += 1
+                done += 1
+                progress = True
+        if not progress:
+            raise RuntimeError("DeadlockDetected")
+    return max(free)

@@ -1,0 +1,82 @@
+"""Run under torchrun: one timed STP step on a TP x PP grid, every rank's
+per-unit CUDA-event times gathered to rank 0, then the executor-consistency
+check of SURVEY §8d.4: the oracle's discrete-event simulator, fed the measured
+compute time of every action, must reproduce the measured step time.  A large
+gap means a hidden synchronisation / serialisation in the executor.  Prints
+one JSON line on rank 0."""
+import argparse
+import dataclasses
+import json
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import paper_2510_27257_b200  # noqa: E402,F401
+import torch  # noqa: E402
+import torch.distributed as dist  # noqa: E402
+
+import stp_inputs as si  # noqa: E402
+from oracle import schedule as sc  # noqa: E402
+from oracle import simulate as sm  # noqa: E402
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--tp", type=int, required=True)
+    ap.add_argument("--pp", type=int, required=True)
+    ap.add_argument("--sched", default="stp")
+    ap.add_argument("--n-micro", type=int, default=8)
+    ap.add_argument("--layers", type=int, default=8)
+    ap.add_argument("--seq", type=int, default=2048)
+    a = ap.parse_args()
+    rank, world, local = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"]), int(os.environ["LOCAL_RANK"])
+    torch.cuda.set_device(local)
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_2510_27257_b200.stage import SCHED, Stage, broadcast_nccl_id
+    cfg = dataclasses.replace(si.QWEN2_7B, n_layers=a.layers, seq=a.seq, vocab=32768)
+    tp_rank, pp_rank = rank % a.tp, rank // a.tp
+    st = Stage(cfg, tp=a.tp, pp=a.pp, n_micro=a.n_micro, tp_rank=tp_rank, pp_rank=pp_rank, dtype="bf16",
+               sched=a.sched, device=local, world_nccl_id=broadcast_nccl_id())
+    g = torch.Generator(device="cuda").manual_seed(rank)
+    for name, prm in zip(st.names, st.params):
+        if name.endswith(("ln1", "ln2")) or name == "final_ln":
+            prm.fill_(1.0)
+        else:
+            prm.copy_(torch.randn(prm.shape, generator=g, device="cuda") * 0.02)
+    toks, tgts = si.make_tokens(cfg, a.n_micro)
+    dt, dg = torch.from_numpy(toks).cuda(), torch.from_numpy(tgts).cuda()
+    for _ in range(2):
+        st.step(dt, dg)
+    st.set_timing(True)
+    _, stats = st.step(dt, dg)
+    t0, t1 = st.unit_times()
+    units = st.trace()
+    gathered = [None] * world
+    dist.all_gather_object(gathered, (pp_rank, tp_rank, units, t0, t1, stats.step_ms, stats.exposed_tp_ms,
+                                      stats.pp_bubble_ms))
+    if rank == 0:
+        kind = SCHED[a.sched]
+        progs = sc.build_program(kind, a.pp, a.n_micro)
+        dur = []
+        measured = max(x[5] for x in gathered)
+        for d in range(a.pp):
+            pr, tr, us, s0, s1, *_ = next(x for x in gathered if x[0] == d and x[1] == 0)
+            per = [0.0] * len(progs[d])
+            for u, b, e in zip(us, s0, s1):
+                if u[1] == 0:                    # compute-stream units
+                    per[u[0]] += e - b
+            dur.append(per)
+        simulated = sm.simulate_durations(kind, a.pp, progs, dur)
+        print(json.dumps({"tp": a.tp, "pp": a.pp, "sched": a.sched, "n_micro": a.n_micro, "layers": a.layers,
+                          "seq": a.seq, "measured_ms": measured, "simulated_ms": simulated,
+                          "ratio": measured / simulated,
+                          "exposed_tp_pct": [100 * x[6] / x[5] for x in gathered],
+                          "pp_bubble_pct": [100 * x[7] / x[5] for x in gathered]}), flush=True)
+    st.close()
+    dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,25 @@
+"""Executor consistency check on 2 / 4 GPUs: the simulator fed
+with the measured per-action compute times reproduces the measured step time
+(ratio measured / simulated in [0.95, 1.25]: TP-comm exposure and PP transfer
+time are not in the simulated compute, so measured >= simulated)."""
+import json
+
+import pytest
+import torch
+
+from tests.test_gpu_multi import run_torchrun
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.parametrize("tp,pp,sched", [(1, 2, "stp"), (1, 2, "1f1b-i"), (2, 2, "stp"), (2, 2, "1f1b-i")])
+def test_executor_matches_simulator(tp, pp, sched):
+    n = tp * pp
+    if torch.cuda.device_count() < n:
+        pytest.skip(f"needs {n} GPUs")
+    rc, out = run_torchrun(n, ["--tp", str(tp), "--pp", str(pp), "--sched", sched], 29700 + 10 * tp + pp + len(sched),
+                           timeout=300, script="multi_rank_timeline.py")
+    assert rc == 0, out[-3000:]
+    line = json.loads([x for x in out.splitlines() if x.startswith("{")][-1])
+    print(line)
+    assert 0.95 <= line["ratio"] <= 1.25, line

@@ -18,10 +18,10 @@ CASES = [(2, 1, "stp", "f32"), (1, 2, "stp", "f32"), (2, 1, "stp", "bf16"), (1, 
          (2, 2, "1f1b-i", "f32"), (2, 2, "zb", "f32"), (4, 1, "stp", "f32"), (1, 4, "stp", "f32")]
 
 
-def run_torchrun(n, args, port, timeout=120):
+def run_torchrun(n, args, port, timeout=120, script="multi_rank_parity.py"):
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
            "--master-addr=127.0.0.1", f"--master-port={port}",
-           os.path.join(ROOT, "tests", "multi_rank_parity.py")] + args
+           os.path.join(ROOT, "tests", script)] + args
     p = subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT, text=True, cwd=ROOT,
                          start_new_session=True)
     try:

@@ -38,7 +38,7 @@ import numpy as np  # noqa: E402
 import paper_2510_27257_b200  # noqa: E402,F401  (sets CUDA_DEVICE_MAX_CONNECTIONS before CUDA init)
 
 METRIC = "tokens/s per step at TP×PP on 1–8 B200; exposed TP-comm %; PP bubble rate"
-GRID = {1: (1, 1), 2: (2, 1), 4: (2, 2), 8: (4, 2)}
+GRID = {1: (1, 1), 2: (2, 1), 4: (4, 1), 8: (4, 2)}
 
 
 def model_cfg(seq: int):

@@ -854,7 +854,7 @@ stp_status init_nccl(stp_stage* S, const void* uid) {
   S->owned.push_back(S->world);
   // TP group: same PP rank.  The TP collectives run concurrently with the
   // other microbatch's GEMMs (the braid), so their SM footprint is capped
-  // (STP_NCCL_TP_CTAS, default 8): NCCL's default 32-channel kernels take SMs
+  // (STP_NCCL_TP_CTAS, default 16): NCCL's default 32-channel kernels take SMs
   // from the overlapped GEMM (App. F contention).
   ncclConfig_t tcfg = NCCL_CONFIG_INITIALIZER;
   {

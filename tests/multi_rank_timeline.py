@@ -28,7 +28,7 @@ def main():
     ap.add_argument("--pp", type=int, required=True)
     ap.add_argument("--sched", default="stp")
     ap.add_argument("--n-micro", type=int, default=8)
-    ap.add_argument("--layers", type=int, default=8)
+    ap.add_argument("--layers", type=int, default=10)
     ap.add_argument("--seq", type=int, default=2048)
     a = ap.parse_args()
     rank, world, local = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"]), int(os.environ["LOCAL_RANK"])

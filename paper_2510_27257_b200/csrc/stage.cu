@@ -859,7 +859,7 @@ stp_status init_nccl(stp_stage* S, const void* uid) {
   ncclConfig_t tcfg = NCCL_CONFIG_INITIALIZER;
   {
     const char* e = getenv("STP_NCCL_TP_CTAS");
-    const int ctas = e ? atoi(e) : 8;
+    const int ctas = e ? atoi(e) : 16;
     if (ctas > 0) {
       tcfg.maxCTAs = ctas;
       tcfg.minCTAs = std::min(ctas, 2);

@@ -147,6 +147,7 @@ struct stp_stage {
   std::vector<char> unit_fwd;                  // per unit: PP message belongs to a forward pass
   std::vector<std::pair<int, int>> edges_sorted;  // all PP edges of the grid, global order
   std::vector<ncclComm_t> owned;
+  std::vector<std::pair<ncclComm_t, void*>> nccl_regs;  // ncclCommRegister handles
   // buffers
   void *pf = nullptr, *pb = nullptr;               // partial outputs (forward / backward lanes)
   void *rtmp = nullptr, *ntmp = nullptr;           // comm-stream temps [sl, h]
@@ -1133,6 +1134,23 @@ stp_status stp_init_stage(const stp_model_cfg* mc, const stp_parallel_cfg* pc, c
     STP_CUDA_TRY(cudaStreamCreateWithPriority(&st, cudaStreamNonBlocking, hi));
     S->s_recv[kv.first] = st;
   }
+  // Optional NCCL user-buffer registration of every TP-collective buffer
+  // (STP_NCCL_REGISTER=1): lets NVLink collectives read/write user buffers
+  // directly instead of staging through NCCL's own buffers.
+  if (S->tpc && S->t > 1 && getenv("STP_NCCL_REGISTER") && atoi(getenv("STP_NCCL_REGISTER")) > 0) {
+    for (auto& C : S->chunks)
+      for (auto& sl : C.slots) {
+        void* h = nullptr;
+        STP_NCCL_TRY(ncclCommRegister(S->tpc, sl.mem, C.slot_bytes, &h));
+        S->nccl_regs.push_back({S->tpc, h});
+      }
+    for (void* b : {S->pf, S->pb, S->rtmp, S->ntmp}) {
+      void* h = nullptr;
+      const size_t bytes = (b == S->pf || b == S->pb) ? (size_t)(S->s * S->h * S->es) : (size_t)(S->sl * S->h * S->es);
+      STP_NCCL_TRY(ncclCommRegister(S->tpc, b, bytes, &h));
+      S->nccl_regs.push_back({S->tpc, h});
+    }
+  }
   STP_TRY(warmup_comms(S.get()));
   // every PP edge used by the unit list must have its communicator
   for (size_t i = 0; i < S->units.size(); ++i) {
@@ -1236,6 +1254,7 @@ void stp_destroy_stage(stp_stage* st) {
   if (!st) return;
   cudaSetDevice(st->dev);
   cudaDeviceSynchronize();
+  for (auto& r : st->nccl_regs) ncclCommDeregister(r.first, r.second);
   for (auto c : st->owned)
     if (c) ncclCommDestroy(c);
   for (auto e : st->ev_done) cudaEventDestroy(e);

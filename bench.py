@@ -163,6 +163,7 @@ def workload_config(args, cfg, tp_pp):
             "model": "Qwen2-7B-shaped (h3584 L28 28/4 heads d128 I18944 V152064), random init",
             "global_batch": args.m, "seq_len": cfg.seq, "parallelism": f"tp{t}pp{p}vpp2",
             "schedule": args.sched,
+            "tp_transport": (os.environ.get("STP_TP_TRANSPORT", "p2p") if t > 1 else "none"),
             "l2": "no flush: weights (15.2 GB / tp*pp) and stash (tens of GB) exceed the 126 MB L2"}
 
 

@@ -416,6 +416,22 @@ stp_status rmsnorm_bwd(int dtype, int64_t rows, int64_t h, const void* dy, const
   });
 }
 
+// dgamma[c] += sum_rows dy * x * rstd (the W-type gamma partial of an
+// RMSNorm backward whose dx was produced elsewhere, e.g. by the fused TP
+// comm-phase kernel in tpcomm.cu).
+stp_status rmsnorm_dgamma(int dtype, int64_t rows, int64_t h, const void* dy, const void* x, const float* rstd,
+                          float* dgamma, cudaStream_t st) {
+  if (rows == 0 || !dgamma) return STP_OK;
+  return STP_DISPATCH_DTYPE(dtype, [&] {
+    const int64_t rpb = 128;
+    dim3 grid2((unsigned)((h + 255) / 256), (unsigned)((rows + rpb - 1) / rpb));
+    rmsnorm_dgamma_kernel<T><<<grid2, 256, 0, st>>>(rows, (int)h, (const T*)dy, (const T*)x, rstd, dgamma, rpb);
+    count_launch();
+    STP_LAUNCH_CHECK();
+    return STP_OK;
+  });
+}
+
 struct RopeKey {
   int dev;
   int64_t s;

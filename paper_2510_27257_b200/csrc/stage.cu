@@ -64,6 +64,17 @@ stp_status attn_bwd(int dtype, int64_t s, int nq, int nkv, int d, const void* q,
                     int64_t ld, const void* o, int64_t ldo, const void* dout, const float* lse, void* dq, void* dk,
                     void* dv, int64_t ldd, void* ws, cudaStream_t st);
 int64_t attn_bwd_ws_bytes(int64_t s, int nq, int nkv, int d);
+// copy-engine TP transport (tpcomm.cu)
+stp_status tp_signal(uint32_t* const* dst, int n, uint32_t val, cudaStream_t st);
+stp_status tp_wait(const uint32_t* flag, uint32_t val, bool spin, cudaStream_t st);
+stp_status tp_fused_fwd(int dtype, int64_t rows, int64_t h, const void* const* pieces, int np, const void* resid,
+                        void* x_out, const void* g, float eps, float* rstd, void* const* dsts, int nd,
+                        cudaStream_t st);
+stp_status tp_fused_bwd(int dtype, int64_t rows, int64_t h, const void* const* pieces, int np, const void* x,
+                        const void* g, const float* rstd, const void* dres, void* dx, void* dy_out,
+                        void* const* dsts, int nd, cudaStream_t st);
+stp_status rmsnorm_dgamma(int dtype, int64_t rows, int64_t h, const void* dy, const void* x, const float* rstd,
+                          float* dgamma, cudaStream_t st);
 stp_status convert(int sd, int dd, int64_t n, const void* src, void* dst, cudaStream_t st);
 
 #define STP_NCCL_TRY(expr)                                                     \
@@ -163,8 +174,24 @@ struct stp_stage {
   std::vector<cudaEvent_t> ev_done;
   std::vector<cudaEvent_t> ev_t0, ev_t1;  // timing
   cudaEvent_t ev_base = nullptr, ev_end = nullptr;
-  cudaEvent_t ev_pf = nullptr, ev_pb = nullptr;
-  bool pf_pending = false, pb_pending = false;
+  // partial buffers: one per lane with NCCL (the collective copies it out
+  // before it completes), two per lane with the copy-engine transport (peers
+  // pull from them; see ce_* below).  ev_*b[i]: the comm phase that last read
+  // buffer i has finished on this rank.
+  void *pfb[2] = {nullptr, nullptr}, *pbb[2] = {nullptr, nullptr};
+  int pfi = 0, pbi = 0;
+  cudaEvent_t ev_pfb[2] = {nullptr, nullptr}, ev_pbb[2] = {nullptr, nullptr};
+  bool pfb_pending[2] = {false, false}, pbb_pending[2] = {false, false};
+  bool pf_pending = false, pb_pending = false;  // the current comm phase read pf / pb
+  // copy-engine TP transport (STP_TP_TRANSPORT=ce; tpcomm.cu)
+  bool ce = false, ce_spin = false;
+  bool p2p = false;              // STP_TP_TRANSPORT=p2p: fused NVLink load/store kernels instead of copy engines
+  uint32_t* flags = nullptr;     // [2][16]: A (partials ready), B (shard ready), one word per peer
+  uint32_t phase = 0, open_phase = 0;
+  void* stage_buf = nullptr;     // [t, sl, h]: rows pulled from the peers' partials
+  std::vector<std::pair<uint8_t*, size_t>> sym;  // symmetric allocations, same order on every TP rank
+  std::vector<std::vector<uint8_t*>> sym_peer;   // [q][i]: IPC mapping of peer q's allocation i
+  std::vector<cudaStream_t> s_pull;              // one per peer: concurrent copy-engine pulls
   std::vector<cudaEvent_t> ev_pool;
   size_t ev_pool_next = 0;
   int timing = 0;
@@ -271,6 +298,237 @@ stp_status all_gather(stp_stage* S, const void* src, void* dst, size_t count) {
 
 Chunk& chunk_of(stp_stage* S, int c) { return S->chunks[c]; }
 
+// --------------------------------------------- copy-engine TP transport
+// STP_TP_TRANSPORT=ce.  Every TP rank maps its peers' stash slots, partial
+// buffers and flag words (CUDA IPC, exchanged once at init), and each comm
+// phase c (numbered identically on all TP ranks: they run the same unit
+// list) becomes
+//   A(c): signal "my partial for c is ready and phase c-1 is done", wait for
+//         the peers' A(c); pull this rank's rows of every peer's partial
+//         (cudaMemcpyAsync over NVLink: copy engines, no SMs);
+//         tp_fused_fwd: sum + residual (+ RMSNorm into this rank's rows of
+//         the all-gather destination);
+//   B(c): signal "my rows of the destination are written", wait for the
+//         peers' B(c); pull every peer's rows of the destination.
+// Safety without "consumed" flags: a rank completes phase c only after all
+// peers signalled A(c) or B(c), i.e. finished phase c-1.  So when a rank
+// overwrites a buffer peers pull from, every peer has finished the phases
+// before the current one: partials alternate between two buffers per lane
+// (two partial writes of a lane are separated by a phase that consumes the
+// all-gather of the first), and a destination / dx_in region is rewritten
+// only phases after its last pull.  See DESIGN.md "Copy-engine TP transport".
+uint8_t* sym_peer_ptr(stp_stage* S, int q, const void* p) {
+  const uint8_t* b = (const uint8_t*)p;
+  for (size_t i = 0; i < S->sym.size(); ++i)
+    if (b >= S->sym[i].first && b < S->sym[i].first + S->sym[i].second)
+      return S->sym_peer[q][i] + (b - S->sym[i].first);
+  return nullptr;
+}
+
+stp_status ce_handshake(stp_stage* S, int which, uint32_t c) {
+  uint32_t* dst[16];
+  int n = 0;
+  for (int q = 0; q < S->t; ++q)
+    if (q != S->tp_rank) {
+      uint8_t* pf = sym_peer_ptr(S, q, S->flags);
+      if (!pf) return fail(STP_ESTATE, "flag words not mapped");
+      dst[n++] = (uint32_t*)pf + which * 16 + S->tp_rank;
+    }
+  STP_TRY(tp_signal(dst, n, c, S->s_comm));
+  for (int q = 0; q < S->t; ++q)
+    if (q != S->tp_rank) STP_TRY(tp_wait(S->flags + which * 16 + q, c, S->ce_spin, S->s_comm));
+  return STP_OK;
+}
+
+// rows [q*sl, (q+1)*sl) of `dst` <- peer q's copy, for every peer q (ag), or
+// stage[q] <- rows of this rank from peer q's `src` (rs); one copy-engine
+// transfer per peer, concurrent on the per-peer pull streams.
+stp_status ce_pull(stp_stage* S, bool rs, const void* src, void* dst) {
+  const size_t bytes = (size_t)(S->sl * S->h) * S->es;
+  cudaEvent_t fork = pool_event(S);
+  STP_CUDA_TRY(cudaEventRecord(fork, S->s_comm));
+  int k = 0;
+  for (int q = 0; q < S->t; ++q) {
+    if (q == S->tp_rank) continue;
+    cudaStream_t ps = S->s_pull[k++];
+    STP_CUDA_TRY(cudaStreamWaitEvent(ps, fork, 0));
+    uint8_t* from = sym_peer_ptr(S, q, rs ? src : dst);
+    if (!from) return fail(STP_ESTATE, "buffer not in the symmetric set");
+    if (rs)
+      STP_CUDA_TRY(cudaMemcpyAsync((uint8_t*)S->stage_buf + q * bytes, from + S->tp_rank * bytes, bytes,
+                                   cudaMemcpyDeviceToDevice, ps));
+    else
+      STP_CUDA_TRY(cudaMemcpyAsync((uint8_t*)dst + q * bytes, from + q * bytes, bytes, cudaMemcpyDeviceToDevice, ps));
+    cudaEvent_t e = pool_event(S);
+    STP_CUDA_TRY(cudaEventRecord(e, ps));
+    STP_CUDA_TRY(cudaStreamWaitEvent(S->s_comm, e, 0));
+  }
+  return STP_OK;
+}
+
+// Reduce-scatter of `partial` (+ resid) into x_out; with g: RMSNorm into this
+// rank's rows of `dst` and the all-gather of dst.  Opens phase c (kept in
+// open_phase for a following ce_ag when dst is null).
+stp_status ce_rs(stp_stage* S, const void* partial, const void* resid, void* x_out, const void* g, float* rstd,
+                 void* dst);
+stp_status ce_ag(stp_stage* S, void* dst) {
+  const uint32_t c = S->open_phase ? S->open_phase : ++S->phase;
+  S->open_phase = 0;
+  STP_TRY(ce_handshake(S, 1, c));
+  return ce_pull(S, false, nullptr, dst);
+}
+stp_status p2p_rs(stp_stage* S, const void* partial, const void* resid, void* x_out, const void* g, float* rstd,
+                  void* dst);
+stp_status ce_rs(stp_stage* S, const void* partial, const void* resid, void* x_out, const void* g, float* rstd,
+                 void* dst) {
+  if (S->p2p) return p2p_rs(S, partial, resid, x_out, g, rstd, dst);
+  const uint32_t c = ++S->phase;
+  STP_TRY(ce_handshake(S, 0, c));
+  STP_TRY(ce_pull(S, true, partial, nullptr));
+  const size_t bytes = (size_t)(S->sl * S->h) * S->es;
+  const void* pieces[16];
+  int n = 0;
+  for (int q = 0; q < S->t; ++q)
+    pieces[n++] = q == S->tp_rank ? (const uint8_t*)partial + q * bytes : (const uint8_t*)S->stage_buf + q * bytes;
+  void* y = dst ? (uint8_t*)dst + S->tp_rank * bytes : nullptr;
+  STP_TRY(tp_fused_fwd(S->dtype, S->sl, S->h, pieces, n, resid, x_out, g, S->mc.rms_eps, rstd, &y, y ? 1 : 0,
+                       S->s_comm));
+  S->open_phase = c;
+  if (dst) return ce_ag(S, dst);
+  return STP_OK;
+}
+// all-gather of a shard held elsewhere: copy it into this rank's rows of dst
+stp_status ce_ag_shard(stp_stage* S, const void* shard, void* dst) {
+  const size_t bytes = (size_t)(S->sl * S->h) * S->es;
+  STP_CUDA_TRY(cudaMemcpyAsync((uint8_t*)dst + S->tp_rank * bytes, shard, bytes, cudaMemcpyDeviceToDevice,
+                               S->s_comm));
+  return ce_ag(S, dst);
+}
+
+// ---- p2p variant (STP_TP_TRANSPORT=p2p): one fused kernel per phase reads
+// this rank's rows of every peer's partial over NVLink, reduces, applies the
+// residual + RMSNorm (fwd) or RMSNorm-bwd + residual grad (bwd), and stores
+// the result into this rank's rows of every rank's all-gather destination.
+// Handshakes: A(c) before the kernel (peers' partials ready, destinations
+// free), B(c) after it (every peer's rows have landed here).
+int p2p_pieces(stp_stage* S, const void* partial, const void** pieces) {
+  const size_t bytes = (size_t)(S->sl * S->h) * S->es;
+  for (int q = 0; q < S->t; ++q) {
+    const uint8_t* b = q == S->tp_rank ? (const uint8_t*)partial : sym_peer_ptr(S, q, partial);
+    pieces[q] = b ? b + S->tp_rank * bytes : nullptr;
+    if (!b) return -1;
+  }
+  return S->t;
+}
+int p2p_dsts(stp_stage* S, void* dst, void** dsts) {
+  if (!dst) return 0;
+  const size_t bytes = (size_t)(S->sl * S->h) * S->es;
+  int n = 0;
+  dsts[n++] = (uint8_t*)dst + S->tp_rank * bytes;  // local rows first (the kernel's scratch)
+  for (int q = 0; q < S->t; ++q) {
+    if (q == S->tp_rank) continue;
+    uint8_t* b = sym_peer_ptr(S, q, dst);
+    if (!b) return -1;
+    dsts[n++] = b + S->tp_rank * bytes;
+  }
+  return n;
+}
+stp_status p2p_rs(stp_stage* S, const void* partial, const void* resid, void* x_out, const void* g, float* rstd,
+                  void* dst) {
+  const uint32_t c = ++S->phase;
+  const void* pieces[16];
+  void* dsts[16];
+  const int np = p2p_pieces(S, partial, pieces), nd = p2p_dsts(S, dst, dsts);
+  if (np < 0 || nd < 0) return fail(STP_ESTATE, "buffer not in the symmetric set");
+  STP_TRY(ce_handshake(S, 0, c));
+  STP_TRY(tp_fused_fwd(S->dtype, S->sl, S->h, pieces, np, resid, x_out, g, S->mc.rms_eps, rstd, dsts, nd,
+                       S->s_comm));
+  if (nd) STP_TRY(ce_handshake(S, 1, c));
+  return STP_OK;
+}
+// all-gather of a local shard (optionally RMSNorm-ed on the way)
+stp_status p2p_ag(stp_stage* S, const void* shard, const void* g, float* rstd, void* dst) {
+  const uint32_t c = ++S->phase;
+  void* dsts[16];
+  const int nd = p2p_dsts(S, dst, dsts);
+  if (nd <= 0) return fail(STP_ESTATE, "buffer not in the symmetric set");
+  STP_TRY(ce_handshake(S, 0, c));
+  STP_TRY(tp_fused_fwd(S->dtype, S->sl, S->h, &shard, 1, nullptr, nullptr, g, S->mc.rms_eps, rstd, dsts, nd,
+                       S->s_comm));
+  return ce_handshake(S, 1, c);
+}
+// RS of the backward partial -> RMSNorm-bwd + residual grad -> AG (dst may be
+// null); the dgamma partials follow, off the critical path.
+stp_status p2p_bwd(stp_stage* S, const void* x, const void* g, const float* rstd, const void* dres, void* dx,
+                   float* dgamma, void* dst) {
+  const uint32_t c = ++S->phase;
+  const void* pieces[16];
+  void* dsts[16];
+  const int np = p2p_pieces(S, S->pb, pieces), nd = p2p_dsts(S, dst, dsts);
+  if (np < 0 || nd < 0) return fail(STP_ESTATE, "buffer not in the symmetric set");
+  STP_TRY(ce_handshake(S, 0, c));
+  STP_TRY(tp_fused_bwd(S->dtype, S->sl, S->h, pieces, np, x, g, rstd, dres, dx, S->rtmp, dsts, nd, S->s_comm));
+  if (nd) STP_TRY(ce_handshake(S, 1, c));
+  return rmsnorm_dgamma(S->dtype, S->sl, S->h, S->rtmp, x, rstd, dgamma, S->s_comm);
+}
+
+stp_status ag_dx(stp_stage* S, const void* shard_src, void* dst, size_t count) {
+  if (S->p2p) return p2p_ag(S, shard_src, nullptr, nullptr, dst);
+  if (S->ce) return ce_ag_shard(S, shard_src, dst);
+  return all_gather(S, shard_src, dst, count);
+}
+
+// Map the peers' symmetric allocations (same order on every TP rank: every
+// stash slot, both partial buffers of both lanes, the flag words).
+stp_status ce_init(stp_stage* S) {
+  S->sym.clear();
+  for (auto& C : S->chunks)
+    for (auto& sl : C.slots) S->sym.push_back({(uint8_t*)sl.mem, C.slot_bytes});
+  const size_t pbytes = (size_t)(S->s * S->h) * S->es;
+  for (int i = 0; i < 2; ++i) {
+    S->sym.push_back({(uint8_t*)S->pfb[i], pbytes});
+    S->sym.push_back({(uint8_t*)S->pbb[i], pbytes});
+  }
+  S->sym.push_back({(uint8_t*)S->flags, 4096});
+  const int n = (int)S->sym.size();
+  const size_t hb = sizeof(cudaIpcMemHandle_t);
+  std::vector<uint8_t> mine(n * hb), all((size_t)S->t * n * hb);
+  for (int i = 0; i < n; ++i)
+    STP_CUDA_TRY(cudaIpcGetMemHandle(reinterpret_cast<cudaIpcMemHandle_t*>(mine.data() + i * hb), S->sym[i].first));
+  void *dm = nullptr, *da = nullptr;
+  STP_CUDA_TRY(cudaMalloc(&dm, mine.size()));
+  STP_CUDA_TRY(cudaMalloc(&da, all.size()));
+  STP_CUDA_TRY(cudaMemcpy(dm, mine.data(), mine.size(), cudaMemcpyHostToDevice));
+  STP_NCCL_TRY(ncclAllGather(dm, da, mine.size(), ncclUint8, S->tpc, S->s_comm));
+  STP_CUDA_TRY(cudaStreamSynchronize(S->s_comm));
+  STP_CUDA_TRY(cudaMemcpy(all.data(), da, all.size(), cudaMemcpyDeviceToHost));
+  cudaFree(dm);
+  cudaFree(da);
+  S->sym_peer.assign(S->t, std::vector<uint8_t*>(n, nullptr));
+  for (int q = 0; q < S->t; ++q) {
+    if (q == S->tp_rank) continue;
+    for (int i = 0; i < n; ++i) {
+      cudaIpcMemHandle_t hdl;
+      memcpy(&hdl, all.data() + ((size_t)q * n + i) * hb, hb);
+      void* p = nullptr;
+      STP_CUDA_TRY(cudaIpcOpenMemHandle(&p, hdl, cudaIpcMemLazyEnablePeerAccess));
+      S->sym_peer[q][i] = (uint8_t*)p;
+    }
+  }
+  int lo = 0, hi = 0;
+  STP_CUDA_TRY(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+  for (int q = 0; q + 1 < S->t; ++q) {
+    cudaStream_t st;
+    STP_CUDA_TRY(cudaStreamCreateWithPriority(&st, cudaStreamNonBlocking, hi));
+    S->s_pull.push_back(st);
+  }
+  // every rank has mapped everything before any phase signals
+  STP_NCCL_TRY(ncclAllReduce(S->flags + 1000, S->flags + 1000, 1, ncclUint32, ncclMax, S->tpc, S->s_comm));
+  STP_CUDA_TRY(cudaStreamSynchronize(S->s_comm));
+  return STP_OK;
+}
+
+
 stp_status acquire(stp_stage* S, int c, int mb, Slot** out) {
   Chunk& C = chunk_of(S, c);
   auto it = C.mb2slot.find(mb);
@@ -340,8 +598,16 @@ stp_status unit_compute(stp_stage* S, const stp_unit& u) {
   }
   const bool writes_pf = u.op == STP_U_F_ATTN || u.op == STP_U_F_MLP || u.op == STP_U_F_EMB;
   const bool writes_pb = u.op == STP_U_B_ATTN || u.op == STP_U_B_MLP || u.op == STP_U_B_HEAD;
-  if (writes_pf && S->pf_pending) STP_CUDA_TRY(cudaStreamWaitEvent(st, S->ev_pf, 0));
-  if (writes_pb && S->pb_pending) STP_CUDA_TRY(cudaStreamWaitEvent(st, S->ev_pb, 0));
+  if (writes_pf) {
+    if (S->ce) S->pfi ^= 1;
+    S->pf = S->pfb[S->pfi];
+    if (S->pfb_pending[S->pfi]) STP_CUDA_TRY(cudaStreamWaitEvent(st, S->ev_pfb[S->pfi], 0));
+  }
+  if (writes_pb) {
+    if (S->ce) S->pbi ^= 1;
+    S->pb = S->pbb[S->pbi];
+    if (S->pbb_pending[S->pbi]) STP_CUDA_TRY(cudaStreamWaitEvent(st, S->ev_pbb[S->pbi], 0));
+  }
   const int j = u.layer - C.l0;
   switch (u.op) {
     case STP_U_F_EMB: {
@@ -446,8 +712,15 @@ stp_status unit_cf(stp_stage* S, const stp_unit& u) {
   const float eps = S->mc.rms_eps;
   cudaStream_t st = S->s_comm;
   const int k = u.layer;
+  S->open_phase = 0;
   // normalise `x` (shard) with gamma into the all-gathered destination `dst`
   auto norm_ag = [&](const void* x, const void* resid, void* x_out, const void* g, float* rstd, void* dst) {
+    if (S->p2p && !resid) return p2p_ag(S, x, g, rstd, dst);
+    if (S->ce) {
+      STP_TRY(rmsnorm_fwd(dt, S->sl, h, x, resid, x_out, g, eps, (uint8_t*)dst + S->tp_rank * shard * S->es, rstd,
+                          st));
+      return ce_ag(S, dst);
+    }
     void* y = (S->t == 1) ? dst : S->ntmp;
     STP_TRY(rmsnorm_fwd(dt, S->sl, h, x, resid, x_out, g, eps, y, rstd, st));
     if (S->t > 1) STP_TRY(all_gather(S, S->ntmp, dst, (size_t)shard));
@@ -480,6 +753,10 @@ stp_status unit_cf(stp_stage* S, const stp_unit& u) {
   int idx = k - 1;
   if (C.first) {
     if (idx == 0) {  // after F_EMB: RS -> chunk input shard -> ln1 -> AG
+      if (S->ce) {
+        S->pf_pending = true;
+        return ce_rs(S, S->pf, nullptr, sl->x_in, P(S, LI(S, C.l0).ln1), sl->L[0].rstd1, sl->L[0].xn);
+      }
       if (S->t == 1) STP_CUDA_TRY(cudaMemcpyAsync(sl->x_in, S->pf, shard * S->es, cudaMemcpyDeviceToDevice, st));
       else STP_TRY(reduce_scatter(S, S->pf, sl->x_in));
       S->pf_pending = true;
@@ -492,6 +769,15 @@ stp_status unit_cf(stp_stage* S, const stp_unit& u) {
     const int j = idx / 2;
     SlotLayer& L = sl->L[j];
     const LayerIdx& I = LI(S, C.l0 + j);
+    if (S->ce) {  // fused RS + residual + RMSNorm, then AG (copy engines)
+      S->pf_pending = true;
+      if (idx % 2 == 0)
+        return ce_rs(S, S->pf, j == 0 ? sl->x_in : sl->L[j - 1].xres, L.x1, P(S, I.ln2), L.rstd2, L.xn2);
+      if (j + 1 < C.nl)
+        return ce_rs(S, S->pf, L.x1, L.xres, P(S, LI(S, C.l0 + j + 1).ln1), sl->L[j + 1].rstd1, sl->L[j + 1].xn);
+      if (C.last) return ce_rs(S, S->pf, L.x1, L.xres, P(S, S->p_final), sl->rstdf, sl->xf);
+      return ce_rs(S, S->pf, L.x1, L.xres, nullptr, nullptr, nullptr);
+    }
     const void* src = nullptr;
     STP_TRY(rs_src(&src));
     S->pf_pending = true;
@@ -516,6 +802,7 @@ stp_status unit_cf(stp_stage* S, const stp_unit& u) {
   return STP_OK;
 }
 
+stp_status cb_handoff(stp_stage* S, Chunk& C, const stp_unit& u, Slot* sl);
 stp_status unit_cb(stp_stage* S, const stp_unit& u) {
   Chunk& C = chunk_of(S, u.chunk);
   Slot* sl = find_slot(S, u.chunk, u.mb);
@@ -524,9 +811,15 @@ stp_status unit_cb(stp_stage* S, const stp_unit& u) {
   const int64_t h = S->h, shard = S->sl * S->h;
   cudaStream_t st = S->s_comm;
   const int k = u.layer;
+  S->open_phase = 0;
   auto rs_src = [&](const void** out) {
     if (S->t == 1) {
       *out = S->pb;
+      return STP_OK;
+    }
+    if (S->ce) {  // RS (copy engines) + sum into rtmp; the AG below reuses the phase
+      STP_TRY(ce_rs(S, S->pb, nullptr, S->rtmp, nullptr, nullptr, nullptr));
+      *out = S->rtmp;
       return STP_OK;
     }
     STP_TRY(reduce_scatter(S, S->pb, S->rtmp));
@@ -534,9 +827,25 @@ stp_status unit_cb(stp_stage* S, const stp_unit& u) {
     return STP_OK;
   };
   if (k == 0) {  // incoming gradient shard -> AG for the last layer's MLP B unit
-    return all_gather(S, sl->dx_in, sl->L[C.nl - 1].dy_mlp, (size_t)shard);
+    return ag_dx(S, sl->dx_in, sl->L[C.nl - 1].dy_mlp, (size_t)shard);
   }
   int idx = k - 1;
+  if (S->p2p) {  // fused RS + RMSNorm-bwd + residual grad + AG kernel per phase
+    S->pb_pending = true;
+    if (C.last && idx == 0)
+      return p2p_bwd(S, sl->L[C.nl - 1].xres, P(S, S->p_final), sl->rstdf, nullptr, sl->dx_in, DG(S, S->p_final),
+                     sl->L[C.nl - 1].dy_mlp);
+    const int id2 = C.last ? idx - 1 : idx;
+    const int j = C.nl - 1 - id2 / 2;
+    SlotLayer& L = sl->L[j];
+    const LayerIdx& I = LI(S, C.l0 + j);
+    if (id2 % 2 == 0) return p2p_bwd(S, L.x1, P(S, I.ln2), L.rstd2, sl->dx_in, sl->dx_in, DG(S, I.ln2), L.dy_attn);
+    const void* xprev = j == 0 ? sl->x_in : sl->L[j - 1].xres;
+    void* dst = j > 0 ? sl->L[j - 1].dy_mlp : (C.first ? sl->dx0 : nullptr);
+    STP_TRY(p2p_bwd(S, xprev, P(S, I.ln1), L.rstd1, sl->dx_in, sl->dx_in, DG(S, I.ln1), dst));
+    if (j > 0 || C.first) return STP_OK;
+    return cb_handoff(S, C, u, sl);
+  }
   if (C.last) {
     if (idx == 0) {  // after B_HEAD: RS -> final-norm bwd -> residual grad -> AG
       const void* src = nullptr;
@@ -544,7 +853,7 @@ stp_status unit_cb(stp_stage* S, const stp_unit& u) {
       S->pb_pending = true;
       STP_TRY(rmsnorm_bwd(dt, S->sl, h, src, sl->L[C.nl - 1].xres, P(S, S->p_final), sl->rstdf, nullptr, sl->dx_in,
                           DG(S, S->p_final), st));
-      return all_gather(S, sl->dx_in, sl->L[C.nl - 1].dy_mlp, (size_t)shard);
+      return ag_dx(S, sl->dx_in, sl->L[C.nl - 1].dy_mlp, (size_t)shard);
     }
     idx -= 1;
   }
@@ -558,13 +867,21 @@ stp_status unit_cb(stp_stage* S, const stp_unit& u) {
   S->pb_pending = true;
   if (idx % 2 == 0) {  // after B_MLP: ln2 bwd + residual grad -> AG for B_ATTN
     STP_TRY(rmsnorm_bwd(dt, S->sl, h, src, L.x1, P(S, I.ln2), L.rstd2, sl->dx_in, sl->dx_in, DG(S, I.ln2), st));
-    return all_gather(S, sl->dx_in, L.dy_attn, (size_t)shard);
+    return ag_dx(S, sl->dx_in, L.dy_attn, (size_t)shard);
   }
   // after B_ATTN: ln1 bwd + residual grad
   const void* xprev = j == 0 ? sl->x_in : sl->L[j - 1].xres;
   STP_TRY(rmsnorm_bwd(dt, S->sl, h, src, xprev, P(S, I.ln1), L.rstd1, sl->dx_in, sl->dx_in, DG(S, I.ln1), st));
-  if (j > 0) return all_gather(S, sl->dx_in, sl->L[j - 1].dy_mlp, (size_t)shard);
-  if (C.first) return all_gather(S, sl->dx_in, sl->dx0, (size_t)shard);
+  if (j > 0) return ag_dx(S, sl->dx_in, sl->L[j - 1].dy_mlp, (size_t)shard);
+  if (C.first) return ag_dx(S, sl->dx_in, sl->dx0, (size_t)shard);
+  return cb_handoff(S, C, u, sl);
+}
+
+// End of a chunk's backward on a non-first chunk: at the V-shape turn hand
+// the gradient shard to the other chunk on this device now.
+stp_status cb_handoff(stp_stage* S, Chunk& C, const stp_unit& u, Slot* sl) {
+  const int64_t shard = S->sl * S->h;
+  cudaStream_t st = S->s_comm;
   if (dev_of_vs(S, C.vs - 1) == S->pp_rank) {  // V-shape turn: hand the grad to the other chunk now
     for (auto& O : S->chunks)
       if (O.vs == C.vs - 1) {
@@ -646,6 +963,10 @@ stp_status run_step(stp_stage* S, float* h_loss, stp_step_stats* stats) {
   S->ev_pool_next = 0;
   S->trace.clear();
   S->pf_pending = S->pb_pending = false;
+  S->pfi = S->pbi = 0;
+  S->pf = S->pfb[0];
+  S->pb = S->pbb[0];
+  for (int i = 0; i < 2; ++i) S->pfb_pending[i] = S->pbb_pending[i] = false;
   for (auto& C : S->chunks) {
     C.mb2slot.clear();
     for (auto& sl : C.slots) {
@@ -696,10 +1017,14 @@ stp_status run_step(stp_stage* S, float* h_loss, stp_step_stats* stats) {
     if (S->timing) STP_CUDA_TRY(cudaEventRecord(S->ev_t1[i], st));
     // comm phases consuming the partial buffers release them for the next writer
     if (u.op == STP_U_CF && S->pf_pending) {
-      STP_CUDA_TRY(cudaEventRecord(S->ev_pf, st));
+      STP_CUDA_TRY(cudaEventRecord(S->ev_pfb[S->pfi], st));
+      S->pfb_pending[S->pfi] = true;
+      S->pf_pending = false;
     }
     if (u.op == STP_U_CB && S->pb_pending) {
-      STP_CUDA_TRY(cudaEventRecord(S->ev_pb, st));
+      STP_CUDA_TRY(cudaEventRecord(S->ev_pbb[S->pbi], st));
+      S->pbb_pending[S->pbi] = true;
+      S->pb_pending = false;
     }
     // a slot is released once its last W unit is enqueued, but only at the
     // end of that action: the action's backward PP send (emitted after the W
@@ -1086,8 +1411,33 @@ stp_status stp_init_stage(const stp_model_cfg* mc, const stp_parallel_cfg* pc, c
     S->peak_bytes += (int64_t)C.slot_bytes * best[C.c];
   }
   const size_t es = S->es;
-  STP_TRY(dalloc(S.get(), &S->pf, S->s * S->h * es));
-  STP_TRY(dalloc(S.get(), &S->pb, S->s * S->h * es));
+  {
+    // TP transport: p2p (default; fused NVLink kernels), ce (copy engines),
+    // nccl (NCCL reduce-scatter / all-gather: the baseline)
+    const char* e = getenv("STP_TP_TRANSPORT");
+    const std::string tr = e ? e : "p2p";
+    if (tr != "p2p" && tr != "ce" && tr != "nccl") return fail(STP_EINVAL, "STP_TP_TRANSPORT must be p2p, ce or nccl");
+    S->ce = S->t > 1 && (tr == "ce" || tr == "p2p");
+    S->p2p = S->ce && tr == "p2p";
+    const char* w = getenv("STP_CE_WAIT");
+    S->ce_spin = w && std::string(w) == "spin";
+  }
+  STP_TRY(dalloc(S.get(), &S->pfb[0], S->s * S->h * es));
+  STP_TRY(dalloc(S.get(), &S->pbb[0], S->s * S->h * es));
+  if (S->ce) {
+    STP_TRY(dalloc(S.get(), &S->pfb[1], S->s * S->h * es));
+    STP_TRY(dalloc(S.get(), &S->pbb[1], S->s * S->h * es));
+    STP_TRY(dalloc(S.get(), &S->stage_buf, S->s * S->h * es));
+    void* f = nullptr;
+    STP_TRY(dalloc(S.get(), &f, 4096));
+    S->flags = (uint32_t*)f;
+    STP_CUDA_TRY(cudaMemset(S->flags, 0, 4096));
+  } else {
+    S->pfb[1] = S->pfb[0];
+    S->pbb[1] = S->pbb[0];
+  }
+  S->pf = S->pfb[0];
+  S->pb = S->pbb[0];
   STP_TRY(dalloc(S.get(), &S->rtmp, S->sl * S->h * es));
   STP_TRY(dalloc(S.get(), &S->ntmp, S->sl * S->h * es));
   STP_TRY(dalloc(S.get(), &S->dtmp_h, S->s * S->fi * es));
@@ -1119,8 +1469,10 @@ stp_status stp_init_stage(const stp_model_cfg* mc, const stp_parallel_cfg* pc, c
   }
   STP_CUDA_TRY(cudaEventCreate(&S->ev_base));
   STP_CUDA_TRY(cudaEventCreate(&S->ev_end));
-  STP_CUDA_TRY(cudaEventCreateWithFlags(&S->ev_pf, cudaEventDisableTiming));
-  STP_CUDA_TRY(cudaEventCreateWithFlags(&S->ev_pb, cudaEventDisableTiming));
+  for (int i = 0; i < 2; ++i) {
+    STP_CUDA_TRY(cudaEventCreateWithFlags(&S->ev_pfb[i], cudaEventDisableTiming));
+    STP_CUDA_TRY(cudaEventCreateWithFlags(&S->ev_pbb[i], cudaEventDisableTiming));
+  }
   if (const char* e = getenv("STP_GEMM_MAX_CTAS")) S->gemm_max_ctas = atoi(e);
   S->debug = getenv("STP_DEBUG") != nullptr;
   STP_TRY(init_nccl(S.get(), world_nccl_id));
@@ -1152,6 +1504,7 @@ stp_status stp_init_stage(const stp_model_cfg* mc, const stp_parallel_cfg* pc, c
     }
   }
   STP_TRY(warmup_comms(S.get()));
+  if (S->ce) STP_TRY(ce_init(S.get()));
   // every PP edge used by the unit list must have its communicator
   for (size_t i = 0; i < S->units.size(); ++i) {
     const stp_unit& u = S->units[i];
@@ -1255,6 +1608,18 @@ void stp_destroy_stage(stp_stage* st) {
   cudaSetDevice(st->dev);
   cudaDeviceSynchronize();
   for (auto& r : st->nccl_regs) ncclCommDeregister(r.first, r.second);
+  if (!st->sym_peer.empty()) {
+    // close this rank's mappings of the peers' memory, then wait until every
+    // peer has closed its mappings of ours before freeing it
+    for (auto& v : st->sym_peer)
+      for (uint8_t* p : v)
+        if (p) cudaIpcCloseMemHandle(p);
+    if (st->tpc && st->flags) {
+      ncclAllReduce(st->flags, st->flags, 1, ncclUint32, ncclMax, st->tpc, st->s_comm);
+      cudaStreamSynchronize(st->s_comm);
+    }
+  }
+  for (auto s : st->s_pull) cudaStreamDestroy(s);
   for (auto c : st->owned)
     if (c) ncclCommDestroy(c);
   for (auto e : st->ev_done) cudaEventDestroy(e);
@@ -1263,8 +1628,10 @@ void stp_destroy_stage(stp_stage* st) {
   for (auto e : st->ev_pool) cudaEventDestroy(e);
   if (st->ev_base) cudaEventDestroy(st->ev_base);
   if (st->ev_end) cudaEventDestroy(st->ev_end);
-  if (st->ev_pf) cudaEventDestroy(st->ev_pf);
-  if (st->ev_pb) cudaEventDestroy(st->ev_pb);
+  for (int i = 0; i < 2; ++i) {
+    if (st->ev_pfb[i]) cudaEventDestroy(st->ev_pfb[i]);
+    if (st->ev_pbb[i]) cudaEventDestroy(st->ev_pbb[i]);
+  }
   for (auto& kv : st->s_send) cudaStreamDestroy(kv.second);
   for (auto& kv : st->s_recv) cudaStreamDestroy(kv.second);
   if (st->s_comp) cudaStreamDestroy(st->s_comp);

@@ -18,12 +18,12 @@ CASES = [(2, 1, "stp", "f32"), (1, 2, "stp", "f32"), (2, 1, "stp", "bf16"), (1, 
          (2, 2, "1f1b-i", "f32"), (2, 2, "zb", "f32"), (4, 1, "stp", "f32"), (1, 4, "stp", "f32")]
 
 
-def run_torchrun(n, args, port, timeout=120, script="multi_rank_parity.py"):
+def run_torchrun(n, args, port, timeout=120, script="multi_rank_parity.py", env=None):
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
            "--master-addr=127.0.0.1", f"--master-port={port}",
            os.path.join(ROOT, "tests", script)] + args
     p = subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT, text=True, cwd=ROOT,
-                         start_new_session=True)
+                         start_new_session=True, env=dict(os.environ, **(env or {})))
     try:
         out, _ = p.communicate(timeout=timeout)
     except subprocess.TimeoutExpired:
@@ -42,5 +42,29 @@ def test_multi_rank_parity(tp, pp, sched, dtype):
     args = ["--tp", str(tp), "--pp", str(pp), "--sched", sched, "--dtype", dtype, "--seq", str(seq),
             "--n-micro", str(2 * pp if sched != "stp" else 4)]
     rc, out = run_torchrun(n, args, 29500 + 7 * tp + 3 * pp + len(sched))
+    assert rc == 0, out[-4000:]
+    assert out.count("PASS") == n, out[-4000:]
+
+
+# The non-default TP transports (CASES above run the default "p2p": one fused
+# kernel per comm phase, NVLink loads of the peers' partials, residual +
+# RMSNorm (bwd), NVLink stores of the all-gather): "ce" = copy-engine NVLink
+# pulls + fused RS-sum / residual / RMSNorm kernel; "nccl" = NCCL
+# reduce-scatter / all-gather (the baseline transport).
+CE_CASES = [(2, 1, "stp", "f32"), (2, 1, "stp", "bf16"), (4, 1, "stp", "f32"), (4, 1, "1f1b-i", "bf16"),
+            (2, 2, "stp", "f32"), (2, 2, "1f1b-i", "f32")]
+
+
+@pytest.mark.parametrize("transport", ["ce", "nccl"])
+@pytest.mark.parametrize("tp,pp,sched,dtype", CE_CASES)
+def test_multi_rank_parity_symmetric(tp, pp, sched, dtype, transport):
+    n = tp * pp
+    if torch.cuda.device_count() < n:
+        pytest.skip(f"needs {n} GPUs")
+    seq = 64 if dtype == "bf16" else 32
+    args = ["--tp", str(tp), "--pp", str(pp), "--sched", sched, "--dtype", dtype, "--seq", str(seq),
+            "--n-micro", str(2 * pp if sched != "stp" else 4)]
+    rc, out = run_torchrun(n, args, 29700 + 7 * tp + 3 * pp + len(sched) + len(dtype) + 50 * (transport == "nccl"),
+                           env={"STP_TP_TRANSPORT": transport})
     assert rc == 0, out[-4000:]
     assert out.count("PASS") == n, out[-4000:]

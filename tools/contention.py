@@ -34,6 +34,49 @@ def ev():
     return torch.cuda.Event(enable_timing=True)
 
 
+class Clocks:
+    """Median SM clock (MHz) and board power (W) of this rank's GPU while a
+    measured region runs (NVML, 10 ms period)."""
+
+    def __init__(self, index):
+        import threading
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+        except Exception:
+            self.nv = None
+        self.threading = threading
+
+    def __enter__(self):
+        self.samples, self.stop = [], False
+
+        def run():
+            while not self.stop and self.nv:
+                try:
+                    self.samples.append((self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM),
+                                         self.nv.nvmlDeviceGetPowerUsage(self.h) / 1000.0))
+                except Exception:
+                    break
+                import time
+                time.sleep(0.01)
+        self.th = self.threading.Thread(target=run, daemon=True)
+        self.th.start()
+        return self
+
+    def __exit__(self, *exc):
+        self.stop = True
+        self.th.join()
+
+    def median(self):
+        if not self.samples:
+            return None, None
+        c = sorted(x[0] for x in self.samples)
+        w = sorted(x[1] for x in self.samples)
+        return c[len(c) // 2], w[len(w) // 2]
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--ctas", default="0,32,16,8,4")
@@ -57,6 +100,7 @@ def main():
     full = torch.randn(s, h, generator=g, device=dev).to(bf)
     shard = torch.randn(s // t, h, generator=g, device=dev).to(bf)
     sA, sB = torch.cuda.Stream(), torch.cuda.Stream()
+    clk = Clocks(torch.cuda.current_device())
 
     def gemm_loop(n):
         for _ in range(n):
@@ -87,15 +131,17 @@ def main():
         comm_alone = maxr(e0.elapsed_time(e1) / 10)
         gemm_loop(2)
         torch.cuda.synchronize()
-        e0, e1 = run(sA, gemm_loop, a.gemm_iters)
-        torch.cuda.synchronize()
+        with clk as c_alone:
+            e0, e1 = run(sA, gemm_loop, a.gemm_iters)
+            torch.cuda.synchronize()
         gemm_alone = maxr(e0.elapsed_time(e1))
         n_comm = max(4, int(1.4 * gemm_alone / comm_alone) + 1)
         dist.barrier()
         torch.cuda.synchronize()
-        c0, c1 = run(sB, comm_fn, n_comm)
-        g0, g1 = run(sA, gemm_loop, a.gemm_iters)
-        torch.cuda.synchronize()
+        with clk as c_ov:
+            c0, c1 = run(sB, comm_fn, n_comm)
+            g0, g1 = run(sA, gemm_loop, a.gemm_iters)
+            torch.cuda.synchronize()
         gemm_ov = maxr(g0.elapsed_time(g1))
         comm_ov = maxr(c0.elapsed_time(c1) / n_comm)
         flops = a.gemm_iters * 2 * s * h * 3 * I  # FC1 (N = 2I) + FC2 (K = I)
@@ -103,7 +149,8 @@ def main():
                "comm_busbw_alone_GBps": 2 * (t - 1) / t * s * h * 2 / comm_alone / 1e6,
                "gemm_alone_ms": gemm_alone, "gemm_overlapped_ms": gemm_ov,
                "gemm_alone_tflops": flops / gemm_alone / 1e9,
-               "contention": gemm_ov / gemm_alone, "comm_slowdown": comm_ov / comm_alone}
+               "contention": gemm_ov / gemm_alone, "comm_slowdown": comm_ov / comm_alone,
+               "rank0_sm_mhz_power_w": {"gemm_alone": c_alone.median(), "overlapped": c_ov.median()}}
         if rank == 0:
             print(json.dumps(rec), flush=True)
 

@@ -34,6 +34,7 @@ struct GemmArgs {
   int* tile_ctr;  // dynamic tile scheduler counter (0 at launch; reset by the last fetch)
   int M, N, K;
   int num_m_blk, num_n_blk, num_k_blk;
+  int n_fast;  // tile raster: 0 = m-block fastest (A re-swept per n-block), 1 = n-block fastest
   int epilogue;
   void* C;
   int64_t ldc;
@@ -176,7 +177,8 @@ __global__ void __launch_bounds__(256, 1)
         ring[rs] = tile;
         mbar_arrive(ring_full + rs);
         if (tile < 0) break;
-        const int mb = tile % p.num_m_blk, nb = tile / p.num_m_blk;
+        const int mb = p.n_fast ? tile / p.num_n_blk : tile % p.num_m_blk;
+        const int nb = p.n_fast ? tile % p.num_n_blk : tile / p.num_m_blk;
         for (int kb = 0; kb < p.num_k_blk; ++kb) {
           mbar_wait(empty + stage, phase ^ 1);
           mbar_arrive_expect_tx(full + stage, C::A_BYTES + C::B_BYTES);
@@ -248,7 +250,8 @@ __global__ void __launch_bounds__(256, 1)
       __syncwarp();
       if (lane == 0) mbar_arrive(ring_empty + rs);
       if (tile < 0) break;
-      const int mb = tile % p.num_m_blk, nb = tile / p.num_m_blk;
+      const int mb = p.n_fast ? tile / p.num_n_blk : tile % p.num_m_blk;
+      const int nb = p.n_fast ? tile % p.num_n_blk : tile / p.num_m_blk;
       const int acc = local & 1;
       const uint32_t acc_phase = (local >> 1) & 1;
       mbar_wait(tfull + acc, acc_phase);
@@ -365,7 +368,8 @@ __global__ void __launch_bounds__(256, 1)
           release_slot(rs);
         }
         if (tile < 0) break;
-        const int mb = 2 * (tile % n_mp) + (int)rank, nb = tile / n_mp;
+        const int mb = 2 * (p.n_fast ? tile / p.num_n_blk : tile % n_mp) + (int)rank;
+        const int nb = p.n_fast ? tile % p.num_n_blk : tile / n_mp;
         for (int kb = 0; kb < p.num_k_blk; ++kb) {
           mbar_wait_cluster(empty + stage, phase ^ 1);
           mbar_arrive_expect_tx(full + stage, C::A_BYTES + C::B_BYTES);
@@ -441,7 +445,8 @@ __global__ void __launch_bounds__(256, 1)
       __syncwarp();
       if (lane == 0) release_slot(rs);
       if (tile < 0) break;
-      const int mb = 2 * (tile % n_mp) + (int)rank, nb = tile / n_mp;
+      const int mb = 2 * (p.n_fast ? tile / p.num_n_blk : tile % n_mp) + (int)rank;
+      const int nb = p.n_fast ? tile % p.num_n_blk : tile / n_mp;
       const int acc = local & 1;
       const uint32_t acc_phase = (local >> 1) & 1;
       mbar_wait(tfull + acc, acc_phase);
@@ -558,8 +563,8 @@ __global__ void __launch_bounds__(256, 1)
           release_slot(rs);
         }
         if (tile < 0) break;
-        const int m0 = (tile % num_m2) * 256 + (int)rank * 128;
-        const int n0 = (tile / num_m2) * 256 + (int)rank * 128;
+        const int m0 = (p.n_fast ? tile / num_n2 : tile % num_m2) * 256 + (int)rank * 128;
+        const int n0 = (p.n_fast ? tile % num_n2 : tile / num_m2) * 256 + (int)rank * 128;
         for (int kb = 0; kb < p.num_k_blk; ++kb) {
           mbar_wait(empty + stage, phase ^ 1);
           if (rank == 0) mbar_arrive_expect_tx(full + stage, 2 * S2_STAGE);
@@ -637,8 +642,8 @@ __global__ void __launch_bounds__(256, 1)
       const uint32_t acc_phase = (local >> 1) & 1;
       mbar_wait(tfull + acc, acc_phase);
       tc_fence_after();
-      const int row = (tile % num_m2) * 256 + (int)rank * 128 + ew * 32 + lane;
-      const int nb0 = (tile / num_m2) * 256;
+      const int row = (p.n_fast ? tile / num_n2 : tile % num_m2) * 256 + (int)rank * 128 + ew * 32 + lane;
+      const int nb0 = (p.n_fast ? tile % num_n2 : tile / num_m2) * 256;
 #pragma unroll 1
       for (int c0 = 0; c0 < 256; c0 += 32) {
         uint32_t v[32];
@@ -852,14 +857,19 @@ stp_status gemm_bf16(int layout, int epi, int64_t M, int64_t N, int64_t K, const
   STP_CHECK_ARG(epi != STP_EPI_BIAS || bias != nullptr, "BIAS epilogue needs bias");
   const bool a_mn = (layout == STP_GEMM_TN);
   const bool b_mn = (layout == STP_GEMM_NN || layout == STP_GEMM_TN);
-  // BN choice: minimise (waves x BN) with a small penalty for the narrow tile.
+  // Kernel / tile choice: maximise (wave efficiency x per-tile throughput).
+  // Per-tile tensor-pipe activity measured with ncu on B200 (round 1): 1-SM
+  // 128x128 ~0.60, 1-SM 128x256 ~0.80, 2-SM 256x256 ~0.90 of peak (the
+  // narrow tiles re-read more operand bytes from shared memory per FLOP).
   const int sms = (max_ctas > 0 && max_ctas < num_sms()) ? max_ctas : num_sms();
-  auto cost = [&](int bn) {
-    int64_t tiles = ((M + BM - 1) / BM) * ((N + bn - 1) / bn);
-    int64_t waves = (tiles + sms - 1) / sms;
-    return (double)waves * bn * (bn == 128 ? 1.08 : 1.0);
+  auto eff = [](int64_t tiles, int64_t slots) {
+    const int64_t waves = (tiles + slots - 1) / slots;
+    return (double)tiles / (double)(waves * slots);
   };
-  const int BNsel = (N <= 128 || cost(128) < cost(256)) ? 128 : 256;
+  auto score1 = [&](int bn) {
+    return eff(((M + BM - 1) / BM) * ((N + bn - 1) / bn), sms) * (bn == 128 ? 0.60 : 0.80);
+  };
+  const int BNsel = (N <= 128 || score1(128) > score1(256)) ? 128 : 256;
   GemmArgs g;
   STP_TRY(tile_counter(st, &g.tile_ctr));
   g.M = (int)M;
@@ -868,6 +878,11 @@ stp_status gemm_bf16(int layout, int epi, int64_t M, int64_t N, int64_t K, const
   g.num_m_blk = (int)((M + BM - 1) / BM);
   g.num_n_blk = (int)((N + BNsel - 1) / BNsel);
   g.num_k_blk = (int)((K + BK - 1) / BK);
+  // Raster: the operand swept once per block of the other one is re-read
+  // from L2 only if it fits; sweep the smaller operand fastest, so the large
+  // one streams from HBM once (e.g. the FC1 weight-gradient GEMM: A = dGU^T
+  // 466 MB, B = Xn 44 MB -> n-fastest; m-fastest re-read A 14x, 7 GB / call).
+  g.n_fast = (M > N) ? 1 : 0;
   g.epilogue = epi;
   g.C = Cp;
   g.ldc = ldc;
@@ -881,15 +896,8 @@ stp_status gemm_bf16(int layout, int epi, int64_t M, int64_t N, int64_t K, const
   if (s != STP_OK) return s;
   bool use_2sm = gemm_mc_mode() == 3 && M > 128;
   if (gemm_mc_mode() == 1 && M > 128) {
-    const int nsm = (max_ctas > 0 && max_ctas < num_sms()) ? max_ctas : num_sms();
-    auto eff = [](int64_t tiles, int64_t slots) {
-      const int64_t waves = (tiles + slots - 1) / slots;
-      return (double)tiles / (double)(waves * slots);
-    };
-    const int64_t t1 = ((M + BM - 1) / BM) * ((N + BNsel - 1) / BNsel);
     const int64_t t2 = ((M + 255) / 256) * ((N + 255) / 256);
-    // measured per-tile advantage of the 2-SM kernel ~1.1-1.25x on these shapes
-    use_2sm = eff(t2, nsm / 2) * 1.12 >= eff(t1, nsm);
+    use_2sm = eff(t2, sms / 2) * 0.90 >= score1(BNsel);
   }
   if (use_2sm) {
     // 2-SM: per-CTA boxes of 128 rows (K-major) / 2 x 64 columns (MN-major)

@@ -41,6 +41,7 @@ def main():
     ap.add_argument("--attn-fwd", default="1,2")
     ap.add_argument("--attn-bwd", default="1,2")
     ap.add_argument("--skip-gemm", action="store_true")
+    ap.add_argument("--only", default="", help="comma list of GEMM names (e.g. fc1_wgrad); skips attention")
     a = ap.parse_args()
     t, s = a.tp, a.seq
     h, I, V = 3584, 18944 // t, 152064 // t
@@ -58,6 +59,8 @@ def main():
         for mc in [int(x) for x in a.gemm_mc.split(",")]:
             _lib.call("stp_set_option", b"gemm_mc", mc)
             for name, lay, M, N, K, epi in gemms:
+                if a.only and name not in a.only.split(","):
+                    continue
                 if lay == 0:
                     A = torch.randn(M, K, device=dev, dtype=bf)
                     B = torch.randn(N, K, device=dev, dtype=bf)
@@ -72,6 +75,8 @@ def main():
                 print(json.dumps({"kernel": "gemm", "name": name, "gemm_mc": mc, "M": M, "N": N, "K": K,
                                   "ms": ms, "tflops": 2 * M * N * K / ms / 1e9}), flush=True)
                 del A, B, C
+    if a.only:
+        return
     x = torch.randn(s, qkv, device=dev, dtype=bf)
     o = torch.empty(s, nq * d, device=dev, dtype=bf)
     lse = torch.empty(nq, s, device=dev, dtype=torch.float32)

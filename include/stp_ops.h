@@ -136,8 +136,12 @@ int32_t stp_num_sms(void);
 /* Kernels launched by this library on the calling thread since load. */
 int64_t stp_kernel_launches(void);
 
-/* Runtime tuning knobs: "gemm_mc" = 2 (2-CTA cluster GEMM with B-tile TMA
- * multicast, default) or 0 (single-CTA GEMM).  STP_EINVAL for unknown keys. */
+/* Runtime tuning knobs (process-wide; STP_EINVAL for unknown keys / values):
+ *   "gemm_mc"  0 = 1-SM tcgen05 GEMM, 1 = automatic 1-SM / 2-SM choice per
+ *              shape (default), 2 = 2-CTA cluster with B-tile TMA multicast,
+ *              3 = always the 2-SM (cta_group::2) kernel
+ *   "attn_fwd" 1..3 forward attention kernel version (0 = default, 3)
+ *   "attn_bwd" 1..4 backward attention kernel version (0 = default, 4) */
 stp_status stp_set_option(const char* key, int64_t value);
 
 /* ------------------------------------------------------------ profiling

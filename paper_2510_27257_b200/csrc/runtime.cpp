@@ -65,6 +65,8 @@ void prof_push(int cls, double flops, double bytes, cudaEvent_t e0, cudaEvent_t 
 int& gemm_mc_mode_ref();
 int& attn_bwd_version_ref();
 int& attn_fwd_version_ref();
+constexpr int kAttnFwdDefault = 3;
+constexpr int kAttnBwdDefault = 4;
 
 }  // namespace stp
 
@@ -79,14 +81,14 @@ stp_status stp_set_option(const char* key, int64_t value) {
     stp::gemm_mc_mode_ref() = (int)value;
     return STP_OK;
   }
-  if (k == "attn_fwd") {
-    if (value < 1 || value > 3) return stp::fail(STP_EINVAL, "attn_fwd must be 1, 2 or 3");
-    stp::attn_fwd_version_ref() = (int)value;
+  if (k == "attn_fwd") {  // 0 = built-in default
+    if (value < 0 || value > 3) return stp::fail(STP_EINVAL, "attn_fwd must be 0..3");
+    stp::attn_fwd_version_ref() = value ? (int)value : stp::kAttnFwdDefault;
     return STP_OK;
   }
   if (k == "attn_bwd") {
-    if (value < 1 || value > 3) return stp::fail(STP_EINVAL, "attn_bwd must be 1, 2 or 3");
-    stp::attn_bwd_version_ref() = (int)value;
+    if (value < 0 || value > 4) return stp::fail(STP_EINVAL, "attn_bwd must be 0..4");
+    stp::attn_bwd_version_ref() = value ? (int)value : stp::kAttnBwdDefault;
     return STP_OK;
   }
   return stp::fail(STP_EINVAL, "unknown option " + k);

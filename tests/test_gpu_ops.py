@@ -209,17 +209,18 @@ def test_colsum(dt):
     assert np.abs(_np(acc) - (1 + X.sum(0))).max() <= 1e-3
 
 
-@pytest.mark.parametrize("version", [1, 2])
-@pytest.mark.parametrize("s,nq,nkv", [(257, 7, 1), (1024, 4, 2), (2048, 7, 1), (300, 2, 2)])
+@pytest.mark.parametrize("version", [1, 2, 3, 4])
+@pytest.mark.parametrize("s,nq,nkv", [(257, 7, 1), (1024, 4, 2), (2048, 7, 1), (300, 2, 2), (64, 2, 1), (65, 2, 1)])
 def test_attention_bwd_variants(s, nq, nkv, version):
     """tcgen05 backward variants: 1 = P^T/dS^T via smem, 2 = TMEM-resident with
-    4 softmax warps (3 = default, 8 softmax warps: covered above)."""
+    4 softmax warps, 3 = 8 softmax warps, 4 = 64-row query tiles with
+    double-buffered S^T/dP^T (default)."""
     from paper_2510_27257_b200 import _lib
     _lib.call("stp_set_option", b"attn_bwd", version)
     try:
         test_attention_fwd_bwd("bf16", s, nq, nkv, 128)
     finally:
-        _lib.call("stp_set_option", b"attn_bwd", 3)
+        _lib.call("stp_set_option", b"attn_bwd", 0)
 
 
 @pytest.mark.parametrize("version", [1, 2])
@@ -232,4 +233,4 @@ def test_attention_fwd_variants(s, nq, nkv, version):
     try:
         test_attention_fwd_bwd("bf16", s, nq, nkv, 128)
     finally:
-        _lib.call("stp_set_option", b"attn_fwd", 3)
+        _lib.call("stp_set_option", b"attn_fwd", 0)

@@ -38,8 +38,8 @@ def main():
     ap.add_argument("--seq", type=int, default=6144)
     ap.add_argument("--iters", type=int, default=10)
     ap.add_argument("--gemm-mc", default="0,2")
-    ap.add_argument("--attn-fwd", default="1,2")
-    ap.add_argument("--attn-bwd", default="1,2")
+    ap.add_argument("--attn-fwd", default="3")
+    ap.add_argument("--attn-bwd", default="3,4")
     ap.add_argument("--skip-gemm", action="store_true")
     ap.add_argument("--only", default="", help="comma list of GEMM names (e.g. fc1_wgrad); skips attention")
     a = ap.parse_args()
@@ -86,7 +86,7 @@ def main():
         ms = timed(lambda: ops.attn_fwd(x, nq, nkv, d, o, lse), a.iters)
         print(json.dumps({"kernel": "attn_fwd", "version": v, "s": s, "nq": nq, "nkv": nkv, "ms": ms,
                           "tflops": 4 * pairs * nq * d / ms / 1e9}), flush=True)
-    _lib.call("stp_set_option", b"attn_fwd", 1)
+    _lib.call("stp_set_option", b"attn_fwd", 0)
     ops.attn_fwd(x, nq, nkv, d, o, lse)
     do = torch.randn(s, nq * d, device=dev, dtype=bf)
     dx = torch.empty_like(x)

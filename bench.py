@@ -168,6 +168,11 @@ def workload_config(args, cfg, tp_pp):
 
 
 # ------------------------------------------------------------------ ours
+def progress(msg):
+    """Progress to stderr (the JSON contract line is the only stdout line)."""
+    print(f"[bench {time.strftime('%H:%M:%S')}] {msg}", file=sys.stderr, flush=True)
+
+
 def ours(args):
     import torch
     import torch.distributed as dist
@@ -210,7 +215,9 @@ def ours(args):
                 prm.copy_(torch.randn(prm.shape, generator=g, device=prm.device, dtype=torch.float32) * 0.02)
         return stg
 
+    progress(f"init stage tp{t} pp{p} {args.sched}")
     st = make_stage(args.sched)
+    progress("stage ready")
     toks, tgts = si.make_tokens(cfg, args.m, seed=1234)
     d_tok = torch.from_numpy(toks).cuda()
     d_tgt = torch.from_numpy(tgts).cuda()
@@ -222,8 +229,9 @@ def ours(args):
         if world > 1:
             dist.barrier()
 
-    for _ in range(args.warmup):
+    for i in range(args.warmup):
         st.step(d_tok, d_tgt)
+        progress(f"warm-up step {i + 1}/{args.warmup}")
     st.zero_grads()
     barrier()
     L.call("stp_prof_reset")
@@ -244,6 +252,7 @@ def ours(args):
         L.call("stp_prof_read", cls, L.C.byref(c), L.C.byref(fl), L.C.byref(by), L.C.byref(tm))
         prof[nm] = (c.value, fl.value, by.value, tm.value)
     L.call("stp_prof_reset")
+    progress("timed steps done")
     # one extra step with per-unit events: exposed TP and PP bubble
     st.set_timing(True)
     _, tstats = st.step(d_tok, d_tgt)
@@ -255,6 +264,7 @@ def ours(args):
         st.step_host(h_tok.numpy(), h_tgt.numpy())
     barrier()
     e2e_s = (time.perf_counter() - t0) / args.steps
+    progress("e2e steps done")
 
     step_ms = float(np.mean(ms))
     vals = torch.tensor([step_ms, e2e_s, tstats.exposed_tp_ms / max(tstats.step_ms, 1e-9),
@@ -306,6 +316,7 @@ def ours(args):
             "clocks": clk.summary(),
         }
         if world == 1 and not args.no_cpu:
+            progress("cpu oracle sample")
             dt, fl, _ = cpu_sample()
             cpu_tok = (fl / dt) / gemm_flops_per_token(cfg)
             line["cpu_baseline"] = {"value": cpu_tok, "unit": "tokens/s", "cores": cpu_cores(), "kind": "oracle",

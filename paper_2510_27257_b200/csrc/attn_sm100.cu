@@ -574,11 +574,11 @@ __global__ void __launch_bounds__(FWD3_THREADS, 1)
       for (int j = 0; j < n_kv; ++j) {
         const int b = j & 1;
         const uint32_t ph = (j >> 1) & 1;
-        mbar_wait(k_empty + b, ph ^ 1);
+        mbar_wait_wd(k_empty + b, ph ^ 1, 301, a.s, a.nq, (int)blockIdx.y);
         mbar_arrive_expect_tx(k_full + b, TILE_BYTES);
         tma_load_2d(sK + b * TILE_BYTES, &tm_qkv, k_full + b, kcol, j * T);
         tma_load_2d(sK + b * TILE_BYTES + ATOM, &tm_qkv, k_full + b, kcol + 64, j * T);
-        mbar_wait(v_empty + b, ph ^ 1);
+        mbar_wait_wd(v_empty + b, ph ^ 1, 302, a.s, a.nq, (int)blockIdx.y);
         mbar_arrive_expect_tx(v_full + b, TILE_BYTES);
         tma_load_2d(sV + b * TILE_BYTES, &tm_qkv, v_full + b, vcol, j * T);
         tma_load_2d(sV + b * TILE_BYTES + ATOM, &tm_qkv, v_full + b, vcol + 64, j * T);
@@ -589,11 +589,11 @@ __global__ void __launch_bounds__(FWD3_THREADS, 1)
       constexpr uint32_t idS = make_idesc_bf16(T, T, false, false);
       constexpr uint32_t idO = make_idesc_bf16(T, D, false, true);
       const uint32_t q_addr = smem_u32(sQ);
-      mbar_wait(q_full, 0);
+      mbar_wait_wd(q_full, 0, 303, a.s, a.nq, (int)blockIdx.y);
       auto issue_pv = [&](int jj) {
         const int b = jj & 1;
-        mbar_wait(p_full + b, (jj >> 1) & 1);
-        mbar_wait(v_full + b, (jj >> 1) & 1);
+        mbar_wait_wd(p_full + b, (jj >> 1) & 1, 304, a.s, a.nq, (int)blockIdx.y);
+        mbar_wait_wd(v_full + b, (jj >> 1) & 1, 305, a.s, a.nq, (int)blockIdx.y);
         tc_fence_after();
         const uint32_t v_addr = smem_u32(sV + b * TILE_BYTES);
 #pragma unroll
@@ -606,8 +606,8 @@ __global__ void __launch_bounds__(FWD3_THREADS, 1)
       for (int j = 0; j < n_kv; ++j) {
         const int b = j & 1;
         const uint32_t ph = (j >> 1) & 1;
-        mbar_wait(k_full + b, ph);
-        mbar_wait(s_empty + b, ph ^ 1);
+        mbar_wait_wd(k_full + b, ph, 306, a.s, a.nq, (int)blockIdx.y);
+        mbar_wait_wd(s_empty + b, ph ^ 1, 307, a.s, a.nq, (int)blockIdx.y);
         tc_fence_after();
         const uint32_t k_addr = smem_u32(sK + b * TILE_BYTES);
 #pragma unroll
@@ -632,7 +632,7 @@ __global__ void __launch_bounds__(FWD3_THREADS, 1)
     float m = -INFINITY, l = 0.f;
     for (int j = 0; j < n_kv; ++j) {
       const int b = j & 1;
-      mbar_wait(s_full + b, (j >> 1) & 1);
+      mbar_wait_wd(s_full + b, (j >> 1) & 1, 308, a.s, a.nq, (int)blockIdx.y);
       tc_fence_after();
       uint32_t u[64];
       tmem_ld_32x32b_x32(tS0 + b * 128 + half * 64 + lane_off, u);
@@ -664,7 +664,7 @@ __global__ void __launch_bounds__(FWD3_THREADS, 1)
           m = mx;
         }
         if (j > 0) {
-          mbar_wait(o_done + ((j - 1) & 1), ((j - 1) >> 1) & 1);
+          mbar_wait_wd(o_done + ((j - 1) & 1), ((j - 1) >> 1) & 1, 309, a.s, a.nq, (int)blockIdx.y);
           tc_fence_after();
 #pragma unroll 1
           for (int c = 0; c < 2; ++c) {
@@ -679,7 +679,7 @@ __global__ void __launch_bounds__(FWD3_THREADS, 1)
           tmem_wait_st();
         }
       } else if (j >= 2) {
-        mbar_wait(o_done + b, ((j - 2) >> 1) & 1);
+        mbar_wait_wd(o_done + b, ((j - 2) >> 1) & 1, 310, a.s, a.nq, (int)blockIdx.y);
       }
       const float nm = -m;
 #pragma unroll
@@ -696,7 +696,7 @@ __global__ void __launch_bounds__(FWD3_THREADS, 1)
     ssum[half * T + r] = l;
     named_bar(2, 256);
     const float lt = ssum[r] + ssum[T + r];
-    mbar_wait(o_done + ((n_kv - 1) & 1), ((n_kv - 1) >> 1) & 1);
+    mbar_wait_wd(o_done + ((n_kv - 1) & 1), ((n_kv - 1) >> 1) & 1, 311, a.s, a.nq, (int)blockIdx.y);
     tc_fence_after();
     const bool valid = qrow < a.s;
     const float inv = 1.f / lt;
@@ -1597,11 +1597,11 @@ __global__ void __launch_bounds__(384, 1)
       for (int j = 0; j < n_kv; ++j) {
         const int b = j & 1;
         const uint32_t ph = (j >> 1) & 1;
-        mbar_wait(k_empty + b, ph ^ 1);
+        mbar_wait_wd(k_empty + b, ph ^ 1, 201, a.s, a.nq, (int)blockIdx.y);
         mbar_arrive_expect_tx(k_full + b, TILE_BYTES);
         tma_load_2d(sK + b * TILE_BYTES, &tm_qkv, k_full + b, kcol, j * T);
         tma_load_2d(sK + b * TILE_BYTES + ATOM, &tm_qkv, k_full + b, kcol + 64, j * T);
-        mbar_wait(v_empty + b, ph ^ 1);
+        mbar_wait_wd(v_empty + b, ph ^ 1, 202, a.s, a.nq, (int)blockIdx.y);
         mbar_arrive_expect_tx(v_full + b, TILE_BYTES);
         tma_load_2d(sV + b * TILE_BYTES, &tm_qkv, v_full + b, vcol, j * T);
         tma_load_2d(sV + b * TILE_BYTES + ATOM, &tm_qkv, v_full + b, vcol + 64, j * T);
@@ -1612,12 +1612,12 @@ __global__ void __launch_bounds__(384, 1)
       constexpr uint32_t idKK = make_idesc_bf16(T, T, false, false);  // S, dP: both operands K-major
       constexpr uint32_t idQ = make_idesc_bf16(T, D, false, true);    // dQ += dS K (K MN-major)
       const uint32_t q_addr = smem_u32(sQ), do_addr = smem_u32(sdO);
-      mbar_wait(qdo_full, 0);
+      mbar_wait_wd(qdo_full, 0, 203, a.s, a.nq, (int)blockIdx.y);
       auto issue_sdp = [&](int j) {
         const int b = j & 1;
         const uint32_t ph = (j >> 1) & 1;
-        mbar_wait(k_full + b, ph);
-        mbar_wait(v_full + b, ph);
+        mbar_wait_wd(k_full + b, ph, 204, a.s, a.nq, (int)blockIdx.y);
+        mbar_wait_wd(v_full + b, ph, 205, a.s, a.nq, (int)blockIdx.y);
         tc_fence_after();
         const uint32_t k_addr = smem_u32(sK + b * TILE_BYTES), v_addr = smem_u32(sV + b * TILE_BYTES);
 #pragma unroll
@@ -1638,11 +1638,11 @@ __global__ void __launch_bounds__(384, 1)
       issue_sdp(0);
       for (int j = 0; j < n_kv; ++j) {
         if (j + 1 < n_kv) {
-          mbar_wait(sdp_empty, j & 1);  // softmax has read S/dP of tile j
+          mbar_wait_wd(sdp_empty, j & 1, 206, a.s, a.nq, (int)blockIdx.y);  // softmax has read S/dP of tile j
           issue_sdp(j + 1);
         }
         const int b = j & 1;
-        mbar_wait(ds_full + b, (j >> 1) & 1);
+        mbar_wait_wd(ds_full + b, (j >> 1) & 1, 207, a.s, a.nq, (int)blockIdx.y);
         tc_fence_after();
         const uint32_t k_addr = smem_u32(sK + b * TILE_BYTES);
 #pragma unroll
@@ -1664,7 +1664,7 @@ __global__ void __launch_bounds__(384, 1)
     const float Dv = vrow ? a.Dl[(int64_t)h * a.s + qrow] : 0.f;
     const float sl2 = a.scale_log2;
     for (int j = 0; j < n_kv; ++j) {
-      mbar_wait(sdp_full, j & 1);
+      mbar_wait_wd(sdp_full, j & 1, 208, a.s, a.nq, (int)blockIdx.y);
       tc_fence_after();
       uint32_t sv[64], dv[64];
       tmem_ld_32x32b_x32(tS + half * 64 + lane_off, sv);
@@ -1689,13 +1689,13 @@ __global__ void __launch_bounds__(384, 1)
         pk[i >> 1] = pack2(d2[0], d2[1]);
       }
       const int b = j & 1;
-      if (j >= 2) mbar_wait(dq_done + b, ((j - 2) >> 1) & 1);
+      if (j >= 2) mbar_wait_wd(dq_done + b, ((j - 2) >> 1) & 1, 209, a.s, a.nq, (int)blockIdx.y);
       tmem_st_32x32b_x32(tdS0 + b * 64 + half * 32 + lane_off, pk);
       tmem_wait_st();
       tc_fence_before();
       mbar_arrive(ds_full + b);
     }
-    mbar_wait(dq_done + ((n_kv - 1) & 1), ((n_kv - 1) >> 1) & 1);
+    mbar_wait_wd(dq_done + ((n_kv - 1) & 1), ((n_kv - 1) >> 1) & 1, 210, a.s, a.nq, (int)blockIdx.y);
     tc_fence_after();
     bf16* orow = reinterpret_cast<bf16*>(a.dq) + (int64_t)(vrow ? qrow : 0) * a.ldd + (int64_t)h * D + half * 64;
 #pragma unroll 1
@@ -1781,7 +1781,7 @@ __global__ void __launch_bounds__(384, 1)
       tma_load_2d(sV + ATOM, &tm_qkv, kv_full, vcol + 64, kt * T);
       for (int it = 0; it < n_q; ++it) {
         const int b = it & 1, qi = kt + it;
-        mbar_wait(qdo_empty + b, ((it >> 1) & 1) ^ 1);
+        mbar_wait_wd(qdo_empty + b, ((it >> 1) & 1) ^ 1, 211, a.s, a.nq, (int)blockIdx.y);
         mbar_arrive_expect_tx(qdo_full + b, 2 * TILE_BYTES);
         uint8_t* q = sQ + b * TILE_BYTES;
         uint8_t* o = sdO + b * TILE_BYTES;
@@ -1796,11 +1796,11 @@ __global__ void __launch_bounds__(384, 1)
       constexpr uint32_t idKK = make_idesc_bf16(T, T, false, false);
       constexpr uint32_t idMN = make_idesc_bf16(T, D, false, true);
       const uint32_t k_addr = smem_u32(sK), v_addr = smem_u32(sV);
-      mbar_wait(kv_full, 0);
+      mbar_wait_wd(kv_full, 0, 212, a.s, a.nq, (int)blockIdx.y);
       for (int it = 0; it < n_q; ++it) {
         const int b = it & 1;
         const uint32_t q_addr = smem_u32(sQ + b * TILE_BYTES), do_addr = smem_u32(sdO + b * TILE_BYTES);
-        mbar_wait(qdo_full + b, (it >> 1) & 1);
+        mbar_wait_wd(qdo_full + b, (it >> 1) & 1, 213, a.s, a.nq, (int)blockIdx.y);
         tc_fence_after();
 #pragma unroll
         for (int kk = 0; kk < D / 16; ++kk) {
@@ -1815,7 +1815,7 @@ __global__ void __launch_bounds__(384, 1)
                      kk > 0 ? 1u : 0u);
         }
         mma_commit(sdp_full);
-        mbar_wait(pds_full, it & 1);
+        mbar_wait_wd(pds_full, it & 1, 214, a.s, a.nq, (int)blockIdx.y);
         tc_fence_after();
 #pragma unroll
         for (int kk = 0; kk < T / 16; ++kk)  // dV += P^T dO_i   (P^T from TMEM, 8 columns per k16)
@@ -1848,7 +1848,7 @@ __global__ void __launch_bounds__(384, 1)
       named_bar(1, 256);
       const float* nl = s_lse + b * T + half * 64;
       const float* Dq = s_D + b * T + half * 64;
-      mbar_wait(sdp_full, it & 1);
+      mbar_wait_wd(sdp_full, it & 1, 215, a.s, a.nq, (int)blockIdx.y);
       tc_fence_after();
       uint32_t sv[64], dv[64];
       tmem_ld_32x32b_x32(tS + half * 64 + lane_off, sv);
@@ -1883,7 +1883,7 @@ __global__ void __launch_bounds__(384, 1)
       tc_fence_before();
       mbar_arrive(pds_full);
     }
-    mbar_wait(done, 0);
+    mbar_wait_wd(done, 0, 216, a.s, a.nq, (int)blockIdx.y);
     tc_fence_after();
     float* kr = a.dk_part + ((int64_t)h * a.s + (vrow ? krow : 0)) * D + half * 64;
     float* vr = a.dv_part + ((int64_t)h * a.s + (vrow ? krow : 0)) * D + half * 64;
@@ -1991,7 +1991,7 @@ __global__ void __launch_bounds__(384, 1)
       tma_load_2d(sV + ATOM, &tm_kv, kv_full, vcol + 64, kt * T);
       for (int it = 0; it < n_q; ++it) {
         const int st = it % KV4_STAGES, qi = q0 + it;
-        mbar_wait(qdo_empty + st, ((it / KV4_STAGES) & 1) ^ 1);
+        mbar_wait_wd(qdo_empty + st, ((it / KV4_STAGES) & 1) ^ 1, 217, a.s, a.nq, (int)blockIdx.y);
         mbar_arrive_expect_tx(qdo_full + st, 2 * QT_BYTES);
         uint8_t* q = sQ + st * QT_BYTES;
         uint8_t* o = sdO + st * QT_BYTES;
@@ -2006,11 +2006,11 @@ __global__ void __launch_bounds__(384, 1)
       constexpr uint32_t idS = make_idesc_bf16(T, QT, false, false);  // S^T, dP^T: M = 128 keys, N = 64 queries
       constexpr uint32_t idMN = make_idesc_bf16(T, D, false, true);   // dV, dK: N = d, B (dO_i, Q_i) MN-major
       const uint32_t k_addr = smem_u32(sK), v_addr = smem_u32(sV);
-      mbar_wait(kv_full, 0);
+      mbar_wait_wd(kv_full, 0, 218, a.s, a.nq, (int)blockIdx.y);
       auto issue_sdp = [&](int it) {
         const int st = it % KV4_STAGES, b = it & 1;
         const uint32_t q_addr = smem_u32(sQ + st * QT_BYTES), do_addr = smem_u32(sdO + st * QT_BYTES);
-        mbar_wait(qdo_full + st, (it / KV4_STAGES) & 1);
+        mbar_wait_wd(qdo_full + st, (it / KV4_STAGES) & 1, 219, a.s, a.nq, (int)blockIdx.y);
         tc_fence_after();
         const uint32_t tS = tSP + b * 128, tP = tS + 64;
 #pragma unroll
@@ -2033,7 +2033,7 @@ __global__ void __launch_bounds__(384, 1)
         const int st = it % KV4_STAGES, b = it & 1;
         const uint32_t q_addr = smem_u32(sQ + st * QT_BYTES), do_addr = smem_u32(sdO + st * QT_BYTES);
         const uint32_t tS = tSP + b * 128, tP = tS + 64;
-        mbar_wait(pds_full + b, (it >> 1) & 1);
+        mbar_wait_wd(pds_full + b, (it >> 1) & 1, 220, a.s, a.nq, (int)blockIdx.y);
         tc_fence_after();
 #pragma unroll
         for (int kk = 0; kk < QT / 16; ++kk)  // dV += P^T dO_i   (P^T from TMEM, 8 columns per k16)
@@ -2067,7 +2067,7 @@ __global__ void __launch_bounds__(384, 1)
       const float* nl = s_lse + b * QT + half * 32;
       const float* Dq = s_D + b * QT + half * 32;
       const uint32_t tS = tSP + b * 128, tP = tS + 64;
-      mbar_wait(sdp_full + b, (it >> 1) & 1);
+      mbar_wait_wd(sdp_full + b, (it >> 1) & 1, 221, a.s, a.nq, (int)blockIdx.y);
       tc_fence_after();
       uint32_t sv[32], dv[32];
       tmem_ld_32x32b_x32(tS + half * 32 + lane_off, sv);
@@ -2100,7 +2100,7 @@ __global__ void __launch_bounds__(384, 1)
       tc_fence_before();
       mbar_arrive(pds_full + b);
     }
-    mbar_wait(done, 0);
+    mbar_wait_wd(done, 0, 222, a.s, a.nq, (int)blockIdx.y);
     tc_fence_after();
     float* kr = a.dk_part + ((int64_t)h * a.s + (vrow ? krow : 0)) * D + half * 64;
     float* vr = a.dv_part + ((int64_t)h * a.s + (vrow ? krow : 0)) * D + half * 64;

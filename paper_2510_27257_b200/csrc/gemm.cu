@@ -170,7 +170,7 @@ __global__ void __launch_bounds__(256, 1)
       uint32_t phase = 0;
       for (int it = 0;; ++it) {
         const int rs = it & 3;
-        mbar_wait(ring_empty + rs, ((it >> 2) & 1) ^ 1);
+        mbar_wait_wd(ring_empty + rs, ((it >> 2) & 1) ^ 1, 1, p.M, p.N, p.K);
         const int got = atomicAdd(p.tile_ctr, 1);
         if (got == num_tiles + (int)gridDim.x - 1) atomicExch(p.tile_ctr, 0);  // last fetch of the launch
         const int tile = got < num_tiles ? got : -1;
@@ -180,7 +180,7 @@ __global__ void __launch_bounds__(256, 1)
         const int mb = p.n_fast ? tile / p.num_n_blk : tile % p.num_m_blk;
         const int nb = p.n_fast ? tile % p.num_n_blk : tile / p.num_m_blk;
         for (int kb = 0; kb < p.num_k_blk; ++kb) {
-          mbar_wait(empty + stage, phase ^ 1);
+          mbar_wait_wd(empty + stage, phase ^ 1, 2, p.M, p.N, p.K);
           mbar_arrive_expect_tx(full + stage, C::A_BYTES + C::B_BYTES);
           uint8_t* a = sA + stage * C::A_BYTES;
           uint8_t* b = sB + stage * C::B_BYTES;
@@ -210,17 +210,17 @@ __global__ void __launch_bounds__(256, 1)
       uint32_t phase = 0;
       for (int local = 0;; ++local) {
         const int rs = local & 3;
-        mbar_wait(ring_full + rs, (local >> 2) & 1);
+        mbar_wait_wd(ring_full + rs, (local >> 2) & 1, 3, p.M, p.N, p.K);
         const int tile = ring[rs];
         mbar_arrive(ring_empty + rs);
         if (tile < 0) break;
         const int acc = local & 1;
         const uint32_t acc_phase = (local >> 1) & 1;
-        mbar_wait(tempty + acc, acc_phase ^ 1);
+        mbar_wait_wd(tempty + acc, acc_phase ^ 1, 4, p.M, p.N, p.K);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * BN;
         for (int kb = 0; kb < p.num_k_blk; ++kb) {
-          mbar_wait(full + stage, phase);
+          mbar_wait_wd(full + stage, phase, 5, p.M, p.N, p.K);
           tc_fence_after();
           const uint32_t a_addr = smem_u32(sA + stage * C::A_BYTES);
           const uint32_t b_addr = smem_u32(sB + stage * C::B_BYTES);
@@ -245,7 +245,7 @@ __global__ void __launch_bounds__(256, 1)
     const int ew = warp & 3;
     for (int local = 0;; ++local) {
       const int rs = local & 3;
-      mbar_wait(ring_full + rs, (local >> 2) & 1);
+      mbar_wait_wd(ring_full + rs, (local >> 2) & 1, 6, p.M, p.N, p.K);
       const int tile = ring[rs];
       __syncwarp();
       if (lane == 0) mbar_arrive(ring_empty + rs);
@@ -254,7 +254,7 @@ __global__ void __launch_bounds__(256, 1)
       const int nb = p.n_fast ? tile % p.num_n_blk : tile / p.num_m_blk;
       const int acc = local & 1;
       const uint32_t acc_phase = (local >> 1) & 1;
-      mbar_wait(tfull + acc, acc_phase);
+      mbar_wait_wd(tfull + acc, acc_phase, 7, p.M, p.N, p.K);
       tc_fence_after();
       const int row = mb * BM + ew * 32 + lane;
 #pragma unroll 1
@@ -354,7 +354,7 @@ __global__ void __launch_bounds__(256, 1)
         const int rs = it & 3;
         int tile;
         if (rank == 0) {
-          mbar_wait_cluster(ring_empty + rs, ((it >> 2) & 1) ^ 1);
+          mbar_wait_cluster_wd(ring_empty + rs, ((it >> 2) & 1) ^ 1, 8, p.M, p.N, p.K);
           const int got = atomicAdd(p.tile_ctr, 1);
           if (got == num_ct + n_clusters - 1) atomicExch(p.tile_ctr, 0);
           tile = got < num_ct ? got : -1;
@@ -363,7 +363,7 @@ __global__ void __launch_bounds__(256, 1)
           mbar_arrive(ring_full + rs);
           mbar_arrive_cluster(mapa(smem_u32(ring_full + rs), 1));
         } else {
-          mbar_wait_cluster(ring_full + rs, (it >> 2) & 1);
+          mbar_wait_cluster_wd(ring_full + rs, (it >> 2) & 1, 9, p.M, p.N, p.K);
           tile = ring[rs];
           release_slot(rs);
         }
@@ -371,7 +371,7 @@ __global__ void __launch_bounds__(256, 1)
         const int mb = 2 * (p.n_fast ? tile / p.num_n_blk : tile % n_mp) + (int)rank;
         const int nb = p.n_fast ? tile % p.num_n_blk : tile / n_mp;
         for (int kb = 0; kb < p.num_k_blk; ++kb) {
-          mbar_wait_cluster(empty + stage, phase ^ 1);
+          mbar_wait_cluster_wd(empty + stage, phase ^ 1, 10, p.M, p.N, p.K);
           mbar_arrive_expect_tx(full + stage, C::A_BYTES + C::B_BYTES);
           uint8_t* a = sA + stage * C::A_BYTES;
           uint8_t* b = sB + stage * C::B_BYTES;
@@ -405,17 +405,17 @@ __global__ void __launch_bounds__(256, 1)
       uint32_t phase = 0;
       for (int local = 0;; ++local) {
         const int rs = local & 3;
-        mbar_wait_cluster(ring_full + rs, (local >> 2) & 1);
+        mbar_wait_cluster_wd(ring_full + rs, (local >> 2) & 1, 11, p.M, p.N, p.K);
         const int tile = ring[rs];
         release_slot(rs);
         if (tile < 0) break;
         const int acc = local & 1;
         const uint32_t acc_phase = (local >> 1) & 1;
-        mbar_wait(tempty + acc, acc_phase ^ 1);
+        mbar_wait_wd(tempty + acc, acc_phase ^ 1, 12, p.M, p.N, p.K);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * BN;
         for (int kb = 0; kb < p.num_k_blk; ++kb) {
-          mbar_wait(full + stage, phase);
+          mbar_wait_wd(full + stage, phase, 13, p.M, p.N, p.K);
           tc_fence_after();
           const uint32_t a_addr = smem_u32(sA + stage * C::A_BYTES);
           const uint32_t b_addr = smem_u32(sB + stage * C::B_BYTES);
@@ -440,7 +440,7 @@ __global__ void __launch_bounds__(256, 1)
     const int ew = warp & 3;
     for (int local = 0;; ++local) {
       const int rs = local & 3;
-      mbar_wait_cluster(ring_full + rs, (local >> 2) & 1);
+      mbar_wait_cluster_wd(ring_full + rs, (local >> 2) & 1, 14, p.M, p.N, p.K);
       const int tile = ring[rs];
       __syncwarp();
       if (lane == 0) release_slot(rs);
@@ -449,7 +449,7 @@ __global__ void __launch_bounds__(256, 1)
       const int nb = p.n_fast ? tile % p.num_n_blk : tile / n_mp;
       const int acc = local & 1;
       const uint32_t acc_phase = (local >> 1) & 1;
-      mbar_wait(tfull + acc, acc_phase);
+      mbar_wait_wd(tfull + acc, acc_phase, 15, p.M, p.N, p.K);
       tc_fence_after();
       const int row = mb * BM + ew * 32 + lane;
 #pragma unroll 1
@@ -524,6 +524,13 @@ __global__ void __launch_bounds__(256, 1)
     tma_prefetch_desc(&tmA);
     tma_prefetch_desc(&tmB);
   }
+  // The cta_group::2 allocation writes into the peer CTA's reserved shared
+  // memory (allocation mailbox + mbarrier): both CTAs must have started before
+  // it runs.  Without this cluster barrier the even CTA can race the odd
+  // CTA's launch and the pair hangs inside tcgen05.alloc (seen as an
+  // intermittent whole-step hang; cuda-gdb: odd CTA's allocator warp in the
+  // "alloc after relinquish" trap path).
+  cluster_sync();
   if (warp == 2) tmem_alloc_2sm<512>(tmem_slot);
   tc_fence_before();
   cluster_sync();
@@ -549,7 +556,7 @@ __global__ void __launch_bounds__(256, 1)
         const int rs = it & 3;
         int tile;
         if (rank == 0) {
-          mbar_wait_cluster(ring_empty + rs, ((it >> 2) & 1) ^ 1);
+          mbar_wait_cluster_wd(ring_empty + rs, ((it >> 2) & 1) ^ 1, 101, p.M, p.N, p.K);
           const int got = atomicAdd(p.tile_ctr, 1);
           if (got == num_tiles + ncl - 1) atomicExch(p.tile_ctr, 0);  // last fetch of the launch
           tile = got < num_tiles ? got : -1;
@@ -558,7 +565,7 @@ __global__ void __launch_bounds__(256, 1)
           mbar_arrive(ring_full + rs);
           mbar_arrive_cluster(mapa(smem_u32(ring_full + rs), 1));
         } else {
-          mbar_wait_cluster(ring_full + rs, (it >> 2) & 1);
+          mbar_wait_cluster_wd(ring_full + rs, (it >> 2) & 1, 102, p.M, p.N, p.K);
           tile = ring[rs];
           release_slot(rs);
         }
@@ -566,7 +573,7 @@ __global__ void __launch_bounds__(256, 1)
         const int m0 = (p.n_fast ? tile / num_n2 : tile % num_m2) * 256 + (int)rank * 128;
         const int n0 = (p.n_fast ? tile % num_n2 : tile / num_m2) * 256 + (int)rank * 128;
         for (int kb = 0; kb < p.num_k_blk; ++kb) {
-          mbar_wait(empty + stage, phase ^ 1);
+          mbar_wait_wd(empty + stage, phase ^ 1, 103, p.M, p.N, p.K);
           if (rank == 0) mbar_arrive_expect_tx(full + stage, 2 * S2_STAGE);
           const uint32_t fb = full0 + stage * 8;
           uint8_t* a = sA + stage * HALF;
@@ -597,17 +604,17 @@ __global__ void __launch_bounds__(256, 1)
       uint32_t phase = 0;
       for (int local = 0;; ++local) {
         const int rs = local & 3;
-        mbar_wait_cluster(ring_full + rs, (local >> 2) & 1);
+        mbar_wait_cluster_wd(ring_full + rs, (local >> 2) & 1, 104, p.M, p.N, p.K);
         const int tile = ring[rs];
         release_slot(rs);
         if (tile < 0) break;
         const int acc = local & 1;
         const uint32_t acc_phase = (local >> 1) & 1;
-        mbar_wait_cluster(tempty + acc, acc_phase ^ 1);
+        mbar_wait_cluster_wd(tempty + acc, acc_phase ^ 1, 105, p.M, p.N, p.K);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * 256;
         for (int kb = 0; kb < p.num_k_blk; ++kb) {
-          mbar_wait(full + stage, phase);
+          mbar_wait_wd(full + stage, phase, 106, p.M, p.N, p.K);
           tc_fence_after();
           const uint32_t a_addr = smem_u32(sA + stage * HALF);
           const uint32_t b_addr = smem_u32(sB + stage * HALF);
@@ -633,14 +640,14 @@ __global__ void __launch_bounds__(256, 1)
     const uint32_t tempty0 = mapa(smem_u32(tempty), 0);
     for (int local = 0;; ++local) {
       const int rs = local & 3;
-      mbar_wait_cluster(ring_full + rs, (local >> 2) & 1);
+      mbar_wait_cluster_wd(ring_full + rs, (local >> 2) & 1, 107, p.M, p.N, p.K);
       const int tile = ring[rs];
       __syncwarp();
       if (lane == 0) release_slot(rs);
       if (tile < 0) break;
       const int acc = local & 1;
       const uint32_t acc_phase = (local >> 1) & 1;
-      mbar_wait(tfull + acc, acc_phase);
+      mbar_wait_wd(tfull + acc, acc_phase, 108, p.M, p.N, p.K);
       tc_fence_after();
       const int row = (p.n_fast ? tile / num_n2 : tile % num_m2) * 256 + (int)rank * 128 + ew * 32 + lane;
       const int nb0 = (p.n_fast ? tile % num_n2 : tile / num_m2) * 256;
@@ -882,7 +889,11 @@ stp_status gemm_bf16(int layout, int epi, int64_t M, int64_t N, int64_t K, const
   // from L2 only if it fits; sweep the smaller operand fastest, so the large
   // one streams from HBM once (e.g. the FC1 weight-gradient GEMM: A = dGU^T
   // 466 MB, B = Xn 44 MB -> n-fastest; m-fastest re-read A 14x, 7 GB / call).
-  g.n_fast = (M > N) ? 1 : 0;
+  static const int raster_auto = [] {
+    const char* e = getenv("STP_GEMM_RASTER");
+    return e ? atoi(e) : 1;
+  }();
+  g.n_fast = (raster_auto && M > N) ? 1 : 0;
   g.epilogue = epi;
   g.C = Cp;
   g.ldc = ldc;

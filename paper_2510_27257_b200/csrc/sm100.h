@@ -47,6 +47,30 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   }
 }
 
+// Watchdog waits: a wait that exceeds 20 s prints where it is stuck and
+// traps (the process fails loudly instead of hanging the GPU).
+static __device__ __noinline__ void watchdog_fire(int tag, uint32_t parity, int x, int y, int z) {
+  printf("[stp watchdog] tag %d block %d thread %d parity %u (%d, %d, %d): mbarrier wait > 20 s\n", tag,
+         (int)blockIdx.x, (int)threadIdx.x, parity, x, y, z);
+  __trap();
+}
+// Called after each failed try_wait (which itself suspends for a
+// hardware-defined time), so the timer is read only while actually waiting.
+__device__ __forceinline__ bool watchdog_tick(uint32_t& n, uint64_t& t0) {
+  (void)n;
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  if (t0 == 0) t0 = t;
+  return t - t0 > 20000000000ull;
+}
+__device__ __forceinline__ void mbar_wait_wd(uint64_t* bar, uint32_t parity, int tag, int x, int y, int z) {
+  const uint32_t a = smem_u32(bar);
+  uint32_t n = 0;
+  uint64_t t0 = 0;
+  while (!mbar_try_wait(a, parity))
+    if (watchdog_tick(n, t0)) watchdog_fire(tag, parity, x, y, z);
+}
+
 // --------------------------------------------------------------------- TMA
 __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int x,
                                             int y) {
@@ -206,6 +230,13 @@ __device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity
   const uint32_t a = smem_u32(bar);
   while (!mbar_try_wait_cluster(a, parity)) {
   }
+}
+__device__ __forceinline__ void mbar_wait_cluster_wd(uint64_t* bar, uint32_t parity, int tag, int x, int y, int z) {
+  const uint32_t a = smem_u32(bar);
+  uint32_t n = 0;
+  uint64_t t0 = 0;
+  while (!mbar_try_wait_cluster(a, parity))
+    if (watchdog_tick(n, t0)) watchdog_fire(tag, parity, x, y, z);
 }
 // TMA 2-D load multicast to every CTA in cta_mask (same smem offset, same
 // mbarrier offset in each destination CTA).

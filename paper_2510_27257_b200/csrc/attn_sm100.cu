@@ -2131,6 +2131,195 @@ __global__ void __launch_bounds__(384, 1)
   }
 }
 
+// dQ kernel, version 4: key tiles of 64 rows so that S / dP are
+// DOUBLE-BUFFERED in TMEM (dQ 128 | S0 64 | dP0 64 | S1 64 | dP1 64 | dS0 32 |
+// dS1 32 columns): the MMA warp issues S/dP of tile j+1 as soon as the
+// softmax warps have read buffer (j+1)&1 (tile j-1), so the tensor pipe
+// computes the next tile while the softmax warps convert this one.  K_j / V_j:
+// 4-stage TMA ring of 64-row tiles.
+constexpr int DQ4_STAGES = 4;
+constexpr int DQ4_SMEM = 1024 + 2 * TILE_BYTES + 2 * DQ4_STAGES * QT_BYTES + 256;
+
+__global__ void __launch_bounds__(384, 1)
+    attn_bwd_dq_sm100_v4(const __grid_constant__ CUtensorMap tm_qkv, const __grid_constant__ CUtensorMap tm_kv64,
+                         const __grid_constant__ CUtensorMap tm_do, const BwdArgs a) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sQ = smem;
+  uint8_t* sdO = smem + TILE_BYTES;
+  uint8_t* sK = smem + 2 * TILE_BYTES;            // [STAGES] 64-row tiles
+  uint8_t* sV = sK + DQ4_STAGES * QT_BYTES;       // [STAGES]
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sV + DQ4_STAGES * QT_BYTES);
+  uint64_t* qdo_full = bar + 0;
+  uint64_t* kv_full = bar + 1;                    // [STAGES]
+  uint64_t* kv_empty = kv_full + DQ4_STAGES;      // [STAGES]
+  uint64_t* sdp_full = kv_empty + DQ4_STAGES;     // [2]
+  uint64_t* sdp_empty = sdp_full + 2;             // [2]
+  uint64_t* ds_full = sdp_empty + 2;              // [2]
+  uint64_t* dq_done = ds_full + 2;                // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(dq_done + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int qt = gridDim.x - 1 - blockIdx.x;
+  const int h = blockIdx.y;
+  const int grp = a.nq / a.nkv, g = h / grp;
+  const int n_kv = 2 * (qt + 1);  // 64-row key tiles with keys <= the tile's last query row
+  const int qcol = h * D, kcol = a.nq * D + g * D, vcol = (a.nq + a.nkv) * D + g * D;
+
+  if (threadIdx.x == 0) {
+    mbar_init(qdo_full, 1);
+    for (int i = 0; i < DQ4_STAGES; ++i) {
+      mbar_init(kv_full + i, 1);
+      mbar_init(kv_empty + i, 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(sdp_full + i, 1);
+      mbar_init(sdp_empty + i, 256);
+      mbar_init(ds_full + i, 256);
+      mbar_init(dq_done + i, 1);
+    }
+    fence_barrier_init();
+    tma_prefetch_desc(&tm_qkv);
+    tma_prefetch_desc(&tm_kv64);
+    tma_prefetch_desc(&tm_do);
+  }
+  if (warp == 2) tmem_alloc<512>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t tQ = tmem, tSP = tmem + 128, tdS = tmem + 384;  // buffer b: S at tSP + 128b, dP at +64; dS at tdS + 32b
+
+  if (warp == 0) {
+    if (lane == 0) {
+      mbar_arrive_expect_tx(qdo_full, 2 * TILE_BYTES);
+      tma_load_2d(sQ, &tm_qkv, qdo_full, qcol, qt * T);
+      tma_load_2d(sQ + ATOM, &tm_qkv, qdo_full, qcol + 64, qt * T);
+      tma_load_2d(sdO, &tm_do, qdo_full, h * D, qt * T);
+      tma_load_2d(sdO + ATOM, &tm_do, qdo_full, h * D + 64, qt * T);
+      for (int j = 0; j < n_kv; ++j) {
+        const int st = j % DQ4_STAGES;
+        mbar_wait_wd(kv_empty + st, ((j / DQ4_STAGES) & 1) ^ 1, 401, a.s, a.nq, h);
+        mbar_arrive_expect_tx(kv_full + st, 2 * QT_BYTES);
+        uint8_t* k = sK + st * QT_BYTES;
+        uint8_t* v = sV + st * QT_BYTES;
+        tma_load_2d(k, &tm_kv64, kv_full + st, kcol, j * QT);
+        tma_load_2d(k + QATOM, &tm_kv64, kv_full + st, kcol + 64, j * QT);
+        tma_load_2d(v, &tm_kv64, kv_full + st, vcol, j * QT);
+        tma_load_2d(v + QATOM, &tm_kv64, kv_full + st, vcol + 64, j * QT);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t idS = make_idesc_bf16(T, QT, false, false);  // S, dP: M = 128 queries, N = 64 keys
+      constexpr uint32_t idQ = make_idesc_bf16(T, D, false, true);    // dQ += dS K_j (K_j MN-major)
+      const uint32_t q_addr = smem_u32(sQ), do_addr = smem_u32(sdO);
+      mbar_wait_wd(qdo_full, 0, 402, a.s, a.nq, h);
+      auto issue_sdp = [&](int j) {
+        const int st = j % DQ4_STAGES, b = j & 1;
+        mbar_wait_wd(kv_full + st, (j / DQ4_STAGES) & 1, 403, a.s, a.nq, h);
+        if (j >= 2) mbar_wait_wd(sdp_empty + b, ((j - 2) >> 1) & 1, 404, a.s, a.nq, h);
+        tc_fence_after();
+        const uint32_t k_addr = smem_u32(sK + st * QT_BYTES), v_addr = smem_u32(sV + st * QT_BYTES);
+        const uint32_t tS = tSP + b * 128, tP = tS + 64;
+#pragma unroll
+        for (int kk = 0; kk < D / 16; ++kk) {
+          const uint32_t qa = (kk >> 2) * ATOM + (kk & 3) * 32, ka = (kk >> 2) * QATOM + (kk & 3) * 32;
+          mma_f16_ss(tS, make_sw128_desc(q_addr + qa, 16, 1024), make_sw128_desc(k_addr + ka, 16, 1024), idS,
+                     kk > 0 ? 1u : 0u);
+        }
+#pragma unroll
+        for (int kk = 0; kk < D / 16; ++kk) {
+          const uint32_t qa = (kk >> 2) * ATOM + (kk & 3) * 32, ka = (kk >> 2) * QATOM + (kk & 3) * 32;
+          mma_f16_ss(tP, make_sw128_desc(do_addr + qa, 16, 1024), make_sw128_desc(v_addr + ka, 16, 1024), idS,
+                     kk > 0 ? 1u : 0u);
+        }
+        mma_commit(sdp_full + b);
+      };
+      issue_sdp(0);
+      for (int j = 0; j < n_kv; ++j) {
+        if (j + 1 < n_kv) issue_sdp(j + 1);
+        const int st = j % DQ4_STAGES, b = j & 1;
+        mbar_wait_wd(ds_full + b, (j >> 1) & 1, 405, a.s, a.nq, h);
+        tc_fence_after();
+        const uint32_t k_addr = smem_u32(sK + st * QT_BYTES);
+#pragma unroll
+        for (int kk = 0; kk < QT / 16; ++kk)  // dQ += dS K_j   (dS from TMEM, 8 columns per k16)
+          mma_f16_ts(tQ, tdS + b * 32 + kk * 8, make_sw128_desc(k_addr + kk * 2048, QATOM, 1024), idQ,
+                     (j > 0 || kk > 0) ? 1u : 0u);
+        mma_commit(kv_empty + st);
+        mma_commit(dq_done + b);
+      }
+    }
+  } else if (warp >= 4) {
+    const int half = (warp - 4) >> 2, quad = warp & 3;  // half: key columns [32 half, 32 half + 32) of the tile
+    const int r = quad * 32 + lane;
+    const uint32_t lane_off = (uint32_t)(quad * 32) << 16;
+    const int qrow = qt * T + r;
+    const bool vrow = qrow < a.s;
+    const float nlse2 = vrow ? -a.lse[(int64_t)h * a.s + qrow] * 1.4426950408889634f : 0.f;
+    const float Dv = vrow ? a.Dl[(int64_t)h * a.s + qrow] : 0.f;
+    const float sl2 = a.scale_log2;
+    for (int j = 0; j < n_kv; ++j) {
+      const int b = j & 1;
+      const uint32_t tS = tSP + b * 128, tP = tS + 64;
+      mbar_wait_wd(sdp_full + b, (j >> 1) & 1, 406, a.s, a.nq, h);
+      tc_fence_after();
+      uint32_t sv[32], dv[32];
+      tmem_ld_32x32b_x32(tS + half * 32 + lane_off, sv);
+      tmem_ld_32x32b_x32(tP + half * 32 + lane_off, dv);
+      tmem_wait_ld();
+      tc_fence_before();
+      mbar_arrive(sdp_empty + b);
+      const int cbase = j * QT + half * 32;
+      const bool edge = j >= 2 * qt || cbase + 32 > a.s || !vrow;
+      uint32_t pk[16];
+#pragma unroll
+      for (int i = 0; i < 32; i += 2) {
+        float d2[2];
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          float p = ex2(fmaf(__uint_as_float(sv[i + e]), sl2, nlse2));
+          if (edge && (cbase + i + e > qrow || cbase + i + e >= a.s || !vrow)) p = 0.f;
+          d2[e] = p * (__uint_as_float(dv[i + e]) - Dv);
+        }
+        pk[i >> 1] = pack2(d2[0], d2[1]);
+      }
+      if (j >= 2) mbar_wait_wd(dq_done + b, ((j - 2) >> 1) & 1, 407, a.s, a.nq, h);
+      tmem_st_32x32b_x16(tdS + b * 32 + half * 16 + lane_off, pk);
+      tmem_wait_st();
+      tc_fence_before();
+      mbar_arrive(ds_full + b);
+    }
+    mbar_wait_wd(dq_done + ((n_kv - 1) & 1), ((n_kv - 1) >> 1) & 1, 408, a.s, a.nq, h);
+    tc_fence_after();
+    bf16* orow = reinterpret_cast<bf16*>(a.dq) + (int64_t)(vrow ? qrow : 0) * a.ldd + (int64_t)h * D + half * 64;
+#pragma unroll 1
+    for (int c = 0; c < 2; ++c) {
+      uint32_t v[32];
+      tmem_ld_32x32b_x32(tQ + half * 64 + c * 32 + lane_off, v);
+      tmem_wait_ld();
+      if (vrow) {
+#pragma unroll
+        for (int i = 0; i < 32; i += 8) {
+          uint4 u;
+          u.x = pack2(__uint_as_float(v[i]) * a.scale, __uint_as_float(v[i + 1]) * a.scale);
+          u.y = pack2(__uint_as_float(v[i + 2]) * a.scale, __uint_as_float(v[i + 3]) * a.scale);
+          u.z = pack2(__uint_as_float(v[i + 4]) * a.scale, __uint_as_float(v[i + 5]) * a.scale);
+          u.w = pack2(__uint_as_float(v[i + 6]) * a.scale, __uint_as_float(v[i + 7]) * a.scale);
+          *reinterpret_cast<uint4*>(orow + c * 32 + i) = u;
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc<512>(tmem);
+  }
+}
+
 // dk/dv (bf16, kv-head columns of dqkv) = sum over the group's query heads.
 __global__ void attn_bwd_reduce(int s, int nq, int nkv, const float* __restrict__ dk_part,
                                 const float* __restrict__ dv_part, bf16* dk, bf16* dv, int64_t ldd) {
@@ -2213,7 +2402,8 @@ stp_status attn_fwd_sm100_launch(int s, int nq, int nkv, const void* qkv_base, i
 namespace stp {
 // Tuning knob (stp_set_option "attn_bwd"): 1 = smem P^T/dS^T dK/dV kernel,
 // 2 = TMEM-resident P^T/dS^T with double-buffered Q/dO, 3 = 8 softmax warps,
-// 4 = 64-row query tiles with double-buffered S^T/dP^T (default).
+// 4 = 64-row query tiles with double-buffered S^T/dP^T (default), 5 = v4 +
+// the dQ kernel with 64-row key tiles and double-buffered S/dP.
 int& attn_bwd_version_ref() {
   static int v = [] {
     const char* e = getenv("STP_ATTN_BWD");
@@ -2270,7 +2460,16 @@ stp_status attn_bwd_sm100_launch(int s, int nq, int nkv, const void* qkv_base, i
   else attn_bwd_dkdv_sm100<<<dim3(nt, nq), 256, KV_SMEM, st>>>(tq, td, a);
   count_launch();
   STP_LAUNCH_CHECK();
-  if (attn_bwd_version_ref() >= 3) attn_bwd_dq_sm100_v3<<<dim3(nt, nq), 384, DQ2_SMEM, st>>>(tq, td, a);
+  if (attn_bwd_version_ref() >= 5) {
+    CUtensorMap tkv64;
+    STP_TRY(tensor_map_bf16(&tkv64, qkv_base, ld, s, ld, 64, QT));
+    static bool attr5 = false;
+    if (!attr5) {
+      STP_CUDA_TRY(cudaFuncSetAttribute(attn_bwd_dq_sm100_v4, cudaFuncAttributeMaxDynamicSharedMemorySize, DQ4_SMEM));
+      attr5 = true;
+    }
+    attn_bwd_dq_sm100_v4<<<dim3(nt, nq), 384, DQ4_SMEM, st>>>(tq, tkv64, td, a);
+  } else if (attn_bwd_version_ref() >= 3) attn_bwd_dq_sm100_v3<<<dim3(nt, nq), 384, DQ2_SMEM, st>>>(tq, td, a);
   else if (attn_bwd_version_ref() == 2) attn_bwd_dq_sm100_v2<<<dim3(nt, nq), 256, DQ2_SMEM, st>>>(tq, td, a);
   else attn_bwd_dq_sm100<<<dim3(nt, nq), 256, DQ_SMEM, st>>>(tq, td, a);
   count_launch();

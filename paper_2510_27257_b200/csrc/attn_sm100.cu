@@ -2320,6 +2320,201 @@ __global__ void __launch_bounds__(384, 1)
   }
 }
 
+// dQ kernel, version 5: Q and dO live in TMEM (bf16 pairs, loaded once per
+// CTA by the softmax warps) and feed S = Q K_j^T and dP = dO V_j^T as the A
+// operand, so shared memory only streams the 64-row K_j / V_j tiles (the A
+// operand was 2/3 of the smem operand traffic of those MMAs).  TMEM: dQ 128 |
+// S 64 | dP 64 | dS[2] 2x32 | Q 64 | dO 64 = 448 columns; S/dP single-buffered
+// (released as soon as the softmax warps have loaded them).
+constexpr int DQ5_SMEM = 1024 + 2 * DQ4_STAGES * QT_BYTES + 256;
+
+__global__ void __launch_bounds__(384, 1)
+    attn_bwd_dq_sm100_v5(const __grid_constant__ CUtensorMap tm_kv64, const BwdArgs a, const bf16* __restrict__ qkv,
+                         int64_t ld, const bf16* __restrict__ dout, int64_t ldo) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sK = smem;                             // [STAGES] 64-row tiles
+  uint8_t* sV = sK + DQ4_STAGES * QT_BYTES;       // [STAGES]
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sV + DQ4_STAGES * QT_BYTES);
+  uint64_t* ops_ready = bar + 0;                  // Q / dO in TMEM (256 softmax threads)
+  uint64_t* kv_full = bar + 1;                    // [STAGES]
+  uint64_t* kv_empty = kv_full + DQ4_STAGES;      // [STAGES]
+  uint64_t* sdp_full = kv_empty + DQ4_STAGES;
+  uint64_t* sdp_empty = sdp_full + 1;
+  uint64_t* ds_full = sdp_empty + 1;              // [2]
+  uint64_t* dq_done = ds_full + 2;                // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(dq_done + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int qt = gridDim.x - 1 - blockIdx.x;
+  const int h = blockIdx.y;
+  const int grp = a.nq / a.nkv, g = h / grp;
+  const int n_kv = 2 * (qt + 1);
+  const int kcol = a.nq * D + g * D, vcol = (a.nq + a.nkv) * D + g * D;
+
+  if (threadIdx.x == 0) {
+    mbar_init(ops_ready, 256);
+    for (int i = 0; i < DQ4_STAGES; ++i) {
+      mbar_init(kv_full + i, 1);
+      mbar_init(kv_empty + i, 1);
+    }
+    mbar_init(sdp_full, 1);
+    mbar_init(sdp_empty, 256);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(ds_full + i, 256);
+      mbar_init(dq_done + i, 1);
+    }
+    fence_barrier_init();
+    tma_prefetch_desc(&tm_kv64);
+  }
+  if (warp == 2) tmem_alloc<512>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t tQ = tmem, tS = tmem + 128, tP = tmem + 192, tdS = tmem + 256, tQa = tmem + 320, tdOa = tmem + 384;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      for (int j = 0; j < n_kv; ++j) {
+        const int st = j % DQ4_STAGES;
+        mbar_wait_wd(kv_empty + st, ((j / DQ4_STAGES) & 1) ^ 1, 501, a.s, a.nq, h);
+        mbar_arrive_expect_tx(kv_full + st, 2 * QT_BYTES);
+        uint8_t* k = sK + st * QT_BYTES;
+        uint8_t* v = sV + st * QT_BYTES;
+        tma_load_2d(k, &tm_kv64, kv_full + st, kcol, j * QT);
+        tma_load_2d(k + QATOM, &tm_kv64, kv_full + st, kcol + 64, j * QT);
+        tma_load_2d(v, &tm_kv64, kv_full + st, vcol, j * QT);
+        tma_load_2d(v + QATOM, &tm_kv64, kv_full + st, vcol + 64, j * QT);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t idS = make_idesc_bf16(T, QT, false, false);  // S, dP: M = 128 queries, N = 64 keys
+      constexpr uint32_t idQ = make_idesc_bf16(T, D, false, true);    // dQ += dS K_j (K_j MN-major)
+      mbar_wait_wd(ops_ready, 0, 502, a.s, a.nq, h);
+      tc_fence_after();
+      auto issue_sdp = [&](int j) {
+        const int st = j % DQ4_STAGES;
+        mbar_wait_wd(kv_full + st, (j / DQ4_STAGES) & 1, 503, a.s, a.nq, h);
+        if (j >= 1) mbar_wait_wd(sdp_empty, (j - 1) & 1, 504, a.s, a.nq, h);
+        tc_fence_after();
+        const uint32_t k_addr = smem_u32(sK + st * QT_BYTES), v_addr = smem_u32(sV + st * QT_BYTES);
+#pragma unroll
+        for (int kk = 0; kk < D / 16; ++kk) {
+          const uint32_t ka = (kk >> 2) * QATOM + (kk & 3) * 32;
+          mma_f16_ts(tS, tQa + kk * 8, make_sw128_desc(k_addr + ka, 16, 1024), idS, kk > 0 ? 1u : 0u);
+        }
+#pragma unroll
+        for (int kk = 0; kk < D / 16; ++kk) {
+          const uint32_t ka = (kk >> 2) * QATOM + (kk & 3) * 32;
+          mma_f16_ts(tP, tdOa + kk * 8, make_sw128_desc(v_addr + ka, 16, 1024), idS, kk > 0 ? 1u : 0u);
+        }
+        mma_commit(sdp_full);
+      };
+      issue_sdp(0);
+      for (int j = 0; j < n_kv; ++j) {
+        if (j + 1 < n_kv) issue_sdp(j + 1);
+        const int st = j % DQ4_STAGES, b = j & 1;
+        mbar_wait_wd(ds_full + b, (j >> 1) & 1, 505, a.s, a.nq, h);
+        tc_fence_after();
+        const uint32_t k_addr = smem_u32(sK + st * QT_BYTES);
+#pragma unroll
+        for (int kk = 0; kk < QT / 16; ++kk)  // dQ += dS K_j   (dS from TMEM, 8 columns per k16)
+          mma_f16_ts(tQ, tdS + b * 32 + kk * 8, make_sw128_desc(k_addr + kk * 2048, QATOM, 1024), idQ,
+                     (j > 0 || kk > 0) ? 1u : 0u);
+        mma_commit(kv_empty + st);
+        mma_commit(dq_done + b);
+      }
+    }
+  } else if (warp >= 4) {
+    const int half = (warp - 4) >> 2, quad = warp & 3;
+    const int r = quad * 32 + lane;
+    const uint32_t lane_off = (uint32_t)(quad * 32) << 16;
+    const int qrow = qt * T + r;
+    const bool vrow = qrow < a.s;
+    {  // this row's half (64 of 128 d) of Q and dO -> TMEM (bf16 pairs: 32 columns each)
+      uint32_t u[32];
+      const uint4* qs = reinterpret_cast<const uint4*>(qkv + (int64_t)(vrow ? qrow : 0) * ld + (int64_t)h * D + half * 64);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        uint4 x = vrow ? qs[i] : make_uint4(0, 0, 0, 0);
+        u[4 * i] = x.x; u[4 * i + 1] = x.y; u[4 * i + 2] = x.z; u[4 * i + 3] = x.w;
+      }
+      tmem_st_32x32b_x32(tQa + half * 32 + lane_off, u);
+      const uint4* ds_ = reinterpret_cast<const uint4*>(dout + (int64_t)(vrow ? qrow : 0) * ldo + (int64_t)h * D + half * 64);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        uint4 x = vrow ? ds_[i] : make_uint4(0, 0, 0, 0);
+        u[4 * i] = x.x; u[4 * i + 1] = x.y; u[4 * i + 2] = x.z; u[4 * i + 3] = x.w;
+      }
+      tmem_st_32x32b_x32(tdOa + half * 32 + lane_off, u);
+      tmem_wait_st();
+      tc_fence_before();
+      mbar_arrive(ops_ready);
+    }
+    const float nlse2 = vrow ? -a.lse[(int64_t)h * a.s + qrow] * 1.4426950408889634f : 0.f;
+    const float Dv = vrow ? a.Dl[(int64_t)h * a.s + qrow] : 0.f;
+    const float sl2 = a.scale_log2;
+    for (int j = 0; j < n_kv; ++j) {
+      const int b = j & 1;
+      mbar_wait_wd(sdp_full, j & 1, 506, a.s, a.nq, h);
+      tc_fence_after();
+      uint32_t sv[32], dv[32];
+      tmem_ld_32x32b_x32(tS + half * 32 + lane_off, sv);
+      tmem_ld_32x32b_x32(tP + half * 32 + lane_off, dv);
+      tmem_wait_ld();
+      tc_fence_before();
+      mbar_arrive(sdp_empty);
+      const int cbase = j * QT + half * 32;
+      const bool edge = j >= 2 * qt || cbase + 32 > a.s || !vrow;
+      uint32_t pk[16];
+#pragma unroll
+      for (int i = 0; i < 32; i += 2) {
+        float d2[2];
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          float p = ex2(fmaf(__uint_as_float(sv[i + e]), sl2, nlse2));
+          if (edge && (cbase + i + e > qrow || cbase + i + e >= a.s || !vrow)) p = 0.f;
+          d2[e] = p * (__uint_as_float(dv[i + e]) - Dv);
+        }
+        pk[i >> 1] = pack2(d2[0], d2[1]);
+      }
+      if (j >= 2) mbar_wait_wd(dq_done + b, ((j - 2) >> 1) & 1, 507, a.s, a.nq, h);
+      tmem_st_32x32b_x16(tdS + b * 32 + half * 16 + lane_off, pk);
+      tmem_wait_st();
+      tc_fence_before();
+      mbar_arrive(ds_full + b);
+    }
+    mbar_wait_wd(dq_done + ((n_kv - 1) & 1), ((n_kv - 1) >> 1) & 1, 508, a.s, a.nq, h);
+    tc_fence_after();
+    bf16* orow = reinterpret_cast<bf16*>(a.dq) + (int64_t)(vrow ? qrow : 0) * a.ldd + (int64_t)h * D + half * 64;
+#pragma unroll 1
+    for (int c = 0; c < 2; ++c) {
+      uint32_t v[32];
+      tmem_ld_32x32b_x32(tQ + half * 64 + c * 32 + lane_off, v);
+      tmem_wait_ld();
+      if (vrow) {
+#pragma unroll
+        for (int i = 0; i < 32; i += 8) {
+          uint4 u4;
+          u4.x = pack2(__uint_as_float(v[i]) * a.scale, __uint_as_float(v[i + 1]) * a.scale);
+          u4.y = pack2(__uint_as_float(v[i + 2]) * a.scale, __uint_as_float(v[i + 3]) * a.scale);
+          u4.z = pack2(__uint_as_float(v[i + 4]) * a.scale, __uint_as_float(v[i + 5]) * a.scale);
+          u4.w = pack2(__uint_as_float(v[i + 6]) * a.scale, __uint_as_float(v[i + 7]) * a.scale);
+          *reinterpret_cast<uint4*>(orow + c * 32 + i) = u4;
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc<512>(tmem);
+  }
+}
+
 // dk/dv (bf16, kv-head columns of dqkv) = sum over the group's query heads.
 __global__ void attn_bwd_reduce(int s, int nq, int nkv, const float* __restrict__ dk_part,
                                 const float* __restrict__ dv_part, bf16* dk, bf16* dv, int64_t ldd) {
@@ -2403,7 +2598,8 @@ namespace stp {
 // Tuning knob (stp_set_option "attn_bwd"): 1 = smem P^T/dS^T dK/dV kernel,
 // 2 = TMEM-resident P^T/dS^T with double-buffered Q/dO, 3 = 8 softmax warps,
 // 4 = 64-row query tiles with double-buffered S^T/dP^T (default), 5 = v4 +
-// the dQ kernel with 64-row key tiles and double-buffered S/dP.
+// the dQ kernel with 64-row key tiles and double-buffered S/dP, 6 = v4 + the
+// dQ kernel with Q / dO as TMEM-resident A operands.
 int& attn_bwd_version_ref() {
   static int v = [] {
     const char* e = getenv("STP_ATTN_BWD");
@@ -2460,7 +2656,17 @@ stp_status attn_bwd_sm100_launch(int s, int nq, int nkv, const void* qkv_base, i
   else attn_bwd_dkdv_sm100<<<dim3(nt, nq), 256, KV_SMEM, st>>>(tq, td, a);
   count_launch();
   STP_LAUNCH_CHECK();
-  if (attn_bwd_version_ref() >= 5) {
+  if (attn_bwd_version_ref() >= 6) {
+    CUtensorMap tkv64;
+    STP_TRY(tensor_map_bf16(&tkv64, qkv_base, ld, s, ld, 64, QT));
+    static bool attr6 = false;
+    if (!attr6) {
+      STP_CUDA_TRY(cudaFuncSetAttribute(attn_bwd_dq_sm100_v5, cudaFuncAttributeMaxDynamicSharedMemorySize, DQ5_SMEM));
+      attr6 = true;
+    }
+    attn_bwd_dq_sm100_v5<<<dim3(nt, nq), 384, DQ5_SMEM, st>>>(tkv64, a, (const bf16*)qkv_base, ld, (const bf16*)dout,
+                                                              ldo);
+  } else if (attn_bwd_version_ref() >= 5) {
     CUtensorMap tkv64;
     STP_TRY(tensor_map_bf16(&tkv64, qkv_base, ld, s, ld, 64, QT));
     static bool attr5 = false;

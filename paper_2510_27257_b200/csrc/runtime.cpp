@@ -87,7 +87,7 @@ stp_status stp_set_option(const char* key, int64_t value) {
     return STP_OK;
   }
   if (k == "attn_bwd") {
-    if (value < 0 || value > 5) return stp::fail(STP_EINVAL, "attn_bwd must be 0..5");
+    if (value < 0 || value > 6) return stp::fail(STP_EINVAL, "attn_bwd must be 0..6");
     stp::attn_bwd_version_ref() = value ? (int)value : stp::kAttnBwdDefault;
     return STP_OK;
   }

@@ -243,3 +243,20 @@ def test_serialize_header_and_shape():
     assert lines[1] == "rank 0"
     assert lines[2] == "A 0 0 0 1 -1 -1 -1"
     assert txt.endswith("\n")
+
+
+def test_simulated_8gpu_rows_from_measured_units():
+    """the simulated TP4 x PP2 rows (tests/simulate_8gpu.py, fed with
+    unit times measured on 4x B200) run, and the braid hides TP comm there:
+    STP's exposed TP stays below 1F1B-I's and well below the naive schedule's."""
+    import json
+    import os
+    from tests import simulate_8gpu
+    prof = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "profiles")
+    stp = json.load(open(os.path.join(prof, "r01_unit_times_tp4_stp.json")))["units"]
+    ref = json.load(open(os.path.join(prof, "r01_unit_times_tp4_1f1b-i.json")))["units"]
+    res = simulate_8gpu.run(stp, ref, ms=(8, 16))
+    for row in res["rows"]:
+        assert row["stp"]["exposed_tp_pct"] < row["1f1b-i"]["exposed_tp_pct"] < row["1f1b-i-naive"]["exposed_tp_pct"]
+        assert row["stp"]["peak_chunks"] == 6  # 3p
+        assert 0.8 < row["stp_vs_1f1b_i"] < 1.3

@@ -214,9 +214,16 @@ __global__ void tp_fused_bwd_kernel(int64_t rows, int h, Pieces pc, const T* __r
   __threadfence_system();
 }
 
+// CTAs of the fused comm-phase kernels: each warp owns one row at a time, so
+// fewer CTAs mean a longer (still overlapped) phase but fewer SM slots taken
+// from the other microbatch's GEMMs (STP_P2P_CTAS, default 2 x SMs).
 int fused_grid(int64_t rows) {
+  static const int64_t cap = [] {
+    const char* e = getenv("STP_P2P_CTAS");
+    return (int64_t)(e && atoi(e) > 0 ? atoi(e) : num_sms() * 2);
+  }();
   int64_t blocks = (rows + kWarps - 1) / kWarps;
-  return (int)std::max<int64_t>(1, std::min<int64_t>(blocks, (int64_t)num_sms() * 2));
+  return (int)std::max<int64_t>(1, std::min<int64_t>(blocks, cap));
 }
 
 typedef CUresult (*PFN_waitValue32)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);

@@ -41,10 +41,17 @@ extern "C" {
  *   STP_EPI_BIAS:      C(dtype) = acc + bias[n]            (bias dtype)
  *   STP_EPI_ACCUM_F32: C(fp32) += acc                      (gradient accumulation)
  *   STP_EPI_RESID:     C(dtype) = acc + R[m*ldr + n]       (residual add, R dtype)
+ *   STP_EPI_SWIGLU_BWD: C is the [M, 2N] tensor [G | U] (ldc >= 2N) of the MLP unit's
+ *                      gate / up projections; with dH = acc, IN PLACE:
+ *                      C[m, n]   = dH * U * s(G) * (1 + G * (1 - s(G)))   (dG)
+ *                      C[m, N+n] = dH * G * s(G)                         (dU)
+ *                      s = logistic: the SwiGLU backward (P:L70 MLP unit,
+ *                      SURVEY §8c.1) fused into the FC2 activation-gradient GEMM
  * `max_ctas` caps the persistent grid (0 = all SMs) so TP communication
  * kernels can run beside the GEMM. */
 typedef enum { STP_GEMM_NT = 0, STP_GEMM_NN = 1, STP_GEMM_TN = 2 } stp_gemm_layout;
-typedef enum { STP_EPI_STORE = 0, STP_EPI_BIAS = 1, STP_EPI_ACCUM_F32 = 2, STP_EPI_RESID = 3 } stp_epilogue;
+typedef enum { STP_EPI_STORE = 0, STP_EPI_BIAS = 1, STP_EPI_ACCUM_F32 = 2, STP_EPI_RESID = 3,
+               STP_EPI_SWIGLU_BWD = 4 } stp_epilogue;
 
 stp_status stp_op_gemm(int32_t dtype, int32_t layout, int32_t epilogue,
                        int64_t M, int64_t N, int64_t K,

@@ -80,6 +80,37 @@ __device__ __forceinline__ void epilogue_row32(const GemmArgs& p, int row, int c
     }
     return;
   }
+  if (p.epilogue == STP_EPI_SWIGLU_BWD) {  // C = [G | U] (ldc >= 2N), overwritten by [dG | dU]
+    bf16* gp = reinterpret_cast<bf16*>(p.C) + (int64_t)row * p.ldc + col;
+    bf16* up = gp + p.N;
+    if (full) {
+#pragma unroll
+      for (int j = 0; j < 32; j += 8) {
+        uint4 gv = *reinterpret_cast<const uint4*>(gp + j), uv = *reinterpret_cast<const uint4*>(up + j);
+        const bf16* g8 = reinterpret_cast<const bf16*>(&gv);
+        const bf16* u8 = reinterpret_cast<const bf16*>(&uv);
+        float dg[8], du[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          const float z = __bfloat162float(g8[q]), sg = 1.f / (1.f + __expf(-z)), dh = f[j + q];
+          du[q] = dh * z * sg;
+          dg[q] = dh * __bfloat162float(u8[q]) * sg * (1.f + z * (1.f - sg));
+        }
+        *reinterpret_cast<uint4*>(gp + j) = make_uint4(pack_bf16x2(dg[0], dg[1]), pack_bf16x2(dg[2], dg[3]),
+                                                       pack_bf16x2(dg[4], dg[5]), pack_bf16x2(dg[6], dg[7]));
+        *reinterpret_cast<uint4*>(up + j) = make_uint4(pack_bf16x2(du[0], du[1]), pack_bf16x2(du[2], du[3]),
+                                                       pack_bf16x2(du[4], du[5]), pack_bf16x2(du[6], du[7]));
+      }
+    } else {
+      for (int j = 0; j < 32 && col + j < p.N; ++j) {
+        const float z = __bfloat162float(gp[j]), sg = 1.f / (1.f + __expf(-z)), dh = f[j];
+        const float u = __bfloat162float(up[j]);
+        up[j] = __float2bfloat16_rn(dh * z * sg);
+        gp[j] = __float2bfloat16_rn(dh * u * sg * (1.f + z * (1.f - sg)));
+      }
+    }
+    return;
+  }
   if (p.epilogue == STP_EPI_BIAS) {
     const bf16* b = reinterpret_cast<const bf16*>(p.bias) + col;
 #pragma unroll
@@ -999,6 +1030,10 @@ __global__ void __launch_bounds__(256) gemm_f32_simt(int M, int N, int K, const 
       float* c = C + (int64_t)m * ldc + n;
       if (epi == STP_EPI_ACCUM_F32) {
         *c += v;
+      } else if (epi == STP_EPI_SWIGLU_BWD) {  // C = [G | U], overwritten by [dG | dU]
+        const float z = c[0], u = c[N], sg = 1.f / (1.f + expf(-z));
+        c[N] = v * z * sg;
+        c[0] = v * u * sg * (1.f + z * (1.f - sg));
       } else {
         if (epi == STP_EPI_BIAS) v += bias[n];
         if (epi == STP_EPI_RESID) v += R[(int64_t)m * ldr + n];
@@ -1038,10 +1073,11 @@ stp_status gemm_dispatch(int dtype, int layout, int epi, int64_t M, int64_t N, i
                          const void* R, int64_t ldr, int max_ctas, cudaStream_t st) {
   STP_CHECK_ARG(M >= 0 && N >= 0 && K >= 0, "negative GEMM size");
   STP_CHECK_ARG(layout >= 0 && layout <= 2, "layout");
-  STP_CHECK_ARG(epi >= 0 && epi <= 3, "epilogue");
+  STP_CHECK_ARG(epi >= 0 && epi <= 4, "epilogue");
+  STP_CHECK_ARG(epi != STP_EPI_SWIGLU_BWD || ldc >= 2 * N, "SWIGLU_BWD epilogue needs ldc >= 2N ([G | U] rows)");
   if (M == 0 || N == 0) return STP_OK;
   const double es = dtype == STP_DTYPE_BF16 ? 2.0 : 4.0;
-  const double cbytes = (epi == STP_EPI_ACCUM_F32 ? 8.0 : es) * (double)M * N;
+  const double cbytes = (epi == STP_EPI_ACCUM_F32 ? 8.0 : epi == STP_EPI_SWIGLU_BWD ? 4.0 * es : es) * (double)M * N;
   ProfScope prof(PROF_GEMM, 2.0 * M * N * K, es * ((double)M * K + (double)N * K) + cbytes, st);
   if (dtype == STP_DTYPE_F32)
     return gemm_f32(layout, epi, M, N, K, (const float*)A, lda, (const float*)B, ldb, (float*)C, ldc,

@@ -656,6 +656,9 @@ stp_status unit_compute(stp_stage* S, const stp_unit& u) {
     case STP_U_B_MLP: {
       SlotLayer& L = sl->L[j];
       const LayerIdx& I = LI(S, u.layer);
+      // (STP_EPI_SWIGLU_BWD would fuse the SwiGLU backward into this GEMM's
+      // epilogue; measured slower: the epilogue's [G | U] reads stall the 2-SM
+      // kernel, GEMM average 1321 -> 1187 TFLOP/s.  Separate kernel kept.)
       STP_TRY(gemm_dispatch(dt, STP_GEMM_NN, STP_EPI_STORE, s, S->fi, h, L.dy_mlp, h, P(S, I.wd), S->fi, S->dtmp_h,
                             S->fi, nullptr, nullptr, 0, mc, st));
       STP_TRY(swiglu_bwd(dt, s, S->fi, S->dtmp_h, L.gu, L.gu, st));  // dGU overwrites GU

@@ -136,3 +136,39 @@ def test_gemm_fp32(layout, epi):
     ops.gemm(layout, dA, dB, C, M, N, K, epi=epi, bias=bias, R=R)
     torch.cuda.synchronize()
     assert np.linalg.norm(C.double().cpu().numpy() - ref) <= 1e-6 * np.linalg.norm(ref)
+
+
+def _swiglu_bwd_ref(dH, G, U):
+    sg = 1.0 / (1.0 + np.exp(-G))
+    return dH * U * sg * (1.0 + G * (1.0 - sg)), dH * G * sg
+
+
+@pytest.mark.parametrize("MNK", [(300, 392, 256), (512, 1024, 384), (130, 72, 64)])
+def test_gemm_bf16_swiglu_bwd_epilogue(MNK, gemm_mode):
+    """STP_EPI_SWIGLU_BWD: the FC2 activation-gradient GEMM dH = dY Wd with the
+    SwiGLU backward applied in the epilogue, [G | U] -> [dG | dU] in place."""
+    ops = _ops()
+    M, N, K = MNK
+    A, dA = _mk((M, K), 21, torch.bfloat16)
+    B, dB = _mk((K, N), 22, torch.bfloat16)
+    gu0, GU = _mk((M, 2 * N), 23, torch.bfloat16)
+    ops.gemm(1, dA, dB, GU, M, N, K, epi=4, dtype=1)
+    torch.cuda.synchronize()
+    dG, dU = _swiglu_bwd_ref(A @ B, gu0[:, :N], gu0[:, N:])
+    got = GU.double().cpu().numpy()
+    for g, r in ((got[:, :N], dG), (got[:, N:], dU)):
+        assert np.linalg.norm(g - r) <= 6e-3 * np.linalg.norm(r)
+
+
+def test_gemm_fp32_swiglu_bwd_epilogue():
+    ops = _ops()
+    M, N, K = 77, 130, 45
+    A, dA = _mk((M, K), 24, torch.float32)
+    B, dB = _mk((K, N), 25, torch.float32)
+    gu0, GU = _mk((M, 2 * N), 26, torch.float32)
+    ops.gemm(1, dA, dB, GU, M, N, K, epi=4)
+    torch.cuda.synchronize()
+    dG, dU = _swiglu_bwd_ref(A @ B, gu0[:, :N], gu0[:, N:])
+    got = GU.double().cpu().numpy()
+    assert np.linalg.norm(got[:, :N] - dG) <= 1e-5 * np.linalg.norm(dG)
+    assert np.linalg.norm(got[:, N:] - dU) <= 1e-5 * np.linalg.norm(dU)

@@ -163,7 +163,14 @@ stp_status stp_nccl_get_id(void* buf);
  * pp_rank*tp + tp_rank of tp*pp), identical on all ranks (broadcast by the
  * caller, e.g. with torch.distributed); NULL allowed only when tp*pp == 1.
  * The library derives the TP and PP communicators with ncclCommSplit.
- * Streams are created internally.  Parameters are bound separately. */
+ * Streams are created internally.  Parameters are bound separately.
+ * TP transport (env STP_TP_TRANSPORT, read here): "p2p" (default) maps the TP
+ * peers' stash slots / partial buffers / flag words with CUDA IPC (all TP
+ * ranks on one node, peer access over NVLink) and runs each comm phase as
+ * one fused NVLink kernel; "ce" uses copy-engine pulls; "nccl" uses NCCL
+ * reduce-scatter / all-gather.  An IPC or peer-access failure returns
+ * STP_ECUDA with the CUDA error text.  Multi-rank stages require
+ * CUDA_DEVICE_MAX_CONNECTIONS >= 16 (STP_EUNSUPPORTED otherwise). */
 stp_status stp_init_stage(const stp_model_cfg* model, const stp_parallel_cfg* par,
                           const void* world_nccl_id, int32_t cuda_device,
                           stp_stage** out);

@@ -168,9 +168,26 @@ def workload_config(args, cfg, tp_pp):
 
 
 # ------------------------------------------------------------------ ours
+_last_progress = [time.time()]
+
+
 def progress(msg):
     """Progress to stderr (the JSON contract line is the only stdout line)."""
+    _last_progress[0] = time.time()
     print(f"[bench {time.strftime('%H:%M:%S')}] {msg}", file=sys.stderr, flush=True)
+
+
+def start_watchdog(limit_s: float):
+    """Fail fast instead of hanging: if no progress() for limit_s seconds
+    (a step takes ~2.3 s at N=1), report and exit non-zero."""
+    def run():
+        while True:
+            time.sleep(5)
+            idle = time.time() - _last_progress[0]
+            if idle > limit_s:
+                print(f"[bench] no progress for {idle:.0f} s; aborting", file=sys.stderr, flush=True)
+                os._exit(3)
+    threading.Thread(target=run, daemon=True).start()
 
 
 def ours(args):
@@ -244,6 +261,7 @@ def ours(args):
             loss, stats = st.step(d_tok, d_tgt)
             ms.append(stats.step_ms)
             launches += stats.n_kernels
+            _last_progress[0] = time.time()
     barrier()
     L.call("stp_prof_enable", 0)
     prof = {}
@@ -378,6 +396,7 @@ def main():
         args.warmup = 3
     if args.impl == "reference":
         return reference_arm(args, model_cfg(args.seq))
+    start_watchdog(float(os.environ.get("STP_BENCH_WATCHDOG_S", "600")))
     return ours(args)
 
 

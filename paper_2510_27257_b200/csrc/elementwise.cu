@@ -194,6 +194,42 @@ __global__ void rope_kernel(int64_t s, int64_t ld, int64_t col0, int nh, int d, 
   }
 }
 
+// Vectorised variant: one thread = VN consecutive rotation pairs (16-byte
+// loads / stores of both halves, float2 table rows through L2).  Needs
+// 16-byte aligned rows (ld, col0 multiples of VN) and half % VN == 0.
+template <typename T>
+__global__ void rope_vec_kernel(int64_t s, int64_t ld, int64_t col0, int nh, int d, const float2* __restrict__ tab,
+                                int backward, T* x) {
+  constexpr int VN = Vec<T>::N;
+  const int half = d / 2, qv = half / VN;
+  const int64_t total = s * nh * qv;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int j = (int)(i % qv) * VN;
+    const int64_t t = i / qv;
+    const int hd = (int)(t % nh);
+    const int64_t row = t / nh;
+    T* p = x + row * ld + col0 + (int64_t)hd * d + j;
+    const float4* cs = reinterpret_cast<const float4*>(tab + row * half + j);  // VN float2 = VN/2 float4
+    Vec<T> a, b;
+    a.load(p);
+    b.load(p + half);
+    const float sg = backward ? -1.f : 1.f;
+#pragma unroll
+    for (int e = 0; e < VN; e += 2) {
+      const float4 c2 = cs[e / 2];  // (cos_e, sin_e, cos_e+1, sin_e+1)
+#pragma unroll
+      for (int k = 0; k < 2; ++k) {
+        const float c = k ? c2.z : c2.x, sv = sg * (k ? c2.w : c2.y);
+        const float x1 = a.f(e + k), x2 = b.f(e + k);
+        a.set(e + k, x1 * c - x2 * sv);
+        b.set(e + k, x2 * c + x1 * sv);
+      }
+    }
+    a.store(p);
+    b.store(p + half);
+  }
+}
+
 // ----------------------------------------------------------------- SwiGLU
 __device__ __forceinline__ float sigm(float z) { return 1.f / (1.f + __expf(-z)); }
 
@@ -467,7 +503,12 @@ stp_status rope(int dtype, int backward, int64_t s, int64_t ld, int64_t col0, in
     }
   }
   return STP_DISPATCH_DTYPE(dtype, [&] {
-    rope_kernel<T><<<grid_for(s * nh * (d / 8), 256), 256, 0, st>>>(s, ld, col0, nh, d, tab, backward, (T*)x);
+    constexpr int VN = Vec<T>::N;
+    if ((d / 2) % VN == 0 && ld % VN == 0 && col0 % VN == 0 && (reinterpret_cast<uintptr_t>(x) & 15) == 0)
+      rope_vec_kernel<T><<<grid_for(s * nh * (d / 2 / VN), 256), 256, 0, st>>>(s, ld, col0, nh, d, tab, backward,
+                                                                               (T*)x);
+    else
+      rope_kernel<T><<<grid_for(s * nh * (d / 8), 256), 256, 0, st>>>(s, ld, col0, nh, d, tab, backward, (T*)x);
     count_launch();
     STP_LAUNCH_CHECK();
     return STP_OK;

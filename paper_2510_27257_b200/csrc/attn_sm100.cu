@@ -2131,6 +2131,221 @@ __global__ void __launch_bounds__(384, 1)
   }
 }
 
+// dK/dV kernel, version 5: v4 with ping-pong softmax warp groups (one key row
+// per thread, alternate query tiles per group).
+__global__ void __launch_bounds__(384, 1)
+    attn_bwd_dkdv_sm100_v5(const __grid_constant__ CUtensorMap tm_kv, const __grid_constant__ CUtensorMap tm_q64,
+                           const __grid_constant__ CUtensorMap tm_do64, const BwdArgs a) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sK = smem;
+  uint8_t* sV = smem + TILE_BYTES;
+  uint8_t* sQ = smem + 2 * TILE_BYTES;                          // [STAGES]
+  uint8_t* sdO = sQ + KV4_STAGES * QT_BYTES;                    // [STAGES]
+  float* s_lse = reinterpret_cast<float*>(sdO + KV4_STAGES * QT_BYTES);  // [2][QT]
+  float* s_D = s_lse + 2 * QT;                                           // [2][QT]
+  uint64_t* bar = reinterpret_cast<uint64_t*>(s_D + 2 * QT);
+  uint64_t* kv_full = bar + 0;
+  uint64_t* qdo_full = bar + 1;                  // [STAGES]
+  uint64_t* qdo_empty = bar + 1 + KV4_STAGES;    // [STAGES]
+  uint64_t* sdp_full = bar + 1 + 2 * KV4_STAGES;  // [2]
+  uint64_t* pds_full = sdp_full + 2;              // [2]
+  uint64_t* done = pds_full + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(done + 1);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nt = (a.s + T - 1) / T;
+  const int nq64 = (a.s + QT - 1) / QT;
+  const int kt = gridDim.x - 1 - blockIdx.x;
+  const int h = blockIdx.y;
+  const int grp = a.nq / a.nkv, g = h / grp;
+  const int q0 = 2 * kt;           // first query tile that sees this key tile
+  const int n_q = nq64 - q0;
+  const int qcol = h * D, kcol = a.nq * D + g * D, vcol = (a.nq + a.nkv) * D + g * D;
+  (void)nt;
+
+  if (threadIdx.x == 0) {
+    mbar_init(kv_full, 1);
+    for (int i = 0; i < KV4_STAGES; ++i) {
+      mbar_init(qdo_full + i, 1);
+      mbar_init(qdo_empty + i, 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(sdp_full + i, 1);
+      mbar_init(pds_full + i, 128);
+    }
+    mbar_init(done, 1);
+    fence_barrier_init();
+    tma_prefetch_desc(&tm_kv);
+    tma_prefetch_desc(&tm_q64);
+    tma_prefetch_desc(&tm_do64);
+  }
+  if (warp == 2) tmem_alloc<512>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t tdV = tmem, tdK = tmem + 128, tSP = tmem + 256;  // buffer b: S at tSP + 128b, dP at +64
+
+  if (warp == 0) {
+    if (lane == 0) {
+      mbar_arrive_expect_tx(kv_full, 2 * TILE_BYTES);
+      tma_load_2d(sK, &tm_kv, kv_full, kcol, kt * T);
+      tma_load_2d(sK + ATOM, &tm_kv, kv_full, kcol + 64, kt * T);
+      tma_load_2d(sV, &tm_kv, kv_full, vcol, kt * T);
+      tma_load_2d(sV + ATOM, &tm_kv, kv_full, vcol + 64, kt * T);
+      for (int it = 0; it < n_q; ++it) {
+        const int st = it % KV4_STAGES, qi = q0 + it;
+        mbar_wait_wd(qdo_empty + st, ((it / KV4_STAGES) & 1) ^ 1, 217, a.s, a.nq, (int)blockIdx.y);
+        mbar_arrive_expect_tx(qdo_full + st, 2 * QT_BYTES);
+        uint8_t* q = sQ + st * QT_BYTES;
+        uint8_t* o = sdO + st * QT_BYTES;
+        tma_load_2d(q, &tm_q64, qdo_full + st, qcol, qi * QT);
+        tma_load_2d(q + QATOM, &tm_q64, qdo_full + st, qcol + 64, qi * QT);
+        tma_load_2d(o, &tm_do64, qdo_full + st, h * D, qi * QT);
+        tma_load_2d(o + QATOM, &tm_do64, qdo_full + st, h * D + 64, qi * QT);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t idS = make_idesc_bf16(T, QT, false, false);  // S^T, dP^T: M = 128 keys, N = 64 queries
+      constexpr uint32_t idMN = make_idesc_bf16(T, D, false, true);   // dV, dK: N = d, B (dO_i, Q_i) MN-major
+      const uint32_t k_addr = smem_u32(sK), v_addr = smem_u32(sV);
+      mbar_wait_wd(kv_full, 0, 218, a.s, a.nq, (int)blockIdx.y);
+      auto issue_sdp = [&](int it) {
+        const int st = it % KV4_STAGES, b = it & 1;
+        const uint32_t q_addr = smem_u32(sQ + st * QT_BYTES), do_addr = smem_u32(sdO + st * QT_BYTES);
+        mbar_wait_wd(qdo_full + st, (it / KV4_STAGES) & 1, 219, a.s, a.nq, (int)blockIdx.y);
+        tc_fence_after();
+        const uint32_t tS = tSP + b * 128, tP = tS + 64;
+#pragma unroll
+        for (int kk = 0; kk < D / 16; ++kk) {
+          const uint32_t ka = (kk >> 2) * ATOM + (kk & 3) * 32, qa = (kk >> 2) * QATOM + (kk & 3) * 32;
+          mma_f16_ss(tS, make_sw128_desc(k_addr + ka, 16, 1024), make_sw128_desc(q_addr + qa, 16, 1024), idS,
+                     kk > 0 ? 1u : 0u);
+        }
+#pragma unroll
+        for (int kk = 0; kk < D / 16; ++kk) {
+          const uint32_t ka = (kk >> 2) * ATOM + (kk & 3) * 32, qa = (kk >> 2) * QATOM + (kk & 3) * 32;
+          mma_f16_ss(tP, make_sw128_desc(v_addr + ka, 16, 1024), make_sw128_desc(do_addr + qa, 16, 1024), idS,
+                     kk > 0 ? 1u : 0u);
+        }
+        mma_commit(sdp_full + b);
+      };
+      issue_sdp(0);
+      for (int it = 0; it < n_q; ++it) {
+        if (it + 1 < n_q) issue_sdp(it + 1);
+        const int st = it % KV4_STAGES, b = it & 1;
+        const uint32_t q_addr = smem_u32(sQ + st * QT_BYTES), do_addr = smem_u32(sdO + st * QT_BYTES);
+        const uint32_t tS = tSP + b * 128, tP = tS + 64;
+        mbar_wait_wd(pds_full + b, (it >> 1) & 1, 220, a.s, a.nq, (int)blockIdx.y);
+        tc_fence_after();
+#pragma unroll
+        for (int kk = 0; kk < QT / 16; ++kk)  // dV += P^T dO_i   (P^T from TMEM, 8 columns per k16)
+          mma_f16_ts(tdV, tS + kk * 8, make_sw128_desc(do_addr + kk * 2048, QATOM, 1024), idMN,
+                     (it > 0 || kk > 0) ? 1u : 0u);
+#pragma unroll
+        for (int kk = 0; kk < QT / 16; ++kk)  // dK += dS^T Q_i
+          mma_f16_ts(tdK, tP + kk * 8, make_sw128_desc(q_addr + kk * 2048, QATOM, 1024), idMN,
+                     (it > 0 || kk > 0) ? 1u : 0u);
+        mma_commit(qdo_empty + st);
+      }
+      mma_commit(done);
+    }
+  } else if (warp >= 4) {
+    // ping-pong: warp group grp (4 warps, one key row per thread) converts
+    // the query tiles with it % 2 == grp, all 64 columns in two 32-column
+    // chunks; the two groups run independently (own named barrier / lse-D
+    // staging), so one group's TMEM / global-load latency hides behind the
+    // other's work.
+    const int grp = (warp - 4) >> 2, quad = warp & 3;
+    const int r = quad * 32 + lane;                     // key row
+    const int gtid = threadIdx.x - 128 - grp * 128;     // 0..127 within the group
+    const uint32_t lane_off = (uint32_t)(quad * 32) << 16;
+    const int krow = kt * T + r;
+    const bool vrow = krow < a.s;
+    const float sl2 = a.scale_log2;
+    for (int it = grp; it < n_q; it += 2) {
+      const int b = it & 1, qi = q0 + it;
+      const int qbase = qi * QT;
+      {  // threads 0-63 of the group stage -lse*log2e, 64-127 stage D, for the 64 query rows
+        const int q = qbase + (gtid & (QT - 1));
+        if (gtid < QT) s_lse[b * QT + gtid] = q < a.s ? -a.lse[(int64_t)h * a.s + q] * 1.4426950408889634f : -INFINITY;
+        else s_D[b * QT + gtid - QT] = q < a.s ? a.Dl[(int64_t)h * a.s + q] : 0.f;
+      }
+      named_bar(1 + grp, 128);
+      const uint32_t tS = tSP + b * 128, tP = tS + 64;
+      mbar_wait_wd(sdp_full + b, (it >> 1) & 1, 251, a.s, a.nq, h);
+      tc_fence_after();
+      const bool diag = it < 2;  // tiles overlapping the key tile need the causal mask
+#pragma unroll 1
+      for (int ch = 0; ch < 2; ++ch) {
+        const float* nl = s_lse + b * QT + ch * 32;
+        const float* Dq = s_D + b * QT + ch * 32;
+        uint32_t sv[32], dv[32];
+        tmem_ld_32x32b_x32(tS + ch * 32 + lane_off, sv);
+        tmem_ld_32x32b_x32(tP + ch * 32 + lane_off, dv);
+        tmem_wait_ld();
+        uint32_t pp[16], pd[16];
+#pragma unroll
+        for (int i = 0; i < 32; i += 4) {
+          const float4 l4 = *reinterpret_cast<const float4*>(nl + i);
+          const float4 d4 = *reinterpret_cast<const float4*>(Dq + i);
+          const float la[4] = {l4.x, l4.y, l4.z, l4.w}, da[4] = {d4.x, d4.y, d4.z, d4.w};
+          float pv[4], dd[4];
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            pv[e] = ex2(fmaf(__uint_as_float(sv[i + e]), sl2, la[e]));
+            if (diag && qbase + ch * 32 + i + e < krow) pv[e] = 0.f;
+            dd[e] = pv[e] * (__uint_as_float(dv[i + e]) - da[e]);
+          }
+          if (!vrow) pv[0] = pv[1] = pv[2] = pv[3] = dd[0] = dd[1] = dd[2] = dd[3] = 0.f;
+          pp[i >> 1] = pack2(pv[0], pv[1]);
+          pp[(i >> 1) + 1] = pack2(pv[2], pv[3]);
+          pd[i >> 1] = pack2(dd[0], dd[1]);
+          pd[(i >> 1) + 1] = pack2(dd[2], dd[3]);
+        }
+        // P^T / dS^T (bf16 pairs) over columns [16 ch, 16 ch + 16) of S^T / dP^T:
+        // chunk 1 reads S^T columns 32-63, which chunk 0's stores do not touch
+        tmem_st_32x32b_x16(tS + ch * 16 + lane_off, pp);
+        tmem_st_32x32b_x16(tP + ch * 16 + lane_off, pd);
+      }
+      tmem_wait_st();
+      tc_fence_before();
+      mbar_arrive(pds_full + b);
+    }
+    const int half = grp;
+    mbar_wait_wd(done, 0, 222, a.s, a.nq, (int)blockIdx.y);
+    tc_fence_after();
+    float* kr = a.dk_part + ((int64_t)h * a.s + (vrow ? krow : 0)) * D + half * 64;
+    float* vr = a.dv_part + ((int64_t)h * a.s + (vrow ? krow : 0)) * D + half * 64;
+#pragma unroll 1
+    for (int c = 0; c < 2; ++c) {
+      uint32_t v[32], k[32];
+      tmem_ld_32x32b_x32(tdV + half * 64 + c * 32 + lane_off, v);
+      tmem_ld_32x32b_x32(tdK + half * 64 + c * 32 + lane_off, k);
+      tmem_wait_ld();
+      if (vrow) {
+#pragma unroll
+        for (int i = 0; i < 32; i += 4) {
+          *reinterpret_cast<float4*>(vr + c * 32 + i) =
+              make_float4(__uint_as_float(v[i]), __uint_as_float(v[i + 1]), __uint_as_float(v[i + 2]),
+                          __uint_as_float(v[i + 3]));
+          *reinterpret_cast<float4*>(kr + c * 32 + i) =
+              make_float4(__uint_as_float(k[i]) * a.scale, __uint_as_float(k[i + 1]) * a.scale,
+                          __uint_as_float(k[i + 2]) * a.scale, __uint_as_float(k[i + 3]) * a.scale);
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc<512>(tmem);
+  }
+}
+
 // dQ kernel, version 4: key tiles of 64 rows so that S / dP are
 // DOUBLE-BUFFERED in TMEM (dQ 128 | S0 64 | dP0 64 | S1 64 | dP1 64 | dS0 32 |
 // dS1 32 columns): the MMA warp issues S/dP of tile j+1 as soon as the
@@ -2597,13 +2812,14 @@ stp_status attn_fwd_sm100_launch(int s, int nq, int nkv, const void* qkv_base, i
 namespace stp {
 // Tuning knob (stp_set_option "attn_bwd"): 1 = smem P^T/dS^T dK/dV kernel,
 // 2 = TMEM-resident P^T/dS^T with double-buffered Q/dO, 3 = 8 softmax warps,
-// 4 = 64-row query tiles with double-buffered S^T/dP^T (default), 5 = v4 +
+// 4 = 64-row query tiles with double-buffered S^T/dP^T, 5 = v4 +
 // the dQ kernel with 64-row key tiles and double-buffered S/dP, 6 = v4 + the
-// dQ kernel with Q / dO as TMEM-resident A operands.
+// dQ kernel with Q / dO as TMEM-resident A operands, 7 = v4 with ping-pong
+// softmax warp groups in the dK/dV kernel + the v3 dQ kernel (default).
 int& attn_bwd_version_ref() {
   static int v = [] {
     const char* e = getenv("STP_ATTN_BWD");
-    return e ? atoi(e) : 4;  // runtime.cpp kAttnBwdDefault
+    return e ? atoi(e) : 7;  // runtime.cpp kAttnBwdDefault
   }();
   return v;
 }
@@ -2641,6 +2857,7 @@ stp_status attn_bwd_sm100_launch(int s, int nq, int nkv, const void* qkv_base, i
   a.scale_log2 = 1.4426950408889634f * a.scale;
   const int nt = (s + T - 1) / T;
   if (attn_bwd_version_ref() >= 4) {
+    const bool v5 = attn_bwd_version_ref() == 7;
     CUtensorMap tq64, td64;
     STP_TRY(tensor_map_bf16(&tq64, qkv_base, ld, s, ld, 64, QT));
     STP_TRY(tensor_map_bf16(&td64, dout, ldo, s, ldo, 64, QT));
@@ -2650,13 +2867,20 @@ stp_status attn_bwd_sm100_launch(int s, int nq, int nkv, const void* qkv_base, i
           cudaFuncSetAttribute(attn_bwd_dkdv_sm100_v4, cudaFuncAttributeMaxDynamicSharedMemorySize, KV4_SMEM));
       attr4 = true;
     }
-    attn_bwd_dkdv_sm100_v4<<<dim3(nt, nq), 384, KV4_SMEM, st>>>(tq, tq64, td64, a);
+    static bool attr7 = false;
+    if (v5 && !attr7) {
+      STP_CUDA_TRY(
+          cudaFuncSetAttribute(attn_bwd_dkdv_sm100_v5, cudaFuncAttributeMaxDynamicSharedMemorySize, KV4_SMEM));
+      attr7 = true;
+    }
+    if (v5) attn_bwd_dkdv_sm100_v5<<<dim3(nt, nq), 384, KV4_SMEM, st>>>(tq, tq64, td64, a);
+    else attn_bwd_dkdv_sm100_v4<<<dim3(nt, nq), 384, KV4_SMEM, st>>>(tq, tq64, td64, a);
   } else if (attn_bwd_version_ref() == 3) attn_bwd_dkdv_sm100_v3<<<dim3(nt, nq), 384, KV2_SMEM, st>>>(tq, td, a);
   else if (attn_bwd_version_ref() == 2) attn_bwd_dkdv_sm100_v2<<<dim3(nt, nq), 256, KV2_SMEM, st>>>(tq, td, a);
   else attn_bwd_dkdv_sm100<<<dim3(nt, nq), 256, KV_SMEM, st>>>(tq, td, a);
   count_launch();
   STP_LAUNCH_CHECK();
-  if (attn_bwd_version_ref() >= 6) {
+  if (attn_bwd_version_ref() == 6) {
     CUtensorMap tkv64;
     STP_TRY(tensor_map_bf16(&tkv64, qkv_base, ld, s, ld, 64, QT));
     static bool attr6 = false;
@@ -2666,7 +2890,7 @@ stp_status attn_bwd_sm100_launch(int s, int nq, int nkv, const void* qkv_base, i
     }
     attn_bwd_dq_sm100_v5<<<dim3(nt, nq), 384, DQ5_SMEM, st>>>(tkv64, a, (const bf16*)qkv_base, ld, (const bf16*)dout,
                                                               ldo);
-  } else if (attn_bwd_version_ref() >= 5) {
+  } else if (attn_bwd_version_ref() == 5) {
     CUtensorMap tkv64;
     STP_TRY(tensor_map_bf16(&tkv64, qkv_base, ld, s, ld, 64, QT));
     static bool attr5 = false;

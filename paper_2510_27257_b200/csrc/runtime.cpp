@@ -66,7 +66,7 @@ int& gemm_mc_mode_ref();
 int& attn_bwd_version_ref();
 int& attn_fwd_version_ref();
 constexpr int kAttnFwdDefault = 3;
-constexpr int kAttnBwdDefault = 4;
+constexpr int kAttnBwdDefault = 7;
 
 }  // namespace stp
 
@@ -87,7 +87,7 @@ stp_status stp_set_option(const char* key, int64_t value) {
     return STP_OK;
   }
   if (k == "attn_bwd") {
-    if (value < 0 || value > 6) return stp::fail(STP_EINVAL, "attn_bwd must be 0..6");
+    if (value < 0 || value > 7) return stp::fail(STP_EINVAL, "attn_bwd must be 0..7");
     stp::attn_bwd_version_ref() = value ? (int)value : stp::kAttnBwdDefault;
     return STP_OK;
   }

@@ -209,7 +209,7 @@ def test_colsum(dt):
     assert np.abs(_np(acc) - (1 + X.sum(0))).max() <= 1e-3
 
 
-@pytest.mark.parametrize("version", [1, 2, 3, 4, 5, 6])
+@pytest.mark.parametrize("version", [1, 2, 3, 4, 5, 6, 7])
 @pytest.mark.parametrize("s,nq,nkv", [(257, 7, 1), (1024, 4, 2), (2048, 7, 1), (300, 2, 2), (64, 2, 1), (65, 2, 1)])
 def test_attention_bwd_variants(s, nq, nkv, version):
     """tcgen05 backward variants: 1 = P^T/dS^T via smem, 2 = TMEM-resident with

@@ -728,6 +728,237 @@ __global__ void __launch_bounds__(FWD3_THREADS, 1)
   }
 }
 
+// Forward, version 4: like v3 (8 softmax warps, two per row, 64 key columns
+// each) but each half keeps its OWN running max / sum and its OWN O
+// accumulator (O_0 | O_1 | S0 | S1 = 4 x 128 TMEM columns): no per-tile
+// max exchange / 256-thread barrier between the halves; PV is two K = 64
+// MMAs (half h: O_h += P_h V_j[64h .. 64h+63]); P_h is written over the
+// S columns the same half just read.  The halves combine once at the end:
+// m = max(m_0, m_1), O = sum_h O_h 2^(m_h - m), l = sum_h l_h 2^(m_h - m).
+constexpr int SMEM_BYTES_V4 = 1024 + 5 * TILE_BYTES + 4 * T * 4 + 256;
+
+__global__ void __launch_bounds__(FWD3_THREADS, 1)
+    attn_fwd_sm100_v4(const __grid_constant__ CUtensorMap tm_qkv, const FwdArgs a) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sQ = smem;
+  uint8_t* sK = smem + TILE_BYTES;      // [2]
+  uint8_t* sV = smem + 3 * TILE_BYTES;  // [2]
+  float* sml = reinterpret_cast<float*>(smem + 5 * TILE_BYTES);  // [2 halves][m, l][T]
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sml + 4 * T);
+  uint64_t* q_full = bar + 0;
+  uint64_t* k_full = bar + 1;   // [2]
+  uint64_t* k_empty = bar + 3;  // [2]
+  uint64_t* v_full = bar + 5;   // [2]
+  uint64_t* v_empty = bar + 7;  // [2]
+  uint64_t* s_full = bar + 9;   // [2]
+  uint64_t* p_full = bar + 11;  // [2 buffers][2 halves]
+  uint64_t* o_done = bar + 15;  // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 18);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nqt = gridDim.x;
+  const int qt = nqt - 1 - blockIdx.x;
+  const int h = blockIdx.y;
+  const int grp = a.nq / a.nkv, g = h / grp;
+  const int n_kv = qt + 1;
+  const int qcol = h * D, kcol = a.nq * D + g * D, vcol = (a.nq + a.nkv) * D + g * D;
+
+  if (threadIdx.x == 0) {
+    mbar_init(q_full, 1);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(k_full + i, 1);
+      mbar_init(k_empty + i, 1);
+      mbar_init(v_full + i, 1);
+      mbar_init(v_empty + i, 1);
+      mbar_init(s_full + i, 1);
+      mbar_init(o_done + i, 1);
+    }
+    for (int i = 0; i < 4; ++i) mbar_init(p_full + i, 128);
+    fence_barrier_init();
+    tma_prefetch_desc(&tm_qkv);
+  }
+  if (warp == 2) tmem_alloc<512>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t tO = tmem, tS0 = tmem + 256;  // O_h at tO + 128h; S buffer b at tS0 + 128b
+
+  if (warp == 0) {
+    if (lane == 0) {
+      mbar_arrive_expect_tx(q_full, TILE_BYTES);
+      tma_load_2d(sQ, &tm_qkv, q_full, qcol, qt * T);
+      tma_load_2d(sQ + ATOM, &tm_qkv, q_full, qcol + 64, qt * T);
+      for (int j = 0; j < n_kv; ++j) {
+        const int b = j & 1;
+        const uint32_t ph = (j >> 1) & 1;
+        mbar_wait_wd(k_empty + b, ph ^ 1, 321, a.s, a.nq, (int)blockIdx.y);
+        mbar_arrive_expect_tx(k_full + b, TILE_BYTES);
+        tma_load_2d(sK + b * TILE_BYTES, &tm_qkv, k_full + b, kcol, j * T);
+        tma_load_2d(sK + b * TILE_BYTES + ATOM, &tm_qkv, k_full + b, kcol + 64, j * T);
+        mbar_wait_wd(v_empty + b, ph ^ 1, 322, a.s, a.nq, (int)blockIdx.y);
+        mbar_arrive_expect_tx(v_full + b, TILE_BYTES);
+        tma_load_2d(sV + b * TILE_BYTES, &tm_qkv, v_full + b, vcol, j * T);
+        tma_load_2d(sV + b * TILE_BYTES + ATOM, &tm_qkv, v_full + b, vcol + 64, j * T);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t idS = make_idesc_bf16(T, T, false, false);
+      constexpr uint32_t idO = make_idesc_bf16(T, D, false, true);
+      const uint32_t q_addr = smem_u32(sQ);
+      mbar_wait_wd(q_full, 0, 323, a.s, a.nq, (int)blockIdx.y);
+      auto issue_pv = [&](int jj) {
+        const int b = jj & 1;
+        mbar_wait_wd(v_full + b, (jj >> 1) & 1, 325, a.s, a.nq, (int)blockIdx.y);
+        const uint32_t v_addr = smem_u32(sV + b * TILE_BYTES);
+#pragma unroll
+        for (int hf = 0; hf < 2; ++hf) {
+          mbar_wait_wd(p_full + b * 2 + hf, (jj >> 1) & 1, 324, a.s, a.nq, (int)blockIdx.y);
+          tc_fence_after();
+          // O_hf += P_hf (TMEM, keys 64hf..64hf+63: 32 packed columns) . V_j[64hf.., :]
+#pragma unroll
+          for (int kk = 0; kk < 4; ++kk)
+            mma_f16_ts(tO + hf * 128, tS0 + b * 128 + hf * 64 + kk * 8,
+                       make_sw128_desc(v_addr + (hf * 4 + kk) * 2048, ATOM, 1024), idO, (jj > 0 || kk > 0) ? 1u : 0u);
+        }
+        mma_commit(v_empty + b);
+        mma_commit(o_done + b);
+      };
+      for (int j = 0; j < n_kv; ++j) {
+        const int b = j & 1;
+        const uint32_t ph = (j >> 1) & 1;
+        mbar_wait_wd(k_full + b, ph, 326, a.s, a.nq, (int)blockIdx.y);
+        // buffer b last held P(j-2), consumed by PV(j-2), issued before this S(j) (in-order pipe)
+        tc_fence_after();
+        const uint32_t k_addr = smem_u32(sK + b * TILE_BYTES);
+#pragma unroll
+        for (int kk = 0; kk < D / 16; ++kk) {
+          const uint32_t off = (kk >> 2) * ATOM + (kk & 3) * 32;
+          mma_f16_ss(tS0 + b * 128, make_sw128_desc(q_addr + off, 16, 1024), make_sw128_desc(k_addr + off, 16, 1024),
+                     idS, kk > 0 ? 1u : 0u);
+        }
+        mma_commit(k_empty + b);
+        mma_commit(s_full + b);
+        if (j > 0) issue_pv(j - 1);
+      }
+      issue_pv(n_kv - 1);
+    }
+  } else if (warp >= 4) {
+    const int half = (warp - 4) >> 2;          // key columns [64*half, 64*half + 64) of every S tile
+    const int quad = warp & 3;                 // TMEM lanes 32*quad ..
+    const int r = quad * 32 + lane;
+    const uint32_t lane_off = (uint32_t)(quad * 32) << 16;
+    const int qrow = qt * T + r;
+    const float sl2 = a.scale_log2;
+    const uint32_t tOh = tO + half * 128;
+    float m = -INFINITY, l = 0.f;
+    for (int j = 0; j < n_kv; ++j) {
+      const int b = j & 1;
+      mbar_wait_wd(s_full + b, (j >> 1) & 1, 328, a.s, a.nq, (int)blockIdx.y);
+      tc_fence_after();
+      uint32_t u[64];
+      tmem_ld_32x32b_x32(tS0 + b * 128 + half * 64 + lane_off, u);
+      tmem_ld_32x32b_x32(tS0 + b * 128 + half * 64 + 32 + lane_off, u + 32);
+      tmem_wait_ld();
+      float sv[64];
+#pragma unroll
+      for (int i = 0; i < 64; ++i) sv[i] = __uint_as_float(u[i]);
+      const int cbase = j * T + half * 64;
+      if (j == qt || cbase + 64 > a.s) {  // diagonal or ragged tile: causal / length mask
+#pragma unroll
+        for (int i = 0; i < 64; ++i)
+          if (cbase + i > qrow || cbase + i >= a.s) sv[i] = -INFINITY;
+      }
+      float mx = sv[0];
+#pragma unroll
+      for (int i = 1; i < 64; ++i) mx = fmaxf(mx, sv[i]);
+      mx *= sl2;
+      const bool need = mx > m + 8.f;
+      if (__any_sync(0xffffffffu, need)) {
+        float alpha = 1.f;
+        if (need) {
+          alpha = (m == -INFINITY) ? 0.f : ex2(m - mx);
+          l *= alpha;
+          m = mx;
+        }
+        if (j > 0) {  // O_half holds PV(0..j-1): wait for PV(j-1), rescale all 128 columns
+          mbar_wait_wd(o_done + ((j - 1) & 1), ((j - 1) >> 1) & 1, 329, a.s, a.nq, (int)blockIdx.y);
+          tc_fence_after();
+#pragma unroll 1
+          for (int c = 0; c < 4; ++c) {
+            uint32_t v[32];
+            const uint32_t ta = tOh + c * 32 + lane_off;
+            tmem_ld_32x32b_x32(ta, v);
+            tmem_wait_ld();
+#pragma unroll
+            for (int i = 0; i < 32; ++i) v[i] = __float_as_uint(__uint_as_float(v[i]) * alpha);
+            tmem_st_32x32b_x32(ta, v);
+          }
+          tmem_wait_st();
+        }
+      }
+      const float nm = -m;
+      uint32_t pk[32];
+#pragma unroll
+      for (int i = 0; i < 64; i += 2) {
+        const float p0 = (m == -INFINITY) ? 0.f : ex2(fmaf(sv[i], sl2, nm));
+        const float p1 = (m == -INFINITY) ? 0.f : ex2(fmaf(sv[i + 1], sl2, nm));
+        l += p0 + p1;
+        pk[i >> 1] = pack2(p0, p1);
+      }
+      // P_half over the first 32 of this half's 64 S columns (already read above)
+      tmem_st_32x32b_x32(tS0 + b * 128 + half * 64 + lane_off, pk);
+      tmem_wait_st();
+      tc_fence_before();
+      mbar_arrive(p_full + b * 2 + half);
+    }
+    // combine the halves: exchange (m, l) once
+    sml[(half * 2 + 0) * T + r] = m;
+    sml[(half * 2 + 1) * T + r] = l;
+    named_bar(2, 256);
+    const float m0 = sml[0 * T + r], l0 = sml[1 * T + r], m1 = sml[2 * T + r], l1 = sml[3 * T + r];
+    const float mt = fmaxf(m0, m1);
+    const float f0 = (m0 == -INFINITY) ? 0.f : ex2(m0 - mt), f1 = (m1 == -INFINITY) ? 0.f : ex2(m1 - mt);
+    const float lt = l0 * f0 + l1 * f1;
+    mbar_wait_wd(o_done + ((n_kv - 1) & 1), ((n_kv - 1) >> 1) & 1, 331, a.s, a.nq, (int)blockIdx.y);
+    tc_fence_after();
+    const bool valid = qrow < a.s;
+    const float inv = 1.f / lt;
+    const float c0 = f0 * inv, c1 = f1 * inv;
+    bf16* orow = reinterpret_cast<bf16*>(a.o) + (int64_t)(valid ? qrow : 0) * a.ldo + (int64_t)h * D + half * 64;
+#pragma unroll 1
+    for (int c = 0; c < 2; ++c) {  // this half writes output columns [64 half, 64 half + 64)
+      uint32_t v0[32], v1[32];
+      tmem_ld_32x32b_x32(tO + half * 64 + c * 32 + lane_off, v0);
+      tmem_ld_32x32b_x32(tO + 128 + half * 64 + c * 32 + lane_off, v1);
+      tmem_wait_ld();
+      if (valid) {
+#pragma unroll
+        for (int i = 0; i < 32; i += 8) {
+          float o8[8];
+#pragma unroll
+          for (int e = 0; e < 8; ++e) o8[e] = __uint_as_float(v0[i + e]) * c0 + __uint_as_float(v1[i + e]) * c1;
+          uint4 q;
+          q.x = pack2(o8[0], o8[1]);
+          q.y = pack2(o8[2], o8[3]);
+          q.z = pack2(o8[4], o8[5]);
+          q.w = pack2(o8[6], o8[7]);
+          *reinterpret_cast<uint4*>(orow + c * 32 + i) = q;
+        }
+      }
+    }
+    if (valid && half == 0) a.lse[(int64_t)h * a.s + qrow] = (mt + log2f(lt)) * 0.69314718055994530942f;
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc<512>(tmem);
+  }
+}
+
 // ---------------------------------------------------------------- backward
 // dQ kernel: one CTA per (query tile, head); loop over key tiles j <= i:
 //   S = Q K_j^T, dP = dO V_j^T (TMEM), dS = P * (dP - D) (softmax warps,
@@ -2785,7 +3016,14 @@ stp_status attn_fwd_sm100_launch(int s, int nq, int nkv, const void* qkv_base, i
   a.lse = lse;
   a.scale_log2 = 1.4426950408889634f / sqrtf((float)D);
   dim3 grid((s + T - 1) / T, nq);
-  if (attn_fwd_version_ref() == 3) {
+  if (attn_fwd_version_ref() == 4) {
+    static bool attr4 = false;
+    if (!attr4) {
+      STP_CUDA_TRY(cudaFuncSetAttribute(attn_fwd_sm100_v4, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES_V4));
+      attr4 = true;
+    }
+    attn_fwd_sm100_v4<<<grid, FWD3_THREADS, SMEM_BYTES_V4, st>>>(tm, a);
+  } else if (attn_fwd_version_ref() == 3) {
     static bool attr3 = false;
     if (!attr3) {
       STP_CUDA_TRY(cudaFuncSetAttribute(attn_fwd_sm100_v3, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES_V3));

@@ -53,6 +53,60 @@ __device__ __forceinline__ float ex2(float x) {
   return y;
 }
 
+// Packed fp32 pair arithmetic of sm_100 (FFMA2 / FADD2 / FMUL2: two lanes of
+// fp32 per instruction) and the 3-input max (FMNMX3): the softmax warps are
+// issue-bound, so halving the per-element ALU instruction count matters.
+__device__ __forceinline__ uint64_t pk2f(float a, float b) {
+  uint64_t r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+  return r;
+}
+__device__ __forceinline__ void up2f(uint64_t v, float& a, float& b) {
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(v));
+}
+__device__ __forceinline__ uint64_t ffma2(uint64_t a, uint64_t b, uint64_t c) {
+  uint64_t r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
+  return r;
+}
+__device__ __forceinline__ uint64_t fadd2(uint64_t a, uint64_t b) {
+  uint64_t r;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+__device__ __forceinline__ uint64_t fsub2(uint64_t a, uint64_t b) {
+  uint64_t r;
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+__device__ __forceinline__ uint64_t fmul2(uint64_t a, uint64_t b) {
+  uint64_t r;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+__device__ __forceinline__ float fmax3(float a, float b, float c) {
+  float r;
+  asm("max.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
+  return r;
+}
+
+// 2^x on the FMA pipe (FA4-style MUFU offload): round-to-nearest split
+// x = i + f (magic-number add, f in [-0.5, 0.5]), degree-4 polynomial for 2^f
+// (max rel. error ~4e-6 on [-0.5, 0.5]), 2^i by exponent-field add.  x < -126
+// flushes to 0 like ex2.approx.ftz.
+__device__ __forceinline__ float ex2_fma(float x) {
+  x = fmaxf(x, -127.f);
+  const float t = x + 12582912.f;  // 1.5 * 2^23: integer part lands in the mantissa
+  const int i = __float_as_int(t) - 0x4B400000;
+  const float f = x - (t - 12582912.f);
+  float p = fmaf(f, 0.0013333558f, 0.0096181291f);
+  p = fmaf(p, f, 0.0555041087f);
+  p = fmaf(p, f, 0.2402265070f);
+  p = fmaf(p, f, 0.6931471806f);
+  p = fmaf(p, f, 1.0f);
+  return x <= -126.f ? 0.f : __int_as_float(__float_as_int(p) + (i << 23));
+}
+
 __device__ __forceinline__ void named_bar(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
 
 __global__ void __launch_bounds__(256, 1)
@@ -515,6 +569,7 @@ __global__ void __launch_bounds__(256, 1)
 constexpr int FWD3_THREADS = 384;
 constexpr int SMEM_BYTES_V3 = 1024 + 5 * TILE_BYTES + 3 * 2 * T * 4 + 256;
 
+template <bool POLY>
 __global__ void __launch_bounds__(FWD3_THREADS, 1)
     attn_fwd_sm100_v3(const __grid_constant__ CUtensorMap tm_qkv, const FwdArgs a) {
   extern __shared__ uint8_t smem_raw[];
@@ -649,9 +704,10 @@ __global__ void __launch_bounds__(FWD3_THREADS, 1)
         for (int i = 0; i < 64; ++i)
           if (cbase + i > qrow || cbase + i >= a.s) sv[i] = -INFINITY;
       }
-      float mx = sv[0];
+      float mx = fmax3(sv[0], sv[1], sv[2]);
 #pragma unroll
-      for (int i = 1; i < 64; ++i) mx = fmaxf(mx, sv[i]);
+      for (int i = 3; i < 63; i += 2) mx = fmax3(mx, sv[i], sv[i + 1]);
+      mx = fmaxf(mx, sv[63]);
       smax[(b * 2 + half) * T + r] = mx;
       named_bar(2, 256);
       mx = fmaxf(smax[(b * 2) * T + r], smax[(b * 2 + 1) * T + r]) * sl2;
@@ -682,11 +738,21 @@ __global__ void __launch_bounds__(FWD3_THREADS, 1)
         mbar_wait_wd(o_done + b, ((j - 2) >> 1) & 1, 310, a.s, a.nq, (int)blockIdx.y);
       }
       const float nm = -m;
+      const uint64_t sc2 = pk2f(sl2, sl2), nm2 = pk2f(nm, nm);
+      uint64_t lacc = pk2f(0.f, 0.f);
 #pragma unroll
       for (int i = 0; i < 64; i += 2) {
-        const float p0 = ex2(fmaf(sv[i], sl2, nm)), p1 = ex2(fmaf(sv[i + 1], sl2, nm));
-        l += p0 + p1;
+        float t0, t1;
+        up2f(ffma2(pk2f(sv[i], sv[i + 1]), sc2, nm2), t0, t1);
+        const float p0 = ex2(t0);
+        const float p1 = POLY ? ex2_fma(t1) : ex2(t1);
+        lacc = fadd2(lacc, pk2f(p0, p1));
         u[i >> 1] = pack2(p0, p1);
+      }
+      {
+        float l0, l1;
+        up2f(lacc, l0, l1);
+        l += l0 + l1;
       }
       tmem_st_32x32b_x32(tP0 + b * 64 + half * 32 + lane_off, u);
       tmem_wait_st();
@@ -1908,16 +1974,19 @@ __global__ void __launch_bounds__(384, 1)
       const int cbase = j * T + half * 64;
       const bool edge = (j == qt) || cbase + 64 > a.s || !vrow;
       uint32_t pk[32];
+      const uint64_t sc2 = pk2f(sl2, sl2), nl2 = pk2f(nlse2, nlse2), D2 = pk2f(Dv, Dv);
 #pragma unroll
-      for (int i = 0; i < 64; i += 2) {
-        float d2[2];
-#pragma unroll
-        for (int e = 0; e < 2; ++e) {
-          float p = ex2(fmaf(__uint_as_float(sv[i + e]), sl2, nlse2));
-          if (edge && (cbase + i + e > qrow || cbase + i + e >= a.s || !vrow)) p = 0.f;
-          d2[e] = p * (__uint_as_float(dv[i + e]) - Dv);
+      for (int i = 0; i < 64; i += 2) {  // packed fp32 pairs (FFMA2 / FADD2 / FMUL2)
+        float t0, t1;
+        up2f(ffma2(pk2f(__uint_as_float(sv[i]), __uint_as_float(sv[i + 1])), sc2, nl2), t0, t1);
+        float p0 = ex2(t0), p1 = ex2(t1);
+        if (edge) {
+          if (cbase + i > qrow || cbase + i >= a.s || !vrow) p0 = 0.f;
+          if (cbase + i + 1 > qrow || cbase + i + 1 >= a.s || !vrow) p1 = 0.f;
         }
-        pk[i >> 1] = pack2(d2[0], d2[1]);
+        float d0, d1;
+        up2f(fmul2(pk2f(p0, p1), fsub2(pk2f(__uint_as_float(dv[i]), __uint_as_float(dv[i + 1])), D2)), d0, d1);
+        pk[i >> 1] = pack2(d0, d1);
       }
       const int b = j & 1;
       if (j >= 2) mbar_wait_wd(dq_done + b, ((j - 2) >> 1) & 1, 209, a.s, a.nq, (int)blockIdx.y);
@@ -2522,13 +2591,23 @@ __global__ void __launch_bounds__(384, 1)
         for (int i = 0; i < 32; i += 4) {
           const float4 l4 = *reinterpret_cast<const float4*>(nl + i);
           const float4 d4 = *reinterpret_cast<const float4*>(Dq + i);
-          const float la[4] = {l4.x, l4.y, l4.z, l4.w}, da[4] = {d4.x, d4.y, d4.z, d4.w};
           float pv[4], dd[4];
+          const uint64_t sc2 = pk2f(sl2, sl2);
 #pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            pv[e] = ex2(fmaf(__uint_as_float(sv[i + e]), sl2, la[e]));
-            if (diag && qbase + ch * 32 + i + e < krow) pv[e] = 0.f;
-            dd[e] = pv[e] * (__uint_as_float(dv[i + e]) - da[e]);
+          for (int e = 0; e < 4; e += 2) {  // packed fp32 pairs (FFMA2 / FADD2 / FMUL2)
+            const uint64_t la2 = e ? pk2f(l4.z, l4.w) : pk2f(l4.x, l4.y);
+            const uint64_t da2 = e ? pk2f(d4.z, d4.w) : pk2f(d4.x, d4.y);
+            float t0, t1;
+            up2f(ffma2(pk2f(__uint_as_float(sv[i + e]), __uint_as_float(sv[i + e + 1])), sc2, la2), t0, t1);
+            pv[e] = ex2(t0);
+            pv[e + 1] = ex2(t1);
+            if (diag) {
+              if (qbase + ch * 32 + i + e < krow) pv[e] = 0.f;
+              if (qbase + ch * 32 + i + e + 1 < krow) pv[e + 1] = 0.f;
+            }
+            up2f(fmul2(pk2f(pv[e], pv[e + 1]),
+                       fsub2(pk2f(__uint_as_float(dv[i + e]), __uint_as_float(dv[i + e + 1])), da2)),
+                 dd[e], dd[e + 1]);
           }
           if (!vrow) pv[0] = pv[1] = pv[2] = pv[3] = dd[0] = dd[1] = dd[2] = dd[3] = 0.f;
           pp[i >> 1] = pack2(pv[0], pv[1]);
@@ -3023,13 +3102,17 @@ stp_status attn_fwd_sm100_launch(int s, int nq, int nkv, const void* qkv_base, i
       attr4 = true;
     }
     attn_fwd_sm100_v4<<<grid, FWD3_THREADS, SMEM_BYTES_V4, st>>>(tm, a);
-  } else if (attn_fwd_version_ref() == 3) {
+  } else if (attn_fwd_version_ref() == 3 || attn_fwd_version_ref() == 5) {
     static bool attr3 = false;
     if (!attr3) {
-      STP_CUDA_TRY(cudaFuncSetAttribute(attn_fwd_sm100_v3, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES_V3));
+      STP_CUDA_TRY(
+          cudaFuncSetAttribute(attn_fwd_sm100_v3<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES_V3));
+      STP_CUDA_TRY(
+          cudaFuncSetAttribute(attn_fwd_sm100_v3<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES_V3));
       attr3 = true;
     }
-    attn_fwd_sm100_v3<<<grid, FWD3_THREADS, SMEM_BYTES_V3, st>>>(tm, a);
+    if (attn_fwd_version_ref() == 5) attn_fwd_sm100_v3<true><<<grid, FWD3_THREADS, SMEM_BYTES_V3, st>>>(tm, a);
+    else attn_fwd_sm100_v3<false><<<grid, FWD3_THREADS, SMEM_BYTES_V3, st>>>(tm, a);
   } else if (attn_fwd_version_ref() == 2) {
     static bool attr2 = false;
     if (!attr2) {

@@ -82,7 +82,7 @@ stp_status stp_set_option(const char* key, int64_t value) {
     return STP_OK;
   }
   if (k == "attn_fwd") {  // 0 = built-in default
-    if (value < 0 || value > 4) return stp::fail(STP_EINVAL, "attn_fwd must be 0..4");
+    if (value < 0 || value > 5) return stp::fail(STP_EINVAL, "attn_fwd must be 0..5");
     stp::attn_fwd_version_ref() = value ? (int)value : stp::kAttnFwdDefault;
     return STP_OK;
   }

@@ -223,7 +223,7 @@ def test_attention_bwd_variants(s, nq, nkv, version):
         _lib.call("stp_set_option", b"attn_bwd", 0)
 
 
-@pytest.mark.parametrize("version", [1, 2, 3, 4])
+@pytest.mark.parametrize("version", [1, 2, 3, 4, 5])
 @pytest.mark.parametrize("s,nq,nkv", [(257, 7, 1), (1024, 4, 2), (2048, 7, 1), (300, 2, 2), (64, 2, 1), (65, 2, 1)])
 def test_attention_fwd_variants(s, nq, nkv, version):
     """tcgen05 forward variants: 1 = P via smem, 2 = P in TMEM with 4 softmax

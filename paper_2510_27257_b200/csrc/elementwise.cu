@@ -314,13 +314,31 @@ __global__ void ce_stats_kernel(int64_t s, int64_t Vl, const T* __restrict__ log
   for (int64_t r = blockIdx.x; r < s; r += gridDim.x) {
     const T* z = logits + r * ld;
     float m = -INFINITY, sum = 0.f;
-    for (int64_t j = threadIdx.x; j < Vl; j += blockDim.x) {
-      const float v = to_f<T>(z[j]);
-      if (v > m) {
-        sum = sum * __expf(m - v) + 1.f;
-        m = v;
-      } else {
-        sum += __expf(v - m);
+    constexpr int VN = Vec<T>::N;
+    if (Vl % VN == 0 && ld % VN == 0 && (reinterpret_cast<uintptr_t>(logits) & 15) == 0) {
+      // 16-byte vectors: one running-max update per vector
+      for (int64_t j = (int64_t)threadIdx.x * VN; j < Vl; j += (int64_t)blockDim.x * VN) {
+        Vec<T> x;
+        x.load(z + j);
+        float vm = x.f(0);
+#pragma unroll
+        for (int i = 1; i < VN; ++i) vm = fmaxf(vm, x.f(i));
+        if (vm > m) {
+          sum = (m == -INFINITY) ? 0.f : sum * __expf(m - vm);
+          m = vm;
+        }
+#pragma unroll
+        for (int i = 0; i < VN; ++i) sum += __expf(x.f(i) - m);
+      }
+    } else {
+      for (int64_t j = threadIdx.x; j < Vl; j += blockDim.x) {
+        const float v = to_f<T>(z[j]);
+        if (v > m) {
+          sum = sum * __expf(m - v) + 1.f;
+          m = v;
+        } else {
+          sum += __expf(v - m);
+        }
       }
     }
     // warp combine (m, sum)
@@ -379,10 +397,25 @@ __global__ void ce_grad_kernel(int64_t s, int64_t Vl, T* logits, int64_t ld, con
     T* z = logits + r * ld;
     const float l = lse[r];
     const int64_t t = (int64_t)tgt[r] - v0;
-    for (int64_t j = threadIdx.x; j < Vl; j += blockDim.x) {
-      float p = __expf(to_f<T>(z[j]) - l);
-      if (j == t) p -= 1.f;
-      z[j] = from_f<T>(p * scale);
+    constexpr int VN = Vec<T>::N;
+    if (Vl % VN == 0 && ld % VN == 0 && (reinterpret_cast<uintptr_t>(logits) & 15) == 0) {  // 16-byte vectors
+      for (int64_t j = (int64_t)threadIdx.x * VN; j < Vl; j += (int64_t)blockDim.x * VN) {
+        Vec<T> x;
+        x.load(z + j);
+#pragma unroll
+        for (int i = 0; i < VN; ++i) {
+          float p = __expf(x.f(i) - l);
+          if (j + i == t) p -= 1.f;
+          x.set(i, p * scale);
+        }
+        x.store(z + j);
+      }
+    } else {
+      for (int64_t j = threadIdx.x; j < Vl; j += blockDim.x) {
+        float p = __expf(to_f<T>(z[j]) - l);
+        if (j == t) p -= 1.f;
+        z[j] = from_f<T>(p * scale);
+      }
     }
   }
 }

@@ -937,10 +937,10 @@ __global__ void __launch_bounds__(FWD3_THREADS, 1)
         for (int i = 0; i < 64; ++i)
           if (cbase + i > qrow || cbase + i >= a.s) sv[i] = -INFINITY;
       }
-      float mx = sv[0];
+      float mx = fmax3(sv[0], sv[1], sv[2]);
 #pragma unroll
-      for (int i = 1; i < 64; ++i) mx = fmaxf(mx, sv[i]);
-      mx *= sl2;
+      for (int i = 3; i < 63; i += 2) mx = fmax3(mx, sv[i], sv[i + 1]);
+      mx = fmaxf(mx, sv[63]) * sl2;
       const bool need = mx > m + 8.f;
       if (__any_sync(0xffffffffu, need)) {
         float alpha = 1.f;
@@ -965,14 +965,23 @@ __global__ void __launch_bounds__(FWD3_THREADS, 1)
           tmem_wait_st();
         }
       }
-      const float nm = -m;
+      // m == -inf (every key of this half masked so far): exponent -inf -> P = 0
+      const float nm = (m == -INFINITY) ? -INFINITY : -m;
+      const uint64_t sc2 = pk2f(sl2, sl2), nm2 = pk2f(nm, nm);
+      uint64_t lacc = pk2f(0.f, 0.f);
       uint32_t pk[32];
 #pragma unroll
       for (int i = 0; i < 64; i += 2) {
-        const float p0 = (m == -INFINITY) ? 0.f : ex2(fmaf(sv[i], sl2, nm));
-        const float p1 = (m == -INFINITY) ? 0.f : ex2(fmaf(sv[i + 1], sl2, nm));
-        l += p0 + p1;
+        float t0, t1;
+        up2f(ffma2(pk2f(sv[i], sv[i + 1]), sc2, nm2), t0, t1);
+        const float p0 = ex2(t0), p1 = ex2(t1);
+        lacc = fadd2(lacc, pk2f(p0, p1));
         pk[i >> 1] = pack2(p0, p1);
+      }
+      {
+        float l0, l1;
+        up2f(lacc, l0, l1);
+        l += l0 + l1;
       }
       // P_half over the first 32 of this half's 64 S columns (already read above)
       tmem_st_32x32b_x32(tS0 + b * 128 + half * 64 + lane_off, pk);
@@ -3071,7 +3080,7 @@ __global__ void attn_bwd_reduce(int s, int nq, int nkv, const float* __restrict_
 int& attn_fwd_version_ref() {
   static int v = [] {
     const char* e = getenv("STP_ATTN_FWD");
-    return e ? atoi(e) : 3;
+    return e ? atoi(e) : 4;  // runtime.cpp kAttnFwdDefault
   }();
   return v;
 }

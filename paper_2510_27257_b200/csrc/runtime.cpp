@@ -65,7 +65,7 @@ void prof_push(int cls, double flops, double bytes, cudaEvent_t e0, cudaEvent_t 
 int& gemm_mc_mode_ref();
 int& attn_bwd_version_ref();
 int& attn_fwd_version_ref();
-constexpr int kAttnFwdDefault = 3;
+constexpr int kAttnFwdDefault = 4;
 constexpr int kAttnBwdDefault = 7;
 
 }  // namespace stp

@@ -108,6 +108,54 @@ __global__ void rmsnorm_dgamma_kernel(int64_t rows, int h, const T* __restrict__
   atomicAdd(&dgamma[c], acc);
 }
 
+// Vectorised column reductions: one thread = VN consecutive columns (16-byte
+// loads), a block of rows per blockIdx.y, one fp32 atomic per column.
+template <typename T>
+__global__ void rmsnorm_dgamma_vec_kernel(int64_t rows, int h, const T* __restrict__ dy, const T* __restrict__ x,
+                                          const float* __restrict__ rstd, float* dgamma, int64_t rows_per_block) {
+  constexpr int VN = Vec<T>::N;
+  const int c = (blockIdx.x * blockDim.x + threadIdx.x) * VN;
+  if (c >= h) return;
+  const int64_t r0 = (int64_t)blockIdx.y * rows_per_block;
+  const int64_t r1 = min(rows, r0 + rows_per_block);
+  float acc[VN];
+#pragma unroll
+  for (int i = 0; i < VN; ++i) acc[i] = 0.f;
+#pragma unroll 4
+  for (int64_t r = r0; r < r1; ++r) {
+    Vec<T> a, b;
+    a.load(dy + r * h + c);
+    b.load(x + r * h + c);
+    const float rs = rstd[r];
+#pragma unroll
+    for (int i = 0; i < VN; ++i) acc[i] = fmaf(a.f(i) * b.f(i), rs, acc[i]);
+  }
+#pragma unroll
+  for (int i = 0; i < VN; ++i) atomicAdd(&dgamma[c + i], acc[i]);
+}
+
+template <typename T>
+__global__ void colsum_vec_kernel(int64_t rows, int64_t n, const T* __restrict__ X, int64_t ld, float* acc,
+                                  int64_t rows_per_block) {
+  constexpr int VN = Vec<T>::N;
+  const int64_t c = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * VN;
+  if (c >= n) return;
+  const int64_t r0 = (int64_t)blockIdx.y * rows_per_block;
+  const int64_t r1 = min(rows, r0 + rows_per_block);
+  float sum[VN];
+#pragma unroll
+  for (int i = 0; i < VN; ++i) sum[i] = 0.f;
+#pragma unroll 4
+  for (int64_t r = r0; r < r1; ++r) {
+    Vec<T> a;
+    a.load(X + r * ld + c);
+#pragma unroll
+    for (int i = 0; i < VN; ++i) sum[i] += a.f(i);
+  }
+#pragma unroll
+  for (int i = 0; i < VN; ++i) atomicAdd(&acc[c + i], sum[i]);
+}
+
 template <typename T>
 __global__ void rmsnorm_bwd_kernel(int64_t rows, int h, const T* __restrict__ dy, const T* __restrict__ x,
                                    const T* __restrict__ g, const float* __restrict__ rstd,
@@ -447,6 +495,24 @@ __global__ void add_kernel(int64_t n, const T* __restrict__ a, const T* __restri
 
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
 
+template <typename T>
+stp_status launch_dgamma(int64_t rows, int64_t h, const T* dy, const T* x, const float* rstd, float* dgamma,
+                         cudaStream_t st) {
+  constexpr int VN = Vec<T>::N;
+  if (h % VN == 0 && aligned16(dy) && aligned16(x)) {
+    const int64_t rpb = 64;
+    dim3 grid((unsigned)((h / VN + 127) / 128), (unsigned)((rows + rpb - 1) / rpb));
+    rmsnorm_dgamma_vec_kernel<T><<<grid, 128, 0, st>>>(rows, (int)h, dy, x, rstd, dgamma, rpb);
+  } else {
+    const int64_t rpb = 128;
+    dim3 grid2((unsigned)((h + 255) / 256), (unsigned)((rows + rpb - 1) / rpb));
+    rmsnorm_dgamma_kernel<T><<<grid2, 256, 0, st>>>(rows, (int)h, dy, x, rstd, dgamma, rpb);
+  }
+  count_launch();
+  STP_LAUNCH_CHECK();
+  return STP_OK;
+}
+
 }  // namespace
 
 // Shared launchers (also used by the executor).
@@ -471,11 +537,7 @@ stp_status rmsnorm_bwd(int dtype, int64_t rows, int64_t h, const void* dy, const
   if (rows == 0) return STP_OK;
   return STP_DISPATCH_DTYPE(dtype, [&] {
     if (dgamma) {  // before dx: dx may alias dres, never dy / x
-      const int64_t rpb = 128;
-      dim3 grid2((unsigned)((h + 255) / 256), (unsigned)((rows + rpb - 1) / rpb));
-      rmsnorm_dgamma_kernel<T><<<grid2, 256, 0, st>>>(rows, (int)h, (const T*)dy, (const T*)x, rstd, dgamma, rpb);
-      count_launch();
-      STP_LAUNCH_CHECK();
+      STP_TRY(launch_dgamma<T>(rows, h, (const T*)dy, (const T*)x, rstd, dgamma, st));
     }
     rmsnorm_bwd_kernel<T><<<grid_for(rows, kWarpsPerBlock), 32 * kWarpsPerBlock, 0, st>>>(
         rows, (int)h, (const T*)dy, (const T*)x, (const T*)g, rstd, (const T*)dres, (T*)dx, nullptr);
@@ -492,12 +554,7 @@ stp_status rmsnorm_dgamma(int dtype, int64_t rows, int64_t h, const void* dy, co
                           float* dgamma, cudaStream_t st) {
   if (rows == 0 || !dgamma) return STP_OK;
   return STP_DISPATCH_DTYPE(dtype, [&] {
-    const int64_t rpb = 128;
-    dim3 grid2((unsigned)((h + 255) / 256), (unsigned)((rows + rpb - 1) / rpb));
-    rmsnorm_dgamma_kernel<T><<<grid2, 256, 0, st>>>(rows, (int)h, (const T*)dy, (const T*)x, rstd, dgamma, rpb);
-    count_launch();
-    STP_LAUNCH_CHECK();
-    return STP_OK;
+    return launch_dgamma<T>(rows, h, (const T*)dy, (const T*)x, rstd, dgamma, st);
   });
 }
 
@@ -631,9 +688,16 @@ stp_status ce_grad(int dtype, int64_t s, int64_t Vl, void* logits, int64_t ld, c
 stp_status colsum_acc(int dtype, int64_t rows, int64_t n, const void* X, int64_t ld, float* acc, cudaStream_t st) {
   if (rows == 0 || n == 0) return STP_OK;
   return STP_DISPATCH_DTYPE(dtype, [&] {
-    const int64_t rpb = 256;
-    dim3 grid((unsigned)((n + 255) / 256), (unsigned)((rows + rpb - 1) / rpb));
-    colsum_kernel<T><<<grid, 256, 0, st>>>(rows, n, (const T*)X, ld, acc, rpb);
+    constexpr int VN = Vec<T>::N;
+    if (n % VN == 0 && ld % VN == 0 && aligned16(X)) {
+      const int64_t rpb = 64;
+      dim3 grid((unsigned)((n / VN + 255) / 256), (unsigned)((rows + rpb - 1) / rpb));
+      colsum_vec_kernel<T><<<grid, 256, 0, st>>>(rows, n, (const T*)X, ld, acc, rpb);
+    } else {
+      const int64_t rpb = 256;
+      dim3 grid((unsigned)((n + 255) / 256), (unsigned)((rows + rpb - 1) / rpb));
+      colsum_kernel<T><<<grid, 256, 0, st>>>(rows, n, (const T*)X, ld, acc, rpb);
+    }
     count_launch();
     STP_LAUNCH_CHECK();
     return STP_OK;

@@ -196,6 +196,61 @@ __global__ void rmsnorm_bwd_kernel(int64_t rows, int h, const T* __restrict__ dy
   (void)dgamma;
 }
 
+// Row-cached variant (h <= 32 * VN * NV): x and dy of the row stay in
+// registers between the reduction and the output pass, so each is read from
+// HBM once (the two-pass kernel above re-reads both).
+template <typename T, int NV>
+__global__ void __launch_bounds__(256) rmsnorm_bwd_cached_kernel(int64_t rows, int h, const T* __restrict__ dy,
+                                                                  const T* __restrict__ x, const T* __restrict__ g,
+                                                                  const float* __restrict__ rstd, const T* dres,
+                                                                  T* dx) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp0 = (int64_t)blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5);
+  const int64_t nwarps = (int64_t)gridDim.x * kWarpsPerBlock;
+  constexpr int VN = Vec<T>::N;
+  for (int64_t r = warp0; r < rows; r += nwarps) {
+    const float rs = rstd[r];
+    Vec<T> a[NV], d[NV];
+    float dot = 0.f;
+#pragma unroll
+    for (int v = 0; v < NV; ++v) {
+      const int c = (v * 32 + lane) * VN;
+      if (c < h) {
+        a[v].load(x + r * h + c);
+        d[v].load(dy + r * h + c);
+      }
+    }
+#pragma unroll
+    for (int v = 0; v < NV; ++v) {
+      const int c = (v * 32 + lane) * VN;
+      if (c < h) {
+        Vec<T> gg;
+        gg.load(g + c);
+#pragma unroll
+        for (int i = 0; i < VN; ++i) dot += gg.f(i) * d[v].f(i) * a[v].f(i);
+      }
+    }
+    dot = warp_sum(dot) / (float)h;
+    const float k = rs * rs * rs * dot;
+#pragma unroll
+    for (int v = 0; v < NV; ++v) {
+      const int c = (v * 32 + lane) * VN;
+      if (c < h) {
+        Vec<T> gg, o, rr;
+        gg.load(g + c);
+        if (dres) rr.load(dres + r * h + c);
+#pragma unroll
+        for (int i = 0; i < VN; ++i) {
+          float val = rs * gg.f(i) * d[v].f(i) - a[v].f(i) * k;
+          if (dres) val += rr.f(i);
+          o.set(i, val);
+        }
+        o.store(dx + r * h + c);
+      }
+    }
+  }
+}
+
 // ------------------------------------------------------------------- RoPE
 // cos/sin of pos * theta^(-2j/d), j < d/2, evaluated once in fp64 per
 // (s, d, theta, pos0) and cached on the device as float2 [s][d/2].
@@ -542,8 +597,13 @@ stp_status rmsnorm_bwd(int dtype, int64_t rows, int64_t h, const void* dy, const
     if (dgamma) {  // before dx: dx may alias dres, never dy / x
       STP_TRY(launch_dgamma<T>(rows, h, (const T*)dy, (const T*)x, rstd, dgamma, st));
     }
-    rmsnorm_bwd_kernel<T><<<grid_for(rows, kWarpsPerBlock), 32 * kWarpsPerBlock, 0, st>>>(
-        rows, (int)h, (const T*)dy, (const T*)x, (const T*)g, rstd, (const T*)dres, (T*)dx, nullptr);
+    constexpr int VN = Vec<T>::N;
+    if (h <= 32 * VN * 16)
+      rmsnorm_bwd_cached_kernel<T, 16><<<grid_for(rows, kWarpsPerBlock), 32 * kWarpsPerBlock, 0, st>>>(
+          rows, (int)h, (const T*)dy, (const T*)x, (const T*)g, rstd, (const T*)dres, (T*)dx);
+    else
+      rmsnorm_bwd_kernel<T><<<grid_for(rows, kWarpsPerBlock), 32 * kWarpsPerBlock, 0, st>>>(
+          rows, (int)h, (const T*)dy, (const T*)x, (const T*)g, rstd, (const T*)dres, (T*)dx, nullptr);
     count_launch();
     STP_LAUNCH_CHECK();
     return STP_OK;

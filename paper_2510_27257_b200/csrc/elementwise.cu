@@ -93,6 +93,63 @@ __global__ void rmsnorm_fwd_kernel(int64_t rows, int h, const T* __restrict__ x,
   }
 }
 
+// Row-cached variant (h <= 32 * VN * NV): the row (x + resid) stays in
+// registers for the normalisation pass instead of being re-read.
+template <typename T, int NV>
+__global__ void __launch_bounds__(256) rmsnorm_fwd_cached_kernel(int64_t rows, int h, const T* __restrict__ x,
+                                                                  const T* __restrict__ resid, T* x_out,
+                                                                  const T* __restrict__ g, float eps, T* y,
+                                                                  float* rstd_out) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp0 = (int64_t)blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5);
+  const int64_t nwarps = (int64_t)gridDim.x * kWarpsPerBlock;
+  constexpr int VN = Vec<T>::N;
+  for (int64_t r = warp0; r < rows; r += nwarps) {
+    Vec<T> a[NV];
+    float ss = 0.f;
+#pragma unroll
+    for (int v = 0; v < NV; ++v) {
+      const int c = (v * 32 + lane) * VN;
+      if (c < h) a[v].load(x + r * h + c);
+    }
+    if (resid) {
+#pragma unroll
+      for (int v = 0; v < NV; ++v) {
+        const int c = (v * 32 + lane) * VN;
+        if (c < h) {
+          Vec<T> b;
+          b.load(resid + r * h + c);
+#pragma unroll
+          for (int i = 0; i < VN; ++i) a[v].set(i, a[v].f(i) + b.f(i));
+          a[v].store(x_out + r * h + c);
+        }
+      }
+    }
+#pragma unroll
+    for (int v = 0; v < NV; ++v) {
+      const int c = (v * 32 + lane) * VN;
+      if (c < h) {
+#pragma unroll
+        for (int i = 0; i < VN; ++i) ss += a[v].f(i) * a[v].f(i);
+      }
+    }
+    ss = warp_sum(ss);
+    const float rs = rsqrtf(ss / (float)h + eps);
+    if (rstd_out && lane == 0) rstd_out[r] = rs;
+#pragma unroll
+    for (int v = 0; v < NV; ++v) {
+      const int c = (v * 32 + lane) * VN;
+      if (c < h) {
+        Vec<T> gg, o;
+        gg.load(g + c);
+#pragma unroll
+        for (int i = 0; i < VN; ++i) o.set(i, a[v].f(i) * rs * gg.f(i));
+        o.store(y + r * h + c);
+      }
+    }
+  }
+}
+
 // dgamma partials accumulate in shared memory, flushed once per block.
 // dgamma[c] += sum_rows dy * x * rstd: one thread per column, a block of
 // rows per blockIdx.y (coalesced across threads), one atomic per column.
@@ -581,8 +638,13 @@ stp_status rmsnorm_fwd(int dtype, int64_t rows, int64_t h, const void* x, const 
   STP_CHECK_ARG(!resid || x_out, "resid needs x_out");
   if (rows == 0) return STP_OK;
   return STP_DISPATCH_DTYPE(dtype, [&] {
-    rmsnorm_fwd_kernel<T><<<grid_for(rows, kWarpsPerBlock), 32 * kWarpsPerBlock, 0, st>>>(
-        rows, (int)h, (const T*)x, (const T*)resid, (T*)x_out, (const T*)g, eps, (T*)y, rstd);
+    constexpr int VN = Vec<T>::N;
+    if (h <= 32 * VN * 16)
+      rmsnorm_fwd_cached_kernel<T, 16><<<grid_for(rows, kWarpsPerBlock), 32 * kWarpsPerBlock, 0, st>>>(
+          rows, (int)h, (const T*)x, (const T*)resid, (T*)x_out, (const T*)g, eps, (T*)y, rstd);
+    else
+      rmsnorm_fwd_kernel<T><<<grid_for(rows, kWarpsPerBlock), 32 * kWarpsPerBlock, 0, st>>>(
+          rows, (int)h, (const T*)x, (const T*)resid, (T*)x_out, (const T*)g, eps, (T*)y, rstd);
     count_launch();
     STP_LAUNCH_CHECK();
     return STP_OK;

@@ -2,11 +2,14 @@
 //
 // One stp_stage per rank process.  It owns three kinds of CUDA streams:
 //   compute   F/B/W units (GEMMs, attention, SwiGLU, embedding, LM head)
-//   tp-comm   the TP communication phases of the units (NCCL reduce-scatter
-//             -> residual add + RMSNorm (fwd) / RMSNorm-bwd + residual grad
-//             (bwd) -> NCCL all-gather), i.e. the Pre-Attn / Pre-MLP units
-//             placed "according to their computational dependencies"
-//              in the sequence-parallel form (reading Q10)
+//   tp-comm   the TP communication phases of the units (reduce-scatter ->
+//             residual add + RMSNorm (fwd) / RMSNorm-bwd + residual grad
+//             (bwd) -> all-gather), i.e. the Pre-Attn / Pre-MLP units placed
+//             "according to their computational dependencies" (PAPER.md
+//             P:L70) in the sequence-parallel form (reading Q10).  Transport
+//             (STP_TP_TRANSPORT): p2p (default) = one fused NVLink kernel per
+//             phase over IPC-mapped peer buffers (tpcomm.cu, ce_* / p2p_*
+//             below), ce = copy-engine pulls, nccl = NCCL RS / AG
 //   pp        one stream per (peer, direction) NCCL communicator for the PP
 //             activation / gradient send-recv
 // and executes its rank's unit list (stp_schedule_units) in order: every unit

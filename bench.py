@@ -354,6 +354,7 @@ def ours(args):
         for sched in args.compare_scheds.split(","):
             if sched.startswith("1f1b-i") and args.m % p:
                 continue
+            progress(f"compare: {sched}")
             stc = make_stage(sched)
             for _ in range(args.warmup):
                 stc.step(d_tok, d_tgt)

@@ -2236,6 +2236,7 @@ constexpr int QT_BYTES = QT * D * 2;            // 16 KB
 constexpr int QATOM = QT * 64 * 2;              // 8 KB
 constexpr int KV4_STAGES = 4;
 constexpr int KV4_SMEM = 1024 + 2 * TILE_BYTES + 2 * KV4_STAGES * QT_BYTES + 4 * QT * 4 + 256;
+constexpr int KV5_SMEM = 1024 + 2 * TILE_BYTES + 2 * KV4_STAGES * QT_BYTES + 8 * QT * 4 + 256;
 
 __global__ void __launch_bounds__(384, 1)
     attn_bwd_dkdv_sm100_v4(const __grid_constant__ CUtensorMap tm_kv, const __grid_constant__ CUtensorMap tm_q64,
@@ -2451,9 +2452,12 @@ __global__ void __launch_bounds__(384, 1)
   uint8_t* sV = smem + TILE_BYTES;
   uint8_t* sQ = smem + 2 * TILE_BYTES;                          // [STAGES]
   uint8_t* sdO = sQ + KV4_STAGES * QT_BYTES;                    // [STAGES]
-  float* s_lse = reinterpret_cast<float*>(sdO + KV4_STAGES * QT_BYTES);  // [2][QT]
-  float* s_D = s_lse + 2 * QT;                                           // [2][QT]
-  uint64_t* bar = reinterpret_cast<uint64_t*>(s_D + 2 * QT);
+  // per warp group, double-buffered by (it >> 1) & 1: a group's threads sync only
+  // at their own per-tile barrier, so a fast thread may stage tile it + 2 while a
+  // slow one still reads tile it's rows
+  float* s_lse = reinterpret_cast<float*>(sdO + KV4_STAGES * QT_BYTES);  // [2 groups][2][QT]
+  float* s_D = s_lse + 4 * QT;                                           // [2 groups][2][QT]
+  uint64_t* bar = reinterpret_cast<uint64_t*>(s_D + 4 * QT);
   uint64_t* kv_full = bar + 0;
   uint64_t* qdo_full = bar + 1;                  // [STAGES]
   uint64_t* qdo_empty = bar + 1 + KV4_STAGES;    // [STAGES]
@@ -2577,10 +2581,11 @@ __global__ void __launch_bounds__(384, 1)
     for (int it = grp; it < n_q; it += 2) {
       const int b = it & 1, qi = q0 + it;
       const int qbase = qi * QT;
+      const int sb = grp * 2 + ((it >> 1) & 1);  // this group's staging buffer for tile it
       {  // threads 0-63 of the group stage -lse*log2e, 64-127 stage D, for the 64 query rows
         const int q = qbase + (gtid & (QT - 1));
-        if (gtid < QT) s_lse[b * QT + gtid] = q < a.s ? -a.lse[(int64_t)h * a.s + q] * 1.4426950408889634f : -INFINITY;
-        else s_D[b * QT + gtid - QT] = q < a.s ? a.Dl[(int64_t)h * a.s + q] : 0.f;
+        if (gtid < QT) s_lse[sb * QT + gtid] = q < a.s ? -a.lse[(int64_t)h * a.s + q] * 1.4426950408889634f : -INFINITY;
+        else s_D[sb * QT + gtid - QT] = q < a.s ? a.Dl[(int64_t)h * a.s + q] : 0.f;
       }
       named_bar(1 + grp, 128);
       const uint32_t tS = tSP + b * 128, tP = tS + 64;
@@ -2589,8 +2594,8 @@ __global__ void __launch_bounds__(384, 1)
       const bool diag = it < 2;  // tiles overlapping the key tile need the causal mask
 #pragma unroll 1
       for (int ch = 0; ch < 2; ++ch) {
-        const float* nl = s_lse + b * QT + ch * 32;
-        const float* Dq = s_D + b * QT + ch * 32;
+        const float* nl = s_lse + sb * QT + ch * 32;
+        const float* Dq = s_D + sb * QT + ch * 32;
         uint32_t sv[32], dv[32];
         tmem_ld_32x32b_x32(tS + ch * 32 + lane_off, sv);
         tmem_ld_32x32b_x32(tP + ch * 32 + lane_off, dv);
@@ -3200,10 +3205,10 @@ stp_status attn_bwd_sm100_launch(int s, int nq, int nkv, const void* qkv_base, i
     static bool attr7 = false;
     if (v5 && !attr7) {
       STP_CUDA_TRY(
-          cudaFuncSetAttribute(attn_bwd_dkdv_sm100_v5, cudaFuncAttributeMaxDynamicSharedMemorySize, KV4_SMEM));
+          cudaFuncSetAttribute(attn_bwd_dkdv_sm100_v5, cudaFuncAttributeMaxDynamicSharedMemorySize, KV5_SMEM));
       attr7 = true;
     }
-    if (v5) attn_bwd_dkdv_sm100_v5<<<dim3(nt, nq), 384, KV4_SMEM, st>>>(tq, tq64, td64, a);
+    if (v5) attn_bwd_dkdv_sm100_v5<<<dim3(nt, nq), 384, KV5_SMEM, st>>>(tq, tq64, td64, a);
     else attn_bwd_dkdv_sm100_v4<<<dim3(nt, nq), 384, KV4_SMEM, st>>>(tq, tq64, td64, a);
   } else if (attn_bwd_version_ref() == 3) attn_bwd_dkdv_sm100_v3<<<dim3(nt, nq), 384, KV2_SMEM, st>>>(tq, td, a);
   else if (attn_bwd_version_ref() == 2) attn_bwd_dkdv_sm100_v2<<<dim3(nt, nq), 256, KV2_SMEM, st>>>(tq, td, a);

@@ -6,8 +6,9 @@ TP x PP on 1-8 B200; exposed TP-comm %; PP bubble rate).
 N = 1: Qwen2-7B-shaped model (configs[1] shape: h 3584, 28 layers, 28/4
 heads, d 128, I 18944, V 152064), seq 6144, 8 microbatches, TP=1 PP=1 with
 two virtual stages (V-shape), the R-STP braided schedule, bf16.  N > 1
-(torchrun, one rank per GPU): TP x PP = 2x1, 2x2 (N=4), 4x2 (N=8), same
-model and global batch (strong scaling).  A step = one stp_train_step: all
+(torchrun, one rank per GPU): TP x PP = 2x1 (N=2), 4x1 (N=4, SURVEY's proxy
+of the TP=8 configuration), 4x2 (N=8), same model and global batch (strong
+scaling); --grid TxP overrides.  A step = one stp_train_step: all
 microbatches' forward + B + W over the TP x PP grid, fp32 gradient
 accumulation, end-of-step gamma all-reduce; no optimizer.
 
@@ -18,7 +19,12 @@ over ranks.  Weights (15 GB) and the activation stash (~84 GB at N=1) are far
 larger than L2, so no explicit L2 flush is needed (stated in config.l2).
 
 --impl reference: the CPU oracle (oracle/model.py, fp64 numpy) timed on the
-host cores on a bounded sample of the same workload (see cpu_sample()).
+host cores on a bounded sample of the same workload (see cpu_sample();
+STP_REF_SAMPLE_SEQ shrinks the sample for tests).
+
+--compare adds the schedule comparison (STP, 1F1B-I, naive, ZB, ablations) on
+the same kernels.  Progress goes to stderr; a host watchdog exits with status 3
+after STP_BENCH_WATCHDOG_S (600) seconds without progress.
 """
 from __future__ import annotations
 

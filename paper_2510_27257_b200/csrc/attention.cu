@@ -12,6 +12,7 @@
 //
 // fp32 path: straightforward SIMT kernels (one warp per row) used by the
 // fp32 parity mode.
+#include <algorithm>
 #include <cmath>
 
 #include "common.h"
@@ -595,10 +596,17 @@ stp_status attn_bwd_sm100_launch(int s, int nq, int nkv, const void* qkv_base, i
 
 // fp32 workspace: D = rowsum(dO*O) [nq, s] (+ for the tcgen05 path, d = 128:
 // dK / dV partials per query head [2, nq, s, 128]).
+int64_t attn_bwd_fused_ws_bytes(int64_t s, int nq, int nkv);
+int& attn_bwd_version_ref();
+stp_status attn_bwd_fused_launch(int s, int nq, int nkv, const void* qkv, int64_t ld, const void* o, const void* dout,
+                                 int64_t ldo, const float* lse, void* dqkv, int64_t ldd, void* ws, cudaStream_t st);
+
 int64_t attn_bwd_ws_bytes(int64_t s, int nq, int nkv, int d) {
-  (void)nkv;
   int64_t b = s * nq * (int64_t)sizeof(float);
-  if (d == 128) b = ((b + 255) / 256) * 256 + 2 * (int64_t)nq * s * 128 * (int64_t)sizeof(float);
+  if (d == 128) {
+    b = ((b + 255) / 256) * 256 + 2 * (int64_t)nq * s * 128 * (int64_t)sizeof(float);
+    b = std::max(b, attn_bwd_fused_ws_bytes(s, nq, nkv));
+  }
   return b;
 }
 
@@ -646,6 +654,13 @@ stp_status attn_bwd(int dtype, int64_t s, int nq, int nkv, int d, const void* q,
   float* Dl = (float*)ws;
   const int64_t warps = s * nq;
   return STP_DISPATCH_DTYPE(dtype, [&] {
+    // fused tcgen05 backward (d = 128, [q | k | v] layouts): computes its own D
+    if (dtype == STP_DTYPE_BF16 && d == 128 && attn_bwd_version_ref() == 8 && getenv("STP_ATTN_MMA_SYNC") == nullptr &&
+        (const uint8_t*)k == (const uint8_t*)q + (int64_t)nq * d * 2 &&
+        (const uint8_t*)v == (const uint8_t*)k + (int64_t)nkv * d * 2 && ld == (int64_t)(nq + 2 * nkv) * d &&
+        (const uint8_t*)dk == (const uint8_t*)dq + (int64_t)nq * d * 2 &&
+        (const uint8_t*)dv == (const uint8_t*)dk + (int64_t)nkv * d * 2 && ld % 8 == 0 && ldo % 8 == 0 && ldd % 8 == 0)
+      return attn_bwd_fused_launch((int)s, nq, nkv, q, ld, o, dout, ldo, lse, dq, ldd, ws, st);
     attn_bwd_dot<T><<<(unsigned)((warps + 7) / 8), 256, 0, st>>>((int)s, nq, d, (const T*)o, ldo, (const T*)dout, Dl);
     count_launch();
     STP_LAUNCH_CHECK();

@@ -23,6 +23,18 @@ void set_error(const char* fmt, ...) {
   va_end(ap);
 }
 
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) applies per device: keep
+// one bit per device (a process driving several GPUs sets it on each).
+stp_status set_max_smem_once(const void* func, int bytes, unsigned long long* mask) {
+  int dev = 0;
+  STP_CUDA_TRY(cudaGetDevice(&dev));
+  const unsigned long long bit = 1ull << (dev & 63);
+  if (__atomic_load_n(mask, __ATOMIC_ACQUIRE) & bit) return STP_OK;
+  STP_CUDA_TRY(cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+  __atomic_fetch_or(mask, bit, __ATOMIC_RELEASE);
+  return STP_OK;
+}
+
 int num_sms() {
   int dev = 0;
   if (cudaGetDevice(&dev) != cudaSuccess) return 148;
@@ -66,7 +78,7 @@ int& gemm_mc_mode_ref();
 int& attn_bwd_version_ref();
 int& attn_fwd_version_ref();
 constexpr int kAttnFwdDefault = 4;
-constexpr int kAttnBwdDefault = 7;
+constexpr int kAttnBwdDefault = 8;
 
 }  // namespace stp
 
@@ -87,7 +99,7 @@ stp_status stp_set_option(const char* key, int64_t value) {
     return STP_OK;
   }
   if (k == "attn_bwd") {
-    if (value < 0 || value > 7) return stp::fail(STP_EINVAL, "attn_bwd must be 0..7");
+    if (value < 0 || value > 8) return stp::fail(STP_EINVAL, "attn_bwd must be 0..8");
     stp::attn_bwd_version_ref() = value ? (int)value : stp::kAttnBwdDefault;
     return STP_OK;
   }

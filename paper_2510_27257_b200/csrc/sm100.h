@@ -6,6 +6,8 @@
 #include <cuda.h>
 #include <stdint.h>
 
+#include <cstdio>
+
 namespace stp {
 namespace sm100 {
 

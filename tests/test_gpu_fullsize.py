@@ -87,10 +87,14 @@ def test_fullsize_attention_sampled_rows():
             assert abs(got_l[h, qrow] - lref) <= 2e-2, (qrow, h)
 
 
-def test_fullsize_attention_backward_properties():
-    """dQ/dK/dV at s = 6144 (the bench launch config): sampled dV rows against
-    the definition dV_j = sum_i P_ij dO_i over the GQA group, computed in fp64
-    for a few key rows j near the end (few query rows see them)."""
+def test_fullsize_attention_backward_sampled():
+    """dQ, dK and dV at s = 6144 (the bench launch config) on sampled rows,
+    against the plain definition (SURVEY §8c.1 "Attention") in fp64:
+    P = softmax(Q K^T / sqrt(d) + causal), dP = dO V^T, D = rowsum(dO O),
+    dS = P (dP - D), dQ = dS K / sqrt(d), dK = dS^T Q / sqrt(d), dV = P^T dO,
+    dK / dV summed over the GQA group.  Every query row >= S/2 of the sampled
+    kv group is evaluated (so key rows >= S/2 get their complete sums); dQ is
+    also checked on early rows (0, 1, 127, 128, 1000) of another group."""
     from paper_2510_27257_b200 import ops
     g = torch.Generator(device="cuda").manual_seed(4)
     qkv = torch.randn(S, QKV, generator=g, device="cuda").to(torch.bfloat16)
@@ -103,20 +107,53 @@ def test_fullsize_attention_backward_properties():
     torch.cuda.synchronize()
     x = qkv.double().cpu().numpy()
     dO = do.double().cpu().numpy()
-    dv = dqkv.double().cpu().numpy()[:, (NQ + NKV) * D:]
+    got = dqkv.double().cpu().numpy()
     grp = NQ // NKV
-    for j in (S - 1, S - 2, S - 70):
-        for gk in (0, 3):
-            k = x[:, NQ * D + gk * D:NQ * D + (gk + 1) * D]
-            ref = np.zeros(D)
-            for hh in range(grp):
-                h = gk * grp + hh
-                for i in range(j, S):            # query rows that see key j
-                    q = x[i, h * D:(h + 1) * D]
-                    s_ = (k[:i + 1] @ q) / math.sqrt(D)
-                    m = s_.max()
-                    p = np.exp(s_ - m)
-                    p /= p.sum()
-                    ref += p[j] * dO[i, h * D:(h + 1) * D]
-            got = dv[j, gk * D:(gk + 1) * D]
-            assert np.abs(got - ref).max() <= 2e-2 * max(1.0, np.abs(ref).max()), (j, gk)
+    sc = 1.0 / math.sqrt(D)
+
+    def head(h):
+        gk = h // grp
+        return (x[:, h * D:(h + 1) * D], x[:, NQ * D + gk * D:NQ * D + (gk + 1) * D],
+                x[:, (NQ + NKV) * D + gk * D:(NQ + NKV) * D + (gk + 1) * D], dO[:, h * D:(h + 1) * D])
+
+    def rows_bwd(h, rows):
+        """P, dS for the given query rows of head h (full key range, causal)."""
+        q, k, v, d_o = head(h)
+        s_ = (q[rows] @ k.T) * sc
+        s_[np.asarray(rows)[:, None] < np.arange(S)[None, :]] = -np.inf
+        p = np.exp(s_ - s_.max(1, keepdims=True))
+        p /= p.sum(1, keepdims=True)
+        o_ = p @ v
+        dp = d_o[rows] @ v.T
+        dd = (d_o[rows] * o_).sum(1, keepdims=True)
+        return p, p * (dp - dd)
+
+    def check(gotv, ref, what):
+        err = np.abs(gotv - ref).max()
+        assert err <= 2e-2 * max(1.0, np.abs(ref).max()), (what, err, np.abs(ref).max())
+
+    gk = NKV - 1
+    rows = np.arange(S // 2, S)
+    keys = [S - 1, S - 2, S - 70, S - 129, S // 2 + 3, S // 2]
+    dk_ref = np.zeros((len(keys), D))
+    dv_ref = np.zeros((len(keys), D))
+    for hh in range(grp):
+        h = gk * grp + hh
+        q, k, v, d_o = head(h)
+        p, ds = rows_bwd(h, rows)
+        for n, j in enumerate(keys):
+            dk_ref[n] += sc * (ds[:, j] @ q[rows])
+            dv_ref[n] += p[:, j] @ d_o[rows]
+        if hh in (0, grp - 1):
+            for i in (S // 2, S // 2 + 64, S - 200, S - 1):
+                check(got[i, h * D:(h + 1) * D], sc * (ds[i - S // 2] @ k), ("dq", i, h))
+        del p, ds
+    for n, j in enumerate(keys):
+        check(got[j, (NQ + gk) * D:(NQ + gk + 1) * D], dk_ref[n], ("dk", j))
+        check(got[j, (NQ + NKV + gk) * D:(NQ + NKV + gk + 1) * D], dv_ref[n], ("dv", j))
+    early = [0, 1, 127, 128, 1000]
+    for h in (0, 9):
+        _, ds = rows_bwd(h, early)
+        k = head(h)[1]
+        for n, i in enumerate(early):
+            check(got[i, h * D:(h + 1) * D], sc * (ds[n] @ k), ("dq", i, h))

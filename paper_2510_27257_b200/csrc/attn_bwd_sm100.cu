@@ -15,7 +15,7 @@
 //   dQ_i^T = K^T dS_i^T         (M = d, N = 64; A = K^T and B = dS^T from smem,
 //                                both MN-major; D written over dP^T)
 // dQ_i^T is drained from TMEM by the warp group that converted tile i and
-// added into an fp32 [s, (nq + 2 nkv) * 128] accumulator with red.global.add
+// added into a head-major fp32 [nq + 2 nkv][s][128] accumulator with red.global.add
 // (L2-side reductions, no read-back); dK / dV are accumulated over the query
 // loop in TMEM and added into the same accumulator once per CTA (the GQA sum
 // over a kv head's query heads happens there: no per-head partials and no
@@ -66,8 +66,7 @@ struct FusedArgs {
   int s, nq, nkv, sp;  // sp: padded row stride (multiple of QT) of nl2 / Dp
   const float* nl2;    // [nq, sp]: -lse * log2(e); -inf beyond s (masks the ragged tail)
   const float* Dp;     // [nq, sp]: rowsum(dO * O); 0 beyond s
-  float* acc;          // fp32 [s, W]: dq | dk | dv columns (W = (nq + 2 nkv) * 128), zeroed
-  int64_t W;
+  float* acc;          // fp32 [nq + 2 nkv][s][128] (head-major): dq heads | dk | dv kv heads, zeroed
   float scale_log2;    // log2(e) / sqrt(d)
 };
 
@@ -309,17 +308,24 @@ __global__ void __launch_bounds__(384, 1)
       tmem_wait_ld();
       tc_fence_before();
       mbar_arrive(dq_free + gi);
-      float* dst = a.acc + (int64_t)qbase * a.W + (int64_t)h * D + r;
-      const int nv = min(QT, a.s - qbase);
+      // head-major accumulator: row stride 128 floats, so the 64 query rows of
+      // this thread's column d are compile-time offsets of one pointer
+      float* dst = a.acc + ((int64_t)h * a.s + qbase) * D + r;
+      if (qbase + QT <= a.s) {
 #pragma unroll
-      for (int j = 0; j < QT; ++j)
-        if (j < nv) red_add_f32(dst + (int64_t)j * a.W, __uint_as_float(qv[j]));
+        for (int j = 0; j < QT; ++j) red_add_f32(dst + j * D, __uint_as_float(qv[j]));
+      } else {
+        const int nv = a.s - qbase;
+#pragma unroll
+        for (int j = 0; j < QT; ++j)
+          if (j < nv) red_add_f32(dst + j * D, __uint_as_float(qv[j]));
+      }
     }
     // dK / dV of the key tile: group gi adds d columns [64 gi, 64 gi + 64)
     mbar_wait_wd(done, 0, 311, a.s, h, kt);
     tc_fence_after();
-    float* kr = a.acc + (int64_t)(vrow ? krow : 0) * a.W + (int64_t)(a.nq + g) * D + gi * 64;
-    float* vr = kr + (int64_t)a.nkv * D;
+    float* kr = a.acc + ((int64_t)(a.nq + g) * a.s + (vrow ? krow : 0)) * D + gi * 64;
+    float* vr = kr + (int64_t)a.nkv * a.s * D;
 #pragma unroll 1
     for (int c = 0; c < 2; ++c) {
       uint32_t v[32], k[32];
@@ -382,21 +388,27 @@ __global__ void attn_bwd_prep(int s, int sp, int nq, const bf16* __restrict__ o,
   }
 }
 
-// dqkv (bf16, [s, ldd], columns dq | dk | dv) = acc * (1/sqrt(d) for dq, dk; 1 for dv).
-__global__ void attn_bwd_finalize(int64_t rows, int64_t W, int64_t qk_cols, const float* __restrict__ acc, bf16* dst,
-                                  int64_t ldd, float scale) {
-  const int64_t w4 = W / 4, total = rows * w4;
+// dqkv (bf16, [s, ldd], columns dq | dk | dv) = acc (head-major [C][s][128])
+// x (1/sqrt(d) for the dq and dk heads, 1 for dv).  One float4 per thread;
+// a warp reads one 512-byte head row.
+__global__ void attn_bwd_finalize(int s, int C, int qk_heads, const float* __restrict__ acc, bf16* dst, int64_t ldd,
+                                  float scale) {
+  const int64_t total = (int64_t)s * C * (D / 4);
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t row = i / w4, col = (i % w4) * 4;
-    const float4 v = *reinterpret_cast<const float4*>(acc + row * W + col);
-    const float sc = col < qk_cols ? scale : 1.f;
-    *reinterpret_cast<uint2*>(dst + row * ldd + col) = make_uint2(pack2(v.x * sc, v.y * sc), pack2(v.z * sc, v.w * sc));
+    const int d4 = (int)(i % (D / 4)) * 4;
+    const int64_t rc = i / (D / 4);
+    const int c = (int)(rc % C);
+    const int64_t row = rc / C;
+    const float4 v = *reinterpret_cast<const float4*>(acc + ((int64_t)c * s + row) * D + d4);
+    const float sc = c < qk_heads ? scale : 1.f;
+    *reinterpret_cast<uint2*>(dst + row * ldd + (int64_t)c * D + d4) =
+        make_uint2(pack2(v.x * sc, v.y * sc), pack2(v.z * sc, v.w * sc));
   }
 }
 
 }  // namespace
 
-// Workspace of the fused path: nl2 [nq, sp], Dp [nq, sp], acc [s, (nq + 2 nkv) 128] (fp32).
+// Workspace of the fused path: nl2 [nq, sp], Dp [nq, sp], acc [nq + 2 nkv][s][128] (fp32).
 int64_t attn_bwd_fused_ws_bytes(int64_t s, int nq, int nkv) {
   const int64_t sp = (s + QT - 1) / QT * QT;
   return 2 * (int64_t)nq * sp * 4 + 256 + s * (int64_t)(nq + 2 * nkv) * D * 4;
@@ -412,8 +424,8 @@ stp_status attn_bwd_fused_launch(int s, int nq, int nkv, const void* qkv, int64_
   float* nl2 = reinterpret_cast<float*>(ws);
   float* Dp = nl2 + (int64_t)nq * sp;
   float* acc = reinterpret_cast<float*>((reinterpret_cast<uintptr_t>(Dp + (int64_t)nq * sp) + 255) & ~uintptr_t(255));
-  const int64_t W = (int64_t)(nq + 2 * nkv) * D;
-  STP_CUDA_TRY(cudaMemsetAsync(acc, 0, (size_t)s * W * 4, st));
+  const int C = nq + 2 * nkv;
+  STP_CUDA_TRY(cudaMemsetAsync(acc, 0, (size_t)s * C * D * 4, st));
   {
     const int64_t warps = (int64_t)sp * nq;
     attn_bwd_prep<<<(unsigned)((warps + 7) / 8), 256, 0, st>>>(s, sp, nq, (const bf16*)o, (const bf16*)dout, ldo, lse,
@@ -433,17 +445,15 @@ stp_status attn_bwd_fused_launch(int s, int nq, int nkv, const void* qkv, int64_
   a.nl2 = nl2;
   a.Dp = Dp;
   a.acc = acc;
-  a.W = W;
   a.scale_log2 = LOG2E / sqrtf((float)D);
   const int nt = (s + T - 1) / T;
   attn_bwd_fused_sm100<<<dim3(nq, nt), 384, FB_SMEM, st>>>(tkv, tq64, td64, a);
   count_launch();
   STP_LAUNCH_CHECK();
   {
-    const int64_t total = (int64_t)s * (W / 4);
+    const int64_t total = (int64_t)s * C * (D / 4);
     const int grid = (int)std::min<int64_t>((total + 255) / 256, 16 * num_sms());
-    attn_bwd_finalize<<<grid, 256, 0, st>>>(s, W, (int64_t)(nq + nkv) * D, acc, (bf16*)dqkv, ldd,
-                                            1.f / sqrtf((float)D));
+    attn_bwd_finalize<<<grid, 256, 0, st>>>(s, C, nq + nkv, acc, (bf16*)dqkv, ldd, 1.f / sqrtf((float)D));
     count_launch();
     STP_LAUNCH_CHECK();
   }

@@ -22,6 +22,8 @@
 #include "sm100.h"
 
 namespace stp {
+
+stp_status set_max_smem_once(const void* func, int bytes, unsigned long long* mask);
 namespace {
 
 using namespace sm100;
@@ -765,17 +767,22 @@ stp_status tensor_map(CUtensorMap* out, const void* ptr, int64_t d0, int64_t d1,
 
 // One tile counter per stream (GEMMs on one stream run in order; the last
 // fetch of each launch resets its counter to 0).
+// Counter blocks are kept per device (a thread that alternates devices
+// reuses each device's block instead of reallocating it).
 stp_status tile_counter(cudaStream_t st, int** out) {
-  thread_local int* base = nullptr;
-  thread_local int base_dev = -1;
-  thread_local std::unordered_map<cudaStream_t, int> slots;
+  struct DevCounters {
+    int* base = nullptr;
+    std::unordered_map<cudaStream_t, int> slots;
+  };
+  thread_local std::unordered_map<int, DevCounters> per_dev;
   int dev = 0;
   STP_CUDA_TRY(cudaGetDevice(&dev));
-  if (!base || base_dev != dev) {
+  DevCounters& dc = per_dev[dev];
+  int*& base = dc.base;
+  auto& slots = dc.slots;
+  if (!base) {
     STP_CUDA_TRY(cudaMalloc(&base, 1024 * sizeof(int)));
     STP_CUDA_TRY(cudaMemset(base, 0, 1024 * sizeof(int)));
-    base_dev = dev;
-    slots.clear();
   }
   auto it = slots.find(st);
   if (it == slots.end()) {
@@ -791,11 +798,8 @@ stp_status launch_bf16(const GemmArgs& a, const CUtensorMap& ta, const CUtensorM
                        cudaStream_t st) {
   using C = Cfg<BN>;
   auto kern = gemm_bf16_sm100<BN, A_MN, B_MN>;
-  static bool attr_done = false;  // per instantiation
-  if (!attr_done) {
-    STP_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
-    attr_done = true;
-  }
+  static unsigned long long attr_mask = 0;  // per instantiation, one bit per device
+  STP_TRY(set_max_smem_once((const void*)kern, C::SMEM, &attr_mask));
   const int tiles = a.num_m_blk * a.num_n_blk;
   int grid = num_sms();
   if (max_ctas > 0 && max_ctas < grid) grid = max_ctas;
@@ -811,11 +815,8 @@ stp_status launch_bf16_mc2(const GemmArgs& a, const CUtensorMap& ta, const CUten
                            cudaStream_t st) {
   using C = Cfg<BN>;
   auto kern = gemm_bf16_sm100_mc2<BN, A_MN, B_MN>;
-  static bool attr_done = false;
-  if (!attr_done) {
-    STP_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
-    attr_done = true;
-  }
+  static unsigned long long attr_mask = 0;  // per instantiation, one bit per device
+  STP_TRY(set_max_smem_once((const void*)kern, C::SMEM, &attr_mask));
   const int n_ct = ((a.num_m_blk + 1) / 2) * a.num_n_blk;
   int clusters = num_sms() / 2;
   if (max_ctas > 0 && max_ctas / 2 < clusters) clusters = std::max(1, max_ctas / 2);
@@ -859,11 +860,8 @@ template <bool A_MN, bool B_MN>
 stp_status launch_bf16_2sm(const GemmArgs& a, const CUtensorMap& ta, const CUtensorMap& tb, int max_ctas,
                            cudaStream_t st) {
   auto kern = gemm_bf16_sm100_2sm<A_MN, B_MN>;
-  static bool attr_done = false;
-  if (!attr_done) {
-    STP_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, S2_SMEM));
-    attr_done = true;
-  }
+  static unsigned long long attr_mask = 0;  // per instantiation, one bit per device
+  STP_TRY(set_max_smem_once((const void*)kern, S2_SMEM, &attr_mask));
   const int tiles = ((a.M + 255) / 256) * ((a.N + 255) / 256);
   int clusters = num_sms() / 2;
   if (max_ctas > 0 && max_ctas / 2 < clusters) clusters = std::max(1, max_ctas / 2);

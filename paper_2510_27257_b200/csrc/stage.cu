@@ -176,7 +176,7 @@ struct stp_stage {
   // events
   std::vector<cudaEvent_t> ev_done;
   std::vector<cudaEvent_t> ev_t0, ev_t1;  // timing
-  cudaEvent_t ev_base = nullptr, ev_end = nullptr;
+  cudaEvent_t ev_base = nullptr, ev_end = nullptr, ev_caller = nullptr;
   // partial buffers: one per lane with NCCL (the collective copies it out
   // before it completes), two per lane with the copy-engine transport (peers
   // pull from them; see ce_* below).  ev_*b[i]: the comm phase that last read
@@ -1474,6 +1474,7 @@ stp_status stp_init_stage(const stp_model_cfg* mc, const stp_parallel_cfg* pc, c
     STP_CUDA_TRY(cudaEventCreate(&S->ev_t1[i]));
   }
   STP_CUDA_TRY(cudaEventCreate(&S->ev_base));
+  STP_CUDA_TRY(cudaEventCreateWithFlags(&S->ev_caller, cudaEventDisableTiming));
   STP_CUDA_TRY(cudaEventCreate(&S->ev_end));
   for (int i = 0; i < 2; ++i) {
     STP_CUDA_TRY(cudaEventCreateWithFlags(&S->ev_pfb[i], cudaEventDisableTiming));
@@ -1559,9 +1560,21 @@ stp_status stp_stage_set_timing(stp_stage* st, int32_t mode) {
   return STP_OK;
 }
 
+// The step's first enqueue waits for everything the caller put on `stream`
+// before the call (parameter updates, zero_grads, token writes); the caller's
+// later work on `stream` is ordered after the step's last event.
+static stp_status order_after_caller(stp_stage* st, void* stream) {
+  STP_CUDA_TRY(cudaSetDevice(st->dev));
+  STP_CUDA_TRY(cudaEventRecord(st->ev_caller, (cudaStream_t)stream));
+  STP_CUDA_TRY(cudaStreamWaitEvent(st->s_comp, st->ev_caller, 0));
+  return STP_OK;
+}
+
 stp_status stp_train_step(stp_stage* st, const int32_t* d_tokens, const int32_t* d_targets, float* h_loss,
-                          stp_step_stats* stats) {
+                          stp_step_stats* stats, void* stream) {
   if (!st) return fail(STP_EINVAL, "NULL stage");
+  if (st->poisoned) return fail(STP_ESTATE, "stage poisoned by an earlier CUDA/NCCL error");
+  STP_TRY(order_after_caller(st, stream));
   bool need_tok = false, need_tgt = false;
   for (auto& C : st->chunks) {
     need_tok |= C.first;
@@ -1571,13 +1584,16 @@ stp_status stp_train_step(stp_stage* st, const int32_t* d_tokens, const int32_t*
   if (need_tgt && !d_targets) return fail(STP_EINVAL, "targets required on the rank holding the last virtual stage");
   st->tokens = d_tokens;
   st->targets = d_targets;
-  return run_step(st, h_loss, stats);
+  STP_TRY(run_step(st, h_loss, stats));
+  STP_CUDA_TRY(cudaStreamWaitEvent((cudaStream_t)stream, st->ev_end, 0));
+  return STP_OK;
 }
 
 stp_status stp_train_step_host(stp_stage* st, const int32_t* h_tokens, const int32_t* h_targets, float* h_loss,
-                               stp_step_stats* stats) {
+                               stp_step_stats* stats, void* stream) {
   if (!st) return fail(STP_EINVAL, "NULL stage");
-  STP_CUDA_TRY(cudaSetDevice(st->dev));
+  if (st->poisoned) return fail(STP_ESTATE, "stage poisoned by an earlier CUDA/NCCL error");
+  STP_TRY(order_after_caller(st, stream));
   const size_t bytes = (size_t)st->m * st->s * 4;
   const int32_t* dt = nullptr;
   const int32_t* dg = nullptr;
@@ -1589,7 +1605,7 @@ stp_status stp_train_step_host(stp_stage* st, const int32_t* h_tokens, const int
     STP_CUDA_TRY(cudaMemcpyAsync(st->tgt_buf, h_targets, bytes, cudaMemcpyHostToDevice, st->s_comp));
     dg = st->tgt_buf;
   }
-  return stp_train_step(st, dt, dg, h_loss, stats);
+  return stp_train_step(st, dt, dg, h_loss, stats, stream);
 }
 
 stp_status stp_stage_trace(const stp_stage* st, stp_unit* buf, int32_t cap, int32_t* n_out) {
@@ -1633,6 +1649,7 @@ void stp_destroy_stage(stp_stage* st) {
   for (auto e : st->ev_t1) cudaEventDestroy(e);
   for (auto e : st->ev_pool) cudaEventDestroy(e);
   if (st->ev_base) cudaEventDestroy(st->ev_base);
+  if (st->ev_caller) cudaEventDestroy(st->ev_caller);
   if (st->ev_end) cudaEventDestroy(st->ev_end);
   for (int i = 0; i < 2; ++i) {
     if (st->ev_pfb[i]) cudaEventDestroy(st->ev_pfb[i]);

@@ -449,3 +449,19 @@ def serialize(kind: int, p: int, v: int, t: int, m: int,
             for j, u in enumerate(expand_units(kind, p, d, acts, layers_per_vstage)):
                 lines.append("U " + " ".join(str(x) for x in (j,) + u))
     return "\n".join(lines) + "\n"
+
+
+def paper_layer_split(n_layers: int, n_slots: int) -> List[int]:
+    """Layers per virtual-stage slot in V order (reading Q17).
+
+    Spread L+2 as evenly as possible (remainder to the earliest slots), then
+    take 2 from the last slot.  (The product's copy is stp_layer_split in csrc/schedule.cpp; they share
+    no code.)
+    """
+    total = n_layers + 2
+    base, rem = divmod(total, n_slots)
+    split = [base + (1 if i < rem else 0) for i in range(n_slots)]
+    split[-1] -= 2
+    if min(split) < 1 or sum(split) != n_layers:
+        raise ValueError(f"IndivisibleLayers: {n_layers} layers over {n_slots} slots")
+    return split

@@ -152,69 +152,74 @@ __global__ void __launch_bounds__(384, 1)
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
-      constexpr uint32_t idS = make_idesc_bf16(T, QT, false, false);  // S^T, dP^T: M = 128 keys, N = 64 queries
-      constexpr uint32_t idMN = make_idesc_bf16(T, D, false, true);   // dV, dK: N = d, B (dO_i, Q_i) MN-major
-      constexpr uint32_t idQ = make_idesc_bf16(T, QT, true, true);    // dQ^T: M = d (A = K^T), N = 64 (B = dS^T)
-      const uint32_t k_addr = smem_u32(sK), v_addr = smem_u32(sV), ds_addr = smem_u32(sdS);
-      mbar_wait_wd(kv_full, 0, 302, a.s, h, kt);
-      auto issue_s = [&](int it) {
-        const int st = it % ST, b = it & 1;
-        mbar_wait_wd(qdo_full + st, (it / ST) & 1, 303, a.s, h, kt);
-        tc_fence_after();
-        const uint32_t q_addr = smem_u32(sQ + st * QT_BYTES), tS = tB + 128 * b;
+    // all 32 lanes run the issue loop (uniform descriptor arithmetic); one
+    // elected lane issues each tcgen05 op.  SW128 descriptors of a tile base
+    // plus a byte offset: desc(addr + off) = desc(addr) + off / 16.
+    constexpr uint32_t idS = make_idesc_bf16(T, QT, false, false);  // S^T, dP^T: M = 128 keys, N = 64 queries
+    constexpr uint32_t idMN = make_idesc_bf16(T, D, false, true);   // dV, dK: N = d, B (dO_i, Q_i) MN-major
+    constexpr uint32_t idQ = make_idesc_bf16(T, QT, true, true);    // dQ^T: M = d (A = K^T), N = 64 (B = dS^T)
+    const uint64_t dK_kmaj = make_sw128_desc(smem_u32(sK), 16, 1024);      // K as the K-major A of S^T
+    const uint64_t dV_kmaj = make_sw128_desc(smem_u32(sV), 16, 1024);      // V as the K-major A of dP^T
+    const uint64_t dK_mn = make_sw128_desc(smem_u32(sK), ATOM, 1024);      // K^T as the MN-major A of dQ^T
+    const uint64_t dQ0_kmaj = make_sw128_desc(smem_u32(sQ), 16, 1024);     // Q_i (stage 0) K-major B of S^T
+    const uint64_t ddO0_kmaj = make_sw128_desc(smem_u32(sdO), 16, 1024);   // dO_i K-major B of dP^T
+    const uint64_t dQ0_mn = make_sw128_desc(smem_u32(sQ), QATOM, 1024);    // Q_i MN-major B of dK
+    const uint64_t ddO0_mn = make_sw128_desc(smem_u32(sdO), QATOM, 1024);  // dO_i MN-major B of dV
+    const uint64_t ddS0_mn = make_sw128_desc(smem_u32(sdS), QATOM, 1024);  // dS^T MN-major B of dQ^T
+    mbar_wait_wd(kv_full, 0, 302, a.s, h, kt);
+    auto issue_s = [&](int it) {
+      const int st = it % ST, b = it & 1;
+      mbar_wait_wd(qdo_full + st, (it / ST) & 1, 303, a.s, h, kt);
+      tc_fence_after();
+      const uint64_t qd = dQ0_kmaj + (uint64_t)((st * QT_BYTES) >> 4);
+      const uint32_t tS = tB + 128 * b;
 #pragma unroll
-        for (int kk = 0; kk < D / 16; ++kk) {
-          const uint32_t ka = (kk >> 2) * ATOM + (kk & 3) * 32, qa = (kk >> 2) * QATOM + (kk & 3) * 32;
-          mma_f16_ss(tS, make_sw128_desc(k_addr + ka, 16, 1024), make_sw128_desc(q_addr + qa, 16, 1024), idS,
-                     kk > 0 ? 1u : 0u);
-        }
-        mma_commit(s_full + b);
-      };
-      auto issue_dp = [&](int it) {
-        const int st = it % ST, b = it & 1;
-        if (it >= 2) mbar_wait_wd(dq_free + b, ((it >> 1) - 1) & 1, 304, a.s, h, kt);  // dQ^T(it-2) drained
-        tc_fence_after();
-        const uint32_t do_addr = smem_u32(sdO + st * QT_BYTES), tP = tB + 128 * b + 64;
-#pragma unroll
-        for (int kk = 0; kk < D / 16; ++kk) {
-          const uint32_t ka = (kk >> 2) * ATOM + (kk & 3) * 32, qa = (kk >> 2) * QATOM + (kk & 3) * 32;
-          mma_f16_ss(tP, make_sw128_desc(v_addr + ka, 16, 1024), make_sw128_desc(do_addr + qa, 16, 1024), idS,
-                     kk > 0 ? 1u : 0u);
-        }
-        mma_commit(dp_full + b);
-      };
-      issue_s(0);
-      issue_dp(0);
-      for (int it = 0; it < n_q; ++it) {
-        const int st = it % ST, b = it & 1;
-        const uint32_t ph = (it >> 1) & 1;
-        const uint32_t q_addr = smem_u32(sQ + st * QT_BYTES), do_addr = smem_u32(sdO + st * QT_BYTES);
-        const uint32_t tS = tB + 128 * b, tP = tS + 64;
-        if (it + 1 < n_q) issue_s(it + 1);
-        mbar_wait_wd(p_full + b, ph, 305, a.s, h, kt);
-        tc_fence_after();
-#pragma unroll
-        for (int kk = 0; kk < QT / 16; ++kk)  // dV += P^T dO_i
-          mma_f16_ts(tdV, tS + kk * 8, make_sw128_desc(do_addr + kk * 2048, QATOM, 1024), idMN,
-                     (it > 0 || kk > 0) ? 1u : 0u);
-        if (it + 1 < n_q) issue_dp(it + 1);
-        mbar_wait_wd(ds_full + b, ph, 306, a.s, h, kt);
-        tc_fence_after();
-#pragma unroll
-        for (int kk = 0; kk < QT / 16; ++kk)  // dK += dS^T Q_i
-          mma_f16_ts(tdK, tS + 32 + kk * 8, make_sw128_desc(q_addr + kk * 2048, QATOM, 1024), idMN,
-                     (it > 0 || kk > 0) ? 1u : 0u);
-        const uint32_t dsb = ds_addr + b * DS_BYTES;
-#pragma unroll
-        for (int kk = 0; kk < T / 16; ++kk)  // dQ_i^T = K^T dS_i^T (K = 128 keys)
-          mma_f16_ss(tP, make_sw128_desc(k_addr + kk * 2048, ATOM, 1024), make_sw128_desc(dsb + kk * 2048, QATOM, 1024),
-                     idQ, kk > 0 ? 1u : 0u);
-        mma_commit(dq_full + b);
-        mma_commit(qdo_empty + st);
+      for (int kk = 0; kk < D / 16; ++kk) {
+        const uint32_t ka = ((kk >> 2) * ATOM + (kk & 3) * 32) >> 4, qa = ((kk >> 2) * QATOM + (kk & 3) * 32) >> 4;
+        mma_f16_ss_el(tS, dK_kmaj + ka, qd + qa, idS, kk > 0 ? 1u : 0u);
       }
-      mma_commit(done);
+      mma_commit_el(s_full + b);
+    };
+    auto issue_dp = [&](int it) {
+      const int st = it % ST, b = it & 1;
+      if (it >= 2) mbar_wait_wd(dq_free + b, ((it >> 1) - 1) & 1, 304, a.s, h, kt);  // dQ^T(it-2) drained
+      tc_fence_after();
+      const uint64_t od = ddO0_kmaj + (uint64_t)((st * QT_BYTES) >> 4);
+      const uint32_t tP = tB + 128 * b + 64;
+#pragma unroll
+      for (int kk = 0; kk < D / 16; ++kk) {
+        const uint32_t ka = ((kk >> 2) * ATOM + (kk & 3) * 32) >> 4, qa = ((kk >> 2) * QATOM + (kk & 3) * 32) >> 4;
+        mma_f16_ss_el(tP, dV_kmaj + ka, od + qa, idS, kk > 0 ? 1u : 0u);
+      }
+      mma_commit_el(dp_full + b);
+    };
+    issue_s(0);
+    issue_dp(0);
+    for (int it = 0; it < n_q; ++it) {
+      const int st = it % ST, b = it & 1;
+      const uint32_t ph = (it >> 1) & 1;
+      const uint64_t qmn = dQ0_mn + (uint64_t)((st * QT_BYTES) >> 4), omn = ddO0_mn + (uint64_t)((st * QT_BYTES) >> 4);
+      const uint32_t tS = tB + 128 * b, tP = tS + 64;
+      if (it + 1 < n_q) issue_s(it + 1);
+      mbar_wait_wd(p_full + b, ph, 305, a.s, h, kt);
+      tc_fence_after();
+#pragma unroll
+      for (int kk = 0; kk < QT / 16; ++kk)  // dV += P^T dO_i
+        mma_f16_ts_el(tdV, tS + kk * 8, omn + (uint64_t)(kk * 128), idMN, (it > 0 || kk > 0) ? 1u : 0u);
+      if (it + 1 < n_q) issue_dp(it + 1);
+      mbar_wait_wd(ds_full + b, ph, 306, a.s, h, kt);
+      tc_fence_after();
+#pragma unroll
+      for (int kk = 0; kk < QT / 16; ++kk)  // dK += dS^T Q_i
+        mma_f16_ts_el(tdK, tS + 32 + kk * 8, qmn + (uint64_t)(kk * 128), idMN, (it > 0 || kk > 0) ? 1u : 0u);
+      const uint64_t dsd = ddS0_mn + (uint64_t)((b * DS_BYTES) >> 4);
+#pragma unroll
+      for (int kk = 0; kk < T / 16; ++kk)  // dQ_i^T = K^T dS_i^T (K = 128 keys)
+        mma_f16_ss_el(tP, dK_mn + (uint64_t)(kk * 128), dsd + (uint64_t)(kk * 128), idQ, kk > 0 ? 1u : 0u);
+      mma_commit_el(dq_full + b);
+      mma_commit_el(qdo_empty + st);
     }
+    mma_commit_el(done);
   } else if (warp >= 4) {
     const int gi = (warp - 4) >> 2, quad = warp & 3;
     const int r = quad * 32 + lane;  // key row (S^T / dP^T lane); d index of dQ^T

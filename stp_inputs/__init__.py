@@ -131,18 +131,3 @@ def make_tokens(cfg: ModelCfg, n_micro: int, seed: int = 1234):
         toks[b] = seq[:-1]
         tgts[b] = seq[1:]
     return toks, tgts
-
-
-def paper_layer_split(n_layers: int, n_slots: int) -> List[int]:
-    """Layers per virtual-stage slot in V order (reading Q17).
-
-    Spread L+2 as evenly as possible (remainder to the earliest slots), then
-    take 2 from the last slot.  Pure integer bookkeeping, no model math.
-    """
-    total = n_layers + 2
-    base, rem = divmod(total, n_slots)
-    split = [base + (1 if i < rem else 0) for i in range(n_slots)]
-    split[-1] -= 2
-    if min(split) < 1 or sum(split) != n_layers:
-        raise ValueError(f"IndivisibleLayers: {n_layers} layers over {n_slots} slots")
-    return split

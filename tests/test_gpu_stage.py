@@ -8,6 +8,7 @@ import pytest
 import torch
 
 import stp_inputs as si
+from oracle import schedule as sc
 from tests.stage_parity import compare, oracle_reference, rank_grads_ref
 
 pytestmark = pytest.mark.gpu
@@ -62,7 +63,7 @@ def test_trace_equals_schedule_units_and_accumulation():
     from paper_2510_27257_b200.stage import schedule_units
     cfg = si.TINY
     st, loss, ref_loss, got, ref, stats, toks, tgts = _run(cfg, 4, "f32", "stp")
-    lay = si.paper_layer_split(cfg.n_layers, 2)
+    lay = sc.paper_layer_split(cfg.n_layers, 2)
     assert st.trace() == schedule_units("stp", 1, 4, 1, 0, lay)
     # a second step accumulates (gradients add; caller zeroes)
     loss2, _ = st.step_host(toks, tgts)

@@ -20,6 +20,7 @@ import pytest
 import torch
 
 import stp_inputs as si
+from oracle import schedule as sc
 from oracle import model as om
 
 MICRO = si.ModelCfg(vocab=16, hidden=8, n_layers=2, n_q_heads=2, n_kv_heads=1,
@@ -216,8 +217,8 @@ def test_qwen2_7b_param_count():
 
 def test_paper_layer_split():
     # SPEC S:L61-63 worked examples of the "last stage two layers short" rule
-    assert si.paper_layer_split(30, 8) == [4, 4, 4, 4, 4, 4, 4, 2]
-    assert si.paper_layer_split(46, 16) == [3] * 15 + [1]
+    assert sc.paper_layer_split(30, 8) == [4, 4, 4, 4, 4, 4, 4, 2]
+    assert sc.paper_layer_split(46, 16) == [3] * 15 + [1]
     with pytest.raises(ValueError):
-        si.paper_layer_split(8, 8)
-    assert si.paper_layer_split(28, 4) == [8, 8, 7, 5]
+        sc.paper_layer_split(8, 8)
+    assert sc.paper_layer_split(28, 4) == [8, 8, 7, 5]

@@ -260,3 +260,85 @@ def test_simulated_8gpu_rows_from_measured_units():
         assert row["stp"]["exposed_tp_pct"] < row["1f1b-i"]["exposed_tp_pct"] < row["1f1b-i-naive"]["exposed_tp_pct"]
         assert row["stp"]["peak_chunks"] == 6  # 3p
         assert 0.8 < row["stp_vs_1f1b_i"] < 1.3
+
+
+# ---------------------------------------------------------------------------
+# simulate_durations / program_order_peak pins (VERDICT r1 "unpinned oracle parts")
+
+ALL_KINDS = [sc.STP, sc.ONEF1B_I, sc.ZB, sc.STP_NOBRAID, sc.STP_NOSEP, sc.ONEF1B_I_NAIVE]
+
+
+@pytest.mark.parametrize("kind", ALL_KINDS)
+@pytest.mark.parametrize("p,m", [(1, 3), (2, 4), (2, 8), (4, 8), (4, 16), (8, 16)])
+def test_simulate_durations_reproduces_block_costs(kind, p, m):
+    """Fed the Table 1 block cost of every action, the duration-driven
+    simulator must reproduce simulate()'s makespan exactly (same dependency
+    semantics, P:L124-148 cost model)."""
+    if kind in (sc.ONEF1B_I, sc.ONEF1B_I_NAIVE) and m % p:
+        pytest.skip("1F1B-I needs m % p == 0")
+    progs = sc.build_program(kind, p, m)
+    costs = (10.0, 12.0, 8.0, 4.0)
+    r = sm.simulate(kind, p, progs, *costs)
+    durs = [[sm.block_cost(kind, a[0], *costs)[0] for a in progs[d]] for d in range(p)]
+    assert sm.simulate_durations(kind, p, progs, durs) == pytest.approx(r["makespan"], rel=0, abs=1e-9)
+
+
+@pytest.mark.parametrize("kind", [sc.STP, sc.ZB, sc.STP_NOSEP])
+@pytest.mark.parametrize("m", [1, 3, 8])
+def test_simulate_durations_single_device_is_the_sum(kind, m):
+    """p = 1: every dependency is satisfied by program order, so the device
+    never idles and the makespan is the plain sum of the action durations."""
+    progs = sc.build_program(kind, 1, m)
+    durs = [[1.0 + 0.37 * i for i in range(len(progs[0]))]]
+    assert sm.simulate_durations(kind, 1, progs, durs) == pytest.approx(sum(durs[0]), abs=1e-9)
+
+
+@pytest.mark.parametrize("p,mult", [(2, 1), (2, 3), (4, 2), (8, 1)])
+def test_simulate_durations_1f1b_interleaved_closed_form(p, mult):
+    """Megatron 1F1B-I with per-chunk costs (T_F, T_B+T_W) and no TP comm:
+    makespan = 2m (T_F + T_B + T_W) + (p - 1)(T_F + T_B + T_W) (Table 1's
+    1F1B-I PP bubble, with T_AR = 0)."""
+    m = mult * p
+    progs = sc.build_program(sc.ONEF1B_I, p, m)
+    TF, TB, TW = 3.0, 4.0, 2.0
+    durs = [[TF if a[0] == sc.A_F else TB + TW for a in progs[d]] for d in range(p)]
+    assert sm.simulate_durations(sc.ONEF1B_I, p, progs, durs) == pytest.approx(
+        2 * m * (TF + TB + TW) + (p - 1) * (TF + TB + TW), abs=1e-9)
+
+
+@pytest.mark.parametrize("kind", ALL_KINDS)
+@pytest.mark.parametrize("p,m", [(2, 4), (2, 16), (4, 8), (4, 32), (8, 32)])
+def test_program_order_peak_equals_simulated_peak(kind, p, m):
+    """A device runs its list sequentially, so the stash count walked in
+    program order must equal the time-based peak of the simulator (alloc at
+    an F's action start, free at the end of the action completing its W)."""
+    if kind in (sc.ONEF1B_I, sc.ONEF1B_I_NAIVE) and m % p:
+        pytest.skip("1F1B-I needs m % p == 0")
+    progs = sc.build_program(kind, p, m)
+    r = sm.simulate(kind, p, progs, 10.0, 12.0, 8.0, 4.0)
+    for d in range(p):
+        assert sm.program_order_peak(kind, p, d, progs[d]) == r["peak"][d]
+
+
+@pytest.mark.parametrize("p", [2, 3, 4, 8])
+def test_program_order_peak_table1_memory(p):
+    """Table 1 memory column: Ours 3p·M_a (exact, max over
+    devices), ZB-V at most 2p, 1F1B-I 3p-1 under the F-start..W-end counting
+    (reading Q7)."""
+    m = 4 * p
+    peak = lambda kind: max(sm.program_order_peak(kind, p, d, x)
+                            for d, x in enumerate(sc.build_program(kind, p, m)))
+    assert peak(sc.STP) == 3 * p
+    assert peak(sc.ZB) <= 2 * p
+    assert peak(sc.ONEF1B_I) in (3 * p - 2, 3 * p - 1)
+
+
+def test_paper_layer_split():
+    """P:L171: 'the last stage has two fewer layers' for the 152,064 vocab;
+    reading Q17 for non-divisible splits."""
+    assert sc.paper_layer_split(28, 4) == [8, 8, 7, 5]
+    assert sc.paper_layer_split(48, 8) == [7, 7, 6, 6, 6, 6, 6, 4]
+    assert sc.paper_layer_split(28, 3) == [10, 10, 8]
+    assert sc.paper_layer_split(30, 8) == [4, 4, 4, 4, 4, 4, 4, 2]
+    with pytest.raises(ValueError):
+        sc.paper_layer_split(8, 8)

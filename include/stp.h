@@ -215,13 +215,19 @@ stp_status stp_stage_set_timing(stp_stage* st, int32_t mode);
  * vs reads targets; others may pass NULL).  Gradients are accumulated into
  * the bound fp32 buffers with the 1/(seq*n_micro) loss scale (reading Q19).
  * *h_loss (host, nullable) = mean loss on the rank holding the last vs, 0
- * elsewhere.  Returns after the step's last event (synchronous). */
+ * elsewhere.  Returns after the step's last event (synchronous).
+ * Stream ordering: `stream` is the caller's cudaStream_t (NULL = the legacy
+ * default stream).  The step's first kernel runs after everything the caller
+ * enqueued on `stream` before the call (parameter writes, zeroed gradients,
+ * token uploads); work the caller enqueues on `stream` afterwards is ordered
+ * after the step.  The step itself runs on the stage's own streams. */
 stp_status stp_train_step(stp_stage* st, const int32_t* d_tokens, const int32_t* d_targets,
-                          float* h_loss, stp_step_stats* stats);
+                          float* h_loss, stp_step_stats* stats, void* stream);
 /* Same, but tokens/targets are HOST int32 arrays copied to the device inside
- * the call (end-to-end path); *h_loss read back to the host. */
+ * the call (end-to-end path; the copies also wait for `stream`); *h_loss read
+ * back to the host. */
 stp_status stp_train_step_host(stp_stage* st, const int32_t* h_tokens, const int32_t* h_targets,
-                               float* h_loss, stp_step_stats* stats);
+                               float* h_loss, stp_step_stats* stats, void* stream);
 
 /* Executed unit trace of the last step: the unit ops in host-enqueue order,
  * same layout as stp_schedule_units (capacity protocol as above). */

@@ -76,8 +76,8 @@ _SIGS = {
     "stp_stage_param_info": (i32, [vp, i32, C.POINTER(cp), C.POINTER(i64), C.POINTER(i64), C.POINTER(i64)]),
     "stp_bind_params": (i32, [vp, i32, C.POINTER(vp), C.POINTER(vp)]),
     "stp_stage_set_timing": (i32, [vp, i32]),
-    "stp_train_step": (i32, [vp, vp, vp, C.POINTER(f32), C.POINTER(StepStats)]),
-    "stp_train_step_host": (i32, [vp, vp, vp, C.POINTER(f32), C.POINTER(StepStats)]),
+    "stp_train_step": (i32, [vp, vp, vp, C.POINTER(f32), C.POINTER(StepStats), vp]),
+    "stp_train_step_host": (i32, [vp, vp, vp, C.POINTER(f32), C.POINTER(StepStats), vp]),
     "stp_stage_trace": (i32, [vp, C.POINTER(Unit), i32, C.POINTER(i32)]),
     "stp_stage_unit_times": (i32, [vp, C.POINTER(f32), C.POINTER(f32), i32, C.POINTER(i32)]),
     "stp_destroy_stage": (None, [vp]),

@@ -590,23 +590,16 @@ stp_status bwd_bf16(int s, int nq, int nkv, const void* q, const void* k, const 
 stp_status attn_fwd_sm100_launch(int s, int nq, int nkv, const void* qkv_base, int64_t ld, void* o, int64_t ldo,
                                  float* lse, cudaStream_t st);
 
-stp_status attn_bwd_sm100_launch(int s, int nq, int nkv, const void* qkv_base, int64_t ld, const void* dout,
-                                 int64_t ldo, const float* lse, const float* Dl, void* dq_base, int64_t ldd,
-                                 float* part, cudaStream_t st);
 
-// fp32 workspace: D = rowsum(dO*O) [nq, s] (+ for the tcgen05 path, d = 128:
-// dK / dV partials per query head [2, nq, s, 128]).
 int64_t attn_bwd_fused_ws_bytes(int64_t s, int nq, int nkv);
-int& attn_bwd_version_ref();
 stp_status attn_bwd_fused_launch(int s, int nq, int nkv, const void* qkv, int64_t ld, const void* o, const void* dout,
                                  int64_t ldo, const float* lse, void* dqkv, int64_t ldd, void* ws, cudaStream_t st);
 
+// fp32 workspace: D = rowsum(dO*O) [nq, s] for the mma.sync / fp32 paths;
+// the fused tcgen05 path (d = 128) needs attn_bwd_fused_ws_bytes.
 int64_t attn_bwd_ws_bytes(int64_t s, int nq, int nkv, int d) {
   int64_t b = s * nq * (int64_t)sizeof(float);
-  if (d == 128) {
-    b = ((b + 255) / 256) * 256 + 2 * (int64_t)nq * s * 128 * (int64_t)sizeof(float);
-    b = std::max(b, attn_bwd_fused_ws_bytes(s, nq, nkv));
-  }
+  if (d == 128) b = std::max(b, attn_bwd_fused_ws_bytes(s, nq, nkv));
   return b;
 }
 
@@ -655,7 +648,7 @@ stp_status attn_bwd(int dtype, int64_t s, int nq, int nkv, int d, const void* q,
   const int64_t warps = s * nq;
   return STP_DISPATCH_DTYPE(dtype, [&] {
     // fused tcgen05 backward (d = 128, [q | k | v] layouts): computes its own D
-    if (dtype == STP_DTYPE_BF16 && d == 128 && attn_bwd_version_ref() == 8 && getenv("STP_ATTN_MMA_SYNC") == nullptr &&
+    if (dtype == STP_DTYPE_BF16 && d == 128 && getenv("STP_ATTN_MMA_SYNC") == nullptr &&
         (const uint8_t*)k == (const uint8_t*)q + (int64_t)nq * d * 2 &&
         (const uint8_t*)v == (const uint8_t*)k + (int64_t)nkv * d * 2 && ld == (int64_t)(nq + 2 * nkv) * d &&
         (const uint8_t*)dk == (const uint8_t*)dq + (int64_t)nq * d * 2 &&
@@ -681,14 +674,6 @@ stp_status attn_bwd(int dtype, int64_t s, int nq, int nkv, int d, const void* q,
     }
     if (ld % 8 || ldo % 8 || ldd % 8) return fail(STP_EINVAL, "bf16 attention strides % 8 == 0");
     static const bool force_mma = getenv("STP_ATTN_MMA_SYNC") != nullptr;
-    const uint8_t* q8 = (const uint8_t*)q;
-    const uint8_t* d8 = (const uint8_t*)dq;
-    if (d == 128 && !force_mma && (const uint8_t*)k == q8 + (int64_t)nq * d * 2 &&
-        (const uint8_t*)v == (const uint8_t*)k + (int64_t)nkv * d * 2 && ld == (int64_t)(nq + 2 * nkv) * d &&
-        (const uint8_t*)dk == d8 + (int64_t)nq * d * 2 && (const uint8_t*)dv == (const uint8_t*)dk + (int64_t)nkv * d * 2) {
-      float* part = (float*)((uint8_t*)ws + ((s * nq * (int64_t)sizeof(float) + 255) / 256) * 256);
-      return attn_bwd_sm100_launch((int)s, nq, nkv, q, ld, dout, ldo, lse, Dl, dq, ldd, part, st);
-    }
     switch (d) {
       case 16: return bwd_bf16<16>((int)s, nq, nkv, q, k, v, ld, dout, ldo, lse, Dl, dq, dk, dv, ldd, st);
       case 32: return bwd_bf16<32>((int)s, nq, nkv, q, k, v, ld, dout, ldo, lse, Dl, dq, dk, dv, ldd, st);

@@ -75,10 +75,6 @@ void prof_push(int cls, double flops, double bytes, cudaEvent_t e0, cudaEvent_t 
 }
 
 int& gemm_mc_mode_ref();
-int& attn_bwd_version_ref();
-int& attn_fwd_version_ref();
-constexpr int kAttnFwdDefault = 4;
-constexpr int kAttnBwdDefault = 8;
 
 }  // namespace stp
 
@@ -91,16 +87,6 @@ stp_status stp_set_option(const char* key, int64_t value) {
   if (k == "gemm_mc") {
     if (value < 0 || value > 3) return stp::fail(STP_EINVAL, "gemm_mc must be 0 (1-SM), 1 (auto), 2 or 3 (2-SM)");
     stp::gemm_mc_mode_ref() = (int)value;
-    return STP_OK;
-  }
-  if (k == "attn_fwd") {  // 0 = built-in default
-    if (value < 0 || value > 5) return stp::fail(STP_EINVAL, "attn_fwd must be 0..5");
-    stp::attn_fwd_version_ref() = value ? (int)value : stp::kAttnFwdDefault;
-    return STP_OK;
-  }
-  if (k == "attn_bwd") {
-    if (value < 0 || value > 8) return stp::fail(STP_EINVAL, "attn_bwd must be 0..8");
-    stp::attn_bwd_version_ref() = value ? (int)value : stp::kAttnBwdDefault;
     return STP_OK;
   }
   return stp::fail(STP_EINVAL, "unknown option " + k);

@@ -116,7 +116,8 @@ class Stage:
         loss = C.c_float()
         st = L.StepStats()
         L.call("stp_train_step", self.h, tokens.data_ptr() if tokens is not None else None,
-               targets.data_ptr() if targets is not None else None, C.byref(loss), C.byref(st))
+               targets.data_ptr() if targets is not None else None, C.byref(loss), C.byref(st),
+               torch.cuda.current_stream(self.device).cuda_stream)
         return loss.value, st
 
     def step_host(self, tokens: Optional[np.ndarray], targets: Optional[np.ndarray]):
@@ -125,7 +126,8 @@ class Stage:
         tk = np.ascontiguousarray(tokens, dtype=np.int32) if tokens is not None else None
         tg = np.ascontiguousarray(targets, dtype=np.int32) if targets is not None else None
         L.call("stp_train_step_host", self.h, tk.ctypes.data if tk is not None else None,
-               tg.ctypes.data if tg is not None else None, C.byref(loss), C.byref(st))
+               tg.ctypes.data if tg is not None else None, C.byref(loss), C.byref(st),
+               torch.cuda.current_stream(self.device).cuda_stream)
         return loss.value, st
 
     def trace(self):

@@ -209,28 +209,32 @@ def test_colsum(dt):
     assert np.abs(_np(acc) - (1 + X.sum(0))).max() <= 1e-3
 
 
-@pytest.mark.parametrize("version", [7, 8])
 @pytest.mark.parametrize("s,nq,nkv", [(257, 7, 1), (1024, 4, 2), (2048, 7, 1), (300, 2, 2), (64, 2, 1), (65, 2, 1),
-                                      (2, 2, 1), (63, 4, 4), (129, 2, 1), (4096, 4, 1)])
-def test_attention_bwd_variants(s, nq, nkv, version):
-    """tcgen05 backward: 8 = the fused kernel (default), 7 = the earlier
-    two-kernel design (dQ kernel + dK/dV kernel + GQA reduce)."""
-    from paper_2510_27257_b200 import _lib
-    _lib.call("stp_set_option", b"attn_bwd", version)
-    try:
-        test_attention_fwd_bwd("bf16", s, nq, nkv, 128)
-    finally:
-        _lib.call("stp_set_option", b"attn_bwd", 0)
+                                      (2, 2, 1), (63, 4, 4), (129, 2, 1), (4096, 4, 1), (6144, 7, 1)])
+def test_attention_tcgen05_shapes(s, nq, nkv):
+    """The tcgen05 forward and fused backward (d = 128) over ragged lengths,
+    GQA group sizes 1-7 and the TP4 bench shape, against the oracle."""
+    test_attention_fwd_bwd("bf16", s, nq, nkv, 128)
 
 
-@pytest.mark.parametrize("version", [1, 2, 3, 4, 5])
-@pytest.mark.parametrize("s,nq,nkv", [(257, 7, 1), (1024, 4, 2), (2048, 7, 1), (300, 2, 2), (64, 2, 1), (65, 2, 1)])
-def test_attention_fwd_variants(s, nq, nkv, version):
-    """tcgen05 forward variants: 1 = P via smem, 2 = P in TMEM with 4 softmax
-    warps (3 = default, 8 softmax warps: covered above)."""
-    from paper_2510_27257_b200 import _lib
-    _lib.call("stp_set_option", b"attn_fwd", version)
-    try:
-        test_attention_fwd_bwd("bf16", s, nq, nkv, 128)
-    finally:
-        _lib.call("stp_set_option", b"attn_fwd", 0)
+def test_attention_bwd_repeatable():
+    """The fused backward adds dQ / dK / dV partials with L2 reductions, so
+    the fp32 summation order varies between runs: two runs must agree to
+    within a few bf16 ulps (the oracle comparison bounds the error itself)."""
+    ops = _ops()
+    s, nq, nkv, d = 2048, 7, 1, 128
+    W = (nq + 2 * nkv) * d
+    _, qkv = _in((s, W), 21, "bf16")
+    o = torch.empty(s, nq * d, dtype=torch.bfloat16, device="cuda")
+    lse = torch.empty(nq, s, dtype=torch.float32, device="cuda")
+    ops.attn_fwd(qkv, nq, nkv, d, o, lse)
+    _, do = _in((s, nq * d), 22, "bf16")
+    outs = []
+    for _ in range(8):
+        dqkv = torch.zeros(s, W, dtype=torch.bfloat16, device="cuda")
+        ops.attn_bwd(qkv, nq, nkv, d, o, do, lse, dqkv)
+        outs.append(dqkv.float())
+    torch.cuda.synchronize()
+    for x in outs[1:]:
+        diff = (x - outs[0]).abs()
+        assert (diff <= 2 ** -6 * outs[0].abs() + 1e-6).all()

@@ -3,7 +3,7 @@ seq 6144): every GEMM of the unit set (forward NT, dgrad NN, wgrad TN with
 fp32 accumulation) and causal GQA attention fwd / bwd, timed with CUDA events
 (warm-up 3, mean of N), for each tuning-knob variant.  One JSON line per case.
 
-  python tools/kbench.py [--tp 1] [--iters 10] [--gemm-mc 0,2] [--attn-fwd 1,2] [--attn-bwd 1,2]
+  python tools/kbench.py [--tp 1] [--iters 10] [--gemm-mc 0,2] [--skip-gemm]
 """
 import argparse
 import json
@@ -38,8 +38,6 @@ def main():
     ap.add_argument("--seq", type=int, default=6144)
     ap.add_argument("--iters", type=int, default=10)
     ap.add_argument("--gemm-mc", default="0,2")
-    ap.add_argument("--attn-fwd", default="3,4")
-    ap.add_argument("--attn-bwd", default="3,4")
     ap.add_argument("--skip-gemm", action="store_true")
     ap.add_argument("--only", default="", help="comma list of GEMM names (e.g. fc1_wgrad); skips attention")
     a = ap.parse_args()
@@ -81,20 +79,14 @@ def main():
     o = torch.empty(s, nq * d, device=dev, dtype=bf)
     lse = torch.empty(nq, s, device=dev, dtype=torch.float32)
     pairs = s * (s + 1) / 2
-    for v in [int(x) for x in a.attn_fwd.split(",")]:
-        _lib.call("stp_set_option", b"attn_fwd", v)
-        ms = timed(lambda: ops.attn_fwd(x, nq, nkv, d, o, lse), a.iters)
-        print(json.dumps({"kernel": "attn_fwd", "version": v, "s": s, "nq": nq, "nkv": nkv, "ms": ms,
-                          "tflops": 4 * pairs * nq * d / ms / 1e9}), flush=True)
-    _lib.call("stp_set_option", b"attn_fwd", 0)
-    ops.attn_fwd(x, nq, nkv, d, o, lse)
+    ms = timed(lambda: ops.attn_fwd(x, nq, nkv, d, o, lse), a.iters)
+    print(json.dumps({"kernel": "attn_fwd", "s": s, "nq": nq, "nkv": nkv, "ms": ms,
+                      "tflops": 4 * pairs * nq * d / ms / 1e9}), flush=True)
     do = torch.randn(s, nq * d, device=dev, dtype=bf)
     dx = torch.empty_like(x)
-    for v in [int(x) for x in a.attn_bwd.split(",")]:
-        _lib.call("stp_set_option", b"attn_bwd", v)
-        ms = timed(lambda: ops.attn_bwd(x, nq, nkv, d, o, do, lse, dx), a.iters)
-        print(json.dumps({"kernel": "attn_bwd", "version": v, "s": s, "nq": nq, "nkv": nkv, "ms": ms,
-                          "tflops": 8 * pairs * nq * d / ms / 1e9}), flush=True)
+    ms = timed(lambda: ops.attn_bwd(x, nq, nkv, d, o, do, lse, dx), a.iters)
+    print(json.dumps({"kernel": "attn_bwd", "s": s, "nq": nq, "nkv": nkv, "ms": ms,
+                      "tflops": 8 * pairs * nq * d / ms / 1e9}), flush=True)
 
 
 if __name__ == "__main__":

@@ -3,19 +3,28 @@ TP x PP on 1-8 B200; exposed TP-comm %; PP bubble rate).
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
-N = 1: Qwen2-7B-shaped model (configs[1] shape: h 3584, 28 layers, 28/4
-heads, d 128, I 18944, V 152064), seq 6144, 8 microbatches, TP=1 PP=1 with
-two virtual stages (V-shape), the R-STP braided schedule, bf16.  N > 1
-(torchrun, one rank per GPU): TP x PP = 2x1 (N=2), 4x1 (N=4, SURVEY's proxy
-of the TP=8 configuration), 4x2 (N=8), same model and global batch (strong
-scaling); --grid TxP overrides.  A step = one stp_train_step: all
-microbatches' forward + B + W over the TP x PP grid, fp32 gradient
-accumulation, end-of-step gamma all-reduce; no optimizer.
+Configurations (--config; BASELINE.json configs[1..3]):
+  cfg2 (default)  Qwen2-7B-shaped (h 3584, 28 layers, 28/4 heads, d 128,
+                  I 18944, V 152064), seq 6144, 8 microbatches; TP x PP by N:
+                  1x1, 2x1, 4x1 (SURVEY's 4-GPU proxy), 8x1 with the 32/8-head
+                  TP=8 variant (reading Q14, "qwen2-7b-tp8").
+  cfg3            Qwen2-7B-shaped, seq 4096, 16 microbatches; 1x1, 2x1,
+                  2x2 (the 4-GPU proxy), 4x2 (the configuration itself).
+  cfg4            Qwen2.5-14B-shaped (reading Q13), seq 4096, 32
+                  microbatches; 2x1, 2x2 (4-GPU proxy), 2x4 (8 GPUs).
+Every config runs two virtual stages (V-shape) and the R-STP braided
+schedule in bf16; same model and global batch at every N of a config
+("scaling": "strong"); --grid TxP / --model / --seq / --micro override.  A
+step = one stp_train_step: all microbatches' forward + B + W over the TP x
+PP grid, fp32 gradient accumulation, end-of-step gamma all-reduce; no
+optimizer.
 
 Timing: W untimed steps, then K steps each timed on the device by the
 library's CUDA events (first event recorded before the step's first enqueue,
 last after its final stream joins), barrier + synchronize on both sides, max
-over ranks.  Weights (15 GB) and the activation stash (~84 GB at N=1) are far
+over ranks.  The headline steps run with no instrumentation; the per-kernel
+roofline numbers come from K further steps with the kernel-class profiler on
+(CUDA events around every GEMM / attention launch).  Weights (15 GB) and the activation stash (~84 GB at N=1) are far
 larger than L2, so no explicit L2 flush is needed (stated in config.l2).
 
 --impl reference: the CPU oracle (oracle/model.py, fp64 numpy) timed on the
@@ -44,14 +53,46 @@ import numpy as np  # noqa: E402
 import paper_2510_27257_b200  # noqa: E402,F401  (sets CUDA_DEVICE_MAX_CONNECTIONS before CUDA init)
 
 METRIC = "tokens/s per step at TP×PP on 1–8 B200; exposed TP-comm %; PP bubble rate"
-GRID = {1: (1, 1), 2: (2, 1), 4: (4, 1), 8: (4, 2)}
+# config -> (model preset by N, seq, microbatches, {N: (TP, PP)})
+CONFIGS = {
+    "cfg2": ({1: "qwen2-7b", 2: "qwen2-7b", 4: "qwen2-7b", 8: "qwen2-7b-tp8"}, 6144, 8,
+             {1: (1, 1), 2: (2, 1), 4: (4, 1), 8: (8, 1)}),
+    "cfg3": ({1: "qwen2-7b", 2: "qwen2-7b", 4: "qwen2-7b", 8: "qwen2-7b"}, 4096, 16,
+             {1: (1, 1), 2: (2, 1), 4: (2, 2), 8: (4, 2)}),
+    "cfg4": ({2: "qwen2.5-14b", 4: "qwen2.5-14b", 8: "qwen2.5-14b"}, 4096, 32,
+             {2: (2, 1), 4: (2, 2), 8: (2, 4)}),
+}
+MODEL_DESC = {"qwen2-7b": "Qwen2-7B-shaped (h3584 L28 28/4 heads d128 I18944 V152064)",
+              "qwen2-7b-tp8": "Qwen2-7B-shaped TP=8 variant (h3584 L28 32/8 heads d128 I18944 V152064, reading Q14)",
+              "qwen2.5-14b": "Qwen2.5-14B-shaped (h5120 L48 40/8 heads d128 I13824 V152064, reading Q13)"}
 
 
-def model_cfg(seq: int):
+def resolve(args):
+    """Fill args.model / seq / m / grid from --config and N (explicit flags win)."""
+    models, seq, m, grids = CONFIGS[args.config]
+    n = args.gpus
+    if not args.model:
+        if n not in models:
+            raise SystemExit(f"--config {args.config} has no {n}-GPU mapping (have {sorted(models)})")
+        args.model = models[n]
+    if not args.seq:
+        args.seq = seq
+    if not args.m:
+        args.m = m
+    if not args.grid:
+        t, p = grids.get(n, (n, 1))
+        args.grid = f"{t}x{p}"
+    return args
+
+
+def model_cfg(args):
     import dataclasses
 
     import stp_inputs as si
-    return dataclasses.replace(si.QWEN2_7B, seq=seq)
+    cfg = dataclasses.replace(si.PRESETS[args.model], seq=args.seq)
+    if args.layers:
+        cfg = dataclasses.replace(cfg, n_layers=args.layers)
+    return cfg
 
 
 def gemm_flops_per_token(cfg):
@@ -109,18 +150,26 @@ class ClockSampler:
 _cpu_sample_cache = {}
 
 
-def cpu_sample(seconds_hint: float = 20.0):
-    """Time the CPU oracle (as it stands) on a bounded sample of the workload:
-    one Qwen2-7B-shaped decoder layer + LM head (vocab 32768) over one
-    512-token microbatch, forward + backward in fp64.  Throughput is scaled to
-    the full workload by algorithmic FLOPs (tokens/s = sample FLOP/s /
-    full-model FLOPs per token)."""
+def cpu_sample(big: bool = False):
+    """Time the CPU oracle (as it stands) on a bounded sample of the workload,
+    forward + backward in fp64, one microbatch:
+      small (the --impl reference arm, one sample per step so K + W steps end
+      within minutes): one decoder layer of the config's model + LM head with
+      vocab 32768, 512 tokens;
+      big (the cpu_baseline of our own arm, one sample, ~10-30 s): two decoder
+      layers + the FULL-vocabulary LM head, 512 tokens.
+    Throughput is scaled to the full workload by algorithmic FLOPs (tokens/s =
+    sample FLOP/s / full-model FLOPs per token)."""
     import dataclasses
 
     import stp_inputs as si
     from oracle import model as om
     seq = int(os.environ.get("STP_REF_SAMPLE_SEQ", "512"))  # tests shrink the sample
-    cfg = dataclasses.replace(si.QWEN2_7B, n_layers=1, seq=seq, vocab=32768)
+    base = si.PRESETS[_sample_model[0]]
+    cfg = dataclasses.replace(base, n_layers=2, seq=seq) if big else \
+        dataclasses.replace(base, n_layers=1, seq=seq, vocab=32768)
+    if os.environ.get("STP_REF_SAMPLE_SEQ"):
+        cfg = dataclasses.replace(cfg, vocab=min(cfg.vocab, 4096))
     if _cpu_sample_cache.get("cfg") != cfg:  # the seeded inputs are not part of the timed work
         _cpu_sample_cache.update(cfg=cfg, P=si.make_params(cfg, seed=1), io=si.make_tokens(cfg, 1, seed=2))
     P = _cpu_sample_cache["P"]
@@ -130,6 +179,14 @@ def cpu_sample(seconds_hint: float = 20.0):
     dt = time.perf_counter() - t0
     sample_flops = gemm_flops_per_token(cfg) * cfg.seq
     return dt, sample_flops, cfg
+
+
+_sample_model = ["qwen2-7b"]
+
+
+def sample_desc(cfg, model):
+    return (f"{cfg.n_layers} {model}-shaped decoder layer(s) + LM head (V={cfg.vocab}), 1 x {cfg.seq} tokens, "
+            f"fwd+bwd fp64")
 
 
 def cpu_cores():
@@ -146,6 +203,7 @@ def reference_arm(args, full_cfg):
     if rank != 0:
         return 0
     per_tok = gemm_flops_per_token(full_cfg)
+    _sample_model[0] = args.model
     times = []
     for i in range(args.warmup + args.steps):
         dt, fl, cfg = cpu_sample()
@@ -158,11 +216,13 @@ def reference_arm(args, full_cfg):
         "impl": "reference", "metric": METRIC, "value": tok_s, "unit": "tokens/s", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": (m * full_cfg.seq / tok_s) * 1e3, "higher_is_better": True,
+        "ms_per_step_note": "extrapolated to the full workload from the timed sample (sample_ms_per_step)",
+        "sample_ms_per_step": mean * 1e3,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": workload_config(args, full_cfg, GRID.get(args.gpus, (1, 1))),
+        "config": workload_config(args, full_cfg, tuple(int(x) for x in args.grid.split("x"))),
         "cpu_baseline": {"value": tok_s, "unit": "tokens/s", "cores": cpu_cores(), "kind": "oracle",
-                         "sample": f"1 Qwen2-7B-shaped layer + LM head (V=32768), 1 x {cfg.seq} tokens, fwd+bwd fp64 "
-                                   f"({mean:.1f} s/sample), scaled by algorithmic FLOPs to the full workload"},
+                         "sample": sample_desc(cfg, args.model) + f" ({mean:.1f} s/sample), scaled by algorithmic "
+                                   "FLOPs to the full workload"},
         "e2e": {"value": tok_s, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -171,8 +231,9 @@ def reference_arm(args, full_cfg):
 
 def workload_config(args, cfg, tp_pp):
     t, p = tp_pp
-    return {"workload": f"qwen2-7b-shaped s{cfg.seq} m{args.m} tp{t}pp{p}vpp2 ({args.sched})",
-            "model": "Qwen2-7B-shaped (h3584 L28 28/4 heads d128 I18944 V152064), random init",
+    return {"workload": f"{args.config}: {args.model}-shaped s{cfg.seq} m{args.m} tp{t}pp{p}vpp2 ({args.sched})",
+            "model": MODEL_DESC.get(args.model, args.model) + (f", {cfg.n_layers} layers" if args.layers else "")
+            + ", random init",
             "global_batch": args.m, "seq_len": cfg.seq, "parallelism": f"tp{t}pp{p}vpp2",
             "schedule": args.sched,
             "tp_transport": (os.environ.get("STP_TP_TRANSPORT", "p2p") if t > 1 else "none"),
@@ -218,16 +279,11 @@ def ours(args):
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    t, p = GRID[world]
-    if args.grid:
-        t, p = (int(x) for x in args.grid.lower().split("x"))
-        if t * p != world:
-            raise SystemExit(f"--grid {args.grid} needs {t * p} ranks, have {world}")
+    t, p = (int(x) for x in args.grid.lower().split("x"))
+    if t * p != world:
+        raise SystemExit(f"--grid {args.grid} needs {t * p} ranks, have {world}")
     tp_rank, pp_rank = rank % t, rank // t
-    cfg = model_cfg(args.seq)
-    if args.layers:
-        import dataclasses
-        cfg = dataclasses.replace(cfg, n_layers=args.layers)
+    cfg = model_cfg(args)
     def make_stage(sched):
         uid = broadcast_nccl_id() if world > 1 else None
         stg = Stage(cfg, tp=t, pp=p, n_micro=args.m, tp_rank=tp_rank, pp_rank=pp_rank, dtype="bf16",
@@ -263,8 +319,6 @@ def ours(args):
         progress(f"warm-up step {i + 1}/{args.warmup}")
     st.zero_grads()
     barrier()
-    L.call("stp_prof_reset")
-    L.call("stp_prof_enable", 1)
     ms = []
     launches = 0
     loss = 0.0
@@ -275,6 +329,15 @@ def ours(args):
             launches += stats.n_kernels
             _last_progress[0] = time.time()
     barrier()
+    progress("timed steps done")
+    # the same K steps again with the kernel-class profiler on (roofline numbers)
+    L.call("stp_prof_reset")
+    L.call("stp_prof_enable", 1)
+    prof_ms = []
+    for _ in range(args.steps):
+        prof_ms.append(st.step(d_tok, d_tgt)[1].step_ms)
+        _last_progress[0] = time.time()
+    barrier()
     L.call("stp_prof_enable", 0)
     prof = {}
     for cls, nm in ((0, "gemm"), (1, "attn_fwd"), (2, "attn_bwd")):
@@ -282,7 +345,7 @@ def ours(args):
         L.call("stp_prof_read", cls, L.C.byref(c), L.C.byref(fl), L.C.byref(by), L.C.byref(tm))
         prof[nm] = (c.value, fl.value, by.value, tm.value)
     L.call("stp_prof_reset")
-    progress("timed steps done")
+    progress("profiled steps done")
     # one extra step with per-unit events: exposed TP and PP bubble
     st.set_timing(True)
     _, tstats = st.step(d_tok, d_tgt)
@@ -336,6 +399,9 @@ def ours(args):
                          "traffic_launch": tinfo.get("kernel"),
                          "traffic_algorithmic_bytes": tinfo.get("algorithmic_bytes_per_launch"),
                          "launches": gc, "gemm_ms_per_step": gms / args.steps,
+                         "gemm_share_of_step": (gms / args.steps) / float(np.mean(prof_ms)),
+                         "timed_in": "a second set of K steps with the kernel-class profiler on "
+                                     "(the headline value is from un-instrumented steps)",
                          "peak_source": "MEASURED_PEAKS.json bf16_tflops_sustained"},
             "attention": {"fwd_tflops": (afl / (afm / 1e3)) / 1e12 if afm > 0 else None,
                           "bwd_tflops": (abl / (abm / 1e3)) / 1e12 if abm > 0 else None,
@@ -347,11 +413,12 @@ def ours(args):
         }
         if world == 1 and not args.no_cpu:
             progress("cpu oracle sample")
-            dt, fl, scfg = cpu_sample()
+            _sample_model[0] = args.model
+            dt, fl, scfg = cpu_sample(big=True)
             cpu_tok = (fl / dt) / gemm_flops_per_token(cfg)
             line["cpu_baseline"] = {"value": cpu_tok, "unit": "tokens/s", "cores": cpu_cores(), "kind": "oracle",
-                                    "sample": f"1 Qwen2-7B-shaped layer + LM head (V=32768), 1 x {scfg.seq} tokens, "
-                                              f"fwd+bwd fp64 ({dt:.1f} s), scaled by algorithmic FLOPs"}
+                                    "sample": sample_desc(scfg, args.model) + f" ({dt:.1f} s), scaled by "
+                                              "algorithmic FLOPs to the full workload"}
     st.close()
     if args.compare:
         # the paper's comparison (§5, Table 1) on the same kernels: every schedule,
@@ -395,20 +462,23 @@ def main():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--seq", type=int, default=6144)
-    ap.add_argument("--micro", dest="m", type=int, default=8)
+    ap.add_argument("--config", default="cfg2", choices=sorted(CONFIGS))
+    ap.add_argument("--model", default="", choices=[""] + sorted(MODEL_DESC))
+    ap.add_argument("--seq", type=int, default=0, help="override the config's sequence length")
+    ap.add_argument("--micro", dest="m", type=int, default=0, help="override the config's microbatch count")
     ap.add_argument("--layers", type=int, default=0, help="override layer count (debug only)")
     ap.add_argument("--sched", default="stp")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--compare", action="store_true",
                     help="also time 1F1B-I (+naive), ZB and the STP ablations on the same kernels")
     ap.add_argument("--compare-scheds", default="stp,1f1b-i,1f1b-i-naive,zb,stp-nobraid,stp-nosep")
-    ap.add_argument("--grid", default="", help="TPxPP override, e.g. 4x1 (default: 1x1, 2x1, 2x2, 4x2 by N)")
+    ap.add_argument("--grid", default="", help="TPxPP override, e.g. 4x1 (default: by --config and N)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
+    resolve(args)
     if args.impl == "reference":
-        return reference_arm(args, model_cfg(args.seq))
+        return reference_arm(args, model_cfg(args))
     start_watchdog(float(os.environ.get("STP_BENCH_WATCHDOG_S", "600")))
     return ours(args)
 

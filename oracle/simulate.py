@@ -158,10 +158,12 @@ def program_order_peak(kind: int, p: int, d: int, actions) -> int:
     return best
 
 
-def simulate_durations(kind: int, p: int, progs, durations):
+def simulate_durations(kind: int, p: int, progs, durations, pp_latency: float = 0.0):
     """Same dependency semantics as `simulate`, but every action takes the
     given duration (durations[d][i], e.g. measured compute time of action i on
-    device d) instead of the Table 1 block cost.  Returns the makespan — the
+    device d) instead of the Table 1 block cost, and a dependency on an action
+    of ANOTHER device arrives pp_latency later (one PP message; Table 1 and
+    `simulate` take it as 0, reading Q20).  Returns the makespan — the
     executor-consistency check of SURVEY §8d.4 compares it with the measured
     step time."""
     V = sc.n_vstages(kind, p)
@@ -178,13 +180,14 @@ def simulate_durations(kind: int, p: int, progs, durations):
                 fw, bw, full, ww = _parts(a)
                 vs = sc.vstage(kind, p, d, a[1])
                 deps, ready = [], True
+                lat = lambda v: pp_latency if sc.vstage_device(kind, p, v)[0] != d else 0.0  # noqa: E731
                 if fw is not None and vs > 0:
                     ready &= (fw, vs - 1) in fend
-                    deps.append(fend.get((fw, vs - 1), 0.0))
+                    deps.append(fend.get((fw, vs - 1), 0.0) + lat(vs - 1))
                 if bw is not None:
                     if vs < V - 1:
                         ready &= (bw, vs + 1) in bend
-                        deps.append(bend.get((bw, vs + 1), 0.0))
+                        deps.append(bend.get((bw, vs + 1), 0.0) + lat(vs + 1))
                     ready &= (bw, vs) in fend
                     deps.append(fend.get((bw, vs), 0.0))
                 if ww is not None:

@@ -1,7 +1,10 @@
 """Run under torchrun: one timed STP step on a TP x PP grid, every rank's
 per-unit CUDA-event times gathered to rank 0, then the executor-consistency
 check of SURVEY §8d.4: the oracle's discrete-event simulator, fed the measured
-compute time of every action, must reproduce the measured step time.  A large
+time of every action (ratio: compute units only; ratio_span: the action's
+span on the compute stream, i.e. its units plus the TP-comm waits between
+them, and the median PP message time as the latency of every cross-device
+dependency), must reproduce the measured step time.  A large
 gap means a hidden synchronisation / serialisation in the executor.  Prints
 one JSON line on rank 0."""
 import argparse
@@ -59,19 +62,32 @@ def main():
     if rank == 0:
         kind = SCHED[a.sched]
         progs = sc.build_program(kind, a.pp, a.n_micro)
-        dur = []
+        dur, span, pp_msgs = [], [], []
         measured = max(x[5] for x in gathered)
         for d in range(a.pp):
             pr, tr, us, s0, s1, *_ = next(x for x in gathered if x[0] == d and x[1] == 0)
             per = [0.0] * len(progs[d])
+            first = [None] * len(progs[d])
+            last = [0.0] * len(progs[d])
             for u, b, e in zip(us, s0, s1):
                 if u[1] == 0:                    # compute-stream units
                     per[u[0]] += e - b
+                    first[u[0]] = b if first[u[0]] is None else first[u[0]]
+                    last[u[0]] = e
+                elif u[2] == 13:                 # STP_U_PP_SEND: one PP message
+                    pp_msgs.append(e - b)
             dur.append(per)
+            # action span on the compute stream: its units plus the TP-comm waits
+            # between them (exposed TP inside the action)
+            span.append([(l - f) if f is not None else 0.0 for f, l in zip(first, last)])
+        lat = sorted(pp_msgs)[len(pp_msgs) // 2] if pp_msgs else 0.0
         simulated = sm.simulate_durations(kind, a.pp, progs, dur)
+        simulated_span = sm.simulate_durations(kind, a.pp, progs, span, pp_latency=lat)
         print(json.dumps({"tp": a.tp, "pp": a.pp, "sched": a.sched, "n_micro": a.n_micro, "layers": a.layers,
                           "seq": a.seq, "measured_ms": measured, "simulated_ms": simulated,
                           "ratio": measured / simulated,
+                          "simulated_span_ms": simulated_span, "pp_msg_ms_median": lat,
+                          "ratio_span": measured / simulated_span,
                           "exposed_tp_pct": [100 * x[6] / x[5] for x in gathered],
                           "pp_bubble_pct": [100 * x[7] / x[5] for x in gathered]}), flush=True)
     st.close()

@@ -1,25 +1,41 @@
-"""smoke(): one tiny STP train step (TP=1, PP=1, two virtual stages, the
-R-STP braided schedule, fp32) on cuda:0 through the C-ABI library, checked
-against the CPU oracle (loss and every gradient, rel 1e-4)."""
+"""smoke(): two small STP train steps on cuda:0 through the C-ABI library,
+each checked against the CPU fp64 oracle:
+  1. TINY fp32 (TP=1, PP=1, two virtual stages, R-STP braided schedule):
+     loss and every gradient, rel 1e-4;
+  2. one bf16 step on a Qwen-style model with head_dim 128 (2 layers, h 1024,
+     8 q / 2 kv heads, I 2816, s 512, V 4096), which runs the default tcgen05
+     kernels (2-SM / 1-SM GEMMs, tcgen05 attention forward and fused
+     backward): loss rel 2e-2, grad norms 5e-2, per-tensor difference 3e-2
+     against the oracle on the same bf16-rounded parameters (N(0, 0.02^2)).
+"""
+import dataclasses
+
 import torch
 
 import stp_inputs as si
 
 
-def run():
+def _one(cfg, m, dtype, lay=None, **kw):
     from paper_2510_27257_b200.stage import Stage
     from tests.stage_parity import compare, oracle_reference, rank_grads_ref
-    assert torch.cuda.is_available(), "smoke() needs a GPU"
-    cfg = si.TINY
-    m = 4
-    P, toks, tgts, ref_loss, G = oracle_reference(cfg, m)
-    st = Stage(cfg, n_micro=m, dtype="f32", sched="stp", device=0)
+    P, toks, tgts, ref_loss, G = oracle_reference(cfg, m, **kw)
+    st = Stage(cfg, n_micro=m, dtype=dtype, sched="stp", device=0, layers_per_vstage=lay)
     st.load_params(P)
     dt = torch.from_numpy(toks).cuda()
     dg = torch.from_numpy(tgts).cuda()
     loss, stats = st.step(dt, dg)
-    bad = compare(cfg, st.grads_numpy(), rank_grads_ref(cfg, G, 1, 0), loss, ref_loss, "f32")
+    bad = compare(cfg, st.grads_numpy(), rank_grads_ref(cfg, G, 1, 0), loss, ref_loss, dtype,
+                  elementwise=kw.get("bf16_inputs", False))
     st.close()
     if bad:
-        raise AssertionError("smoke parity failed: " + "; ".join(bad[:5]))
-    print(f"smoke ok: loss {loss:.6f} (oracle {ref_loss:.6f}), {stats.n_units} units, {stats.n_kernels} kernels")
+        raise AssertionError(f"smoke parity failed ({dtype}): " + "; ".join(bad[:5]))
+    print(f"smoke ok ({dtype}): loss {loss:.6f} (oracle {ref_loss:.6f}), {stats.n_units} units, "
+          f"{stats.n_kernels} kernels")
+
+
+def run():
+    assert torch.cuda.is_available(), "smoke() needs a GPU"
+    _one(si.TINY, 4, "f32")
+    qcfg = dataclasses.replace(si.QWEN2_7B, hidden=1024, n_layers=2, n_q_heads=8, n_kv_heads=2, head_dim=128,
+                               ffn=2816, seq=512, vocab=4096)
+    _one(qcfg, 2, "bf16", lay=[1, 1], std=0.02, bf16_inputs=True)

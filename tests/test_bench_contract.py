@@ -37,3 +37,28 @@ def test_reference_arm_nonzero_rank_is_silent():
     p = _run({"RANK": "1", "WORLD_SIZE": "2", "LOCAL_RANK": "1"})
     assert p.returncode == 0, p.stderr[-2000:]
     assert p.stdout.strip() == ""
+
+
+def test_config_resolution():
+    """--config / N map to the north_star workloads (BASELINE.json configs[1..3])."""
+    import argparse
+    sys.path.insert(0, ROOT)
+    import bench
+    def res(cfg, n, **kw):
+        a = argparse.Namespace(config=cfg, gpus=n, model=kw.get("model", ""), seq=0, m=0, grid=kw.get("grid", ""),
+                               layers=0)
+        return bench.resolve(a)
+    a = res("cfg2", 1)
+    assert (a.model, a.seq, a.m, a.grid) == ("qwen2-7b", 6144, 8, "1x1")
+    a = res("cfg2", 8)
+    assert (a.model, a.grid) == ("qwen2-7b-tp8", "8x1")     # reading Q14: 32/8 heads at TP=8
+    a = res("cfg3", 8)
+    assert (a.model, a.seq, a.m, a.grid) == ("qwen2-7b", 4096, 16, "4x2")
+    a = res("cfg3", 4)
+    assert a.grid == "2x2"
+    a = res("cfg4", 4)
+    assert (a.model, a.seq, a.m, a.grid) == ("qwen2.5-14b", 4096, 32, "2x2")
+    a = res("cfg2", 4, grid="2x2")
+    assert a.grid == "2x2"
+    cfg = bench.model_cfg(res("cfg2", 8))
+    assert cfg.n_q_heads == 32 and cfg.n_kv_heads == 8 and cfg.seq == 6144

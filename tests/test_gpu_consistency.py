@@ -1,7 +1,11 @@
 """Executor consistency check on 2 / 4 GPUs: the simulator fed
-with the measured per-action compute times reproduces the measured step time
-(ratio measured / simulated in [0.95, 1.25]: TP-comm exposure and PP transfer
-time are not in the simulated compute, so measured >= simulated)."""
+with the measured per-action compute times (sum of the action's compute-unit
+durations) reproduces the measured step time within SURVEY's 5%.  The
+"span" variant (action span incl. its internal waits + PP message latency) is
+reported beside it for information only: a braided action's span already
+contains the wait for its backward input from the other device, which the
+simulator adds again as a dependency, so it over-counts (measured 0.89 for
+STP at 1x2, round 2)."""
 import json
 
 import pytest
@@ -22,4 +26,4 @@ def test_executor_matches_simulator(tp, pp, sched):
     assert rc == 0, out[-3000:]
     line = json.loads([x for x in out.splitlines() if x.startswith("{")][-1])
     print(line)
-    assert 0.95 <= line["ratio"] <= 1.25, line
+    assert 0.95 <= line["ratio"] <= 1.05, line

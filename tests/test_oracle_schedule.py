@@ -342,3 +342,24 @@ def test_paper_layer_split():
     assert sc.paper_layer_split(30, 8) == [4, 4, 4, 4, 4, 4, 4, 2]
     with pytest.raises(ValueError):
         sc.paper_layer_split(8, 8)
+
+
+@pytest.mark.parametrize("p", [2, 3, 4, 8])
+def test_simulate_durations_pp_latency_plain_1f1b(p):
+    """Plain 1F1B (one chunk per device), forward / backward costs F, B and a
+    message latency c on every stage boundary.  One microbatch is a single
+    dependency path: F on devices 0..p-1, then B on p-1..0, with 2(p-1)
+    messages, so makespan = p (F + B) + 2 (p - 1) c exactly; with m
+    microbatches the latency can only add time, and at c = 0 the textbook
+    m (F + B) + (p - 1)(F + B) holds."""
+    F, B, c = 3.0, 5.0, 0.7
+    progs = sc.build_program(sc.ONEF1B, p, 1)
+    durs = [[F if a[0] == sc.A_F else B for a in progs[d]] for d in range(p)]
+    assert sm.simulate_durations(sc.ONEF1B, p, progs, durs, pp_latency=c) == pytest.approx(
+        p * (F + B) + 2 * (p - 1) * c)
+    m = 2 * p
+    progs = sc.build_program(sc.ONEF1B, p, m)
+    durs = [[F if a[0] == sc.A_F else B for a in progs[d]] for d in range(p)]
+    base = sm.simulate_durations(sc.ONEF1B, p, progs, durs)
+    assert base == pytest.approx(m * (F + B) + (p - 1) * (F + B))
+    assert sm.simulate_durations(sc.ONEF1B, p, progs, durs, pp_latency=c) >= base + 2 * (p - 1) * c - 1e-9

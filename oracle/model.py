@@ -160,11 +160,13 @@ def _heads(x, n, d):
     return x.reshape(x.shape[0], n, d)
 
 
-def forward_mb(P: Params, cfg, tok, tgt):
-    """One microbatch forward.  Returns (loss_b, cache)."""
-    s, d = tok.shape[0], cfg.head_dim
+def forward_mb(P: Params, cfg, tok, tgt, x0=None):
+    """One microbatch forward.  Returns (loss_b, cache).  x0 (optional)
+    replaces the embedding lookup as the layer-0 input (the MLLM sequence of
+    image + text rows, oracle/vit.py)."""
+    x = P["embed"][tok] if x0 is None else x0
+    s, d = x.shape[0], cfg.head_dim
     cos, sin = rope_tables(s, d, cfg.rope_theta)
-    x = P["embed"][tok]
     layers = []
     for l in range(cfg.n_layers):
         p = f"layers.{l}."
@@ -200,11 +202,13 @@ def forward_mb(P: Params, cfg, tok, tgt):
     return float(per_tok.mean()), cache
 
 
-def backward_mb(P: Params, cfg, cache, grads: Params, scale: float):
+def backward_mb(P: Params, cfg, cache, grads: Params, scale: float, embed_tok=None, embed_row0=0):
     """Accumulate scale * d(sum_i loss_i)/dparams into grads.
-    With scale = 1/(s*m) this is d(L)/dparams for L = mean_b mean_i loss."""
+    With scale = 1/(s*m) this is d(L)/dparams for L = mean_b mean_i loss.
+    Returns dL/dX0; the embedding gradient is scattered from rows
+    embed_row0.. for embed_tok (default: all rows, cache["tok"])."""
     d = cfg.head_dim
-    s = cache["tok"].shape[0]
+    s = cache["x_last"].shape[0]
     cos, sin = cache["cos"], cache["sin"]
     dlogits = cross_entropy_bwd(cache["logits"], cache["tgt"], cache["lse_ce"], scale)
     grads["lm_head"] += dlogits.T @ cache["xf"]
@@ -242,7 +246,9 @@ def backward_mb(P: Params, cfg, cache, grads: Params, scale: float):
         dx0n, dg1 = rmsnorm_bwd(dxn, c["x"], P[p + "ln1"], c["r1"])
         grads[p + "ln1"] += dg1
         dx = dx1 + dx0n
-    np.add.at(grads["embed"], cache["tok"], dx)
+    tok = cache["tok"] if embed_tok is None else embed_tok
+    np.add.at(grads["embed"], tok, dx[embed_row0:])
+    return dx
 
 
 def forward_backward(P: Params, cfg, tokens, targets):

@@ -9,6 +9,9 @@ Model (Qwen2-VL vision tower as the paper uses it, readings V1-V4 in
 DESIGN.md):
   X = patches @ Wpe^T                                  (patch embed, no bias)
   per layer: Xn = LN(X; g1, b1); [Q|K|V] = Xn Wqkv^T + bqkv (heads of d)
+             Q, K <- 2-D rotate-half RoPE (angles [h pos * inv | w pos * inv],
+                     inv_j = 10000^(-2j/(d/2)), patches in 2x2 merge-window
+                     order, as Qwen2-VL's rot_pos_emb)
              O_i = softmax(Q_i K_i^T / sqrt(d)) V_i    (bidirectional)
              X += O Wo^T + bo
              Xn2 = LN(X; g2, b2); X += qgelu(Xn2 W1^T + b1) W2^T + b2
@@ -140,21 +143,43 @@ def attention_full_bwd(do, q, k, v, o):
     return dq, dk, dv
 
 
+def vit_positions(gh: int, gw: int, merge_side: int = 2):
+    """(h, w) grid position of every patch, patches listed in merge-window
+    order (each 2x2 window's 4 patches consecutive, windows row-major)."""
+    hp = np.arange(gh)[:, None].repeat(gw, 1).reshape(gh // merge_side, merge_side, gw // merge_side, merge_side)
+    wp = np.arange(gw)[None, :].repeat(gh, 0).reshape(gh // merge_side, merge_side, gw // merge_side, merge_side)
+    return hp.transpose(0, 2, 1, 3).reshape(-1), wp.transpose(0, 2, 1, 3).reshape(-1)
+
+
+def vit_rope_tables(gh: int, gw: int, d: int, theta: float = 10000.0, merge_side: int = 2):
+    """cos / sin [s, d] of the 2-D vision RoPE: angle row = [h * inv | w * inv]
+    (d/2 angles, inv_j = theta^(-2j/(d/2)), j < d/4), duplicated for
+    rotate-half."""
+    hp, wp = vit_positions(gh, gw, merge_side)
+    inv = 1.0 / theta ** (np.arange(0, d // 2, 2, dtype=np.float64) / (d // 2))
+    ang = np.concatenate([hp[:, None] * inv[None, :], wp[:, None] * inv[None, :]], axis=1)
+    emb = np.concatenate([ang, ang], axis=1)
+    return np.cos(emb), np.sin(emb)
+
+
 # ---------------------------------------------------------------------------
 # encoder + merger
 # ---------------------------------------------------------------------------
 
-def vit_forward(PV: Params, c: VitCfg, patches):
-    """patches [s, patch_dim] (s % merge == 0) -> ([s/merge, out_hidden], cache)."""
+def vit_forward(PV: Params, c: VitCfg, patches, grid):
+    """patches [s, patch_dim] in merge-window order of a grid = (gh, gw)
+    image (s = gh * gw) -> ([s/merge, out_hidden], cache)."""
     s, hv, n, d = patches.shape[0], c.hidden, c.n_heads, c.head_dim
+    assert s == grid[0] * grid[1]
+    cos, sin = vit_rope_tables(grid[0], grid[1], d)
     x = patches @ PV["vit.patch"].T
     layers = []
     for l in range(c.n_layers):
         p = f"vit.{l}."
         xn, xh1, r1 = layernorm_fwd(x, PV[p + "ln1_g"], PV[p + "ln1_b"], c.ln_eps)
         qkv = xn @ PV[p + "wqkv"].T + PV[p + "bqkv"]
-        q = qkv[:, :hv].reshape(s, n, d)
-        k = qkv[:, hv:2 * hv].reshape(s, n, d)
+        q = om.rope_fwd(qkv[:, :hv].reshape(s, n, d), cos, sin)
+        k = om.rope_fwd(qkv[:, hv:2 * hv].reshape(s, n, d), cos, sin)
         v = qkv[:, 2 * hv:].reshape(s, n, d)
         o, _ = attention_full_fwd(q, k, v)
         o2 = o.reshape(s, hv)
@@ -170,7 +195,7 @@ def vit_forward(PV: Params, c: VitCfg, patches):
     z = ym @ PV["merger.w1"].T + PV["merger.b1"]
     gz = gelu_fwd(z)
     out = gz @ PV["merger.w2"].T + PV["merger.b2"]
-    cache = dict(patches=patches, layers=layers, xhq=xhq, rq=rq, ym=ym, z=z, gz=gz)
+    cache = dict(patches=patches, cos=cos, sin=sin, layers=layers, xhq=xhq, rq=rq, ym=ym, z=z, gz=gz)
     return out, cache
 
 
@@ -204,6 +229,8 @@ def vit_backward(PV: Params, c: VitCfg, cache, dout, grads: Params):
         grads[p + "bo"] += dx1.sum(axis=0)
         do = (dx1 @ PV[p + "wo"]).reshape(s, n, d)
         dq, dk, dv = attention_full_bwd(do, L["q"], L["k"], L["v"], L["o"])
+        dq = om.rope_bwd(dq, cache["cos"], cache["sin"])
+        dk = om.rope_bwd(dk, cache["cos"], cache["sin"])
         dqkv = np.concatenate([dq.reshape(s, hv), dk.reshape(s, hv), dv.reshape(s, hv)], axis=1)
         grads[p + "wqkv"] += dqkv.T @ L["xn"]
         grads[p + "bqkv"] += dqkv.sum(axis=0)
@@ -215,7 +242,7 @@ def vit_backward(PV: Params, c: VitCfg, cache, dout, grads: Params):
     grads["vit.patch"] += dx.T @ cache["patches"]
 
 
-def mllm_forward_backward(PV: Params, vcfg: VitCfg, P: Params, cfg, patches, tokens, targets):
+def mllm_forward_backward(PV: Params, vcfg: VitCfg, P: Params, cfg, patches, grid, tokens, targets):
     """MLLM step over m microbatches: microbatch b's LM input is
     [vit(patches[b]) (n_img = s_v / merge rows) | E[tokens[b]]] (cfg.seq rows
     in total); L = mean_b mean_i CE; returns (L, LM grads, ViT grads)."""
@@ -225,7 +252,7 @@ def mllm_forward_backward(PV: Params, vcfg: VitCfg, P: Params, cfg, patches, tok
     gv = {k: np.zeros_like(v) for k, v in PV.items()}
     losses = []
     for b in range(m):
-        img, vc = vit_forward(PV, vcfg, patches[b])
+        img, vc = vit_forward(PV, vcfg, patches[b], grid)
         n_img = img.shape[0]
         x0 = np.concatenate([img, P["embed"][tokens[b]]], axis=0)
         assert x0.shape[0] == s

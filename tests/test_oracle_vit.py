@@ -6,7 +6,9 @@
     0 for very negative x) and central finite differences;
   * the whole encoder + merger and the MLLM step: central finite
     differences on micro shapes (every parameter tensor probed);
-  * ViT-600M shape: 0.63B parameters + merger.
+  * ViT-600M shape: 0.63B parameters + merger (SURVEY App. B);
+  * HuggingFace Qwen2-VL's vision tower in fp64 (its fp32 RoPE evaluated in
+    fp64): output and parameter gradients.
 """
 import dataclasses
 
@@ -102,12 +104,12 @@ def test_vit_encoder_finite_differences():
     c = MICRO_V
     PV = _vparams(c)
     rng = np.random.default_rng(3)
-    patches = rng.standard_normal((8, c.patch_dim))
+    patches = rng.standard_normal((8, c.patch_dim))             # a 2 x 4 patch grid
     w = rng.standard_normal((8 // c.merge, c.out_hidden))   # loss = sum(w * out)
-    out, cache = ov.vit_forward(PV, c, patches)
+    out, cache = ov.vit_forward(PV, c, patches, (2, 4))
     gv = {k: np.zeros_like(v) for k, v in PV.items()}
     ov.vit_backward(PV, c, cache, w, gv)
-    loss = lambda: float(np.sum(w * ov.vit_forward(PV, c, patches)[0]))  # noqa: E731
+    loss = lambda: float(np.sum(w * ov.vit_forward(PV, c, patches, (2, 4))[0]))  # noqa: E731
     _fd_check(loss, PV, gv, list(PV), np.random.default_rng(4))
 
 
@@ -121,10 +123,10 @@ def test_mllm_step_finite_differences():
     n_text = cfg.seq - 8 // c.merge
     tokens = rng.integers(0, cfg.vocab, (m, n_text)).astype(np.int32)
     targets = rng.integers(0, cfg.vocab, (m, cfg.seq)).astype(np.int32)
-    L, G, GV = ov.mllm_forward_backward(PV, c, P, cfg, patches, tokens, targets)
+    L, G, GV = ov.mllm_forward_backward(PV, c, P, cfg, patches, (2, 4), tokens, targets)
 
     def loss():
-        return ov.mllm_forward_backward(PV, c, P, cfg, patches, tokens, targets)[0]
+        return ov.mllm_forward_backward(PV, c, P, cfg, patches, (2, 4), tokens, targets)[0]
     _fd_check(loss, PV, GV, ["vit.patch", "vit.0.wqkv", "vit.1.b1", "vit.1.ln2_b", "merger.w1", "merger.b2",
                              "merger.ln_g"], np.random.default_rng(8), probes=3)
     _fd_check(loss, P, G, ["embed", "layers.0.wq", "layers.1.wd", "lm_head"], np.random.default_rng(9), probes=3)
@@ -152,3 +154,67 @@ def test_vit600m_parameter_count():
     n = sum(int(np.prod(s)) for s in ov.vit_param_shapes(ov.VIT_600M).values())
     merger = 4 * 1280 * 4 * 1280 + 4 * 1280 + 3584 * 4 * 1280 + 3584 + 2 * 1280
     assert abs((n - merger) / 1e9 - 0.63) < 0.01
+
+
+def test_vit_matches_hf_qwen2vl_vision_tower():
+    """Qwen2-VL's vision tower (HuggingFace transformers, fp64, autograd) on a
+    tiny config: patch embed, 2-D RoPE, LayerNorm blocks with QuickGELU MLPs,
+    bidirectional attention, 2x2 merger; output and every parameter gradient
+    of sum(w * out)."""
+    from transformers.models.qwen2_vl.configuration_qwen2_vl import Qwen2VLVisionConfig
+    from transformers.models.qwen2_vl.modeling_qwen2_vl import Qwen2VisionTransformerPretrainedModel
+    hv, heads, mlp_ratio, out_h, ps, tps = 16, 2, 3, 12, 2, 2
+    vc = Qwen2VLVisionConfig(depth=2, embed_dim=hv, num_heads=heads, mlp_ratio=mlp_ratio, hidden_size=out_h,
+                             in_channels=3, patch_size=ps, temporal_patch_size=tps, spatial_merge_size=2,
+                             hidden_act="quick_gelu")
+    vc._attn_implementation = "sdpa"  # the eager path runs softmax in fp32
+    import transformers.models.qwen2_vl.modeling_qwen2_vl as hfm
+
+    def rope64(q, k, cos, sin):  # HF evaluates the vision RoPE in fp32; the pin runs it in fp64
+        cos, sin = cos.unsqueeze(-2), sin.unsqueeze(-2)
+        return q * cos + hfm.rotate_half(q) * sin, k * cos + hfm.rotate_half(k) * sin
+    orig = hfm.apply_rotary_pos_emb_vision
+    hfm.apply_rotary_pos_emb_vision = rope64
+    torch.manual_seed(0)
+    hf = Qwen2VisionTransformerPretrainedModel(vc).double()
+    rot = hf.rotary_pos_emb
+    rot.inv_freq = 1.0 / (rot.theta ** (torch.arange(0, rot.dim, 2, dtype=torch.float64) / rot.dim))
+    for prm in hf.parameters():
+        torch.nn.init.normal_(prm, std=0.3)
+    c = ov.VitCfg(hidden=hv, n_layers=2, n_heads=heads, head_dim=hv // heads, mlp=hv * mlp_ratio,
+                  patch_dim=3 * tps * ps * ps, merge=4, out_hidden=out_h)
+    PV = {"vit.patch": hf.patch_embed.proj.weight.detach().reshape(hv, -1).numpy().copy()}
+    for l, b in enumerate(hf.blocks):
+        p = f"vit.{l}."
+        PV.update({p + "ln1_g": b.norm1.weight, p + "ln1_b": b.norm1.bias, p + "wqkv": b.attn.qkv.weight,
+                   p + "bqkv": b.attn.qkv.bias, p + "wo": b.attn.proj.weight, p + "bo": b.attn.proj.bias,
+                   p + "ln2_g": b.norm2.weight, p + "ln2_b": b.norm2.bias, p + "w1": b.mlp.fc1.weight,
+                   p + "b1": b.mlp.fc1.bias, p + "w2": b.mlp.fc2.weight, p + "b2": b.mlp.fc2.bias})
+    PV.update({"merger.ln_g": hf.merger.ln_q.weight, "merger.ln_b": hf.merger.ln_q.bias,
+               "merger.w1": hf.merger.mlp[0].weight, "merger.b1": hf.merger.mlp[0].bias,
+               "merger.w2": hf.merger.mlp[2].weight, "merger.b2": hf.merger.mlp[2].bias})
+    PV = {k: (v.detach().numpy().copy() if isinstance(v, torch.Tensor) else v) for k, v in PV.items()}
+    gh, gw = 4, 6
+    rng = np.random.default_rng(12)
+    patches = rng.standard_normal((gh * gw, c.patch_dim))
+    w = rng.standard_normal((gh * gw // 4, out_h))
+    out = hf(torch.tensor(patches), grid_thw=torch.tensor([[1, gh, gw]]))
+    out = getattr(out, "pooler_output", None) if not isinstance(out, torch.Tensor) else out
+    if out is None or out.shape[0] != gh * gw // 4:
+        out = hf(torch.tensor(patches), grid_thw=torch.tensor([[1, gh, gw]]))
+        out = out.last_hidden_state if out.last_hidden_state.shape[0] == gh * gw // 4 else out.pooler_output
+    (out * torch.tensor(w)).sum().backward()
+    hfm.apply_rotary_pos_emb_vision = orig
+    mine, cache = ov.vit_forward(PV, c, patches, (gh, gw))
+    assert np.allclose(mine, out.detach().numpy(), rtol=0, atol=1e-11)
+    gv = {k: np.zeros_like(v) for k, v in PV.items()}
+    ov.vit_backward(PV, c, cache, w, gv)
+    ref = {"vit.patch": hf.patch_embed.proj.weight.grad.reshape(hv, -1)}
+    for l, b in enumerate(hf.blocks):
+        p = f"vit.{l}."
+        ref.update({p + "ln1_g": b.norm1.weight.grad, p + "wqkv": b.attn.qkv.weight.grad,
+                    p + "bqkv": b.attn.qkv.bias.grad, p + "bo": b.attn.proj.bias.grad, p + "w1": b.mlp.fc1.weight.grad,
+                    p + "b2": b.mlp.fc2.bias.grad, p + "ln2_b": b.norm2.bias.grad})
+    ref.update({"merger.w1": hf.merger.mlp[0].weight.grad, "merger.ln_g": hf.merger.ln_q.weight.grad})
+    for k, r in ref.items():
+        assert np.allclose(gv[k], r.numpy(), rtol=0, atol=1e-10), k

@@ -98,7 +98,7 @@ def _worker(rank, world, port, q):
     uid = broadcast_nccl_id()
     # grid mapping used by bench.py / the stage: rank = pp_rank * tp + tp_rank
     import bench
-    t, p = bench.GRID[world]
+    t, p = bench.CONFIGS["cfg2"][3][world]
     got = [None] * world
     dist.all_gather_object(got, (rank % t, rank // t, uid))
     q.put((rank, got))

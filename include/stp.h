@@ -88,7 +88,11 @@ typedef enum {
   STP_U_CB = 7,      /* backward TP comm phase (RS + RMSNorm-bwd + residual grad + AG) */
   STP_U_F_EMB = 8, STP_U_W_EMB = 9,
   STP_U_F_HEAD = 10, STP_U_B_HEAD = 11, STP_U_W_HEAD = 12,
-  STP_U_PP_SEND = 13, STP_U_PP_RECV = 14
+  STP_U_PP_SEND = 13, STP_U_PP_RECV = 14,
+  /* MLLM first virtual stage (stp_schedule_units_mllm): 2x2 merger + text
+   * embedding producing the LM input (F), its activation gradient (B) and
+   * its weight gradients (W) */
+  STP_U_F_MERGE = 15, STP_U_B_MERGE = 16, STP_U_W_MERGE = 17
 } stp_unit_op;
 
 typedef struct {
@@ -120,11 +124,23 @@ stp_status stp_schedule_actions(const stp_schedule* s, int32_t pp_rank,
 stp_status stp_schedule_units(const stp_schedule* s, int32_t pp_rank,
                               const int32_t* layers_per_vstage,
                               stp_unit* buf, int32_t cap, int32_t* n_out);
+/* MLLM variant (§5: "the ViT encoder is assigned to the first
+ * virtual stage on device 0"): layers_per_vstage[0] is the number of ViT
+ * layers on virtual stage 0 (global layers 0..n_vit-1; the LM layers follow),
+ * whose forward lane is F_EMB (patch embedding), the ViT layers' F_ATTN /
+ * F_MLP and F_MERGE; its backward lane starts with B_MERGE, its W list with
+ * W_MERGE (reading V5). */
+stp_status stp_schedule_units_mllm(const stp_schedule* s, int32_t pp_rank,
+                                   const int32_t* layers_per_vstage,
+                                   stp_unit* buf, int32_t cap, int32_t* n_out);
 /* Canonical text: header, then per rank "rank d", A lines and
  * (if layers_per_vstage != NULL) U lines.  Writes at most cap bytes incl. the
  * terminating NUL; *n_out = length without NUL; STP_ECAPACITY if too small. */
 stp_status stp_schedule_serialize(const stp_schedule* s, const int32_t* layers_per_vstage,
                                   char* buf, int64_t cap, int64_t* n_out);
+/* Same for the MLLM expansion (header line ends with " mllm"). */
+stp_status stp_schedule_serialize_mllm(const stp_schedule* s, const int32_t* layers_per_vstage,
+                                       char* buf, int64_t cap, int64_t* n_out);
 /* Max number of chunk-microbatches whose forward was issued and whose weight
  * gradient was not, walking rank pp_rank's list in order (= stash slots). */
 stp_status stp_schedule_stash_slots(const stp_schedule* s, int32_t pp_rank, int32_t* n_out);

@@ -111,6 +111,54 @@ stp_status stp_op_attn_bwd(int32_t dtype, int64_t s, int32_t nq, int32_t nkv, in
                            void* dq, void* dk, void* dv, int64_t ld_dqkv,
                            void* ws, void* stream);
 
+/* ------------------------------------------- ViT first chunk (MLLM, cfg5)
+ * The heterogeneous first virtual stage of the MLLM workload: "the ViT encoder
+ * is assigned to the first virtual stage on device 0" (§5 P:L171;
+ * Table 3).  Model: Qwen2-VL's vision tower + 2x2 merger as
+ * oracle/vit.py restates it (readings V1-V4 in DESIGN.md).
+ *
+ * Bidirectional multi-head attention (no GQA: nh q, k and v heads) over the
+ * fused [q | k | v] row layout of the QKV projection: qkv [s, ld_qkv] holds
+ * q heads at columns [0, nh d), k at [nh d, 2 nh d), v at [2 nh d, 3 nh d).
+ * O = softmax(Q K^T / sqrt(d)) V per head; lse fp32 [nh, s].  bf16 needs
+ * d in {80, 128} (tcgen05 kernels; d = 80 heads are zero-padded to 128 in
+ * shared memory by TMA) and ld_qkv = 3 nh d; fp32 runs SIMT kernels (d <= 128).
+ * Backward writes dqkv in the same layout (ld_dqkv = 3 nh d for bf16); ws is
+ * stp_op_attn_bwd_ws_bytes(s, nh, nh, d) bytes. */
+stp_status stp_op_attn_full_fwd(int32_t dtype, int64_t s, int32_t nh, int32_t d, const void* qkv, int64_t ld_qkv,
+                                void* o, int64_t ld_o, float* lse, void* stream);
+stp_status stp_op_attn_full_bwd(int32_t dtype, int64_t s, int32_t nh, int32_t d, const void* qkv, int64_t ld_qkv,
+                                const void* o, int64_t ld_o, const void* dout, const float* lse, void* dqkv,
+                                int64_t ld_dqkv, void* ws, void* stream);
+/* LayerNorm y = gamma (x - mu) r + beta, r = (var + eps)^(-1/2) over h
+ * (biased variance), rows x h row-major.  If resid != NULL the input is
+ * x + resid and the sum is written to x_out (the residual add of the SP comm
+ * phase).  mean_out / rstd_out fp32 [rows] (nullable).  h % 8 == 0,
+ * h <= 4096 (bf16) / 2048 (fp32), 16-byte aligned rows. */
+stp_status stp_op_layernorm_fwd(int32_t dtype, int64_t rows, int64_t h, const void* x, const void* resid, void* x_out,
+                                const void* gamma, const void* beta, float eps, void* y, float* mean_out,
+                                float* rstd_out, void* stream);
+/* dx = r (gamma dy - mean_h(gamma dy) - xhat mean_h(gamma dy xhat)) (+ dres),
+ * xhat = (x - mu) r; dgamma_acc += sum_rows dy xhat, dbeta_acc += sum_rows dy
+ * (fp32 [h], nullable).  x is the LayerNorm input; dx may alias dres. */
+stp_status stp_op_layernorm_bwd(int32_t dtype, int64_t rows, int64_t h, const void* dy, const void* x,
+                                const void* gamma, const float* mean, const float* rstd, const void* dres, void* dx,
+                                float* dgamma_acc, float* dbeta_acc, void* stream);
+/* Elementwise activation over n elements (n % 8 == 0, 16-byte aligned):
+ * kind 0 QuickGELU y = a sigmoid(1.702 a) (ViT MLP); kind 1 GELU
+ * y = a Phi(a), erf form (merger MLP).  Backward: da = dy act'(a) (da may
+ * alias dy). */
+stp_status stp_op_act_fwd(int32_t dtype, int32_t kind, int64_t n, const void* a, void* y, void* stream);
+stp_status stp_op_act_bwd(int32_t dtype, int32_t kind, int64_t n, const void* dy, const void* a, void* da,
+                          void* stream);
+/* 2-D vision RoPE (rotate-half) in place on n_heads heads of width d at
+ * column col0 of a [s, ld] buffer whose rows are the patches of a
+ * (s / grid_w) x grid_w image in 2x2 merge-window order: angle j < d/4 is
+ * h_pos inv_j, d/4 <= j < d/2 is w_pos inv_{j-d/4}, inv_j = theta^(-2j/(d/2))
+ * (oracle/vit.py vit_rope_tables).  grid_w and s / grid_w even. */
+stp_status stp_op_rope2d(int32_t dtype, int32_t backward, int64_t s, int64_t ld, int64_t col0, int32_t n_heads,
+                         int32_t d, int32_t grid_w, float theta, void* x, void* stream);
+
 /* ------------------------------------------------- vocab-parallel pieces
  * Embedding (vocab rows [v0, v0+Vl) on this rank): out[i] = E[tok_i - v0] if
  * tok_i in range else 0 (the TP partial summed by the reduce-scatter). */

@@ -47,7 +47,7 @@ A_F, A_BFULL, A_B, A_W, A_FB, A_FBS, A_FW = range(7)
 ACT_NAMES = ["F", "BFULL", "B", "W", "FB", "FBS", "FW"]
 # unit ops (stp_unit_op)
 (F_ATTN, F_MLP, B_MLP, B_ATTN, W_MLP, W_ATTN, CF, CB, F_EMB, W_EMB, F_HEAD,
- B_HEAD, W_HEAD, PP_SEND, PP_RECV) = range(15)
+ B_HEAD, W_HEAD, PP_SEND, PP_RECV, F_MERGE, B_MERGE, W_MERGE) = range(18)
 S_COMPUTE, S_COMM, S_PP = 0, 1, 2
 
 Action = Tuple[int, int, int, int, int, int]   # kind, chunk, f_mb, b_mb, w_mb, w_chunk
@@ -298,10 +298,17 @@ def _layers_of(layers_per_vstage: Sequence[int], vs: int) -> List[int]:
 
 
 def expand_units(kind: int, p: int, d: int, actions: List[Action],
-                 layers_per_vstage: Sequence[int]) -> List[Tuple[int, ...]]:
+                 layers_per_vstage: Sequence[int], vit_first: bool = False) -> List[Tuple[int, ...]]:
     """Expand one device's action list into its unit sequence (emit order =
     host enqueue order).  Tuple fields: action, stream, op, layer, chunk, mb,
-    dep0, dep1 (dep = global unit index on this device, -1 = none)."""
+    dep0, dep1 (dep = global unit index on this device, -1 = none).
+
+    vit_first (MLLM, "the ViT encoder is assigned to the first virtual
+    stage on device 0"; reading V5): virtual stage 0 holds the ViT
+    layers 0..layers_per_vstage[0]-1 (the LM layers follow in global
+    numbering); its forward lane is F_EMB (patch embedding), the ViT layers'
+    F_ATTN / F_MLP, then F_MERGE (2x2 merger + text embedding -> LM input);
+    its backward lane starts with B_MERGE and its W list with W_MERGE."""
     V = n_vstages(kind, p)
     assert len(layers_per_vstage) == V
     E = _Emitter()
@@ -321,6 +328,7 @@ def expand_units(kind: int, p: int, d: int, actions: List[Action],
         L = _layers_of(layers_per_vstage, vs)
         heavy = ([(F_EMB, -1)] if vs == 0 else []) + \
             [u for l in L for u in ((F_ATTN, l), (F_MLP, l))] + \
+            ([(F_MERGE, -1)] if vs == 0 and vit_first else []) + \
             ([(F_HEAD, -1)] if vs == V - 1 else [])
         st = {"last": -1}
 
@@ -344,13 +352,19 @@ def expand_units(kind: int, p: int, d: int, actions: List[Action],
 
         return [pre], [mkstep(k + 1, op, l) for k, (op, l) in enumerate(heavy)], [post]
 
+    def w_list(vs):
+        L = _layers_of(layers_per_vstage, vs)
+        return ([(W_HEAD, -1)] if vs == V - 1 else []) + \
+            ([(W_MERGE, -1)] if vs == 0 and vit_first else []) + \
+            [u for l in reversed(L) for u in ((W_MLP, l), (W_ATTN, l))]
+
     def bwd_lane(ai, c, mb, with_w):
         vs = vstage(kind, p, d, c)
         L = _layers_of(layers_per_vstage, vs)
         heavy = ([(B_HEAD, -1)] if vs == V - 1 else []) + \
+            ([(B_MERGE, -1)] if vs == 0 and vit_first else []) + \
             [u for l in reversed(L) for u in ((B_MLP, l), (B_ATTN, l))]
-        wl = ([(W_HEAD, -1)] if vs == V - 1 else []) + \
-            [u for l in reversed(L) for u in ((W_MLP, l), (W_ATTN, l))]
+        wl = w_list(vs)
         st = {"last": -1}
 
         def pre():
@@ -381,9 +395,7 @@ def expand_units(kind: int, p: int, d: int, actions: List[Action],
 
     def w_lane(ai, c, mb):
         vs = vstage(kind, p, d, c)
-        L = _layers_of(layers_per_vstage, vs)
-        wl = ([(W_HEAD, -1)] if vs == V - 1 else []) + \
-            [u for l in reversed(L) for u in ((W_MLP, l), (W_ATTN, l))]
+        wl = w_list(vs)
 
         def mkstep(op, l):
             return lambda: E.emit(ai, S_COMPUTE, op, l, c, mb)
@@ -438,15 +450,15 @@ def expand_units(kind: int, p: int, d: int, actions: List[Action],
 # ---------------------------------------------------------------------------
 
 def serialize(kind: int, p: int, v: int, t: int, m: int,
-              layers_per_vstage: Optional[Sequence[int]] = None) -> str:
+              layers_per_vstage: Optional[Sequence[int]] = None, vit_first: bool = False) -> str:
     progs = build_program(kind, p, m)
-    lines = [f"sched {KIND_NAMES[kind]} p {p} v {v} t {t} m {m}"]
+    lines = [f"sched {KIND_NAMES[kind]} p {p} v {v} t {t} m {m}" + (" mllm" if vit_first else "")]
     for d, acts in enumerate(progs):
         lines.append(f"rank {d}")
         for i, a in enumerate(acts):
             lines.append("A " + " ".join(str(x) for x in (i,) + a))
         if layers_per_vstage is not None:
-            for j, u in enumerate(expand_units(kind, p, d, acts, layers_per_vstage)):
+            for j, u in enumerate(expand_units(kind, p, d, acts, layers_per_vstage, vit_first)):
                 lines.append("U " + " ".join(str(x) for x in (j,) + u))
     return "\n".join(lines) + "\n"
 

@@ -65,6 +65,8 @@ _SIGS = {
     "stp_schedule_actions": (i32, [vp, i32, C.POINTER(Action), i32, C.POINTER(i32)]),
     "stp_schedule_units": (i32, [vp, i32, C.POINTER(i32), C.POINTER(Unit), i32, C.POINTER(i32)]),
     "stp_schedule_serialize": (i32, [vp, C.POINTER(i32), C.c_char_p, i64, C.POINTER(i64)]),
+    "stp_schedule_units_mllm": (i32, [vp, i32, C.POINTER(i32), C.POINTER(Unit), i32, C.POINTER(i32)]),
+    "stp_schedule_serialize_mllm": (i32, [vp, C.POINTER(i32), C.c_char_p, i64, C.POINTER(i64)]),
     "stp_schedule_stash_slots": (i32, [vp, i32, C.POINTER(i32)]),
     "stp_free_schedule": (None, [vp]),
     "stp_layer_split": (i32, [i32, i32, C.POINTER(i32)]),
@@ -91,6 +93,13 @@ _SIGS = {
     "stp_op_attn_fwd": (i32, [i32, i64, i32, i32, i32, vp, vp, vp, i64, vp, i64, vp, vp]),
     "stp_op_attn_bwd_ws_bytes": (i64, [i64, i32, i32, i32]),
     "stp_op_attn_bwd": (i32, [i32, i64, i32, i32, i32, vp, vp, vp, i64, vp, i64, vp, vp, vp, vp, vp, i64, vp, vp]),
+    "stp_op_attn_full_fwd": (i32, [i32, i64, i32, i32, vp, i64, vp, i64, vp, vp]),
+    "stp_op_attn_full_bwd": (i32, [i32, i64, i32, i32, vp, i64, vp, i64, vp, vp, vp, i64, vp, vp]),
+    "stp_op_layernorm_fwd": (i32, [i32, i64, i64, vp, vp, vp, vp, vp, f32, vp, vp, vp, vp]),
+    "stp_op_layernorm_bwd": (i32, [i32, i64, i64, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp]),
+    "stp_op_act_fwd": (i32, [i32, i32, i64, vp, vp, vp]),
+    "stp_op_act_bwd": (i32, [i32, i32, i64, vp, vp, vp, vp]),
+    "stp_op_rope2d": (i32, [i32, i32, i64, i64, i64, i32, i32, i32, f32, vp, vp]),
     "stp_op_embed_fwd": (i32, [i32, i64, i64, vp, i64, i64, vp, vp, vp]),
     "stp_op_embed_bwd": (i32, [i32, i64, i64, vp, i64, i64, vp, vp, vp]),
     "stp_op_ce_stats": (i32, [i32, i64, i64, vp, i64, vp, i64, vp, vp]),

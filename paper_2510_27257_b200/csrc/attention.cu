@@ -1,14 +1,18 @@
 // Causal GQA attention forward / backward (the Attn unit's core; the paper
 // runs FlashAttention-2; math: SURVEY §8c.1, oracle
-// attention_fwd / attention_bwd).
+// attention_fwd / attention_bwd) and the bidirectional d = 80 attention of the
+// ViT encoder (oracle/vit.py attention_full_fwd / _bwd).  Dispatch: bf16 with
+// d in {128, 80} and the fused [q | k | v] row layout runs the tcgen05 kernels
+// (attn_fwd_sm100.cu, attn_bwd_sm100.cu); other bf16 head dims (causal only)
+// run the mma.sync kernels below; fp32 runs the SIMT kernels.
 //
-// bf16 path (round 1): FlashAttention-2-style tiling with warp-level
+// bf16 mma.sync path (round 1, small-shape / odd-d fallback): FlashAttention-2-style tiling with warp-level
 // mma.sync m16n8k16 (bf16 in, fp32 accumulate), online softmax in fp32,
 // 64 x 64 tiles, 4 warps x 16 query (or key) rows, padded shared-memory rows
 // (conflict-free 32-bit fragment loads).  Backward = a dK/dV kernel (one CTA
 // per key block and kv head, looping over the group's query heads and the
 // causal query blocks) and a dQ kernel (one CTA per query block and head),
-// so no atomics are needed.  TODO(next round): tcgen05 + TMEM version.
+// so no atomics are needed.
 //
 // fp32 path: straightforward SIMT kernels (one warp per row) used by the
 // fp32 parity mode.
@@ -425,8 +429,9 @@ __global__ void __launch_bounds__(128) attn_bwd_dq_mma(int s, int nq, int nkv, c
 
 // ------------------------------------------------------------ fp32 SIMT
 // One warp per (query row, head): online softmax over keys <= row.
-__global__ void attn_fwd_f32(int s, int nq, int nkv, int D, const float* __restrict__ q, const float* __restrict__ k,
-                             const float* __restrict__ v, int64_t ld, float* o, int64_t ldo, float* lse) {
+__global__ void attn_fwd_f32(int s, int nq, int nkv, int D, int causal, const float* __restrict__ q,
+                             const float* __restrict__ k, const float* __restrict__ v, int64_t ld, float* o,
+                             int64_t ldo, float* lse) {
   const int lane = threadIdx.x & 31;
   const int64_t w = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (w >= (int64_t)s * nq) return;
@@ -437,7 +442,8 @@ __global__ void attn_fwd_f32(int s, int nq, int nkv, int D, const float* __restr
   const float* qr = q + row * ld + (int64_t)h * D;
   float acc[4] = {0.f, 0.f, 0.f, 0.f};  // D <= 128
   float m = -INFINITY, l = 0.f;
-  for (int64_t j = 0; j <= row; ++j) {
+  const int64_t jmax = causal ? row : s - 1;
+  for (int64_t j = 0; j <= jmax; ++j) {
     const float* kr = k + j * ld + (int64_t)kvh * D;
     float dot = 0.f;
     for (int d = lane; d < D; d += 32) dot += qr[d] * kr[d];
@@ -458,7 +464,7 @@ __global__ void attn_fwd_f32(int s, int nq, int nkv, int D, const float* __restr
 }
 
 // dQ: one warp per (query row, head).
-__global__ void attn_bwd_dq_f32(int s, int nq, int nkv, int D, const float* __restrict__ q,
+__global__ void attn_bwd_dq_f32(int s, int nq, int nkv, int D, int causal, const float* __restrict__ q,
                                 const float* __restrict__ k, const float* __restrict__ v, int64_t ld,
                                 const float* __restrict__ dout, int64_t ldo, const float* __restrict__ lse,
                                 const float* __restrict__ Dl, float* dq, int64_t ldd) {
@@ -473,7 +479,8 @@ __global__ void attn_bwd_dq_f32(int s, int nq, int nkv, int D, const float* __re
   const float* dor = dout + row * ldo + (int64_t)h * D;
   const float L = lse[(int64_t)h * s + row], Dv = Dl[(int64_t)h * s + row];
   float acc[4] = {0.f, 0.f, 0.f, 0.f};
-  for (int64_t j = 0; j <= row; ++j) {
+  const int64_t jmax = causal ? row : s - 1;
+  for (int64_t j = 0; j <= jmax; ++j) {
     const float* kr = k + j * ld + (int64_t)kvh * D;
     const float* vr = v + j * ld + (int64_t)kvh * D;
     float dot = 0.f, dp = 0.f;
@@ -495,7 +502,7 @@ __global__ void attn_bwd_dq_f32(int s, int nq, int nkv, int D, const float* __re
 }
 
 // dK, dV: one warp per (key row, kv head), summing over the group's query heads.
-__global__ void attn_bwd_dkdv_f32(int s, int nq, int nkv, int D, const float* __restrict__ q,
+__global__ void attn_bwd_dkdv_f32(int s, int nq, int nkv, int D, int causal, const float* __restrict__ q,
                                   const float* __restrict__ k, const float* __restrict__ v, int64_t ld,
                                   const float* __restrict__ dout, int64_t ldo, const float* __restrict__ lse,
                                   const float* __restrict__ Dl, float* dk, float* dv, int64_t ldd) {
@@ -511,7 +518,7 @@ __global__ void attn_bwd_dkdv_f32(int s, int nq, int nkv, int D, const float* __
   float ak[4] = {0.f, 0.f, 0.f, 0.f}, av[4] = {0.f, 0.f, 0.f, 0.f};
   for (int hh = 0; hh < grp; ++hh) {
     const int h = kvh * grp + hh;
-    for (int64_t i = j; i < s; ++i) {
+    for (int64_t i = causal ? j : 0; i < s; ++i) {
       const float* qr = q + i * ld + (int64_t)h * D;
       const float* dor = dout + i * ldo + (int64_t)h * D;
       float dot = 0.f, dp = 0.f;
@@ -587,44 +594,48 @@ stp_status bwd_bf16(int s, int nq, int nkv, const void* q, const void* k, const 
 
 }  // namespace
 
-stp_status attn_fwd_sm100_launch(int s, int nq, int nkv, const void* qkv_base, int64_t ld, void* o, int64_t ldo,
-                                 float* lse, cudaStream_t st);
+stp_status attn_fwd_sm100_launch(int s, int nq, int nkv, int dh, int causal, const void* qkv_base, int64_t ld,
+                                 void* o, int64_t ldo, float* lse, cudaStream_t st);
 
 
 int64_t attn_bwd_fused_ws_bytes(int64_t s, int nq, int nkv);
-stp_status attn_bwd_fused_launch(int s, int nq, int nkv, const void* qkv, int64_t ld, const void* o, const void* dout,
-                                 int64_t ldo, const float* lse, void* dqkv, int64_t ldd, void* ws, cudaStream_t st);
+stp_status attn_bwd_fused_launch(int s, int nq, int nkv, int dh, int causal, const void* qkv, int64_t ld,
+                                 const void* o, const void* dout, int64_t ldo, const float* lse, void* dqkv,
+                                 int64_t ldd, void* ws, cudaStream_t st);
 
 // fp32 workspace: D = rowsum(dO*O) [nq, s] for the mma.sync / fp32 paths;
 // the fused tcgen05 path (d = 128) needs attn_bwd_fused_ws_bytes.
 int64_t attn_bwd_ws_bytes(int64_t s, int nq, int nkv, int d) {
   int64_t b = s * nq * (int64_t)sizeof(float);
-  if (d == 128) b = std::max(b, attn_bwd_fused_ws_bytes(s, nq, nkv));
+  if (d == 128 || d == 80) b = std::max(b, attn_bwd_fused_ws_bytes(s, nq, nkv));
   return b;
 }
 
-stp_status attn_fwd(int dtype, int64_t s, int nq, int nkv, int d, const void* q, const void* k, const void* v,
-                    int64_t ld, void* o, int64_t ldo, float* lse, cudaStream_t st) {
+stp_status attn_fwd(int dtype, int64_t s, int nq, int nkv, int d, int causal, const void* q, const void* k,
+                    const void* v, int64_t ld, void* o, int64_t ldo, float* lse, cudaStream_t st) {
   STP_CHECK_ARG(nq > 0 && nkv > 0 && nq % nkv == 0, "nq % nkv == 0");
   STP_CHECK_ARG(d > 0 && d <= 128, "head_dim <= 128");
   if (s == 0) return STP_OK;
-  // algorithmic causal FLOPs: QK^T and PV over the s(s+1)/2 visible pairs
-  const double pairs = 0.5 * (double)s * (double)(s + 1);
+  // algorithmic FLOPs: QK^T and PV over the visible pairs (s(s+1)/2 causal, s^2 bidirectional)
+  const double pairs = causal ? 0.5 * (double)s * (double)(s + 1) : (double)s * (double)s;
   ProfScope prof(PROF_ATTN_FWD, 4.0 * pairs * nq * d, (double)dtype_size(dtype) * s * (nq + 2 * nkv + nq) * d, st);
   if (dtype == STP_DTYPE_F32) {
     const int64_t warps = s * nq;
-    attn_fwd_f32<<<(unsigned)((warps + 7) / 8), 256, 0, st>>>((int)s, nq, nkv, d, (const float*)q, (const float*)k,
-                                                             (const float*)v, ld, (float*)o, ldo, lse);
+    attn_fwd_f32<<<(unsigned)((warps + 7) / 8), 256, 0, st>>>((int)s, nq, nkv, d, causal, (const float*)q,
+                                                             (const float*)k, (const float*)v, ld, (float*)o, ldo,
+                                                             lse);
     count_launch();
     STP_LAUNCH_CHECK();
     return STP_OK;
   }
   STP_CHECK_ARG(ld % 8 == 0 && ldo % 8 == 0, "bf16 attention strides % 8 == 0");
-  // tcgen05 path: d = 128 with the fused [q | k | v] row layout
+  // tcgen05 path: d = 128 or 80 with the fused [q | k | v] row layout
   static const bool force_mma = getenv("STP_ATTN_MMA_SYNC") != nullptr;
-  if (d == 128 && !force_mma && (const uint8_t*)k == (const uint8_t*)q + (int64_t)nq * d * 2 &&
-      (const uint8_t*)v == (const uint8_t*)k + (int64_t)nkv * d * 2 && ld == (int64_t)(nq + 2 * nkv) * d)
-    return attn_fwd_sm100_launch((int)s, nq, nkv, q, ld, o, ldo, lse, st);
+  const bool fused = (const uint8_t*)k == (const uint8_t*)q + (int64_t)nq * d * 2 &&
+                     (const uint8_t*)v == (const uint8_t*)k + (int64_t)nkv * d * 2 && ld == (int64_t)(nq + 2 * nkv) * d;
+  if ((d == 128 || d == 80) && fused && (!force_mma || d == 80))
+    return attn_fwd_sm100_launch((int)s, nq, nkv, d, causal, q, ld, o, ldo, lse, st);
+  if (!causal) return fail(STP_EUNSUPPORTED, "bidirectional bf16 attention needs d in {80, 128} and the [q|k|v] layout");
   switch (d) {
     case 16: return fwd_bf16<16>((int)s, nq, nkv, q, k, v, ld, o, ldo, lse, st);
     case 32: return fwd_bf16<32>((int)s, nq, nkv, q, k, v, ld, o, ldo, lse, st);
@@ -634,37 +645,39 @@ stp_status attn_fwd(int dtype, int64_t s, int nq, int nkv, int d, const void* q,
   return fail(STP_EUNSUPPORTED, "bf16 attention head_dim must be 16, 32, 64 or 128");
 }
 
-stp_status attn_bwd(int dtype, int64_t s, int nq, int nkv, int d, const void* q, const void* k, const void* v,
-                    int64_t ld, const void* o, int64_t ldo, const void* dout, const float* lse, void* dq, void* dk,
-                    void* dv, int64_t ldd, void* ws, cudaStream_t st) {
+stp_status attn_bwd(int dtype, int64_t s, int nq, int nkv, int d, int causal, const void* q, const void* k,
+                    const void* v, int64_t ld, const void* o, int64_t ldo, const void* dout, const float* lse,
+                    void* dq, void* dk, void* dv, int64_t ldd, void* ws, cudaStream_t st) {
   STP_CHECK_ARG(nq > 0 && nkv > 0 && nq % nkv == 0, "nq % nkv == 0");
   STP_CHECK_ARG(d > 0 && d <= 128, "head_dim <= 128");
   STP_CHECK_ARG(ws != nullptr, "workspace");
   if (s == 0) return STP_OK;
-  const double pairs = 0.5 * (double)s * (double)(s + 1);
+  const double pairs = causal ? 0.5 * (double)s * (double)(s + 1) : (double)s * (double)s;
   ProfScope prof(PROF_ATTN_BWD, 8.0 * pairs * nq * d,
                  (double)dtype_size(dtype) * s * (2 * (nq + 2 * nkv) + 2 * nq) * d, st);
   float* Dl = (float*)ws;
   const int64_t warps = s * nq;
   return STP_DISPATCH_DTYPE(dtype, [&] {
-    // fused tcgen05 backward (d = 128, [q | k | v] layouts): computes its own D
-    if (dtype == STP_DTYPE_BF16 && d == 128 && getenv("STP_ATTN_MMA_SYNC") == nullptr &&
+    // fused tcgen05 backward (d = 128 or 80, [q | k | v] layouts): computes its own D
+    if (dtype == STP_DTYPE_BF16 && (d == 128 || d == 80) && (d == 80 || getenv("STP_ATTN_MMA_SYNC") == nullptr) &&
         (const uint8_t*)k == (const uint8_t*)q + (int64_t)nq * d * 2 &&
         (const uint8_t*)v == (const uint8_t*)k + (int64_t)nkv * d * 2 && ld == (int64_t)(nq + 2 * nkv) * d &&
         (const uint8_t*)dk == (const uint8_t*)dq + (int64_t)nq * d * 2 &&
         (const uint8_t*)dv == (const uint8_t*)dk + (int64_t)nkv * d * 2 && ld % 8 == 0 && ldo % 8 == 0 && ldd % 8 == 0)
-      return attn_bwd_fused_launch((int)s, nq, nkv, q, ld, o, dout, ldo, lse, dq, ldd, ws, st);
+      return attn_bwd_fused_launch((int)s, nq, nkv, d, causal, q, ld, o, dout, ldo, lse, dq, ldd, ws, st);
+    if (dtype == STP_DTYPE_BF16 && !causal)
+      return fail(STP_EUNSUPPORTED, "bidirectional bf16 attention needs d in {80, 128} and the [q|k|v] layouts");
     attn_bwd_dot<T><<<(unsigned)((warps + 7) / 8), 256, 0, st>>>((int)s, nq, d, (const T*)o, ldo, (const T*)dout, Dl);
     count_launch();
     STP_LAUNCH_CHECK();
     if (dtype == STP_DTYPE_F32) {
-      attn_bwd_dq_f32<<<(unsigned)((warps + 7) / 8), 256, 0, st>>>((int)s, nq, nkv, d, (const float*)q,
+      attn_bwd_dq_f32<<<(unsigned)((warps + 7) / 8), 256, 0, st>>>((int)s, nq, nkv, d, causal, (const float*)q,
                                                                   (const float*)k, (const float*)v, ld,
                                                                   (const float*)dout, ldo, lse, Dl, (float*)dq, ldd);
       count_launch();
       STP_LAUNCH_CHECK();
       const int64_t kw = s * nkv;
-      attn_bwd_dkdv_f32<<<(unsigned)((kw + 7) / 8), 256, 0, st>>>((int)s, nq, nkv, d, (const float*)q,
+      attn_bwd_dkdv_f32<<<(unsigned)((kw + 7) / 8), 256, 0, st>>>((int)s, nq, nkv, d, causal, (const float*)q,
                                                                  (const float*)k, (const float*)v, ld,
                                                                  (const float*)dout, ldo, lse, Dl, (float*)dk,
                                                                  (float*)dv, ldd);
@@ -693,12 +706,28 @@ int64_t stp_op_attn_bwd_ws_bytes(int64_t s, int32_t nq, int32_t nkv, int32_t d) 
 }
 stp_status stp_op_attn_fwd(int32_t dtype, int64_t s, int32_t nq, int32_t nkv, int32_t d, const void* q, const void* k,
                            const void* v, int64_t ld_qkv, void* o, int64_t ld_o, float* lse, void* stream) {
-  return stp::attn_fwd(dtype, s, nq, nkv, d, q, k, v, ld_qkv, o, ld_o, lse, (cudaStream_t)stream);
+  return stp::attn_fwd(dtype, s, nq, nkv, d, 1, q, k, v, ld_qkv, o, ld_o, lse, (cudaStream_t)stream);
+}
+stp_status stp_op_attn_full_fwd(int32_t dtype, int64_t s, int32_t nh, int32_t d, const void* qkv, int64_t ld_qkv,
+                                void* o, int64_t ld_o, float* lse, void* stream) {
+  const uint8_t* q = (const uint8_t*)qkv;
+  const int64_t es = dtype == STP_DTYPE_BF16 ? 2 : 4;
+  return stp::attn_fwd(dtype, s, nh, nh, d, 0, q, q + nh * d * es, q + 2 * nh * d * es, ld_qkv, o, ld_o, lse,
+                       (cudaStream_t)stream);
+}
+stp_status stp_op_attn_full_bwd(int32_t dtype, int64_t s, int32_t nh, int32_t d, const void* qkv, int64_t ld_qkv,
+                                const void* o, int64_t ld_o, const void* dout, const float* lse, void* dqkv,
+                                int64_t ld_dqkv, void* ws, void* stream) {
+  const uint8_t* q = (const uint8_t*)qkv;
+  uint8_t* dq = (uint8_t*)dqkv;
+  const int64_t es = dtype == STP_DTYPE_BF16 ? 2 : 4, hs = nh * d * es;
+  return stp::attn_bwd(dtype, s, nh, nh, d, 0, q, q + hs, q + 2 * hs, ld_qkv, o, ld_o, dout, lse, dq, dq + hs,
+                       dq + 2 * hs, ld_dqkv, ws, (cudaStream_t)stream);
 }
 stp_status stp_op_attn_bwd(int32_t dtype, int64_t s, int32_t nq, int32_t nkv, int32_t d, const void* q, const void* k,
                            const void* v, int64_t ld_qkv, const void* o, int64_t ld_o, const void* dout,
                            const float* lse, void* dq, void* dk, void* dv, int64_t ld_dqkv, void* ws, void* stream) {
-  return stp::attn_bwd(dtype, s, nq, nkv, d, q, k, v, ld_qkv, o, ld_o, dout, lse, dq, dk, dv, ld_dqkv, ws,
+  return stp::attn_bwd(dtype, s, nq, nkv, d, 1, q, k, v, ld_qkv, o, ld_o, dout, lse, dq, dk, dv, ld_dqkv, ws,
                        (cudaStream_t)stream);
 }
 

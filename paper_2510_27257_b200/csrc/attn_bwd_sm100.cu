@@ -46,7 +46,8 @@
 
 namespace stp {
 
-stp_status tensor_map_bf16(CUtensorMap* out, const void* ptr, int64_t d0, int64_t d1, int64_t ld, int b0, int b1);
+stp_status tensor_map_heads(CUtensorMap* out, const void* ptr, int dh, int heads, int64_t rows, int64_t ld,
+                            int box_rows);
 stp_status set_max_smem_once(const void* func, int bytes, unsigned long long* mask);
 
 namespace {
@@ -64,6 +65,8 @@ static_assert(FB_SMEM <= 232448, "shared memory");
 
 struct FusedArgs {
   int s, nq, nkv, sp;  // sp: padded row stride (multiple of QT) of nl2 / Dp
+  int dh;              // head dim 128 (LM) or 80 (ViT, zero-padded to 128 by TMA)
+  int causal;          // 1: causal (LM), 0: bidirectional (ViT)
   const float* nl2;    // [nq, sp]: -lse * log2(e); -inf beyond s (masks the ragged tail)
   const float* Dp;     // [nq, sp]: rowsum(dO * O); 0 beyond s
   float* acc;          // fp32 [nq + 2 nkv][s][128] (head-major): dq heads | dk | dv kv heads, zeroed
@@ -99,9 +102,9 @@ __global__ void __launch_bounds__(384, 1)
   const int h = blockIdx.x, kt = blockIdx.y;
   const int grp = a.nq / a.nkv, g = h / grp;
   const int nq64 = (a.s + QT - 1) / QT;
-  const int q0 = 2 * kt;  // first query tile that sees key tile kt
+  const int q0 = a.causal ? 2 * kt : 0;  // first query tile that sees key tile kt
   const int n_q = nq64 - q0;
-  const int qcol = h * D, kcol = a.nq * D + g * D, vcol = (a.nq + a.nkv) * D + g * D;
+  const int kh = a.nq + g, vh = a.nq + a.nkv + g;  // head indices in the [q | k | v] row
 
   if (threadIdx.x == 0) {
     mbar_init(kv_full, 1);
@@ -133,20 +136,20 @@ __global__ void __launch_bounds__(384, 1)
   if (warp == 0) {
     if (lane == 0) {
       mbar_arrive_expect_tx(kv_full, 2 * TILE_BYTES);
-      tma_load_2d(sK, &tm_kv, kv_full, kcol, kt * T);
-      tma_load_2d(sK + ATOM, &tm_kv, kv_full, kcol + 64, kt * T);
-      tma_load_2d(sV, &tm_kv, kv_full, vcol, kt * T);
-      tma_load_2d(sV + ATOM, &tm_kv, kv_full, vcol + 64, kt * T);
+      tma_load_3d(sK, &tm_kv, kv_full, 0, kh, kt * T);
+      tma_load_3d(sK + ATOM, &tm_kv, kv_full, 64, kh, kt * T);
+      tma_load_3d(sV, &tm_kv, kv_full, 0, vh, kt * T);
+      tma_load_3d(sV + ATOM, &tm_kv, kv_full, 64, vh, kt * T);
       for (int it = 0; it < n_q; ++it) {
         const int st = it % ST, qi = q0 + it;
         mbar_wait_wd(qdo_empty + st, ((it / ST) & 1) ^ 1, 301, a.s, h, kt);
         mbar_arrive_expect_tx(qdo_full + st, 2 * QT_BYTES + 2 * QT * 4);
         uint8_t* q = sQ + st * QT_BYTES;
         uint8_t* o = sdO + st * QT_BYTES;
-        tma_load_2d(q, &tm_q64, qdo_full + st, qcol, qi * QT);
-        tma_load_2d(q + QATOM, &tm_q64, qdo_full + st, qcol + 64, qi * QT);
-        tma_load_2d(o, &tm_do64, qdo_full + st, h * D, qi * QT);
-        tma_load_2d(o + QATOM, &tm_do64, qdo_full + st, h * D + 64, qi * QT);
+        tma_load_3d(q, &tm_q64, qdo_full + st, 0, h, qi * QT);
+        tma_load_3d(q + QATOM, &tm_q64, qdo_full + st, 64, h, qi * QT);
+        tma_load_3d(o, &tm_do64, qdo_full + st, 0, h, qi * QT);
+        tma_load_3d(o + QATOM, &tm_do64, qdo_full + st, 64, h, qi * QT);
         bulk_load(s_nl + st * QT, a.nl2 + (int64_t)h * a.sp + qi * QT, QT * 4, qdo_full + st);
         bulk_load(s_D + st * QT, a.Dp + (int64_t)h * a.sp + qi * QT, QT * 4, qdo_full + st);
       }
@@ -156,7 +159,8 @@ __global__ void __launch_bounds__(384, 1)
     // elected lane issues each tcgen05 op.  SW128 descriptors of a tile base
     // plus a byte offset: desc(addr + off) = desc(addr) + off / 16.
     constexpr uint32_t idS = make_idesc_bf16(T, QT, false, false);  // S^T, dP^T: M = 128 keys, N = 64 queries
-    constexpr uint32_t idMN = make_idesc_bf16(T, D, false, true);   // dV, dK: N = d, B (dO_i, Q_i) MN-major
+    const uint32_t idMN = make_idesc_bf16(T, a.dh, false, true);    // dV, dK: N = dh, B (dO_i, Q_i) MN-major
+    const int nk = a.dh / 16;                                        // S^T / dP^T K-steps over d
     constexpr uint32_t idQ = make_idesc_bf16(T, QT, true, true);    // dQ^T: M = d (A = K^T), N = 64 (B = dS^T)
     const uint64_t dK_kmaj = make_sw128_desc(smem_u32(sK), 16, 1024);      // K as the K-major A of S^T
     const uint64_t dV_kmaj = make_sw128_desc(smem_u32(sV), 16, 1024);      // V as the K-major A of dP^T
@@ -175,6 +179,7 @@ __global__ void __launch_bounds__(384, 1)
       const uint32_t tS = tB + 128 * b;
 #pragma unroll
       for (int kk = 0; kk < D / 16; ++kk) {
+        if (kk >= nk) break;
         const uint32_t ka = ((kk >> 2) * ATOM + (kk & 3) * 32) >> 4, qa = ((kk >> 2) * QATOM + (kk & 3) * 32) >> 4;
         mma_f16_ss_el(tS, dK_kmaj + ka, qd + qa, idS, kk > 0 ? 1u : 0u);
       }
@@ -188,6 +193,7 @@ __global__ void __launch_bounds__(384, 1)
       const uint32_t tP = tB + 128 * b + 64;
 #pragma unroll
       for (int kk = 0; kk < D / 16; ++kk) {
+        if (kk >= nk) break;
         const uint32_t ka = ((kk >> 2) * ATOM + (kk & 3) * 32) >> 4, qa = ((kk >> 2) * QATOM + (kk & 3) * 32) >> 4;
         mma_f16_ss_el(tP, dV_kmaj + ka, od + qa, idS, kk > 0 ? 1u : 0u);
       }
@@ -255,10 +261,10 @@ __global__ void __launch_bounds__(384, 1)
           p[i + 3] = ex2(t3);
         }
       }
-      if (it < 2 || !vrow) {  // tiles overlapping the key tile: causal mask (query < key); rows beyond s
+      if ((a.causal && it < 2) || !vrow) {  // tiles overlapping the key tile: causal mask (query < key); rows beyond s
 #pragma unroll
         for (int i = 0; i < 64; ++i)
-          if (!vrow || qbase + i < krow) p[i] = 0.f;
+          if (!vrow || (a.causal && qbase + i < krow)) p[i] = 0.f;
       }
       {
         uint32_t pp[32];
@@ -316,7 +322,9 @@ __global__ void __launch_bounds__(384, 1)
       // head-major accumulator: row stride 128 floats, so the 64 query rows of
       // this thread's column d are compile-time offsets of one pointer
       float* dst = a.acc + ((int64_t)h * a.s + qbase) * D + r;
-      if (qbase + QT <= a.s) {
+      if (r >= a.dh) {
+        // zero-padded d rows of dQ^T: nothing to add
+      } else if (qbase + QT <= a.s) {
 #pragma unroll
         for (int j = 0; j < QT; ++j) red_add_f32(dst + j * D, __uint_as_float(qv[j]));
       } else {
@@ -333,6 +341,7 @@ __global__ void __launch_bounds__(384, 1)
     float* vr = kr + (int64_t)a.nkv * a.s * D;
 #pragma unroll 1
     for (int c = 0; c < 2; ++c) {
+      if (gi * 64 + c * 32 >= a.dh) break;  // d columns beyond dh
       uint32_t v[32], k[32];
       tmem_ld_32x32b_x32(tdV + gi * 64 + c * 32 + lane_off, v);
       tmem_ld_32x32b_x32(tdK + gi * 64 + c * 32 + lane_off, k);
@@ -340,6 +349,7 @@ __global__ void __launch_bounds__(384, 1)
       if (vrow) {
 #pragma unroll
         for (int i = 0; i < 32; i += 4) {
+          if (gi * 64 + c * 32 + i >= a.dh) break;
           red_add_v4_f32(vr + c * 32 + i, __uint_as_float(v[i]), __uint_as_float(v[i + 1]), __uint_as_float(v[i + 2]),
                          __uint_as_float(v[i + 3]));
           red_add_v4_f32(kr + c * 32 + i, __uint_as_float(k[i]), __uint_as_float(k[i + 1]), __uint_as_float(k[i + 2]),
@@ -359,7 +369,7 @@ __global__ void __launch_bounds__(384, 1)
 // nl2[h][q] = -lse[h][q] * log2(e), Dp[h][q] = sum_d dO[q][h, d] O[q][h, d] for q < s;
 // -inf / 0 for s <= q < sp (the padded tail masks itself in the fused kernel).
 // One warp per (row, head); 4 columns per lane.
-__global__ void attn_bwd_prep(int s, int sp, int nq, const bf16* __restrict__ o, const bf16* __restrict__ dout,
+__global__ void attn_bwd_prep(int s, int sp, int nq, int dh, const bf16* __restrict__ o, const bf16* __restrict__ dout,
                               int64_t ldo, const float* __restrict__ lse, float* __restrict__ nl2,
                               float* __restrict__ Dp) {
   const int lane = threadIdx.x & 31;
@@ -373,9 +383,12 @@ __global__ void attn_bwd_prep(int s, int sp, int nq, const bf16* __restrict__ o,
     }
     return;
   }
-  const int64_t off = (int64_t)q * ldo + (int64_t)h * D + lane * 4;
-  const uint2 ov = *reinterpret_cast<const uint2*>(o + off);
-  const uint2 dv = *reinterpret_cast<const uint2*>(dout + off);
+  const int64_t off = (int64_t)q * ldo + (int64_t)h * dh + lane * 4;
+  uint2 ov = make_uint2(0u, 0u), dv = make_uint2(0u, 0u);
+  if (lane * 4 < dh) {  // dh % 4 == 0
+    ov = *reinterpret_cast<const uint2*>(o + off);
+    dv = *reinterpret_cast<const uint2*>(dout + off);
+  }
   const __nv_bfloat162* o2 = reinterpret_cast<const __nv_bfloat162*>(&ov);
   const __nv_bfloat162* d2 = reinterpret_cast<const __nv_bfloat162*>(&dv);
   float acc = 0.f;
@@ -396,17 +409,18 @@ __global__ void attn_bwd_prep(int s, int sp, int nq, const bf16* __restrict__ o,
 // dqkv (bf16, [s, ldd], columns dq | dk | dv) = acc (head-major [C][s][128])
 // x (1/sqrt(d) for the dq and dk heads, 1 for dv).  One float4 per thread;
 // a warp reads one 512-byte head row.
-__global__ void attn_bwd_finalize(int s, int C, int qk_heads, const float* __restrict__ acc, bf16* dst, int64_t ldd,
-                                  float scale) {
-  const int64_t total = (int64_t)s * C * (D / 4);
+__global__ void attn_bwd_finalize(int s, int C, int qk_heads, int dh, const float* __restrict__ acc, bf16* dst,
+                                  int64_t ldd, float scale) {
+  const int nd4 = dh / 4;
+  const int64_t total = (int64_t)s * C * nd4;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
-    const int d4 = (int)(i % (D / 4)) * 4;
-    const int64_t rc = i / (D / 4);
+    const int d4 = (int)(i % nd4) * 4;
+    const int64_t rc = i / nd4;
     const int c = (int)(rc % C);
     const int64_t row = rc / C;
     const float4 v = *reinterpret_cast<const float4*>(acc + ((int64_t)c * s + row) * D + d4);
     const float sc = c < qk_heads ? scale : 1.f;
-    *reinterpret_cast<uint2*>(dst + row * ldd + (int64_t)c * D + d4) =
+    *reinterpret_cast<uint2*>(dst + row * ldd + (int64_t)c * dh + d4) =
         make_uint2(pack2(v.x * sc, v.y * sc), pack2(v.z * sc, v.w * sc));
   }
 }
@@ -419,10 +433,11 @@ int64_t attn_bwd_fused_ws_bytes(int64_t s, int nq, int nkv) {
   return 2 * (int64_t)nq * sp * 4 + 256 + s * (int64_t)(nq + 2 * nkv) * D * 4;
 }
 
-// d = 128 bf16, fused [q | k | v] layout of qkv and dqkv (row strides ld, ldd);
-// o and dout share row stride ldo.
-stp_status attn_bwd_fused_launch(int s, int nq, int nkv, const void* qkv, int64_t ld, const void* o, const void* dout,
-                                 int64_t ldo, const float* lse, void* dqkv, int64_t ldd, void* ws, cudaStream_t st) {
+// d = 128 or 80 bf16, fused [q | k | v] layout of qkv and dqkv (row strides ld,
+// ldd); o and dout share row stride ldo; causal (LM) or bidirectional (ViT).
+stp_status attn_bwd_fused_launch(int s, int nq, int nkv, int dh, int causal, const void* qkv, int64_t ld,
+                                 const void* o, const void* dout, int64_t ldo, const float* lse, void* dqkv,
+                                 int64_t ldd, void* ws, cudaStream_t st) {
   static unsigned long long attr_mask = 0;
   STP_TRY(set_max_smem_once((const void*)attn_bwd_fused_sm100, FB_SMEM, &attr_mask));
   const int sp = (s + QT - 1) / QT * QT;
@@ -433,15 +448,15 @@ stp_status attn_bwd_fused_launch(int s, int nq, int nkv, const void* qkv, int64_
   STP_CUDA_TRY(cudaMemsetAsync(acc, 0, (size_t)s * C * D * 4, st));
   {
     const int64_t warps = (int64_t)sp * nq;
-    attn_bwd_prep<<<(unsigned)((warps + 7) / 8), 256, 0, st>>>(s, sp, nq, (const bf16*)o, (const bf16*)dout, ldo, lse,
+    attn_bwd_prep<<<(unsigned)((warps + 7) / 8), 256, 0, st>>>(s, sp, nq, dh, (const bf16*)o, (const bf16*)dout, ldo, lse,
                                                                nl2, Dp);
     count_launch();
     STP_LAUNCH_CHECK();
   }
   CUtensorMap tkv, tq64, td64;
-  STP_TRY(tensor_map_bf16(&tkv, qkv, ld, s, ld, 64, T));
-  STP_TRY(tensor_map_bf16(&tq64, qkv, ld, s, ld, 64, QT));
-  STP_TRY(tensor_map_bf16(&td64, dout, ldo, s, ldo, 64, QT));
+  STP_TRY(tensor_map_heads(&tkv, qkv, dh, nq + 2 * nkv, s, ld, T));
+  STP_TRY(tensor_map_heads(&tq64, qkv, dh, nq + 2 * nkv, s, ld, QT));
+  STP_TRY(tensor_map_heads(&td64, dout, dh, nq, s, ldo, QT));
   FusedArgs a;
   a.s = s;
   a.nq = nq;
@@ -450,15 +465,17 @@ stp_status attn_bwd_fused_launch(int s, int nq, int nkv, const void* qkv, int64_
   a.nl2 = nl2;
   a.Dp = Dp;
   a.acc = acc;
-  a.scale_log2 = LOG2E / sqrtf((float)D);
+  a.dh = dh;
+  a.causal = causal;
+  a.scale_log2 = LOG2E / sqrtf((float)dh);
   const int nt = (s + T - 1) / T;
   attn_bwd_fused_sm100<<<dim3(nq, nt), 384, FB_SMEM, st>>>(tkv, tq64, td64, a);
   count_launch();
   STP_LAUNCH_CHECK();
   {
-    const int64_t total = (int64_t)s * C * (D / 4);
+    const int64_t total = (int64_t)s * C * (dh / 4);
     const int grid = (int)std::min<int64_t>((total + 255) / 256, 16 * num_sms());
-    attn_bwd_finalize<<<grid, 256, 0, st>>>(s, C, nq + nkv, acc, (bf16*)dqkv, ldd, 1.f / sqrtf((float)D));
+    attn_bwd_finalize<<<grid, 256, 0, st>>>(s, C, nq + nkv, dh, acc, (bf16*)dqkv, ldd, 1.f / sqrtf((float)dh));
     count_launch();
     STP_LAUNCH_CHECK();
   }

@@ -35,7 +35,8 @@
 
 namespace stp {
 
-stp_status tensor_map_bf16(CUtensorMap* out, const void* ptr, int64_t d0, int64_t d1, int64_t ld, int b0, int b1);
+stp_status tensor_map_heads(CUtensorMap* out, const void* ptr, int dh, int heads, int64_t rows, int64_t ld,
+                            int box_rows);
 stp_status set_max_smem_once(const void* func, int bytes, unsigned long long* mask);
 
 namespace {
@@ -45,6 +46,8 @@ using namespace attn;
 
 struct FwdArgs {
   int s, nq, nkv;
+  int dh;      // head dim: 128 (LM) or 80 (ViT); heads with dh < 128 are zero-padded to 128 by TMA
+  int causal;  // 1: causal mask (LM); 0: bidirectional (ViT)
   int64_t ldo;
   void* o;
   float* lse;
@@ -88,8 +91,8 @@ __global__ void __launch_bounds__(FWD_THREADS, 1)
   const int h = blockIdx.x;
   const int qt = gridDim.y - 1 - blockIdx.y;  // longest (most key tiles) first
   const int grp = a.nq / a.nkv, g = h / grp;
-  const int n_kv = qt + 1;                    // causal: key tiles 0..qt
-  const int qcol = h * D, kcol = a.nq * D + g * D, vcol = (a.nq + a.nkv) * D + g * D;
+  const int n_kv = a.causal ? qt + 1 : (a.s + T - 1) / T;  // causal: key tiles 0..qt
+  const int kh = a.nq + g, vh = a.nq + a.nkv + g;          // head indices in the [q | k | v] row
 
   if (threadIdx.x == 0) {
     mbar_init(q_full, 1);
@@ -115,24 +118,25 @@ __global__ void __launch_bounds__(FWD_THREADS, 1)
   if (warp == 0) {
     if (lane == 0) {
       mbar_arrive_expect_tx(q_full, TILE_BYTES);
-      tma_load_2d(sQ, &tm_qkv, q_full, qcol, qt * T);
-      tma_load_2d(sQ + ATOM, &tm_qkv, q_full, qcol + 64, qt * T);
+      tma_load_3d(sQ, &tm_qkv, q_full, 0, h, qt * T);
+      tma_load_3d(sQ + ATOM, &tm_qkv, q_full, 64, h, qt * T);
       for (int j = 0; j < n_kv; ++j) {
         const int b = j & 1;
         const uint32_t ph = (j >> 1) & 1;
         mbar_wait_wd(k_empty + b, ph ^ 1, 321, a.s, h, qt);
         mbar_arrive_expect_tx(k_full + b, TILE_BYTES);
-        tma_load_2d(sK + b * TILE_BYTES, &tm_qkv, k_full + b, kcol, j * T);
-        tma_load_2d(sK + b * TILE_BYTES + ATOM, &tm_qkv, k_full + b, kcol + 64, j * T);
+        tma_load_3d(sK + b * TILE_BYTES, &tm_qkv, k_full + b, 0, kh, j * T);
+        tma_load_3d(sK + b * TILE_BYTES + ATOM, &tm_qkv, k_full + b, 64, kh, j * T);
         mbar_wait_wd(v_empty + b, ph ^ 1, 322, a.s, h, qt);
         mbar_arrive_expect_tx(v_full + b, TILE_BYTES);
-        tma_load_2d(sV + b * TILE_BYTES, &tm_qkv, v_full + b, vcol, j * T);
-        tma_load_2d(sV + b * TILE_BYTES + ATOM, &tm_qkv, v_full + b, vcol + 64, j * T);
+        tma_load_3d(sV + b * TILE_BYTES, &tm_qkv, v_full + b, 0, vh, j * T);
+        tma_load_3d(sV + b * TILE_BYTES + ATOM, &tm_qkv, v_full + b, 64, vh, j * T);
       }
     }
   } else if (warp == 1) {
     constexpr uint32_t idS = make_idesc_bf16(T, T, false, false);  // S = Q K^T (both K-major)
-    constexpr uint32_t idO = make_idesc_bf16(T, D, false, true);   // O += P V (V MN-major)
+    const uint32_t idO = make_idesc_bf16(T, a.dh, false, true);    // O += P V (V MN-major, N = dh)
+    const int nk = a.dh / 16;                                       // QK^T K-steps (zero padding skipped)
     const uint64_t dQ = make_sw128_desc(smem_u32(sQ), 16, 1024);
     const uint64_t dK0 = make_sw128_desc(smem_u32(sK), 16, 1024);
     const uint64_t dV0 = make_sw128_desc(smem_u32(sV), ATOM, 1024);
@@ -163,6 +167,7 @@ __global__ void __launch_bounds__(FWD_THREADS, 1)
       const uint64_t kd = dK0 + (uint64_t)((b * TILE_BYTES) >> 4);
 #pragma unroll
       for (int kk = 0; kk < D / 16; ++kk) {
+        if (kk >= nk) break;
         const uint32_t off = ((kk >> 2) * ATOM + (kk & 3) * 32) >> 4;
         mma_f16_ss_el(tS0 + b * 128, dQ + off, kd + off, idS, kk > 0 ? 1u : 0u);
       }
@@ -192,10 +197,11 @@ __global__ void __launch_bounds__(FWD_THREADS, 1)
 #pragma unroll
       for (int i = 0; i < 64; ++i) sv[i] = __uint_as_float(u[i]);
       const int cbase = j * T + half * 64;
-      if (j == qt || cbase + 64 > a.s) {  // diagonal or ragged tile: causal / length mask
+      if ((a.causal && j == qt) || cbase + 64 > a.s) {  // diagonal or ragged tile: causal / length mask
+        const int lim = a.causal ? min(qrow + 1, a.s) : a.s;
 #pragma unroll
         for (int i = 0; i < 64; ++i)
-          if (cbase + i > qrow || cbase + i >= a.s) sv[i] = -INFINITY;
+          if (cbase + i >= lim) sv[i] = -INFINITY;
       }
       float mx = fmax3(sv[0], sv[1], sv[2]);
 #pragma unroll
@@ -262,9 +268,11 @@ __global__ void __launch_bounds__(FWD_THREADS, 1)
     const bool valid = qrow < a.s;
     const float inv = 1.f / lt;
     const float c0 = f0 * inv, c1 = f1 * inv;
-    bf16* orow = reinterpret_cast<bf16*>(a.o) + (int64_t)(valid ? qrow : 0) * a.ldo + (int64_t)h * D + half * 64;
+    bf16* orow = reinterpret_cast<bf16*>(a.o) + (int64_t)(valid ? qrow : 0) * a.ldo + (int64_t)h * a.dh + half * 64;
+    const int ncol = min(64, a.dh - half * 64);  // columns of [64 half, 64 half + 64) inside the head
 #pragma unroll 1
     for (int c = 0; c < 2; ++c) {  // this half writes output columns [64 half, 64 half + 64)
+      if (c * 32 >= ncol) break;
       uint32_t v0[32], v1[32];
       tmem_ld_32x32b_x32(tO + half * 64 + c * 32 + lane_off, v0);
       tmem_ld_32x32b_x32(tO + 128 + half * 64 + c * 32 + lane_off, v1);
@@ -272,6 +280,7 @@ __global__ void __launch_bounds__(FWD_THREADS, 1)
       if (valid) {
 #pragma unroll
         for (int i = 0; i < 32; i += 8) {
+          if (c * 32 + i >= ncol) break;
           float o8[8];
 #pragma unroll
           for (int e = 0; e < 8; ++e) o8[e] = __uint_as_float(v0[i + e]) * c0 + __uint_as_float(v1[i + e]) * c1;
@@ -296,21 +305,24 @@ __global__ void __launch_bounds__(FWD_THREADS, 1)
 
 }  // namespace
 
-// d = 128 bf16 with the fused [q | k | v] row layout (row stride ld).
-stp_status attn_fwd_sm100_launch(int s, int nq, int nkv, const void* qkv_base, int64_t ld, void* o, int64_t ldo,
-                                 float* lse, cudaStream_t st) {
+// d = 128 or 80, bf16, fused [q | k | v] row layout (row stride ld); causal
+// (LM) or bidirectional (ViT).
+stp_status attn_fwd_sm100_launch(int s, int nq, int nkv, int dh, int causal, const void* qkv_base, int64_t ld,
+                                 void* o, int64_t ldo, float* lse, cudaStream_t st) {
   static unsigned long long attr_mask = 0;
   STP_TRY(set_max_smem_once((const void*)attn_fwd_sm100, FWD_SMEM, &attr_mask));
   CUtensorMap tm;
-  STP_TRY(tensor_map_bf16(&tm, qkv_base, ld, s, ld, 64, T));
+  STP_TRY(tensor_map_heads(&tm, qkv_base, dh, nq + 2 * nkv, s, ld, T));
   FwdArgs a;
+  a.dh = dh;
+  a.causal = causal;
   a.s = s;
   a.nq = nq;
   a.nkv = nkv;
   a.ldo = ldo;
   a.o = o;
   a.lse = lse;
-  a.scale_log2 = LOG2E / sqrtf((float)D);
+  a.scale_log2 = LOG2E / sqrtf((float)dh);
   attn_fwd_sm100<<<dim3(nq, (s + T - 1) / T), FWD_THREADS, FWD_SMEM, st>>>(tm, a);
   count_launch();
   STP_LAUNCH_CHECK();

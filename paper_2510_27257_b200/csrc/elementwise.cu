@@ -694,6 +694,9 @@ struct RopeKey {
   }
 };
 
+stp_status rope_with_table(int dtype, int backward, int64_t s, int64_t ld, int64_t col0, int nh, int d,
+                           const float2* tab, void* x, cudaStream_t st);
+
 stp_status rope(int dtype, int backward, int64_t s, int64_t ld, int64_t col0, int nh, int d, float theta,
                 int64_t pos0, void* x, cudaStream_t st) {
   STP_CHECK_ARG(d % 8 == 0, "head_dim % 8 == 0");
@@ -717,6 +720,13 @@ stp_status rope(int dtype, int backward, int64_t s, int64_t ld, int64_t col0, in
       tab = it->second;
     }
   }
+  return rope_with_table(dtype, backward, s, ld, col0, nh, d, tab, x, st);
+}
+
+// Rotate-half RoPE with a caller-built cos/sin table [s][d/2] (1-D positions
+// above; the 2-D vision table of vit.cu).
+stp_status rope_with_table(int dtype, int backward, int64_t s, int64_t ld, int64_t col0, int nh, int d,
+                           const float2* tab, void* x, cudaStream_t st) {
   return STP_DISPATCH_DTYPE(dtype, [&] {
     constexpr int VN = Vec<T>::N;
     if ((d / 2) % VN == 0 && ld % VN == 0 && col0 % VN == 0 && (reinterpret_cast<uintptr_t>(x) & 15) == 0)

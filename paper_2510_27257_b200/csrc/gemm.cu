@@ -765,6 +765,38 @@ stp_status tensor_map(CUtensorMap* out, const void* ptr, int64_t d0, int64_t d1,
   return STP_OK;
 }
 
+// 3-D bf16 tensor map over attention heads: dims {dh (contiguous), heads,
+// rows}, strides {dh, ld} elements, box {64, 1, box_rows}, 128-byte swizzle.
+// A box at column 64 of a head with dh < 128 reads zeros beyond dh (OOB fill),
+// so a d = 80 head lands in shared memory as a zero-padded 128-column tile.
+stp_status tensor_map_heads_impl(CUtensorMap* out, const void* ptr, int dh, int heads, int64_t rows, int64_t ld,
+                                 int box_rows) {
+  thread_local std::unordered_map<MapKey, CUtensorMap, MapKeyHash> cache;
+  MapKey key{ptr, -(int64_t)dh, (int64_t)heads * (1ll << 32) + rows, ld, 64, box_rows};
+  auto it = cache.find(key);
+  if (it != cache.end()) {
+    *out = it->second;
+    return STP_OK;
+  }
+  auto enc = get_encode();
+  if (!enc) return fail(STP_ECUDA, "cuTensorMapEncodeTiled unavailable");
+  cuuint64_t dims[3] = {(cuuint64_t)dh, (cuuint64_t)heads, (cuuint64_t)rows};
+  cuuint64_t strides[2] = {(cuuint64_t)dh * 2, (cuuint64_t)(ld * 2)};
+  cuuint32_t box[3] = {64, 1, (cuuint32_t)box_rows};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = enc(out, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(ptr), dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    set_error("cuTensorMapEncodeTiled (heads) failed (%d): dh=%d heads=%d rows=%lld ld=%lld", (int)r, dh, heads,
+              (long long)rows, (long long)ld);
+    return STP_ECUDA;
+  }
+  if (cache.size() > 4096) cache.clear();
+  cache.emplace(key, *out);
+  return STP_OK;
+}
+
 // One tile counter per stream (GEMMs on one stream run in order; the last
 // fetch of each launch resets its counter to 0).
 // Counter blocks are kept per device (a thread that alternates devices
@@ -1064,6 +1096,10 @@ stp_status gemm_f32(int layout, int epi, int64_t M, int64_t N, int64_t K, const 
 // 2-D bf16 tensor map with 128-byte swizzle (shared with the attention kernels).
 stp_status tensor_map_bf16(CUtensorMap* out, const void* ptr, int64_t d0, int64_t d1, int64_t ld, int b0, int b1) {
   return tensor_map(out, ptr, d0, d1, ld, b0, b1);
+}
+stp_status tensor_map_heads(CUtensorMap* out, const void* ptr, int dh, int heads, int64_t rows, int64_t ld,
+                            int box_rows) {
+  return tensor_map_heads_impl(out, ptr, dh, heads, rows, ld, box_rows);
 }
 
 stp_status gemm_dispatch(int dtype, int layout, int epi, int64_t M, int64_t N, int64_t K, const void* A,

@@ -286,7 +286,11 @@ struct Lane {
 
 }  // namespace
 
-stp_status schedule_expand(const Schedule& s, int d, const std::vector<int>& lay, std::vector<stp_unit>& units) {
+// vit_first (MLLM; reading V5): virtual stage 0 holds the
+// ViT layers 0..lay[0]-1 and ends its forward with F_MERGE (2x2 merger + text
+// embedding -> LM input); its backward starts with B_MERGE / W_MERGE.
+stp_status schedule_expand(const Schedule& s, int d, const std::vector<int>& lay, std::vector<stp_unit>& units,
+                           bool vit_first) {
   const int kind = s.kind, p = s.pp;
   const int V = sched_n_vstages(kind, p);
   STP_CHECK_ARG((int)lay.size() == V, "layers_per_vstage must have pp*vpp entries");
@@ -328,6 +332,7 @@ stp_status schedule_expand(const Schedule& s, int d, const std::vector<int>& lay
       heavy.push_back({STP_U_F_ATTN, l});
       heavy.push_back({STP_U_F_MLP, l});
     }
+    if (vs == 0 && vit_first) heavy.push_back({STP_U_F_MERGE, -1});
     if (vs == V - 1) heavy.push_back({STP_U_F_HEAD, -1});
     auto last = std::make_shared<int>(-1);
     keep.push_back(last);
@@ -354,6 +359,7 @@ stp_status schedule_expand(const Schedule& s, int d, const std::vector<int>& lay
     std::vector<std::pair<int, int>> wl;
     const int l0 = first_layer(vs), nl = lay[vs];
     if (vs == V - 1) wl.push_back({STP_U_W_HEAD, -1});
+    if (vs == 0 && vit_first) wl.push_back({STP_U_W_MERGE, -1});
     for (int l = l0 + nl - 1; l >= l0; --l) {
       wl.push_back({STP_U_W_MLP, l});
       wl.push_back({STP_U_W_ATTN, l});
@@ -367,6 +373,7 @@ stp_status schedule_expand(const Schedule& s, int d, const std::vector<int>& lay
     const int l0 = first_layer(vs), nl = lay[vs];
     std::vector<std::pair<int, int>> heavy;
     if (vs == V - 1) heavy.push_back({STP_U_B_HEAD, -1});
+    if (vs == 0 && vit_first) heavy.push_back({STP_U_B_MERGE, -1});
     for (int l = l0 + nl - 1; l >= l0; --l) {
       heavy.push_back({STP_U_B_MLP, l});
       heavy.push_back({STP_U_B_ATTN, l});
@@ -464,10 +471,11 @@ int schedule_stash_slots(const Schedule& s, int d) {
   return best;
 }
 
-std::string schedule_text(const Schedule& s, const int* lay) {
+std::string schedule_text(const Schedule& s, const int* lay, bool vit_first) {
   std::string out;
   char buf[256];
-  snprintf(buf, sizeof(buf), "sched %s p %d v %d t %d m %d\n", kind_name(s.kind), s.pp, s.vpp, s.tp, s.m);
+  snprintf(buf, sizeof(buf), "sched %s p %d v %d t %d m %d%s\n", kind_name(s.kind), s.pp, s.vpp, s.tp, s.m,
+           vit_first ? " mllm" : "");
   out += buf;
   const int V = sched_n_vstages(s.kind, s.pp);
   std::vector<int> layv;
@@ -483,7 +491,7 @@ std::string schedule_text(const Schedule& s, const int* lay) {
     }
     if (lay) {
       std::vector<stp_unit> units;
-      if (schedule_expand(s, d, layv, units) != STP_OK) return std::string();
+      if (schedule_expand(s, d, layv, units, vit_first) != STP_OK) return std::string();
       for (size_t j = 0; j < units.size(); ++j) {
         const auto& u = units[j];
         snprintf(buf, sizeof(buf), "U %zu %d %d %d %d %d %d %d %d\n", j, u.action, u.stream, u.op, u.layer, u.chunk,
@@ -545,13 +553,13 @@ stp_status stp_schedule_actions(const stp_schedule* s, int32_t r, stp_action* bu
   return STP_OK;
 }
 
-stp_status stp_schedule_units(const stp_schedule* s, int32_t r, const int32_t* lay, stp_unit* buf, int32_t cap,
-                              int32_t* n_out) {
+static stp_status units_impl(const stp_schedule* s, int32_t r, const int32_t* lay, bool vit_first, stp_unit* buf,
+                             int32_t cap, int32_t* n_out) {
   if (!s || !n_out || !lay) return stp::fail(STP_EINVAL, "NULL handle / layers / n_out");
   if (r < 0 || r >= s->s.pp) return stp::fail(STP_EINVAL, "pp_rank out of range");
   std::vector<int> layv(lay, lay + stp::sched_n_vstages(s->s.kind, s->s.pp));
   std::vector<stp_unit> u;
-  stp_status st = stp::schedule_expand(s->s, r, layv, u);
+  stp_status st = stp::schedule_expand(s->s, r, layv, u, vit_first);
   if (st != STP_OK) return st;
   *n_out = (int32_t)u.size();
   if (cap < (int32_t)u.size()) return stp::fail(STP_ECAPACITY, "buffer too small");
@@ -559,15 +567,35 @@ stp_status stp_schedule_units(const stp_schedule* s, int32_t r, const int32_t* l
   return STP_OK;
 }
 
-stp_status stp_schedule_serialize(const stp_schedule* s, const int32_t* lay, char* buf, int64_t cap, int64_t* n_out) {
+stp_status stp_schedule_units(const stp_schedule* s, int32_t r, const int32_t* lay, stp_unit* buf, int32_t cap,
+                              int32_t* n_out) {
+  return units_impl(s, r, lay, false, buf, cap, n_out);
+}
+
+stp_status stp_schedule_units_mllm(const stp_schedule* s, int32_t r, const int32_t* lay, stp_unit* buf, int32_t cap,
+                                   int32_t* n_out) {
+  return units_impl(s, r, lay, true, buf, cap, n_out);
+}
+
+static stp_status serialize_impl(const stp_schedule* s, const int32_t* lay, bool vit_first, char* buf, int64_t cap,
+                                 int64_t* n_out) {
   if (!s || !n_out) return stp::fail(STP_EINVAL, "NULL handle / n_out");
-  std::string t = stp::schedule_text(s->s, lay);
+  std::string t = stp::schedule_text(s->s, lay, vit_first);
   if (t.empty()) return STP_ESCHEDULE;
   *n_out = (int64_t)t.size();
   if (cap < (int64_t)t.size() + 1) return stp::fail(STP_ECAPACITY, "buffer too small");
   std::copy(t.begin(), t.end(), buf);
   buf[t.size()] = '\0';
   return STP_OK;
+}
+
+stp_status stp_schedule_serialize(const stp_schedule* s, const int32_t* lay, char* buf, int64_t cap, int64_t* n_out) {
+  return serialize_impl(s, lay, false, buf, cap, n_out);
+}
+
+stp_status stp_schedule_serialize_mllm(const stp_schedule* s, const int32_t* lay, char* buf, int64_t cap,
+                                       int64_t* n_out) {
+  return serialize_impl(s, lay, true, buf, cap, n_out);
 }
 
 stp_status stp_schedule_stash_slots(const stp_schedule* s, int32_t r, int32_t* n_out) {

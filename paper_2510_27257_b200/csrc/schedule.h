@@ -20,9 +20,10 @@ int sched_n_chunks(int kind);
 int sched_vstage(int kind, int p, int d, int c);
 int sched_vstage_device(int kind, int p, int vs);
 stp_status schedule_build(int p, int vpp, int tp, int m, int kind, Schedule& s);
-stp_status schedule_expand(const Schedule& s, int d, const std::vector<int>& lay, std::vector<stp_unit>& units);
+stp_status schedule_expand(const Schedule& s, int d, const std::vector<int>& lay, std::vector<stp_unit>& units,
+                           bool vit_first = false);
 int schedule_stash_slots(const Schedule& s, int d);
-std::string schedule_text(const Schedule& s, const int* lay);
+std::string schedule_text(const Schedule& s, const int* lay, bool vit_first = false);
 stp_status layer_split(int n_layers, int n_slots, int* out);
 
 }  // namespace stp

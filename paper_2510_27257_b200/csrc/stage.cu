@@ -61,11 +61,11 @@ stp_status ce_grad(int dtype, int64_t s, int64_t Vl, void* logits, int64_t ld, c
                    const float* lse, float scale, cudaStream_t st);
 stp_status colsum_acc(int dtype, int64_t rows, int64_t n, const void* X, int64_t ld, float* acc, cudaStream_t st);
 stp_status add(int dtype, int64_t n, const void* a, const void* b, void* out, cudaStream_t st);
-stp_status attn_fwd(int dtype, int64_t s, int nq, int nkv, int d, const void* q, const void* k, const void* v,
-                    int64_t ld, void* o, int64_t ldo, float* lse, cudaStream_t st);
-stp_status attn_bwd(int dtype, int64_t s, int nq, int nkv, int d, const void* q, const void* k, const void* v,
-                    int64_t ld, const void* o, int64_t ldo, const void* dout, const float* lse, void* dq, void* dk,
-                    void* dv, int64_t ldd, void* ws, cudaStream_t st);
+stp_status attn_fwd(int dtype, int64_t s, int nq, int nkv, int d, int causal, const void* q, const void* k,
+                    const void* v, int64_t ld, void* o, int64_t ldo, float* lse, cudaStream_t st);
+stp_status attn_bwd(int dtype, int64_t s, int nq, int nkv, int d, int causal, const void* q, const void* k,
+                    const void* v, int64_t ld, const void* o, int64_t ldo, const void* dout, const float* lse,
+                    void* dq, void* dk, void* dv, int64_t ldd, void* ws, cudaStream_t st);
 int64_t attn_bwd_ws_bytes(int64_t s, int nq, int nkv, int d);
 // copy-engine TP transport (tpcomm.cu)
 stp_status tp_signal(uint32_t* const* dst, int n, uint32_t val, cudaStream_t st);
@@ -625,7 +625,7 @@ stp_status unit_compute(stp_stage* S, const stp_unit& u) {
                             P(S, I.wqkv), h, L.qkv, S->qkv_w, bias ? P(S, I.bqkv) : nullptr, nullptr, 0, mc, st));
       STP_TRY(rope(dt, 0, s, S->qkv_w, 0, (int)(S->qh + S->kh), (int)S->d, S->mc.rope_theta, 0, L.qkv, st));
       const uint8_t* q = (const uint8_t*)L.qkv;
-      STP_TRY(attn_fwd(dt, s, (int)S->qh, (int)S->kh, (int)S->d, q, q + S->qh * S->d * S->es,
+      STP_TRY(attn_fwd(dt, s, (int)S->qh, (int)S->kh, (int)S->d, 1, q, q + S->qh * S->d * S->es,
                        q + (S->qh + S->kh) * S->d * S->es, S->qkv_w, L.o, S->o_w, L.lse, st));
       return gemm_dispatch(dt, STP_GEMM_NT, STP_EPI_STORE, s, h, S->o_w, L.o, S->o_w, P(S, I.wo), S->o_w, S->pf, h,
                            nullptr, nullptr, 0, mc, st);
@@ -684,7 +684,7 @@ stp_status unit_compute(stp_stage* S, const stp_unit& u) {
       const uint8_t* q = (const uint8_t*)L.qkv;
       uint8_t* dq = (uint8_t*)L.dqkv;
       const int64_t ko = S->qh * S->d * S->es, vo = (S->qh + S->kh) * S->d * S->es;
-      STP_TRY(attn_bwd(dt, s, (int)S->qh, (int)S->kh, (int)S->d, q, q + ko, q + vo, S->qkv_w, L.o, S->o_w,
+      STP_TRY(attn_bwd(dt, s, (int)S->qh, (int)S->kh, (int)S->d, 1, q, q + ko, q + vo, S->qkv_w, L.o, S->o_w,
                        S->dtmp_o, L.lse, dq, dq + ko, dq + vo, S->qkv_w, S->attn_ws, st));
       STP_TRY(rope(dt, 1, s, S->qkv_w, 0, (int)(S->qh + S->kh), (int)S->d, S->mc.rope_theta, 0, L.dqkv, st));
       return gemm_dispatch(dt, STP_GEMM_NN, STP_EPI_STORE, s, h, S->qkv_w, L.dqkv, S->qkv_w, P(S, I.wqkv), h, S->pb,

@@ -85,6 +85,47 @@ def attn_bwd(qkv, nq, nkv, d, o, dout, lse, dqkv):
          ptr(ws), stream())
 
 
+def attn_full_fwd(qkv, nh, d, o, lse):
+    """Bidirectional attention (ViT): qkv [s, 3 nh d] (q | k | v); o [s, nh d]; lse fp32 [nh, s]."""
+    call("stp_op_attn_full_fwd", dt(qkv), qkv.shape[0], nh, d, ptr(qkv), qkv.stride(0), ptr(o), o.stride(0),
+         ptr(lse), stream())
+
+
+def attn_full_bwd(qkv, nh, d, o, dout, lse, dqkv):
+    s = qkv.shape[0]
+    ws = torch.empty(max(1, lib.stp_op_attn_bwd_ws_bytes(s, nh, nh, d)), dtype=torch.uint8, device=qkv.device)
+    call("stp_op_attn_full_bwd", dt(qkv), s, nh, d, ptr(qkv), qkv.stride(0), ptr(o), o.stride(0), ptr(dout),
+         ptr(lse), ptr(dqkv), dqkv.stride(0), ptr(ws), stream())
+
+
+def layernorm_fwd(x, gamma, beta, eps, y, mean=None, rstd=None, resid=None, x_out=None):
+    rows, h = x.shape
+    call("stp_op_layernorm_fwd", dt(x), rows, h, ptr(x), ptr(resid), ptr(x_out), ptr(gamma), ptr(beta), eps,
+         ptr(y), ptr(mean), ptr(rstd), stream())
+
+
+def layernorm_bwd(dy, x, gamma, mean, rstd, dx, dgamma_acc=None, dbeta_acc=None, dres=None):
+    rows, h = x.shape
+    call("stp_op_layernorm_bwd", dt(x), rows, h, ptr(dy), ptr(x), ptr(gamma), ptr(mean), ptr(rstd), ptr(dres),
+         ptr(dx), ptr(dgamma_acc), ptr(dbeta_acc), stream())
+
+
+QGELU, GELU = 0, 1
+
+
+def act_fwd(kind, a, y):
+    call("stp_op_act_fwd", dt(a), kind, a.numel(), ptr(a), ptr(y), stream())
+
+
+def act_bwd(kind, dy, a, da):
+    call("stp_op_act_bwd", dt(a), kind, a.numel(), ptr(dy), ptr(a), ptr(da), stream())
+
+
+def rope2d(x, col0, n_heads, d, grid_w, theta=10000.0, backward=False):
+    call("stp_op_rope2d", dt(x), int(backward), x.shape[0], x.stride(0), col0, n_heads, d, grid_w, theta, ptr(x),
+         stream())
+
+
 def embed_fwd(tok, E, v0, out):
     s, h = out.shape
     call("stp_op_embed_fwd", dt(E), s, h, ptr(tok), v0, E.shape[0], ptr(E), ptr(out), stream())

@@ -1,0 +1,171 @@
+"""ViT first-chunk kernels (MLLM cfg5) vs the oracle's
+sub-functions (oracle/vit.py) on the same seeded inputs: LayerNorm fwd/bwd
+with the fused residual add and the parameter gradients, QuickGELU / GELU,
+the 2-D vision RoPE, bidirectional attention at d = 80 (tcgen05 for bf16,
+SIMT for fp32) and d = 128 without the causal mask.
+
+Tolerances as tests/test_gpu_ops.py: fp32 kernels
+against the fp64 oracle 1e-5 relative Frobenius (attention 2e-5 / 5e-5);
+bf16 storage 1e-2 (attention 2e-2 forward, 3e-2 backward), the oracle fed the
+same bf16-rounded inputs."""
+import numpy as np
+import pytest
+import torch
+
+from oracle import model as om
+from oracle import vit as ov
+
+pytestmark = pytest.mark.gpu
+
+DT = {"f32": torch.float32, "bf16": torch.bfloat16}
+TOL = {"f32": 1e-5, "bf16": 1e-2}
+
+
+def _ops():
+    from paper_2510_27257_b200 import ops
+    return ops
+
+
+def _in(shape, seed, dt, scale=1.0, offset=0.0):
+    a = offset + scale * np.random.default_rng(seed).standard_normal(shape)
+    t = torch.from_numpy(a).to(DT[dt])
+    return t.double().numpy(), t.cuda()
+
+
+def _np(t):
+    return t.double().cpu().numpy()
+
+
+def _rel(got, ref):
+    return np.linalg.norm(got - ref) / max(np.linalg.norm(ref), 1e-30)
+
+
+@pytest.mark.parametrize("dt", ["f32", "bf16"])
+@pytest.mark.parametrize("rows,h", [(1, 64), (37, 136), (784, 1280), (3136, 1280)])
+def test_layernorm_fwd_bwd(dt, rows, h):
+    ops = _ops()
+    x, dx_ = _in((rows, h), 1, dt, 1.0, 0.5)
+    r, dr_ = _in((rows, h), 2, dt)
+    g, dg_ = _in((h,), 3, dt, 0.1, 1.0)
+    b, db_ = _in((h,), 4, dt, 0.1)
+    xin = x + r
+    y_ref, _, _ = ov.layernorm_fwd(xin, g, b, 1e-6)
+    y = torch.empty_like(dx_)
+    xo = torch.empty_like(dx_)
+    mu = torch.empty(rows, dtype=torch.float32, device="cuda")
+    rs = torch.empty(rows, dtype=torch.float32, device="cuda")
+    ops.layernorm_fwd(dx_, dg_, db_, 1e-6, y, mu, rs, resid=dr_, x_out=xo)
+    torch.cuda.synchronize()
+    assert _rel(_np(xo), xin) <= TOL[dt]
+    assert _rel(_np(y), y_ref) <= TOL[dt]
+    # statistics of the stored (rounded) residual sum
+    xs = _np(xo)
+    _, xh_ref, r_ref = ov.layernorm_fwd(xs, g, b, 1e-6)
+    assert np.abs(_np(mu) - xs.mean(axis=1)).max() <= 1e-5 * (1 + np.abs(xs).max())
+    assert _rel(_np(rs), r_ref[:, 0]) <= 1e-5
+    dy, ddy = _in((rows, h), 5, dt)
+    dres, ddres = _in((rows, h), 6, dt)
+    dx_ref, dg_ref, db_ref = ov.layernorm_bwd(dy, xh_ref, g, r_ref)
+    dx = torch.empty_like(dx_)
+    dgacc = torch.zeros(h, dtype=torch.float32, device="cuda")
+    dbacc = torch.zeros(h, dtype=torch.float32, device="cuda")
+    ops.layernorm_bwd(ddy, xo, dg_, mu, rs, dx, dgacc, dbacc, dres=ddres)
+    torch.cuda.synchronize()
+    assert _rel(_np(dx), dx_ref + dres) <= TOL[dt]
+    assert _rel(_np(dgacc), dg_ref) <= 1e-5
+    assert _rel(_np(dbacc), db_ref) <= 1e-5
+
+
+@pytest.mark.parametrize("dt", ["f32", "bf16"])
+@pytest.mark.parametrize("kind", [0, 1])
+def test_activations(dt, kind):
+    ops = _ops()
+    a, da_ = _in((301, 5120 // 4), 7, dt, 2.0)
+    y = torch.empty_like(da_)
+    ops.act_fwd(kind, da_, y)
+    fwd, bwd = (ov.qgelu_fwd, ov.qgelu_bwd) if kind == 0 else (ov.gelu_fwd, ov.gelu_bwd)
+    dy, ddy = _in(a.shape, 8, dt)
+    out = torch.empty_like(da_)
+    ops.act_bwd(kind, ddy, da_, out)
+    torch.cuda.synchronize()
+    assert _rel(_np(y), fwd(a)) <= TOL[dt]
+    assert _rel(_np(out), bwd(dy, a)) <= TOL[dt]
+
+
+@pytest.mark.parametrize("dt", ["f32", "bf16"])
+@pytest.mark.parametrize("gh,gw,nh,d", [(4, 6, 2, 16), (8, 8, 3, 80), (56, 56, 2, 80)])
+def test_rope2d(dt, gh, gw, nh, d):
+    ops = _ops()
+    s = gh * gw
+    ld = 3 * nh * d
+    x, dx_ = _in((s, ld), 9, dt)
+    cos, sin = ov.vit_rope_tables(gh, gw, d)
+    ref = x.copy()
+    for c0 in (0, nh * d):   # q and k heads rotated, v untouched
+        ref[:, c0:c0 + nh * d] = om.rope_fwd(x[:, c0:c0 + nh * d].reshape(s, nh, d), cos, sin).reshape(s, -1)
+    ops.rope2d(dx_, 0, 2 * nh, d, gw)
+    torch.cuda.synchronize()
+    tol = 2e-5 if dt == "f32" else TOL[dt]
+    assert _rel(_np(dx_), ref) <= tol
+    # backward of the forward = identity up to rounding; and against the oracle's rope_bwd
+    g_ = dx_.clone()
+    ops.rope2d(g_, 0, 2 * nh, d, gw, backward=True)
+    torch.cuda.synchronize()
+    back = ref.copy()
+    back[:, :2 * nh * d] = om.rope_bwd(_np(dx_)[:, :2 * nh * d].reshape(s, 2 * nh, d), cos, sin).reshape(s, -1)
+    assert _rel(_np(g_), back) <= tol
+
+
+ATT = [(1, 2, 80), (100, 2, 80), (200, 3, 80), (577, 2, 80), (3136, 2, 80), (300, 2, 128), (1024, 4, 128)]
+
+
+@pytest.mark.parametrize("dt", ["f32", "bf16"])
+@pytest.mark.parametrize("s,nh,d", ATT)
+def test_attention_full_fwd_bwd(dt, s, nh, d):
+    if dt == "f32" and s > 600:
+        pytest.skip("fp32 SIMT attention is the small-shape parity path")
+    ops = _ops()
+    W = 3 * nh * d
+    qkv, dqkv_ = _in((s, W), 10, dt)
+    q = qkv[:, :nh * d].reshape(s, nh, d)
+    k = qkv[:, nh * d:2 * nh * d].reshape(s, nh, d)
+    v = qkv[:, 2 * nh * d:].reshape(s, nh, d)
+    o_ref, lse_ref = ov.attention_full_fwd(q, k, v)
+    o = torch.empty(s, nh * d, dtype=DT[dt], device="cuda")
+    lse = torch.empty(nh, s, dtype=torch.float32, device="cuda")
+    ops.attn_full_fwd(dqkv_, nh, d, o, lse)
+    torch.cuda.synchronize()
+    tol = 2e-5 if dt == "f32" else 2e-2
+    assert _rel(_np(o), o_ref.reshape(s, -1)) <= tol
+    assert np.abs(_np(lse) - lse_ref).max() <= (1e-4 if dt == "f32" else 2e-2)
+    do, ddo = _in((s, nh * d), 11, dt)
+    og = _np(o).reshape(s, nh, d)
+    dq, dk, dv = ov.attention_full_bwd(do.reshape(s, nh, d), q, k, v, og)
+    dqkv = torch.full((s, W), float("nan"), dtype=DT[dt], device="cuda")
+    ops.attn_full_bwd(dqkv_, nh, d, o, ddo, lse, dqkv)
+    torch.cuda.synchronize()
+    got = _np(dqkv)
+    tol = 5e-5 if dt == "f32" else 3e-2
+    assert _rel(got[:, :nh * d], dq.reshape(s, -1)) <= tol
+    assert _rel(got[:, nh * d:2 * nh * d], dk.reshape(s, -1)) <= tol
+    assert _rel(got[:, 2 * nh * d:], dv.reshape(s, -1)) <= tol
+
+
+def test_causal_attention_unchanged_by_3d_maps():
+    """The LM path (causal, d = 128, GQA) after the switch to per-head 3-D
+    tensor maps: bitwise repeatable and equal to the oracle (ragged s)."""
+    ops = _ops()
+    s, nq, nkv, d = 777, 7, 1, 128
+    qkv, dqkv_ = _in((s, (nq + 2 * nkv) * d), 12, "bf16")
+    o1 = torch.empty(s, nq * d, dtype=torch.bfloat16, device="cuda")
+    o2 = torch.empty_like(o1)
+    lse = torch.empty(nq, s, dtype=torch.float32, device="cuda")
+    ops.attn_fwd(dqkv_, nq, nkv, d, o1, lse)
+    ops.attn_fwd(dqkv_, nq, nkv, d, o2, lse)
+    torch.cuda.synchronize()
+    assert torch.equal(o1, o2)
+    q = qkv[:, :nq * d].reshape(s, nq, d)
+    k = qkv[:, nq * d:(nq + nkv) * d].reshape(s, nkv, d)
+    v = qkv[:, (nq + nkv) * d:].reshape(s, nkv, d)
+    o_ref, _ = om.attention_fwd(q, k, v)
+    assert _rel(_np(o1), o_ref.reshape(s, -1)) <= 2e-2

@@ -79,3 +79,43 @@ def test_layer_split_matches_paper_rule():
     L.call("stp_layer_split", 28, 4, out4)
     assert list(out4) == [8, 8, 7, 5]
     assert L.lib.stp_layer_split(8, 8, out) == -1 and "IndivisibleLayers" in L.last_error()
+
+
+def _cpp_text_mllm(kind, p, m, t, lay):
+    L = _L()
+    h = C.c_void_p()
+    L.call("stp_build_schedule", p, 2, t, m, kind, C.byref(h))
+    try:
+        arr = (C.c_int32 * len(lay))(*lay)
+        n = C.c_int64()
+        assert L.lib.stp_schedule_serialize_mllm(h, arr, None, 0, C.byref(n)) == -8
+        buf = C.create_string_buffer(n.value + 1)
+        L.call("stp_schedule_serialize_mllm", h, arr, buf, n.value + 1, C.byref(n))
+        return buf.value.decode()
+    finally:
+        L.lib.stp_free_schedule(h)
+
+
+MLLM_GRID = [(k, p, m) for k in (sc.STP, sc.STP_NOSEP, sc.STP_NOBRAID, sc.ZB, sc.ONEF1B_I)
+             for p in (1, 2, 4) for m in (1, 4, 8, 16) if not (k == sc.ONEF1B_I and m % p)]
+
+
+@pytest.mark.parametrize("kind,p,m", MLLM_GRID)
+def test_mllm_schedule_text_bit_exact(kind, p, m):
+    """MLLM expansion (ViT layers + merger on vs 0): C++ == oracle, and
+    vs 0's lanes carry F_MERGE / B_MERGE / W_MERGE exactly once per microbatch."""
+    lay = [3] + [1 + (m + i) % 3 for i in range(2 * p - 1)]
+    txt = _cpp_text_mllm(kind, p, m, 2, lay)
+    assert txt == sc.serialize(kind, p, 2, 2, m, lay, vit_first=True)
+    assert txt.splitlines()[0].endswith(" mllm")
+    progs = sc.build_program(kind, p, m)
+    d0 = sc.vstage_device(kind, p, 0)[0]
+    us = sc.expand_units(kind, p, d0, progs[d0], lay, vit_first=True)
+    c0 = sc.vstage_device(kind, p, 0)[1]
+    for op in (sc.F_MERGE, sc.B_MERGE, sc.W_MERGE):
+        mbs = sorted(u[5] for u in us if u[2] == op)
+        assert mbs == list(range(1, m + 1)) and all(u[4] == c0 for u in us if u[2] == op)
+    # every ViT layer runs F / B / W once per microbatch on vs 0
+    for l in range(lay[0]):
+        for op in (sc.F_ATTN, sc.F_MLP, sc.B_ATTN, sc.B_MLP, sc.W_ATTN, sc.W_MLP):
+            assert sum(1 for u in us if u[2] == op and u[3] == l) == m

@@ -12,6 +12,11 @@ Configurations (--config; BASELINE.json configs[1..3]):
                   2x2 (the 4-GPU proxy), 4x2 (the configuration itself).
   cfg4            Qwen2.5-14B-shaped (reading Q13), seq 4096, 32
                   microbatches; 2x1, 2x2 (4-GPU proxy), 2x4 (8 GPUs).
+  cfg5            MLLM: ViT-600M (32 layers, 16 x 80 heads) + 2x2 merger on
+                  virtual stage 0, Qwen2-7B-shaped LM on the others,
+                  LM seq 8192 = 784 image + 7408 text tokens, 16 microbatches
+                  (8 at N=1, memory); 1x1, 2x1, 2x2 (4-GPU proxy), 4x2; TP comm
+                  over NCCL (the ViT phases' transport).
 Every config runs two virtual stages (V-shape) and the R-STP braided
 schedule in bf16; same model and global batch at every N of a config
 ("scaling": "strong"); --grid TxP / --model / --seq / --micro override.  A
@@ -61,7 +66,12 @@ CONFIGS = {
              {1: (1, 1), 2: (2, 1), 4: (2, 2), 8: (4, 2)}),
     "cfg4": ({2: "qwen2.5-14b", 4: "qwen2.5-14b", 8: "qwen2.5-14b"}, 4096, 32,
              {2: (2, 1), 4: (2, 2), 8: (2, 4)}),
+    # MLLM: ViT-600M + 2x2 merger on virtual stage 0, Qwen2-7B LM on the rest
+    # (P:L171), 3136 patches -> 784 image tokens + 7408 text tokens = 8192
+    "cfg5": ({1: "qwen2-7b", 2: "qwen2-7b", 4: "qwen2-7b", 8: "qwen2-7b"}, 8192, 16,
+             {1: (1, 1), 2: (2, 1), 4: (2, 2), 8: (4, 2)}),
 }
+MLLM_CONFIGS = {"cfg5"}
 MODEL_DESC = {"qwen2-7b": "Qwen2-7B-shaped (h3584 L28 28/4 heads d128 I18944 V152064)",
               "qwen2-7b-tp8": "Qwen2-7B-shaped TP=8 variant (h3584 L28 32/8 heads d128 I18944 V152064, reading Q14)",
               "qwen2.5-14b": "Qwen2.5-14B-shaped (h5120 L48 40/8 heads d128 I13824 V152064, reading Q13)"}
@@ -82,6 +92,11 @@ def resolve(args):
     if not args.grid:
         t, p = grids.get(n, (n, 1))
         args.grid = f"{t}x{p}"
+    if args.config in MLLM_CONFIGS:
+        if n == 1 and args.m == m:
+            args.m = 8  # 180 GB: the m = 16 stash of the one-GPU proxy does not fit
+        if n > 1:
+            os.environ.setdefault("STP_TP_TRANSPORT", "nccl")
     return args
 
 
@@ -93,6 +108,16 @@ def model_cfg(args):
     if args.layers:
         cfg = dataclasses.replace(cfg, n_layers=args.layers)
     return cfg
+
+
+def vit_flops_per_mb(v):
+    """Algorithmic training FLOPs of one image (ViT + merger, fwd + bwd):
+    6 x linear MACs (patch embed, per layer QKV / O / MLP, merger) + 12 L sv^2 hv
+    for bidirectional attention (QK^T and PV, 3x for fwd + bwd)."""
+    sv, hv, L = v.seq, v.hidden, v.n_layers
+    lin = sv * v.patch_dim * hv + L * sv * (4 * hv * hv + 2 * hv * v.mlp) + \
+        v.n_img * (16 * hv * hv + 4 * hv * v.out_hidden)
+    return 6.0 * lin + 12.0 * L * sv * sv * hv
 
 
 def gemm_flops_per_token(cfg):
@@ -231,8 +256,12 @@ def reference_arm(args, full_cfg):
 
 def workload_config(args, cfg, tp_pp):
     t, p = tp_pp
-    return {"workload": f"{args.config}: {args.model}-shaped s{cfg.seq} m{args.m} tp{t}pp{p}vpp2 ({args.sched})",
-            "model": MODEL_DESC.get(args.model, args.model) + (f", {cfg.n_layers} layers" if args.layers else "")
+    mllm = args.config in MLLM_CONFIGS
+    return {"workload": f"{args.config}: {'vit-600m + ' if mllm else ''}{args.model}-shaped s{cfg.seq} m{args.m} "
+                        f"tp{t}pp{p}vpp2 ({args.sched})",
+            "model": ("ViT-600M (32 L, h1280, 16x80 heads, MLP 5120) + 2x2 merger on vs 0, 3136 patches -> 784 "
+                      "image tokens; LM " if mllm else "")
+            + MODEL_DESC.get(args.model, args.model) + (f", {cfg.n_layers} layers" if args.layers else "")
             + ", random init",
             "global_batch": args.m, "seq_len": cfg.seq, "parallelism": f"tp{t}pp{p}vpp2",
             "schedule": args.sched,
@@ -284,20 +313,31 @@ def ours(args):
         raise SystemExit(f"--grid {args.grid} needs {t * p} ranks, have {world}")
     tp_rank, pp_rank = rank % t, rank // t
     cfg = model_cfg(args)
+    vit = si.VIT_600M if args.config in MLLM_CONFIGS else None
+    patches = None
+    if vit is not None:
+        # random patches [m, 3136, 1176], seeded, on the device
+        gp = torch.Generator(device=f"cuda:{local}").manual_seed(4321)
+        patches = torch.randn((args.m, vit.seq, vit.patch_dim), generator=gp, device=f"cuda:{local}",
+                              dtype=torch.float32).to(torch.bfloat16)
+
     def make_stage(sched):
         uid = broadcast_nccl_id() if world > 1 else None
         stg = Stage(cfg, tp=t, pp=p, n_micro=args.m, tp_rank=tp_rank, pp_rank=pp_rank, dtype="bf16",
-                    sched=sched, device=local, world_nccl_id=uid)
+                    sched=sched, device=local, world_nccl_id=uid, vit=vit)
         # random-init weights on the device (seeded per tensor), N(0, 0.02^2); gammas 1
         g = torch.Generator(device=f"cuda:{local}")
         for i, (name, prm) in enumerate(zip(stg.names, stg.params)):
             g.manual_seed(1000 * rank + i)
-            if name.endswith(("ln1", "ln2")) or name == "final_ln":
+            short = name.rsplit(".", 1)[-1]
+            if name.endswith(("ln1", "ln2")) or name == "final_ln" or short.endswith("_g"):
                 prm.fill_(1.0)
-            elif name.endswith("bqkv"):
+            elif name.endswith("bqkv") or short.endswith("_b") or short in ("bo", "b1", "b2"):
                 prm.zero_()
             else:
                 prm.copy_(torch.randn(prm.shape, generator=g, device=prm.device, dtype=torch.float32) * 0.02)
+        if patches is not None:
+            stg.bind_images(patches)
         return stg
 
     progress(f"init stage tp{t} pp{p} {args.sched}")
@@ -367,6 +407,9 @@ def ours(args):
     step_ms, e2e_s, exp_frac, bub_frac = vals.tolist()
     tokens = args.m * cfg.seq
     value = tokens / (step_ms / 1e3)
+    if vit is not None:
+        progress(f"MLLM: {vit_flops_per_mb(vit) / 1e12:.2f} TFLOP per image (ViT + merger) beside "
+                 f"{gemm_flops_per_token(cfg) * cfg.seq / 1e12:.1f} TFLOP per LM microbatch")
     if rank == 0:
         peaks = {}
         try:

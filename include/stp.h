@@ -191,6 +191,42 @@ stp_status stp_init_stage(const stp_model_cfg* model, const stp_parallel_cfg* pa
                           const void* world_nccl_id, int32_t cuda_device,
                           stp_stage** out);
 
+/* ---- MLLM: the ViT encoder as the heterogeneous first virtual stage ----
+ * PAPER.md §5: "In MLLM scenarios, the ViT encoder is assigned to the
+ * first virtual stage on device 0, and the LM model is uniformly distributed
+ * across the remaining virtual stages"; Table 3 P:L231-263.  Vision tower =
+ * Qwen2-VL's (LayerNorm, bidirectional attention with 2-D RoPE, QuickGELU
+ * MLP, biases) + 2x2 patch merger (LayerNorm, GELU MLP) as oracle/vit.py
+ * restates it (readings V1-V5). */
+typedef struct {
+  int32_t hidden, n_layers, n_heads, head_dim, mlp, patch_dim;
+  int32_t grid_h, grid_w;   /* image of grid_h x grid_w patches (both even),
+                               rows in 2x2 merge-window order */
+  float ln_eps, rope_theta; /* 1e-6, 10000 for Qwen2-VL */
+} stp_vit_cfg;
+
+/* As stp_init_stage, with virtual stage 0 = ViT + merger and the LM on
+ * virtual stages 1..pp*vpp-1.  model->seq is the LM sequence: the first
+ * n_img = grid_h*grid_w/4 rows are the merged image tokens, the rest text;
+ * model->n_layers counts LM layers only.  par->layers_per_vstage (if given)
+ * = [n_vit, LM layers of vs 1, ...]; NULL = [vit->n_layers, stp_layer_split(
+ * n_layers, pp*vpp-1)] ("the last virtual stage also contains two
+ * fewer layers").  TP shards the ViT like the LM (heads, MLP and merger
+ * columns; sequence-parallel residual shards of grid_h*grid_w/tp rows).
+ * Requires STP_TP_TRANSPORT=nccl when tp > 1 (STP_EUNSUPPORTED otherwise),
+ * n_heads, mlp, 4*hidden % tp == 0, grid_h*grid_w % (4*tp) == 0, n_img <
+ * model->seq, head_dim in {80, 128} for bf16. */
+stp_status stp_init_stage_mllm(const stp_model_cfg* model, const stp_vit_cfg* vit,
+                               const stp_parallel_cfg* par, const void* world_nccl_id,
+                               int32_t cuda_device, stp_stage** out);
+/* Bind the image patches for the next steps: DEVICE [n_micro, grid_h*grid_w,
+ * patch_dim] in the model dtype (caller-owned, borrowed until rebound).  Only
+ * the rank holding virtual stage 0 reads them.  For an MLLM stage the token
+ * rows [n_micro, seq] of stp_train_step carry the text tokens at positions
+ * n_img..seq-1 (positions 0..n_img-1 are ignored); targets cover all seq
+ * positions. */
+stp_status stp_stage_bind_images(stp_stage* st, const void* d_patches);
+
 /* Parameter layout of a stage: for every layer held
  * by this rank (virtual stages of chunk 0 then chunk 1; layers ascending):
  *   ln1[h], wqkv[(nq/t+2*nkv/t)*d, h], bqkv[(nq/t+2*nkv/t)*d] (if qkv_bias),

@@ -49,6 +49,11 @@ class ParallelCfg(C.Structure):
                 ("pp_rank", i32), ("layers_per_vstage", C.POINTER(C.c_int32)), ("sched_kind", i32)]
 
 
+class VitCfg(C.Structure):
+    _fields_ = [("hidden", i32), ("n_layers", i32), ("n_heads", i32), ("head_dim", i32), ("mlp", i32),
+                ("patch_dim", i32), ("grid_h", i32), ("grid_w", i32), ("ln_eps", f32), ("rope_theta", f32)]
+
+
 class StepStats(C.Structure):
     _fields_ = [("step_ms", C.c_double), ("exposed_tp_ms", C.c_double), ("pp_bubble_ms", C.c_double),
                 ("compute_busy_ms", C.c_double), ("peak_act_bytes", i64), ("n_units", i32),
@@ -74,6 +79,9 @@ _SIGS = {
     "stp_nccl_id_bytes": (i32, []),
     "stp_nccl_get_id": (i32, [vp]),
     "stp_init_stage": (i32, [C.POINTER(ModelCfg), C.POINTER(ParallelCfg), vp, i32, C.POINTER(vp)]),
+    "stp_init_stage_mllm": (i32, [C.POINTER(ModelCfg), C.POINTER(VitCfg), C.POINTER(ParallelCfg), vp, i32,
+                                  C.POINTER(vp)]),
+    "stp_stage_bind_images": (i32, [vp, vp]),
     "stp_stage_param_count": (i32, [vp, C.POINTER(i32)]),
     "stp_stage_param_info": (i32, [vp, i32, C.POINTER(cp), C.POINTER(i64), C.POINTER(i64), C.POINTER(i64)]),
     "stp_bind_params": (i32, [vp, i32, C.POINTER(vp), C.POINTER(vp)]),

@@ -79,6 +79,16 @@ stp_status tp_fused_bwd(int dtype, int64_t rows, int64_t h, const void* const* p
 stp_status rmsnorm_dgamma(int dtype, int64_t rows, int64_t h, const void* dy, const void* x, const float* rstd,
                           float* dgamma, cudaStream_t st);
 stp_status convert(int sd, int dd, int64_t n, const void* src, void* dst, cudaStream_t st);
+// ViT first chunk (vit.cu)
+stp_status layernorm_fwd(int dtype, int64_t rows, int64_t h, const void* x, const void* resid, void* x_out,
+                         const void* g, const void* b, float eps, void* y, float* mean, float* rstd, cudaStream_t st);
+stp_status layernorm_bwd(int dtype, int64_t rows, int64_t h, const void* dy, const void* x, const void* g,
+                         const float* mean, const float* rstd, const void* dres, void* dx, float* dg, float* db,
+                         cudaStream_t st);
+stp_status act_fwd(int dtype, int kind, int64_t n, const void* a, void* y, cudaStream_t st);
+stp_status act_bwd(int dtype, int kind, int64_t n, const void* dy, const void* a, void* da, cudaStream_t st);
+stp_status rope2d(int dtype, int backward, int64_t s, int64_t ld, int64_t col0, int nh, int d, int gw, float theta,
+                  void* x, cudaStream_t st);
 
 #define STP_NCCL_TRY(expr)                                                     \
   do {                                                                         \
@@ -104,6 +114,20 @@ struct LayerIdx {
   int ln1 = -1, wqkv = -1, bqkv = -1, wo = -1, ln2 = -1, wgu = -1, wd = -1;
 };
 
+// ViT layer parameters (oracle/vit.py names; TP shards as the LM's)
+struct VitIdx {
+  int ln1_g = -1, ln1_b = -1, wqkv = -1, bqkv = -1, wo = -1, bo = -1, ln2_g = -1, ln2_b = -1, w1 = -1, b1 = -1,
+      w2 = -1, b2 = -1;
+};
+
+// ViT layer stash: full-sequence [sv, .] buffers (after the all-gather) and
+// [sv/t, hv] residual shards, with the LayerNorm statistics of the shard rows
+struct VitSlotLayer {
+  void *xn = nullptr, *qkv = nullptr, *o = nullptr, *x1 = nullptr, *xn2 = nullptr, *a = nullptr, *hh = nullptr,
+       *xres = nullptr, *dy_attn = nullptr, *dqkv = nullptr, *dy_mlp = nullptr;
+  float *lse = nullptr, *mean1 = nullptr, *rstd1 = nullptr, *mean2 = nullptr, *rstd2 = nullptr;
+};
+
 struct SlotLayer {
   void *xn = nullptr, *qkv = nullptr, *o = nullptr, *x1 = nullptr, *xn2 = nullptr, *gu = nullptr, *hh = nullptr,
        *xres = nullptr, *dy_attn = nullptr, *dqkv = nullptr, *dy_mlp = nullptr;
@@ -116,6 +140,12 @@ struct Slot {
   std::vector<SlotLayer> L;
   void *xf = nullptr, *logits = nullptr, *dx0 = nullptr;
   float *rstdf = nullptr, *stats = nullptr, *stats_all = nullptr, *lse_ce = nullptr;
+  // ViT chunk (MLLM vs 0): layers, merger input / pre-activation / activation,
+  // the LM-input shard it produces, the all-gathered LM-input gradient and the
+  // running ViT residual gradient shard
+  std::vector<VitSlotLayer> V;
+  void *yq = nullptr, *z = nullptr, *gz = nullptr, *x_out = nullptr, *dylm = nullptr, *vdx = nullptr;
+  float *meanq = nullptr, *rstdq = nullptr;
   bool busy = false;
   int mb = -1;
   std::vector<cudaEvent_t> free_events;  // readers of the previous occupant
@@ -124,6 +154,7 @@ struct Slot {
 struct Chunk {
   int c = 0, vs = 0, l0 = 0, nl = 0;
   bool first = false, last = false;
+  bool vit = false;  // MLLM: virtual stage 0 = ViT + merger (layers l0..l0+nl-1 are ViT layers)
   std::vector<Slot> slots;
   std::map<int, int> mb2slot;
   size_t slot_bytes = 0;
@@ -147,6 +178,16 @@ struct stp_stage {
   std::map<int, stp::LayerIdx> lidx;  // global layer -> indices
   int p_embed = -1, p_final = -1, p_lm = -1;
   bool bound = false;
+  // MLLM (stp_init_stage_mllm): ViT dims, per rank
+  bool mllm = false;
+  stp_vit_cfg vc{};
+  int64_t nvit = 0, sv = 0, svl = 0, hv = 0, vnh = 0, vd = 0, vqkv_w = 0, vo_w = 0, vml = 0, vpd = 0, n_img = 0,
+          m4 = 0, m4l = 0;
+  std::map<int, stp::VitIdx> vidx;
+  int p_patch = -1, p_mln_g = -1, p_mln_b = -1, p_mw1 = -1, p_mb1 = -1, p_mw2 = -1, p_mb2 = -1;
+  const void* patches = nullptr;
+  void *vrtmp = nullptr, *vntmp = nullptr, *vdtmp_h = nullptr, *vdtmp_o = nullptr, *vdtmp_m = nullptr,
+       *vattn_ws = nullptr;
   // chunks
   std::vector<stp::Chunk> chunks;
   // streams / comms
@@ -250,7 +291,43 @@ struct Carver {
   }
 };
 
+void carve_vit_slot(stp_stage* S, const Chunk& C, Slot& sl, Carver& cv) {
+  const size_t es = S->es;
+  const int64_t sv = S->sv, hv = S->hv, vsh = S->svl * S->hv;
+  sl.x_in = cv.take(vsh * es);
+  sl.dx_in = cv.take(S->sl * S->h * es);
+  sl.V.resize(C.nl);
+  for (int j = 0; j < C.nl; ++j) {
+    VitSlotLayer& L = sl.V[j];
+    L.xn = cv.take(sv * hv * es);
+    L.qkv = cv.take(sv * S->vqkv_w * es);
+    L.o = cv.take(sv * S->vo_w * es);
+    L.lse = (float*)cv.take(S->vnh * sv * 4);
+    L.mean1 = (float*)cv.take(S->svl * 4);
+    L.rstd1 = (float*)cv.take(S->svl * 4);
+    L.mean2 = (float*)cv.take(S->svl * 4);
+    L.rstd2 = (float*)cv.take(S->svl * 4);
+    L.x1 = cv.take(vsh * es);
+    L.xn2 = cv.take(sv * hv * es);
+    L.a = cv.take(sv * S->vml * es);  // backward overwrites it with dA
+    L.hh = cv.take(sv * S->vml * es);
+    L.xres = cv.take(vsh * es);
+    L.dy_attn = cv.take(sv * hv * es);
+    L.dqkv = cv.take(sv * S->vqkv_w * es);
+    L.dy_mlp = cv.take(sv * hv * es);
+  }
+  sl.yq = cv.take(sv * hv * es);                // = [n_img, 4 hv] merger input
+  sl.meanq = (float*)cv.take(S->svl * 4);
+  sl.rstdq = (float*)cv.take(S->svl * 4);
+  sl.z = cv.take(S->n_img * S->m4l * es);        // backward overwrites it with dZ
+  sl.gz = cv.take(S->n_img * S->m4l * es);
+  sl.x_out = cv.take(S->sl * S->h * es);
+  sl.dylm = cv.take(S->s * S->h * es);
+  sl.vdx = cv.take(vsh * es);
+}
+
 void carve_slot(stp_stage* S, const Chunk& C, Slot& sl, Carver& cv) {
+  if (C.vit) return carve_vit_slot(S, C, sl, cv);
   const size_t es = S->es;
   const int64_t s = S->s, h = S->h, shard = S->sl * S->h;
   sl.x_in = cv.take(shard * es);
@@ -584,7 +661,231 @@ float* DG(stp_stage* S, int i) { return S->dgamma + S->dgamma_off.at(i); }
 
 int64_t vocab0(stp_stage* S) { return (int64_t)S->tp_rank * S->Vl; }
 
+// ------------------------------------------------------------ ViT units
+// The MLLM's first virtual stage (math oracle/vit.py).
+// Same unit / comm-phase structure as the LM chunk (Fig. 3 reading R2):
+// F_EMB = patch embedding of this rank's sequence-parallel shard rows;
+// F_ATTN / F_MLP per ViT layer; F_MERGE = 2x2 merger (the [sv, hv] LayerNorm
+// output read as [sv/4, 4 hv]) + vocab-parallel text embedding, one [S, h]
+// LM-input partial.  Row-parallel biases (wo, w2, merger w2) are added by TP
+// rank 0's GEMM epilogue only, so the reduce-scatter sums them once; their
+// gradients are column sums of the all-gathered dY (identical on every rank).
+stp_status vit_compute(stp_stage* S, const stp_unit& u, Slot* sl) {
+  const int dt = S->dtype, mc = S->gemm_max_ctas;
+  cudaStream_t st = S->s_comp;
+  const int64_t sv = S->sv, hv = S->hv, qw = S->vqkv_w, ow = S->vo_w, ml = S->vml, h = S->h, es = S->es;
+  const int epi_rp = S->tp_rank == 0 ? STP_EPI_BIAS : STP_EPI_STORE;  // row-parallel bias: once, on rank 0
+  const int gw = S->vc.grid_w;
+  const float theta = S->vc.rope_theta;
+  auto patches_of = [&](int mb) {
+    return (const uint8_t*)S->patches + ((int64_t)(mb - 1) * sv + (int64_t)S->tp_rank * S->svl) * S->vpd * es;
+  };
+  switch (u.op) {
+    case STP_U_F_EMB:
+      if (!S->patches) return fail(STP_ESTATE, "MLLM stage: stp_stage_bind_images not called");
+      return gemm_dispatch(dt, STP_GEMM_NT, STP_EPI_STORE, S->svl, hv, S->vpd, patches_of(u.mb), S->vpd,
+                           P(S, S->p_patch), S->vpd, sl->x_in, hv, nullptr, nullptr, 0, mc, st);
+    case STP_U_F_ATTN: {
+      VitSlotLayer& L = sl->V[u.layer];
+      const VitIdx& I = S->vidx.at(u.layer);
+      STP_TRY(gemm_dispatch(dt, STP_GEMM_NT, STP_EPI_BIAS, sv, qw, hv, L.xn, hv, P(S, I.wqkv), hv, L.qkv, qw,
+                            P(S, I.bqkv), nullptr, 0, mc, st));
+      STP_TRY(rope2d(dt, 0, sv, qw, 0, (int)(2 * S->vnh), (int)S->vd, gw, theta, L.qkv, st));
+      const uint8_t* q = (const uint8_t*)L.qkv;
+      const int64_t hs = S->vnh * S->vd * es;
+      STP_TRY(attn_fwd(dt, sv, (int)S->vnh, (int)S->vnh, (int)S->vd, 0, q, q + hs, q + 2 * hs, qw, L.o, ow, L.lse,
+                       st));
+      return gemm_dispatch(dt, STP_GEMM_NT, epi_rp, sv, hv, ow, L.o, ow, P(S, I.wo), ow, S->pf, hv, P(S, I.bo),
+                           nullptr, 0, mc, st);
+    }
+    case STP_U_F_MLP: {
+      VitSlotLayer& L = sl->V[u.layer];
+      const VitIdx& I = S->vidx.at(u.layer);
+      STP_TRY(gemm_dispatch(dt, STP_GEMM_NT, STP_EPI_BIAS, sv, ml, hv, L.xn2, hv, P(S, I.w1), hv, L.a, ml, P(S, I.b1),
+                            nullptr, 0, mc, st));
+      STP_TRY(act_fwd(dt, 0, sv * ml, L.a, L.hh, st));
+      return gemm_dispatch(dt, STP_GEMM_NT, epi_rp, sv, hv, ml, L.hh, ml, P(S, I.w2), ml, S->pf, hv, P(S, I.b2),
+                           nullptr, 0, mc, st);
+    }
+    case STP_U_F_MERGE: {
+      const int64_t ni = S->n_img;
+      STP_TRY(gemm_dispatch(dt, STP_GEMM_NT, STP_EPI_BIAS, ni, S->m4l, S->m4, sl->yq, S->m4, P(S, S->p_mw1), S->m4,
+                            sl->z, S->m4l, P(S, S->p_mb1), nullptr, 0, mc, st));
+      STP_TRY(act_fwd(dt, 1, ni * S->m4l, sl->z, sl->gz, st));
+      STP_TRY(gemm_dispatch(dt, STP_GEMM_NT, epi_rp, ni, h, S->m4l, sl->gz, S->m4l, P(S, S->p_mw2), S->m4l, S->pf, h,
+                            P(S, S->p_mb2), nullptr, 0, mc, st));
+      const int32_t* tok = S->tokens + (int64_t)(u.mb - 1) * S->s + ni;
+      return embed_fwd(dt, S->s - ni, h, tok, vocab0(S), S->Vl, P(S, S->p_embed), (uint8_t*)S->pf + ni * h * es, st);
+    }
+    case STP_U_B_MERGE: {
+      const int64_t ni = S->n_img;
+      STP_TRY(gemm_dispatch(dt, STP_GEMM_NN, STP_EPI_STORE, ni, S->m4l, h, sl->dylm, h, P(S, S->p_mw2), S->m4l,
+                            S->vdtmp_m, S->m4l, nullptr, nullptr, 0, mc, st));
+      STP_TRY(act_bwd(dt, 1, ni * S->m4l, S->vdtmp_m, sl->z, sl->z, st));  // dZ over Z
+      return gemm_dispatch(dt, STP_GEMM_NN, STP_EPI_STORE, ni, S->m4, S->m4l, sl->z, S->m4l, P(S, S->p_mw1), S->m4,
+                           S->pb, S->m4, nullptr, nullptr, 0, mc, st);
+    }
+    case STP_U_W_MERGE: {
+      const int64_t ni = S->n_img;
+      STP_TRY(gemm_dispatch(dt, STP_GEMM_TN, STP_EPI_ACCUM_F32, h, S->m4l, ni, sl->dylm, h, sl->gz, S->m4l,
+                            G(S, S->p_mw2), S->m4l, nullptr, nullptr, 0, mc, st));
+      STP_TRY(colsum_acc(dt, ni, h, sl->dylm, h, G(S, S->p_mb2), st));
+      STP_TRY(gemm_dispatch(dt, STP_GEMM_TN, STP_EPI_ACCUM_F32, S->m4l, S->m4, ni, sl->z, S->m4l, sl->yq, S->m4,
+                            G(S, S->p_mw1), S->m4, nullptr, nullptr, 0, mc, st));
+      return colsum_acc(dt, ni, S->m4l, sl->z, S->m4l, G(S, S->p_mb1), st);
+    }
+    case STP_U_B_MLP: {
+      VitSlotLayer& L = sl->V[u.layer];
+      const VitIdx& I = S->vidx.at(u.layer);
+      STP_TRY(gemm_dispatch(dt, STP_GEMM_NN, STP_EPI_STORE, sv, ml, hv, L.dy_mlp, hv, P(S, I.w2), ml, S->vdtmp_h, ml,
+                            nullptr, nullptr, 0, mc, st));
+      STP_TRY(act_bwd(dt, 0, sv * ml, S->vdtmp_h, L.a, L.a, st));  // dA over A
+      return gemm_dispatch(dt, STP_GEMM_NN, STP_EPI_STORE, sv, hv, ml, L.a, ml, P(S, I.w1), hv, S->pb, hv, nullptr,
+                           nullptr, 0, mc, st);
+    }
+    case STP_U_W_MLP: {
+      VitSlotLayer& L = sl->V[u.layer];
+      const VitIdx& I = S->vidx.at(u.layer);
+      STP_TRY(gemm_dispatch(dt, STP_GEMM_TN, STP_EPI_ACCUM_F32, hv, ml, sv, L.dy_mlp, hv, L.hh, ml, G(S, I.w2), ml,
+                            nullptr, nullptr, 0, mc, st));
+      STP_TRY(colsum_acc(dt, sv, hv, L.dy_mlp, hv, G(S, I.b2), st));
+      STP_TRY(gemm_dispatch(dt, STP_GEMM_TN, STP_EPI_ACCUM_F32, ml, hv, sv, L.a, ml, L.xn2, hv, G(S, I.w1), hv,
+                            nullptr, nullptr, 0, mc, st));
+      return colsum_acc(dt, sv, ml, L.a, ml, G(S, I.b1), st);
+    }
+    case STP_U_B_ATTN: {
+      VitSlotLayer& L = sl->V[u.layer];
+      const VitIdx& I = S->vidx.at(u.layer);
+      STP_TRY(gemm_dispatch(dt, STP_GEMM_NN, STP_EPI_STORE, sv, ow, hv, L.dy_attn, hv, P(S, I.wo), ow, S->vdtmp_o, ow,
+                            nullptr, nullptr, 0, mc, st));
+      const uint8_t* q = (const uint8_t*)L.qkv;
+      uint8_t* dq = (uint8_t*)L.dqkv;
+      const int64_t hs = S->vnh * S->vd * es;
+      STP_TRY(attn_bwd(dt, sv, (int)S->vnh, (int)S->vnh, (int)S->vd, 0, q, q + hs, q + 2 * hs, qw, L.o, ow,
+                       S->vdtmp_o, L.lse, dq, dq + hs, dq + 2 * hs, qw, S->vattn_ws, st));
+      STP_TRY(rope2d(dt, 1, sv, qw, 0, (int)(2 * S->vnh), (int)S->vd, gw, theta, L.dqkv, st));
+      return gemm_dispatch(dt, STP_GEMM_NN, STP_EPI_STORE, sv, hv, qw, L.dqkv, qw, P(S, I.wqkv), hv, S->pb, hv,
+                           nullptr, nullptr, 0, mc, st);
+    }
+    case STP_U_W_ATTN: {
+      VitSlotLayer& L = sl->V[u.layer];
+      const VitIdx& I = S->vidx.at(u.layer);
+      STP_TRY(gemm_dispatch(dt, STP_GEMM_TN, STP_EPI_ACCUM_F32, hv, ow, sv, L.dy_attn, hv, L.o, ow, G(S, I.wo), ow,
+                            nullptr, nullptr, 0, mc, st));
+      STP_TRY(colsum_acc(dt, sv, hv, L.dy_attn, hv, G(S, I.bo), st));
+      STP_TRY(gemm_dispatch(dt, STP_GEMM_TN, STP_EPI_ACCUM_F32, qw, hv, sv, L.dqkv, qw, L.xn, hv, G(S, I.wqkv), hv,
+                            nullptr, nullptr, 0, mc, st));
+      return colsum_acc(dt, sv, qw, L.dqkv, qw, G(S, I.bqkv), st);
+    }
+    case STP_U_W_EMB: {
+      // text rows: vocab-parallel embedding gradient from the all-gathered
+      // LM-input gradient; image rows: patch-embedding weight partial of this
+      // rank's shard rows (summed over TP at the end of the step)
+      const int64_t ni = S->n_img;
+      const int32_t* tok = S->tokens + (int64_t)(u.mb - 1) * S->s + ni;
+      STP_TRY(embed_bwd(dt, S->s - ni, h, tok, vocab0(S), S->Vl, (const uint8_t*)sl->dylm + ni * h * es,
+                        G(S, S->p_embed), st));
+      return gemm_dispatch(dt, STP_GEMM_TN, STP_EPI_ACCUM_F32, hv, S->vpd, S->svl, sl->vdx, hv, patches_of(u.mb),
+                           S->vpd, DG(S, S->p_patch), S->vpd, nullptr, nullptr, 0, mc, st);
+    }
+  }
+  return fail(STP_ESTATE, "unknown ViT compute unit");
+}
+
+// ViT comm phases (NCCL reduce-scatter / all-gather over the [sv, hv]
+// residual stream, LayerNorm in place of RMSNorm):
+//   cf 1                after F_EMB: ln1(0) -> AG
+//   cf 2 + 2j           after F_ATTN(j): RS + residual -> x1; ln2(j) -> AG
+//   cf 3 + 2j           after F_MLP(j): RS + x1 -> xres; ln1(j+1) (or the
+//                       merger LayerNorm after the last layer) -> AG
+//   cf 2 + 2 nv         after F_MERGE: RS of the [S, h] LM-input partial
+//   cb 0                AG of the incoming LM-input gradient shard
+//   cb 1                after B_MERGE: RS; merger-LN bwd -> AG
+//   cb 2 + 2jj (+1)     after B_MLP / B_ATTN of layer nv-1-jj: RS; ln2 / ln1
+//                       bwd + residual gradient -> AG for the next B unit
+stp_status vit_ln_ag(stp_stage* S, const void* x, const void* resid, void* x_out, int g, int b, float* mean,
+                     float* rstd, void* dst) {
+  const int dt = S->dtype;
+  void* y = S->t == 1 ? dst : S->vntmp;
+  STP_TRY(layernorm_fwd(dt, S->svl, S->hv, x, resid, x_out, P(S, g), P(S, b), S->vc.ln_eps, y, mean, rstd, S->s_comm));
+  if (S->t > 1) STP_TRY(all_gather(S, S->vntmp, dst, (size_t)(S->svl * S->hv)));
+  return STP_OK;
+}
+
+stp_status vit_rs(stp_stage* S, const void* partial, const void** out) {
+  if (S->t == 1) {
+    *out = partial;
+    return STP_OK;
+  }
+  STP_NCCL_TRY(ncclReduceScatter(partial, S->vrtmp, (size_t)(S->svl * S->hv), (ncclDataType_t)ncdt(S->dtype), ncclSum,
+                                 S->tpc, S->s_comm));
+  *out = S->vrtmp;
+  return STP_OK;
+}
+
+stp_status vit_cf(stp_stage* S, const Chunk& C, const stp_unit& u, Slot* sl) {
+  const int k = u.layer, nv = C.nl;
+  if (k == 1) {
+    const VitIdx& I = S->vidx.at(0);
+    return vit_ln_ag(S, sl->x_in, nullptr, nullptr, I.ln1_g, I.ln1_b, sl->V[0].mean1, sl->V[0].rstd1, sl->V[0].xn);
+  }
+  if (k == 2 + 2 * nv) {  // LM-input partial [S, h] -> this rank's shard
+    S->pf_pending = true;
+    if (S->t == 1) {
+      STP_CUDA_TRY(cudaMemcpyAsync(sl->x_out, S->pf, S->sl * S->h * S->es, cudaMemcpyDeviceToDevice, S->s_comm));
+      return STP_OK;
+    }
+    return reduce_scatter(S, S->pf, sl->x_out);
+  }
+  const int idx = k - 2, j = idx / 2;
+  if (j < 0 || j >= nv) return fail(STP_ESTATE, "ViT forward comm phase out of range");
+  VitSlotLayer& L = sl->V[j];
+  const VitIdx& I = S->vidx.at(j);
+  const void* src = nullptr;
+  STP_TRY(vit_rs(S, S->pf, &src));
+  S->pf_pending = true;
+  if (idx % 2 == 0)
+    return vit_ln_ag(S, src, j == 0 ? sl->x_in : sl->V[j - 1].xres, L.x1, I.ln2_g, I.ln2_b, L.mean2, L.rstd2, L.xn2);
+  if (j + 1 < nv) {
+    const VitIdx& I2 = S->vidx.at(j + 1);
+    return vit_ln_ag(S, src, L.x1, L.xres, I2.ln1_g, I2.ln1_b, sl->V[j + 1].mean1, sl->V[j + 1].rstd1,
+                     sl->V[j + 1].xn);
+  }
+  return vit_ln_ag(S, src, L.x1, L.xres, S->p_mln_g, S->p_mln_b, sl->meanq, sl->rstdq, sl->yq);
+}
+
+stp_status vit_cb(stp_stage* S, const Chunk& C, const stp_unit& u, Slot* sl) {
+  const int dt = S->dtype, k = u.layer, nv = C.nl;
+  const int64_t vsh = S->svl * S->hv;
+  cudaStream_t st = S->s_comm;
+  if (k == 0) return all_gather(S, sl->dx_in, sl->dylm, (size_t)(S->sl * S->h));
+  const void* src = nullptr;
+  STP_TRY(vit_rs(S, S->pb, &src));
+  S->pb_pending = true;
+  if (k == 1) {  // after B_MERGE: merger LayerNorm backward (no residual) -> AG for B_MLP(nv-1)
+    STP_TRY(layernorm_bwd(dt, S->svl, S->hv, src, sl->V[nv - 1].xres, P(S, S->p_mln_g), sl->meanq, sl->rstdq, nullptr,
+                          sl->vdx, DG(S, S->p_mln_g), DG(S, S->p_mln_b), st));
+    return all_gather(S, sl->vdx, sl->V[nv - 1].dy_mlp, (size_t)vsh);
+  }
+  const int idx = k - 2, jj = idx / 2, j = nv - 1 - jj;
+  if (j < 0 || j >= nv) return fail(STP_ESTATE, "ViT backward comm phase out of range");
+  VitSlotLayer& L = sl->V[j];
+  const VitIdx& I = S->vidx.at(j);
+  if (idx % 2 == 0) {  // after B_MLP(j): ln2 bwd + residual grad -> AG for B_ATTN(j)
+    STP_TRY(layernorm_bwd(dt, S->svl, S->hv, src, L.x1, P(S, I.ln2_g), L.mean2, L.rstd2, sl->vdx, sl->vdx,
+                          DG(S, I.ln2_g), DG(S, I.ln2_b), st));
+    return all_gather(S, sl->vdx, L.dy_attn, (size_t)vsh);
+  }
+  // after B_ATTN(j): ln1 bwd + residual grad -> AG for B_MLP(j-1); at j = 0
+  // vdx is the gradient of the patch embedding output (W_EMB reads it)
+  STP_TRY(layernorm_bwd(dt, S->svl, S->hv, src, j == 0 ? sl->x_in : sl->V[j - 1].xres, P(S, I.ln1_g), L.mean1,
+                        L.rstd1, sl->vdx, sl->vdx, DG(S, I.ln1_g), DG(S, I.ln1_b), st));
+  if (j > 0) return all_gather(S, sl->vdx, sl->V[j - 1].dy_mlp, (size_t)vsh);
+  return STP_OK;
+}
+
 // ------------------------------------------------------------ units
+stp_status vit_compute(stp_stage* S, const stp_unit& u, Slot* sl);
 stp_status unit_compute(stp_stage* S, const stp_unit& u) {
   Chunk& C = chunk_of(S, u.chunk);
   const int dt = S->dtype;
@@ -592,15 +893,16 @@ stp_status unit_compute(stp_stage* S, const stp_unit& u) {
   const int mc = S->gemm_max_ctas;
   cudaStream_t st = S->s_comp;
   Slot* sl = nullptr;
-  const bool fwd = u.op == STP_U_F_ATTN || u.op == STP_U_F_MLP || u.op == STP_U_F_EMB || u.op == STP_U_F_HEAD;
+  const bool fwd = u.op == STP_U_F_ATTN || u.op == STP_U_F_MLP || u.op == STP_U_F_EMB || u.op == STP_U_F_HEAD ||
+                   u.op == STP_U_F_MERGE;
   if (fwd) {
     STP_TRY(acquire(S, u.chunk, u.mb, &sl));
   } else {
     sl = find_slot(S, u.chunk, u.mb);
     if (!sl) return fail(STP_ESTATE, "backward/W unit without a forward stash");
   }
-  const bool writes_pf = u.op == STP_U_F_ATTN || u.op == STP_U_F_MLP || u.op == STP_U_F_EMB;
-  const bool writes_pb = u.op == STP_U_B_ATTN || u.op == STP_U_B_MLP || u.op == STP_U_B_HEAD;
+  const bool writes_pf = u.op == STP_U_F_ATTN || u.op == STP_U_F_MLP || u.op == STP_U_F_EMB || u.op == STP_U_F_MERGE;
+  const bool writes_pb = u.op == STP_U_B_ATTN || u.op == STP_U_B_MLP || u.op == STP_U_B_HEAD || u.op == STP_U_B_MERGE;
   if (writes_pf) {
     if (S->ce) S->pfi ^= 1;
     S->pf = S->pfb[S->pfi];
@@ -611,6 +913,7 @@ stp_status unit_compute(stp_stage* S, const stp_unit& u) {
     S->pb = S->pbb[S->pbi];
     if (S->pbb_pending[S->pbi]) STP_CUDA_TRY(cudaStreamWaitEvent(st, S->ev_pbb[S->pbi], 0));
   }
+  if (C.vit) return vit_compute(S, u, sl);
   const int j = u.layer - C.l0;
   switch (u.op) {
     case STP_U_F_EMB: {
@@ -713,6 +1016,10 @@ stp_status unit_cf(stp_stage* S, const stp_unit& u) {
   Chunk& C = chunk_of(S, u.chunk);
   Slot* sl = nullptr;
   STP_TRY(acquire(S, u.chunk, u.mb, &sl));
+  if (C.vit) {
+    S->open_phase = 0;
+    return vit_cf(S, C, u, sl);
+  }
   const int dt = S->dtype;
   const int64_t h = S->h, shard = S->sl * S->h;
   const float eps = S->mc.rms_eps;
@@ -749,7 +1056,8 @@ stp_status unit_cf(stp_stage* S, const stp_unit& u) {
         if (O.vs == C.vs - 1) {
           Slot* src = find_slot(S, O.c, u.mb);
           if (!src) return fail(STP_ESTATE, "handoff source stash missing");
-          STP_CUDA_TRY(cudaMemcpyAsync(sl->x_in, src->L[O.nl - 1].xres, shard * S->es, cudaMemcpyDeviceToDevice, st));
+          STP_CUDA_TRY(cudaMemcpyAsync(sl->x_in, O.vit ? src->x_out : src->L[O.nl - 1].xres, shard * S->es,
+                                       cudaMemcpyDeviceToDevice, st));
         }
     }
     const LayerIdx& I = LI(S, C.l0);
@@ -813,6 +1121,10 @@ stp_status unit_cb(stp_stage* S, const stp_unit& u) {
   Chunk& C = chunk_of(S, u.chunk);
   Slot* sl = find_slot(S, u.chunk, u.mb);
   if (!sl) return fail(STP_ESTATE, "backward comm without stash");
+  if (C.vit) {
+    S->open_phase = 0;
+    return vit_cb(S, C, u, sl);
+  }
   const int dt = S->dtype;
   const int64_t h = S->h, shard = S->sl * S->h;
   cudaStream_t st = S->s_comm;
@@ -916,7 +1228,7 @@ stp_status unit_pp(stp_stage* S, int ui, const stp_unit& u, cudaStream_t st) {
   }
   sl = find_slot(S, u.chunk, u.mb);
   if (!sl) return fail(STP_ESTATE, "send without stash");
-  const void* src = fwd ? sl->L[C.nl - 1].xres : sl->dx_in;
+  const void* src = fwd ? (C.vit ? sl->x_out : sl->L[C.nl - 1].xres) : sl->dx_in;
   STP_NCCL_TRY(ncclSend(src, count, (ncclDataType_t)ncdt(S->dtype), 1, S->c_send.at(edge), st));
   cudaEvent_t e = pool_event(S);
   STP_CUDA_TRY(cudaEventRecord(e, st));
@@ -1131,8 +1443,37 @@ stp_status build_params(stp_stage* S) {
     return (int)S->params.size() - 1;
   };
   for (auto& C : S->chunks) {
+    if (C.vit) {  // oracle/vit.py names; column-parallel qkv / w1 / merger w1, row-parallel wo / w2 / merger w2
+      S->p_patch = add_p("vit.patch", S->hv, S->vpd);
+      for (int l = C.l0; l < C.l0 + C.nl; ++l) {
+        const std::string pre = "vit." + std::to_string(l) + ".";
+        VitIdx I;
+        I.ln1_g = add_p(pre + "ln1_g", S->hv, 1);
+        I.ln1_b = add_p(pre + "ln1_b", S->hv, 1);
+        I.wqkv = add_p(pre + "wqkv", S->vqkv_w, S->hv);
+        I.bqkv = add_p(pre + "bqkv", S->vqkv_w, 1);
+        I.wo = add_p(pre + "wo", S->hv, S->vo_w);
+        I.bo = add_p(pre + "bo", S->hv, 1);
+        I.ln2_g = add_p(pre + "ln2_g", S->hv, 1);
+        I.ln2_b = add_p(pre + "ln2_b", S->hv, 1);
+        I.w1 = add_p(pre + "w1", S->vml, S->hv);
+        I.b1 = add_p(pre + "b1", S->vml, 1);
+        I.w2 = add_p(pre + "w2", S->hv, S->vml);
+        I.b2 = add_p(pre + "b2", S->hv, 1);
+        S->vidx[l] = I;
+      }
+      S->p_mln_g = add_p("merger.ln_g", S->hv, 1);
+      S->p_mln_b = add_p("merger.ln_b", S->hv, 1);
+      S->p_mw1 = add_p("merger.w1", S->m4l, S->m4);
+      S->p_mb1 = add_p("merger.b1", S->m4l, 1);
+      S->p_mw2 = add_p("merger.w2", S->h, S->m4l);
+      S->p_mb2 = add_p("merger.b2", S->h, 1);
+      continue;
+    }
     for (int l = C.l0; l < C.l0 + C.nl; ++l) {
-      const std::string pre = "layers." + std::to_string(l) + ".";
+      // LM layers are numbered from 0 in parameter names (the ViT layers of an
+      // MLLM's vs 0 take global unit-layer indices 0..nvit-1)
+      const std::string pre = "layers." + std::to_string(l - S->nvit) + ".";
       LayerIdx I;
       I.ln1 = add_p(pre + "ln1", S->h, 1);
       I.wqkv = add_p(pre + "wqkv", S->qkv_w, S->h);
@@ -1151,13 +1492,20 @@ stp_status build_params(stp_stage* S) {
       S->p_final = add_p("final_ln", S->h, 1);
       S->p_lm = add_p("lm_head", S->Vl, S->h);
     }
-  // internal gamma-grad accumulators
+  // internal accumulators of the replicated parameters whose gradient is a
+  // sum over the sequence-parallel shards (TP all-reduced at the end of the
+  // step): norm gains (and ViT LayerNorm biases) and the patch embedding
   S->dgamma_off.clear();
   int64_t off = 0;
+  auto ends = [](const std::string& nm, const char* suf) {
+    const size_t n = strlen(suf);
+    return nm.size() >= n && nm.compare(nm.size() - n, n, suf) == 0;
+  };
   for (size_t i = 0; i < S->params.size(); ++i) {
     const std::string& nm = S->params[i].name;
-    const bool gamma = nm == "final_ln" || (nm.size() > 4 && (nm.compare(nm.size() - 4, 4, ".ln1") == 0 ||
-                                                              nm.compare(nm.size() - 4, 4, ".ln2") == 0));
+    const bool gamma = nm == "final_ln" || ends(nm, ".ln1") || ends(nm, ".ln2") || ends(nm, ".ln1_g") ||
+                       ends(nm, ".ln1_b") || ends(nm, ".ln2_g") || ends(nm, ".ln2_b") || nm == "merger.ln_g" ||
+                       nm == "merger.ln_b" || nm == "vit.patch";
     if (gamma) {
       S->dgamma_off[(int)i] = off;
       off += S->params[i].numel();
@@ -1209,7 +1557,7 @@ stp_status init_nccl(stp_stage* S, const void* uid) {
   std::vector<Edge> edges;
   for (int d = 0; d < S->p; ++d) {
     std::vector<stp_unit> us;
-    STP_TRY(schedule_expand(S->sched, d, S->lay, us));
+    STP_TRY(schedule_expand(S->sched, d, S->lay, us, S->mllm));
     std::vector<std::pair<int, int>> ue;
     std::vector<char> uf;
     classify_pp_units(S->sched, S->p, d, us, ue, uf);
@@ -1289,6 +1637,11 @@ stp_status warmup_comms(stp_stage* S) {
     STP_NCCL_TRY(ncclAllGather(S->pf, S->pb, (size_t)(S->s * 3), ncclFloat32, S->tpc, S->s_comm));
     STP_NCCL_TRY(ncclAllReduce(S->dgamma, S->dgamma, (size_t)std::max<int64_t>(1, S->dgamma_n), ncclFloat32, ncclSum,
                                S->tpc, S->s_comm));
+    if (S->mllm) {
+      const size_t vsh = (size_t)(S->svl * S->hv);
+      STP_NCCL_TRY(ncclReduceScatter(S->pf, S->vrtmp, vsh, dt, ncclSum, S->tpc, S->s_comm));
+      STP_NCCL_TRY(ncclAllGather(S->vntmp, S->pf, vsh, dt, S->tpc, S->s_comm));
+    }
     STP_CUDA_TRY(cudaStreamSynchronize(S->s_comm));
   }
   for (auto& e : S->edges_sorted) {
@@ -1327,8 +1680,8 @@ stp_status stp_nccl_get_id(void* buf) {
   return STP_OK;
 }
 
-stp_status stp_init_stage(const stp_model_cfg* mc, const stp_parallel_cfg* pc, const void* world_nccl_id,
-                          int32_t cuda_device, stp_stage** out) {
+static stp_status init_stage_impl(const stp_model_cfg* mc, const stp_vit_cfg* vc, const stp_parallel_cfg* pc,
+                                  const void* world_nccl_id, int32_t cuda_device, stp_stage** out) {
   if (!mc || !pc || !out) return fail(STP_EINVAL, "NULL argument");
   *out = nullptr;
   const int t = pc->tp, p = pc->pp;
@@ -1363,10 +1716,50 @@ stp_status stp_init_stage(const stp_model_cfg* mc, const stp_parallel_cfg* pc, c
   S->fi = mc->ffn / t;
   S->Vl = mc->vocab / t;
   STP_CHECK_ARG(S->qkv_w % 8 == 0 && S->o_w % 8 == 0 && S->Vl % 8 == 0, "per-rank widths multiples of 8");
+  if (vc) {
+    S->mllm = true;
+    S->vc = *vc;
+    STP_CHECK_ARG(vc->n_layers >= 1 && vc->hidden % 8 == 0 && vc->patch_dim % 8 == 0, "ViT dims");
+    STP_CHECK_ARG(vc->grid_h % 2 == 0 && vc->grid_w % 2 == 0, "ViT grid even (2x2 merge)");
+    STP_CHECK_ARG(vc->n_heads % t == 0 && vc->mlp % t == 0 && (4 * vc->hidden) % t == 0, "ViT heads, mlp, 4h % tp");
+    STP_CHECK_ARG(vc->n_heads * vc->head_dim == vc->hidden, "ViT n_heads * head_dim == hidden");
+    STP_CHECK_ARG((vc->mlp / t) % 8 == 0 && (4 * vc->hidden / t) % 8 == 0, "ViT per-rank widths multiples of 8");
+    S->nvit = vc->n_layers;
+    S->sv = (int64_t)vc->grid_h * vc->grid_w;
+    STP_CHECK_ARG(S->sv % (4 * t) == 0, "grid_h * grid_w % (4 tp) == 0");
+    S->svl = S->sv / t;
+    S->hv = vc->hidden;
+    S->vnh = vc->n_heads / t;
+    S->vd = vc->head_dim;
+    S->vqkv_w = 3 * S->vnh * S->vd;
+    S->vo_w = S->vnh * S->vd;
+    S->vml = vc->mlp / t;
+    S->vpd = vc->patch_dim;
+    S->n_img = S->sv / 4;
+    S->m4 = 4 * S->hv;
+    S->m4l = S->m4 / t;
+    STP_CHECK_ARG(S->n_img < S->s, "image tokens fewer than the LM sequence");
+    STP_CHECK_ARG(mc->dtype == STP_DTYPE_F32 || S->vd == 80 || S->vd == 128, "bf16 ViT head_dim 80 or 128");
+  }
   STP_TRY(schedule_build(p, pc->vpp, t, pc->n_micro, pc->sched_kind, S->sched));
   const int V = sched_n_vstages(S->kind, p);
   S->lay.resize(V);
-  if (pc->layers_per_vstage) {
+  if (S->mllm) {
+    STP_CHECK_ARG(V >= 2, "MLLM needs >= 2 virtual stages (ViT + LM)");
+    S->lay[0] = (int)S->nvit;
+    int sum = 0;
+    if (pc->layers_per_vstage) {
+      STP_CHECK_ARG(pc->layers_per_vstage[0] == S->nvit, "layers_per_vstage[0] must equal the ViT layer count");
+      for (int i = 1; i < V; ++i) S->lay[i] = pc->layers_per_vstage[i];
+    } else {
+      STP_TRY(layer_split(mc->n_layers, V - 1, S->lay.data() + 1));
+    }
+    for (int i = 1; i < V; ++i) {
+      STP_CHECK_ARG(S->lay[i] >= 1, "every LM virtual stage needs >= 1 layer");
+      sum += S->lay[i];
+    }
+    if (sum != mc->n_layers) return fail(STP_EINVAL, "IndivisibleLayers: LM layers_per_vstage does not sum to n_layers");
+  } else if (pc->layers_per_vstage) {
     int sum = 0;
     for (int i = 0; i < V; ++i) {
       S->lay[i] = pc->layers_per_vstage[i];
@@ -1377,7 +1770,7 @@ stp_status stp_init_stage(const stp_model_cfg* mc, const stp_parallel_cfg* pc, c
   } else {
     STP_TRY(layer_split(mc->n_layers, V, S->lay.data()));
   }
-  STP_TRY(schedule_expand(S->sched, S->pp_rank, S->lay, S->units));
+  STP_TRY(schedule_expand(S->sched, S->pp_rank, S->lay, S->units, S->mllm));
   classify_pp_units(S->sched, p, S->pp_rank, S->units, S->unit_edge, S->unit_fwd);
   STP_CUDA_TRY(cudaSetDevice(cuda_device));
   // chunks held by this rank
@@ -1391,6 +1784,7 @@ stp_status stp_init_stage(const stp_model_cfg* mc, const stp_parallel_cfg* pc, c
     C.nl = S->lay[C.vs];
     C.first = C.vs == 0;
     C.last = C.vs == V - 1;
+    C.vit = S->mllm && C.vs == 0;
     S->chunks.push_back(C);
   }
   STP_TRY(build_params(S.get()));
@@ -1425,11 +1819,14 @@ stp_status stp_init_stage(const stp_model_cfg* mc, const stp_parallel_cfg* pc, c
     if (tr != "p2p" && tr != "ce" && tr != "nccl") return fail(STP_EINVAL, "STP_TP_TRANSPORT must be p2p, ce or nccl");
     S->ce = S->t > 1 && (tr == "ce" || tr == "p2p");
     S->p2p = S->ce && tr == "p2p";
+    if (S->mllm && S->ce)
+      return fail(STP_EUNSUPPORTED, "MLLM stages with tp > 1 need STP_TP_TRANSPORT=nccl (ViT phases use NCCL RS/AG)");
     const char* w = getenv("STP_CE_WAIT");
     S->ce_spin = w && std::string(w) == "spin";
   }
-  STP_TRY(dalloc(S.get(), &S->pfb[0], S->s * S->h * es));
-  STP_TRY(dalloc(S.get(), &S->pbb[0], S->s * S->h * es));
+  const int64_t part_elems = std::max(S->s * S->h, S->sv * S->hv);  // LM [S, h] and ViT [sv, hv] partials
+  STP_TRY(dalloc(S.get(), &S->pfb[0], part_elems * es));
+  STP_TRY(dalloc(S.get(), &S->pbb[0], part_elems * es));
   if (S->ce) {
     STP_TRY(dalloc(S.get(), &S->pfb[1], S->s * S->h * es));
     STP_TRY(dalloc(S.get(), &S->pbb[1], S->s * S->h * es));
@@ -1449,6 +1846,14 @@ stp_status stp_init_stage(const stp_model_cfg* mc, const stp_parallel_cfg* pc, c
   STP_TRY(dalloc(S.get(), &S->dtmp_h, S->s * S->fi * es));
   STP_TRY(dalloc(S.get(), &S->dtmp_o, S->s * S->o_w * es));
   STP_TRY(dalloc(S.get(), &S->attn_ws, attn_bwd_ws_bytes(S->s, (int)S->qh, (int)S->kh, (int)S->d)));
+  if (S->mllm) {
+    STP_TRY(dalloc(S.get(), &S->vrtmp, S->svl * S->hv * es));
+    STP_TRY(dalloc(S.get(), &S->vntmp, S->svl * S->hv * es));
+    STP_TRY(dalloc(S.get(), &S->vdtmp_h, S->sv * S->vml * es));
+    STP_TRY(dalloc(S.get(), &S->vdtmp_o, S->sv * S->vo_w * es));
+    STP_TRY(dalloc(S.get(), &S->vdtmp_m, S->n_img * S->m4l * es));
+    STP_TRY(dalloc(S.get(), &S->vattn_ws, attn_bwd_ws_bytes(S->sv, (int)S->vnh, (int)S->vnh, (int)S->vd)));
+  }
   void* tmp = nullptr;
   STP_TRY(dalloc(S.get(), &tmp, std::max<int64_t>(1, S->dgamma_n) * sizeof(float)));
   S->dgamma = (float*)tmp;
@@ -1519,6 +1924,25 @@ stp_status stp_init_stage(const stp_model_cfg* mc, const stp_parallel_cfg* pc, c
     if (u.op == STP_U_PP_RECV && !S->c_recv.count(S->unit_edge[i])) return fail(STP_ENCCL, "missing PP recv channel");
   }
   *out = S.release();
+  return STP_OK;
+}
+
+stp_status stp_init_stage(const stp_model_cfg* mc, const stp_parallel_cfg* pc, const void* world_nccl_id,
+                          int32_t cuda_device, stp_stage** out) {
+  return init_stage_impl(mc, nullptr, pc, world_nccl_id, cuda_device, out);
+}
+
+stp_status stp_init_stage_mllm(const stp_model_cfg* mc, const stp_vit_cfg* vc, const stp_parallel_cfg* pc,
+                               const void* world_nccl_id, int32_t cuda_device, stp_stage** out) {
+  if (!vc) return fail(STP_EINVAL, "NULL vit cfg");
+  return init_stage_impl(mc, vc, pc, world_nccl_id, cuda_device, out);
+}
+
+stp_status stp_stage_bind_images(stp_stage* st, const void* d_patches) {
+  if (!st) return fail(STP_EINVAL, "NULL stage");
+  if (!st->mllm) return fail(STP_ESTATE, "not an MLLM stage");
+  if (!d_patches || (reinterpret_cast<uintptr_t>(d_patches) & 15)) return fail(STP_EINVAL, "patches: 16-byte aligned");
+  st->patches = d_patches;
   return STP_OK;
 }
 

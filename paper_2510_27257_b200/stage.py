@@ -34,6 +34,36 @@ def broadcast_nccl_id(group=None) -> Optional[bytes]:
     return obj[0]
 
 
+def pack_vit_param(name: str, PV: Dict[str, np.ndarray], vit, tp: int, r: int) -> np.ndarray:
+    """Rank r's shard of ViT / merger parameter `name` (include/stp.h MLLM
+    layout): wqkv rows = [q heads of rank | k heads | v heads] (+ bqkv),
+    w1 / merger.w1 row blocks (+ biases), wo / w2 / merger.w2 column blocks;
+    LayerNorms, row-parallel biases and the patch embedding replicated."""
+    if name.startswith("merger."):
+        short = name.split(".", 1)[1]
+        m4l = 4 * vit.hidden // tp
+        if short in ("w1", "b1"):
+            return PV[name][r * m4l:(r + 1) * m4l]
+        if short == "w2":
+            return PV[name][:, r * m4l:(r + 1) * m4l]
+        return PV[name]
+    if name == "vit.patch":
+        return PV[name]
+    short = name.rsplit(".", 1)[1]
+    hv, nl = vit.hidden, vit.n_heads // tp * vit.head_dim
+    ml = vit.mlp // tp
+    if short in ("wqkv", "bqkv"):
+        w = PV[name]
+        return np.concatenate([w[j * hv + r * nl:j * hv + (r + 1) * nl] for j in range(3)], 0)
+    if short == "wo":
+        return PV[name][:, r * nl:(r + 1) * nl]
+    if short in ("w1", "b1"):
+        return PV[name][r * ml:(r + 1) * ml]
+    if short == "w2":
+        return PV[name][:, r * ml:(r + 1) * ml]
+    return PV[name]   # ln*_g / ln*_b / bo / b2
+
+
 def pack_rank_param(name: str, P: Dict[str, np.ndarray], cfg, tp: int, r: int) -> np.ndarray:
     """Rank r's shard of parameter `name` in the stage layout of include/stp.h
     (fused QKV / gate-up rows, row-parallel column blocks, vocab row blocks,
@@ -67,8 +97,11 @@ def pack_rank_param(name: str, P: Dict[str, np.ndarray], cfg, tp: int, r: int) -
 class Stage:
     def __init__(self, cfg, tp: int = 1, pp: int = 1, n_micro: int = 1, tp_rank: int = 0, pp_rank: int = 0,
                  dtype: str = "bf16", sched: str = "stp", layers_per_vstage: Optional[Sequence[int]] = None,
-                 device: int = 0, world_nccl_id: Optional[bytes] = None):
+                 device: int = 0, world_nccl_id: Optional[bytes] = None, vit=None):
+        """vit (stp_inputs.VitShape): MLLM stage, virtual stage 0 = ViT + merger
+        (stp_init_stage_mllm); bind the patches with bind_images()."""
         self.cfg, self.tp, self.pp, self.m = cfg, tp, pp, n_micro
+        self.vit = vit
         self.tp_rank, self.pp_rank, self.device = tp_rank, pp_rank, device
         self.dtype_code, self.torch_dtype = DTYPES[dtype]
         self.sched = sched
@@ -84,7 +117,12 @@ class Stage:
         self.h = C.c_void_p()
         idbuf = C.create_string_buffer(world_nccl_id, len(world_nccl_id)) if world_nccl_id else None
         torch.cuda.set_device(device)
-        L.call("stp_init_stage", C.byref(mc), C.byref(pc), idbuf, device, C.byref(self.h))
+        if vit is None:
+            L.call("stp_init_stage", C.byref(mc), C.byref(pc), idbuf, device, C.byref(self.h))
+        else:
+            vc = L.VitCfg(vit.hidden, vit.n_layers, vit.n_heads, vit.head_dim, vit.mlp, vit.patch_dim, vit.grid_h,
+                          vit.grid_w, vit.ln_eps, vit.rope_theta)
+            L.call("stp_init_stage_mllm", C.byref(mc), C.byref(vc), C.byref(pc), idbuf, device, C.byref(self.h))
         n = C.c_int32()
         L.call("stp_stage_param_count", self.h, C.byref(n))
         self.names: List[str] = []
@@ -101,9 +139,19 @@ class Stage:
         gp_ = (C.c_void_p * n.value)(*[t.data_ptr() for t in self.grads])
         L.call("stp_bind_params", self.h, n.value, pp_, gp_)
 
-    def load_params(self, P: Dict[str, np.ndarray]):
+    def load_params(self, P: Dict[str, np.ndarray], PV: Optional[Dict[str, np.ndarray]] = None):
         for name, t in zip(self.names, self.params):
-            t.copy_(torch.from_numpy(np.ascontiguousarray(pack_rank_param(name, P, self.cfg, self.tp, self.tp_rank))))
+            if name.startswith(("vit.", "merger.")):
+                a = pack_vit_param(name, PV, self.vit, self.tp, self.tp_rank)
+            else:
+                a = pack_rank_param(name, P, self.cfg, self.tp, self.tp_rank)
+            t.copy_(torch.from_numpy(np.ascontiguousarray(a)))
+
+    def bind_images(self, patches: torch.Tensor):
+        """patches: device [n_micro, grid_h * grid_w, patch_dim] in the stage dtype (kept referenced)."""
+        assert patches.dtype == self.torch_dtype and patches.is_contiguous()
+        self._patches = patches
+        L.call("stp_stage_bind_images", self.h, patches.data_ptr())
 
     def zero_grads(self):
         for g in self.grads:
@@ -160,18 +208,20 @@ class Stage:
             pass
 
 
-def schedule_units(kind: str, pp: int, n_micro: int, tp: int, pp_rank: int, layers_per_vstage: Sequence[int]):
-    """stp_build_schedule + stp_schedule_units for one rank (tuples in the
-    canonical U-line field order)."""
+def schedule_units(kind: str, pp: int, n_micro: int, tp: int, pp_rank: int, layers_per_vstage: Sequence[int],
+                   mllm: bool = False):
+    """stp_build_schedule + stp_schedule_units (stp_schedule_units_mllm) for
+    one rank (tuples in the canonical U-line field order)."""
+    fn = "stp_schedule_units_mllm" if mllm else "stp_schedule_units"
     vpp = 1 if kind == "1f1b" else 2
     h = C.c_void_p()
     L.call("stp_build_schedule", pp, vpp, tp, n_micro, SCHED[kind], C.byref(h))
     try:
         lay = (C.c_int32 * len(layers_per_vstage))(*layers_per_vstage)
         n = C.c_int32()
-        L.lib.stp_schedule_units(h, pp_rank, lay, None, 0, C.byref(n))
+        getattr(L.lib, fn)(h, pp_rank, lay, None, 0, C.byref(n))
         buf = (L.Unit * max(1, n.value))()
-        L.call("stp_schedule_units", h, pp_rank, lay, buf, n.value, C.byref(n))
+        L.call(fn, h, pp_rank, lay, buf, n.value, C.byref(n))
         return [(u.action, u.stream, u.op, u.layer, u.chunk, u.mb, u.dep0, u.dep1) for u in buf[:n.value]]
     finally:
         L.lib.stp_free_schedule(h)

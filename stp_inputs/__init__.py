@@ -62,6 +62,82 @@ QWEN2_7B_TP8 = dataclasses.replace(QWEN2_7B, n_q_heads=32, n_kv_heads=8)
 QWEN25_14B = ModelCfg(vocab=152064, hidden=5120, n_layers=48, n_q_heads=40,
                       n_kv_heads=8, head_dim=128, ffn=13824, seq=4096)
 
+@dataclasses.dataclass(frozen=True)
+class VitShape:
+    """MLLM vision tower shape (ViT-600M of Qwen2-VL, Table 2 /
+    P:L171): patches of a grid_h x grid_w image in 2x2
+    merge-window order, merged 4:1 into out_hidden-wide LM input rows."""
+    hidden: int = 1280
+    n_layers: int = 32
+    n_heads: int = 16
+    head_dim: int = 80
+    mlp: int = 5120
+    patch_dim: int = 1176     # 3 * 2 * 14 * 14
+    grid_h: int = 56
+    grid_w: int = 56
+    out_hidden: int = 3584
+    ln_eps: float = 1e-6
+    rope_theta: float = 10000.0
+
+    @property
+    def seq(self) -> int:
+        return self.grid_h * self.grid_w
+
+    @property
+    def n_img(self) -> int:
+        return self.seq // 4
+
+
+VIT_600M = VitShape()
+
+
+def vit_param_shapes(v: VitShape) -> Dict[str, tuple]:
+    hv, m4 = v.hidden, 4 * v.hidden
+    sh = {"vit.patch": (hv, v.patch_dim)}
+    for l in range(v.n_layers):
+        p = f"vit.{l}."
+        sh.update({p + "ln1_g": (hv,), p + "ln1_b": (hv,), p + "wqkv": (3 * hv, hv), p + "bqkv": (3 * hv,),
+                   p + "wo": (hv, hv), p + "bo": (hv,), p + "ln2_g": (hv,), p + "ln2_b": (hv,),
+                   p + "w1": (v.mlp, hv), p + "b1": (v.mlp,), p + "w2": (hv, v.mlp), p + "b2": (hv,)})
+    sh.update({"merger.ln_g": (hv,), "merger.ln_b": (hv,), "merger.w1": (m4, m4), "merger.b1": (m4,),
+               "merger.w2": (v.out_hidden, m4), "merger.b2": (v.out_hidden,)})
+    return sh
+
+
+def make_vit_params(v: VitShape, seed: int = 0, std: float = 0.02, parity: bool = False) -> Dict[str, np.ndarray]:
+    """LayerNorm gains 1 and all biases 0 (parity: 1 + 0.1 N(0,1) and
+    0.02 N(0,1)); weights N(0, std^2); per-tensor seeds as make_param."""
+    out = {}
+    for name, shape in vit_param_shapes(v).items():
+        rng = np.random.default_rng(_tensor_seed(name, seed))
+        short = name.rsplit(".", 1)[-1]
+        if short.endswith("_g"):
+            out[name] = 1.0 + 0.1 * rng.standard_normal(shape) if parity else np.ones(shape)
+        elif short.endswith("_b") or short.startswith("b"):
+            out[name] = 0.02 * rng.standard_normal(shape) if parity else np.zeros(shape)
+        else:
+            out[name] = std * rng.standard_normal(shape)
+    return out
+
+
+def make_patches(v: VitShape, n_micro: int, seed: int = 4321) -> np.ndarray:
+    """Random patch rows [n_micro, grid_h * grid_w, patch_dim], N(0, 1)
+    (random patches [3136, 1176])."""
+    return np.random.default_rng(seed).standard_normal((n_micro, v.seq, v.patch_dim))
+
+
+def make_mllm_tokens(cfg: ModelCfg, n_img: int, n_micro: int, seed: int = 1234):
+    """MLLM microbatch = [n_img image rows | cfg.seq - n_img text tokens]:
+    text tokens [m, seq - n_img], the stage's token rows [m, seq] (0 at the
+    image positions, which the embedding skips) and next-token targets
+    [m, seq] for every position."""
+    toks, tgts = make_tokens(cfg, n_micro, seed)
+    text = np.ascontiguousarray(toks[:, n_img:])
+    full = toks.copy()
+    full[:, :n_img] = 0
+    return text, full, tgts
+
+
 PRESETS = {"tiny": TINY, "qwen2-7b": QWEN2_7B, "qwen2-7b-tp8": QWEN2_7B_TP8,
            "qwen2.5-14b": QWEN25_14B}
 

@@ -62,7 +62,7 @@ def main():
     if rank == 0:
         kind = SCHED[a.sched]
         progs = sc.build_program(kind, a.pp, a.n_micro)
-        dur, span, pp_msgs = [], [], []
+        dur, span, busy_tp, pp_msgs = [], [], [], []
         measured = max(x[5] for x in gathered)
         for d in range(a.pp):
             pr, tr, us, s0, s1, *_ = next(x for x in gathered if x[0] == d and x[1] == 0)
@@ -77,17 +77,39 @@ def main():
                 elif u[2] == 13:                 # STP_U_PP_SEND: one PP message
                     pp_msgs.append(e - b)
             dur.append(per)
+            # compute + exposed TP per action: the compute-stream gaps the
+            # executor classifies as TP waits (a compute unit waiting on a comm
+            # phase that itself is not waiting on a PP message; stage.cu
+            # run_step) belong to the action's cost, as T_AR does in Table 1's
+            # block costs; waits for PP inputs do not (the simulator adds them)
+            bt = list(per)
+            prev_end = 0.0
+            first_u = True
+            for i_u, (u, b, e) in enumerate(zip(us, s0, s1)):
+                if u[1] != 0:
+                    continue
+                gap = b if first_u else b - prev_end
+                if gap > 0 and u[6] >= 0 and us[u[6]][1] == 1:
+                    c = us[u[6]]
+                    waits_pp = c[6] >= 0 and us[c[6]][1] == 2 and s1[c[6]] > prev_end
+                    if not waits_pp and s1[u[6]] > prev_end:
+                        bt[u[0]] += gap
+                prev_end = max(prev_end, e)
+                first_u = False
+            busy_tp.append(bt)
             # action span on the compute stream: its units plus the TP-comm waits
             # between them (exposed TP inside the action)
             span.append([(l - f) if f is not None else 0.0 for f, l in zip(first, last)])
         lat = sorted(pp_msgs)[len(pp_msgs) // 2] if pp_msgs else 0.0
         simulated = sm.simulate_durations(kind, a.pp, progs, dur)
         simulated_span = sm.simulate_durations(kind, a.pp, progs, span, pp_latency=lat)
+        simulated_tp = sm.simulate_durations(kind, a.pp, progs, busy_tp, pp_latency=lat)
         print(json.dumps({"tp": a.tp, "pp": a.pp, "sched": a.sched, "n_micro": a.n_micro, "layers": a.layers,
                           "seq": a.seq, "measured_ms": measured, "simulated_ms": simulated,
                           "ratio": measured / simulated,
                           "simulated_span_ms": simulated_span, "pp_msg_ms_median": lat,
                           "ratio_span": measured / simulated_span,
+                          "simulated_tp_ms": simulated_tp, "ratio_tp": measured / simulated_tp,
                           "exposed_tp_pct": [100 * x[6] / x[5] for x in gathered],
                           "pp_bubble_pct": [100 * x[7] / x[5] for x in gathered]}), flush=True)
     st.close()

@@ -1,6 +1,10 @@
 """Executor consistency check on 2 / 4 GPUs: the simulator fed
-with the measured per-action compute times (sum of the action's compute-unit
-durations) reproduces the measured step time within SURVEY's 5%.  The
+with the measured per-action costs (the action's compute-unit durations plus
+the compute-stream gaps spent waiting on its own TP comm phases, i.e. Table 1's
+block cost with the exposed T_AR, and the median PP message time as the
+latency of every cross-device dependency) reproduces the measured step time
+within SURVEY's 5%.  (Compute-only costs under-predict by the exposed TP time:
+1.08 / 1.13 for STP / 1F1B-I at TP2 x PP2 in round 2's 4-GPU run.)  The
 "span" variant (action span incl. its internal waits + PP message latency) is
 reported beside it for information only: a braided action's span already
 contains the wait for its backward input from the other device, which the
@@ -26,4 +30,4 @@ def test_executor_matches_simulator(tp, pp, sched):
     assert rc == 0, out[-3000:]
     line = json.loads([x for x in out.splitlines() if x.startswith("{")][-1])
     print(line)
-    assert 0.95 <= line["ratio"] <= 1.05, line
+    assert 0.95 <= line["ratio_tp"] <= 1.05, line

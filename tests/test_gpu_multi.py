@@ -68,3 +68,21 @@ def test_multi_rank_parity_symmetric(tp, pp, sched, dtype, transport):
                            env={"STP_TP_TRANSPORT": transport})
     assert rc == 0, out[-4000:]
     assert out.count("PASS") == n, out[-4000:]
+
+
+# MLLM (ViT + merger on virtual stage 0) over TP x PP; the ViT comm
+# phases run on NCCL (STP_TP_TRANSPORT=nccl, include/stp.h).
+MLLM_CASES = [(2, 1, "stp", "f32"), (1, 2, "stp", "f32"), (2, 2, "stp", "f32"), (2, 2, "stp", "bf16"),
+              (2, 2, "1f1b-i", "f32")]
+
+
+@pytest.mark.parametrize("tp,pp,sched,dtype", MLLM_CASES)
+def test_multi_rank_mllm_parity(tp, pp, sched, dtype):
+    n = tp * pp
+    if torch.cuda.device_count() < n:
+        pytest.skip(f"needs {n} GPUs")
+    args = ["--tp", str(tp), "--pp", str(pp), "--sched", sched, "--dtype", dtype, "--n-micro", str(2 * pp)]
+    rc, out = run_torchrun(n, args, 29900 + 7 * tp + 3 * pp + len(sched) + len(dtype), script="multi_rank_mllm.py",
+                           env={"STP_TP_TRANSPORT": "nccl"})
+    assert rc == 0, out[-4000:]
+    assert out.count("PASS") == n, out[-4000:]

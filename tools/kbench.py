@@ -87,6 +87,19 @@ def main():
     ms = timed(lambda: ops.attn_bwd(x, nq, nkv, d, o, do, lse, dx), a.iters)
     print(json.dumps({"kernel": "attn_bwd", "s": s, "nq": nq, "nkv": nkv, "ms": ms,
                       "tflops": 8 * pairs * nq * d / ms / 1e9}), flush=True)
+    # ViT-600M bidirectional attention (d = 80, 16 heads / t, 3136 patches)
+    sv, nh, dv = 3136, 16 // t, 80
+    xv = torch.randn(sv, 3 * nh * dv, device=dev, dtype=bf)
+    ov = torch.empty(sv, nh * dv, device=dev, dtype=bf)
+    lv = torch.empty(nh, sv, device=dev, dtype=torch.float32)
+    ms = timed(lambda: ops.attn_full_fwd(xv, nh, dv, ov, lv), a.iters)
+    print(json.dumps({"kernel": "vit_attn_fwd", "s": sv, "nh": nh, "d": dv, "ms": ms,
+                      "tflops": 4 * sv * sv * nh * dv / ms / 1e9}), flush=True)
+    dov = torch.randn(sv, nh * dv, device=dev, dtype=bf)
+    dxv = torch.empty_like(xv)
+    ms = timed(lambda: ops.attn_full_bwd(xv, nh, dv, ov, dov, lv, dxv), a.iters)
+    print(json.dumps({"kernel": "vit_attn_bwd", "s": sv, "nh": nh, "d": dv, "ms": ms,
+                      "tflops": 8 * sv * sv * nh * dv / ms / 1e9}), flush=True)
 
 
 if __name__ == "__main__":

@@ -40,6 +40,12 @@ def _rel(got, ref):
     return np.linalg.norm(got - ref) / max(np.linalg.norm(ref), 1e-30)
 
 
+def _rel_floor(got, ref):
+    """Relative error with an absolute floor of 1e-3 RMS: at s = 1 the exact dQ
+    and dK are 0 (one key, P = 1, dS = 0), where the fp64 oracle leaves ~1e-17."""
+    return np.linalg.norm(got - ref) / max(np.linalg.norm(ref), 1e-3 * np.sqrt(ref.size))
+
+
 @pytest.mark.parametrize("dt", ["f32", "bf16"])
 @pytest.mark.parametrize("rows,h", [(1, 64), (37, 136), (784, 1280), (3136, 1280)])
 def test_layernorm_fwd_bwd(dt, rows, h):
@@ -146,9 +152,9 @@ def test_attention_full_fwd_bwd(dt, s, nh, d):
     torch.cuda.synchronize()
     got = _np(dqkv)
     tol = 5e-5 if dt == "f32" else 3e-2
-    assert _rel(got[:, :nh * d], dq.reshape(s, -1)) <= tol
-    assert _rel(got[:, nh * d:2 * nh * d], dk.reshape(s, -1)) <= tol
-    assert _rel(got[:, 2 * nh * d:], dv.reshape(s, -1)) <= tol
+    assert _rel_floor(got[:, :nh * d], dq.reshape(s, -1)) <= tol
+    assert _rel_floor(got[:, nh * d:2 * nh * d], dk.reshape(s, -1)) <= tol
+    assert _rel_floor(got[:, 2 * nh * d:], dv.reshape(s, -1)) <= tol
 
 
 def test_causal_attention_unchanged_by_3d_maps():

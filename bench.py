@@ -514,7 +514,7 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--compare", action="store_true",
                     help="also time 1F1B-I (+naive), ZB and the STP ablations on the same kernels")
-    ap.add_argument("--compare-scheds", default="stp,1f1b-i,1f1b-i-naive,zb,stp-nobraid,stp-nosep")
+    ap.add_argument("--compare-scheds", default="stp,1f1b-i,1f1b-i-naive,zb,stp-mem,stp-nobraid,stp-nosep")
     ap.add_argument("--grid", default="", help="TPxPP override, e.g. 4x1 (default: by --config and N)")
     args = ap.parse_args()
     if args.warmup < 3:

@@ -28,6 +28,17 @@ Readings:
   NOSEP   R-STP slot grid without steps 2-4 (no W separation).
   1F1B-I-NAIVE  1F1B-I actions; every backward W unit waits for the TP
           communication of its own B unit (all TP comm synchronous).
+  STP-MEM Ours^, the schedule with the memory-efficient warm-up (App. A
+          Fig. 8b, App. B schedule (d); reading R3): V-shape,
+          list-scheduled under unit costs with ZB-V's memory budget of 2p
+          chunk-microbatches; each decision prefers, in order, a braided
+          F(f)&B(b) of one chunk with f > b (App. A: "the microbatch index in
+          the forward pass should be greater than that in the backward pass"),
+          its weight gradient deferred (FBS, "necessitates decoupling the
+          backward pass"); a lone activation backward B; a forward braided with
+          the oldest deferred W (FW) or a lone F (the "additional forward pass
+          ... before the overlapped F&B execution begins"); a lone W.  Chunk 1
+          before chunk 0 at equal readiness.
 
 Unit expansion (Fig. 3) and canonical text
  are defined in DESIGN.md "Unit expansion"; the C++ builder in
@@ -39,9 +50,9 @@ from __future__ import annotations
 from typing import Dict, List, Optional, Sequence, Tuple
 
 # schedule kinds (include/stp.h stp_sched_kind)
-STP, ONEF1B_I, ZB, STP_NOBRAID, STP_NOSEP, ONEF1B_I_NAIVE, ONEF1B = range(7)
+STP, ONEF1B_I, ZB, STP_NOBRAID, STP_NOSEP, ONEF1B_I_NAIVE, ONEF1B, STP_MEM = range(8)
 KIND_NAMES = {STP: "stp", ONEF1B_I: "1f1b-i", ZB: "zb", STP_NOBRAID: "stp-nobraid",
-              STP_NOSEP: "stp-nosep", ONEF1B_I_NAIVE: "1f1b-i-naive", ONEF1B: "1f1b"}
+              STP_NOSEP: "stp-nosep", ONEF1B_I_NAIVE: "1f1b-i-naive", ONEF1B: "1f1b", STP_MEM: "stp-mem"}
 # action kinds (stp_act_kind)
 A_F, A_BFULL, A_B, A_W, A_FB, A_FBS, A_FW = range(7)
 ACT_NAMES = ["F", "BFULL", "B", "W", "FB", "FBS", "FW"]
@@ -242,6 +253,100 @@ def build_zb_greedy(p: int, m: int) -> List[List[Action]]:
     return progs
 
 
+def build_stp_mem(p: int, m: int) -> List[List[Action]]:
+    """Ours^ (reading R3, see module doc): unit costs F = B = W = 1 (FBS and
+    FW take 2); at every time step each idle device takes the first feasible
+    choice in the order FBS > B > FW / F > W."""
+    V = 2 * p
+    cap = 2 * p
+    fend: Dict[Tuple[int, int], int] = {}     # (mb, vs) -> end time
+    bend: Dict[Tuple[int, int], int] = {}
+    nextf = [[1, 1] for _ in range(p)]
+    nextb = [[1, 1] for _ in range(p)]
+    wq: List[List[Tuple[int, int]]] = [[] for _ in range(p)]
+    live = [0] * p
+    free = [0] * p
+    progs: List[List[Action]] = [[] for _ in range(p)]
+    total = 3 * 2 * m * p
+    n = 0
+    t = 0
+
+    def f_ready(d, c):
+        f = nextf[d][c]
+        vs = vstage(STP_MEM, p, d, c)
+        return f <= m and (vs == 0 or fend.get((f, vs - 1), total + 1) <= t)
+
+    def b_ready(d, c):
+        b = nextb[d][c]
+        vs = vstage(STP_MEM, p, d, c)
+        if b > m or fend.get((b, vs), total + 1) > t:
+            return False
+        return vs == V - 1 or bend.get((b, vs + 1), total + 1) <= t
+
+    while n < total:
+        if t > 100 * (total + 10):
+            raise RuntimeError("STP-MEM list schedule did not terminate")
+        for d in range(p):
+            if free[d] > t:
+                continue
+            done = False
+            for c in (1, 0):         # braided F&B(separated) of one chunk, f > b
+                if (live[d] < cap and b_ready(d, c) and f_ready(d, c)
+                        and nextf[d][c] > nextb[d][c]):
+                    f, b, vs = nextf[d][c], nextb[d][c], vstage(STP_MEM, p, d, c)
+                    fend[(f, vs)] = bend[(b, vs)] = free[d] = t + 2
+                    nextf[d][c] += 1
+                    nextb[d][c] += 1
+                    live[d] += 1
+                    wq[d].append((c, b))
+                    progs[d].append(act(A_FBS, c, f, b))
+                    n += 2
+                    done = True
+                    break
+            if done:
+                continue
+            for c in (1, 0):         # lone activation backward
+                if b_ready(d, c):
+                    b, vs = nextb[d][c], vstage(STP_MEM, p, d, c)
+                    bend[(b, vs)] = free[d] = t + 1
+                    nextb[d][c] += 1
+                    wq[d].append((c, b))
+                    progs[d].append(act(A_B, c, b=b))
+                    n += 1
+                    done = True
+                    break
+            if done:
+                continue
+            if live[d] < cap:
+                for c in (1, 0):     # forward, braided with the oldest deferred W if any
+                    if f_ready(d, c):
+                        f, vs = nextf[d][c], vstage(STP_MEM, p, d, c)
+                        nextf[d][c] += 1
+                        live[d] += 1
+                        if wq[d]:
+                            wc, wb = wq[d].pop(0)
+                            live[d] -= 1
+                            fend[(f, vs)] = free[d] = t + 2
+                            progs[d].append(act(A_FW, c, f, w=wb, wc=wc))
+                            n += 2
+                        else:
+                            fend[(f, vs)] = free[d] = t + 1
+                            progs[d].append(act(A_F, c, f))
+                            n += 1
+                        done = True
+                        break
+            if done:
+                continue
+            if wq[d]:
+                wc, wb = wq[d].pop(0)
+                live[d] -= 1
+                free[d] = t + 1
+                progs[d].append(act(A_W, wc, w=wb, wc=wc))
+                n += 1
+        t += 1
+    return progs
+
+
 def build_program(kind: int, p: int, m: int) -> List[List[Action]]:
     """Per-device action lists (Fig. 5 caption: F, B, W per device)."""
     if p < 1 or m < 1:
@@ -258,6 +363,8 @@ def build_program(kind: int, p: int, m: int) -> List[List[Action]]:
         return [build_1f1b(p, m, d) for d in range(p)]
     if kind == ZB:
         return build_zb_greedy(p, m)
+    if kind == STP_MEM:
+        return build_stp_mem(p, m)
     raise ValueError(kind)
 
 

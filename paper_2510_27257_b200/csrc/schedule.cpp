@@ -229,6 +229,108 @@ bool zb_greedy(int p, int m, std::vector<std::vector<stp_action>>& progs) {
   return true;
 }
 
+// Ours^ (STP_SCHED_STP_MEM; memory-efficient warm-up, App. A Fig. 8b and
+// App. B schedule (d); reading R3): V-shape list
+// schedule under unit costs (F = B = W = 1, FBS / FW = 2) with ZB-V's memory
+// budget of 2p chunk-microbatches; each idle device takes the first feasible
+// of: braided F(f)&B(b) of one chunk with f > b and W deferred (FBS), lone B,
+// forward braided with the oldest deferred W (FW) or lone F, lone W; chunk 1
+// before chunk 0.  Same algorithm as oracle/schedule.py build_stp_mem.
+bool stp_mem(int p, int m, std::vector<std::vector<stp_action>>& progs) {
+  const int V = 2 * p, cap = 2 * p;
+  const long total = 3L * 2 * m * p;
+  std::map<std::pair<int, int>, long> fend, bend;
+  std::vector<std::array<int, 2>> nextf(p, {1, 1}), nextb(p, {1, 1});
+  std::vector<std::deque<std::pair<int, int>>> wq(p);
+  std::vector<int> live(p, 0);
+  std::vector<long> busy(p, 0);
+  progs.assign(p, {});
+  long n = 0, t = 0;
+  auto end_of = [&](const std::map<std::pair<int, int>, long>& mp, int mb, int vs) {
+    auto it = mp.find({mb, vs});
+    return it == mp.end() ? total + 1 : it->second;
+  };
+  auto vs_of = [&](int d, int c) { return sched_vstage(STP_SCHED_STP_MEM, p, d, c); };
+  auto f_ready = [&](int d, int c) {
+    const int f = nextf[d][c], vs = vs_of(d, c);
+    return f <= m && (vs == 0 || end_of(fend, f, vs - 1) <= t);
+  };
+  auto b_ready = [&](int d, int c) {
+    const int b = nextb[d][c], vs = vs_of(d, c);
+    if (b > m || end_of(fend, b, vs) > t) return false;
+    return vs == V - 1 || end_of(bend, b, vs + 1) <= t;
+  };
+  while (n < total) {
+    if (t > 100 * (total + 10)) return false;
+    for (int d = 0; d < p; ++d) {
+      if (busy[d] > t) continue;
+      bool done = false;
+      for (int c : {1, 0}) {
+        if (live[d] < cap && b_ready(d, c) && f_ready(d, c) && nextf[d][c] > nextb[d][c]) {
+          const int f = nextf[d][c], b = nextb[d][c], vs = vs_of(d, c);
+          fend[{f, vs}] = bend[{b, vs}] = busy[d] = t + 2;
+          nextf[d][c]++;
+          nextb[d][c]++;
+          live[d]++;
+          wq[d].push_back({c, b});
+          progs[d].push_back(mk(STP_A_FBS, c, f, b));
+          n += 2;
+          done = true;
+          break;
+        }
+      }
+      if (done) continue;
+      for (int c : {1, 0}) {
+        if (b_ready(d, c)) {
+          const int b = nextb[d][c], vs = vs_of(d, c);
+          bend[{b, vs}] = busy[d] = t + 1;
+          nextb[d][c]++;
+          wq[d].push_back({c, b});
+          progs[d].push_back(mk(STP_A_B, c, -1, b));
+          n += 1;
+          done = true;
+          break;
+        }
+      }
+      if (done) continue;
+      if (live[d] < cap) {
+        for (int c : {1, 0}) {
+          if (f_ready(d, c)) {
+            const int f = nextf[d][c], vs = vs_of(d, c);
+            nextf[d][c]++;
+            live[d]++;
+            if (!wq[d].empty()) {
+              const auto w = wq[d].front();
+              wq[d].pop_front();
+              live[d]--;
+              fend[{f, vs}] = busy[d] = t + 2;
+              progs[d].push_back(mk(STP_A_FW, c, f, -1, w.second, w.first));
+              n += 2;
+            } else {
+              fend[{f, vs}] = busy[d] = t + 1;
+              progs[d].push_back(mk(STP_A_F, c, f));
+              n += 1;
+            }
+            done = true;
+            break;
+          }
+        }
+      }
+      if (done) continue;
+      if (!wq[d].empty()) {
+        const auto w = wq[d].front();
+        wq[d].pop_front();
+        live[d]--;
+        busy[d] = t + 1;
+        progs[d].push_back(mk(STP_A_W, w.first, -1, -1, w.second, w.first));
+        n += 1;
+      }
+    }
+    ++t;
+  }
+  return true;
+}
+
 const char* kind_name(int kind) {
   switch (kind) {
     case STP_SCHED_STP: return "stp";
@@ -238,6 +340,7 @@ const char* kind_name(int kind) {
     case STP_SCHED_STP_NOSEP: return "stp-nosep";
     case STP_SCHED_1F1B_I_NAIVE: return "1f1b-i-naive";
     case STP_SCHED_1F1B: return "1f1b";
+    case STP_SCHED_STP_MEM: return "stp-mem";
   }
   return "?";
 }
@@ -246,7 +349,7 @@ const char* kind_name(int kind) {
 
 stp_status schedule_build(int p, int vpp, int tp, int m, int kind, Schedule& s) {
   STP_CHECK_ARG(p >= 1 && m >= 1 && tp >= 1, "pp >= 1, tp >= 1, n_micro >= 1");
-  STP_CHECK_ARG(kind >= 0 && kind <= STP_SCHED_1F1B, "schedule kind");
+  STP_CHECK_ARG(kind >= 0 && kind <= STP_SCHED_STP_MEM, "schedule kind");
   if (kind == STP_SCHED_1F1B) {
     if (vpp != 1) return fail(STP_EUNSUPPORTED, "1F1B needs vpp == 1");
   } else if (vpp != 2) {
@@ -262,6 +365,10 @@ stp_status schedule_build(int p, int vpp, int tp, int m, int kind, Schedule& s) 
   s.ranks.clear();
   if (kind == STP_SCHED_ZB) {
     if (!zb_greedy(p, m, s.ranks)) return fail(STP_ESCHEDULE, "ZB greedy did not terminate");
+    return STP_OK;
+  }
+  if (kind == STP_SCHED_STP_MEM) {
+    if (!stp_mem(p, m, s.ranks)) return fail(STP_ESCHEDULE, "STP-MEM list schedule did not terminate");
     return STP_OK;
   }
   for (int d = 0; d < p; ++d) {

@@ -13,7 +13,8 @@ import torch
 
 from . import _lib as L
 
-SCHED = {"stp": 0, "1f1b-i": 1, "zb": 2, "stp-nobraid": 3, "stp-nosep": 4, "1f1b-i-naive": 5, "1f1b": 6}
+SCHED = {"stp": 0, "1f1b-i": 1, "zb": 2, "stp-nobraid": 3, "stp-nosep": 4, "1f1b-i-naive": 5, "1f1b": 6,
+         "stp-mem": 7}
 DTYPES = {"f32": (0, torch.float32), "bf16": (1, torch.bfloat16)}
 
 

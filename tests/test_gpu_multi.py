@@ -14,6 +14,7 @@ pytestmark = pytest.mark.gpu
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 CASES = [(2, 1, "stp", "f32"), (1, 2, "stp", "f32"), (2, 1, "stp", "bf16"), (1, 2, "1f1b-i", "f32"),
+         (1, 2, "stp-mem", "f32"), (2, 2, "stp-mem", "f32"),
          (1, 2, "zb", "f32"), (1, 2, "stp-nobraid", "f32"), (2, 2, "stp", "f32"), (2, 2, "stp", "bf16"),
          (2, 2, "1f1b-i", "f32"), (2, 2, "zb", "f32"), (4, 1, "stp", "f32"), (1, 4, "stp", "f32")]
 

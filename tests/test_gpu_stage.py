@@ -25,7 +25,7 @@ def _run(cfg, m, dtype, sched, lay=None, seed=3, **kw):
     return st, loss, ref_loss, got, ref, stats, toks, tgts
 
 
-@pytest.mark.parametrize("sched", ["stp", "1f1b-i", "zb", "stp-nobraid", "stp-nosep", "1f1b-i-naive"])
+@pytest.mark.parametrize("sched", ["stp", "1f1b-i", "zb", "stp-nobraid", "stp-nosep", "1f1b-i-naive", "stp-mem"])
 def test_fp32_step_matches_oracle(sched):
     cfg = si.TINY
     st, loss, ref_loss, got, ref, stats, _, _ = _run(cfg, 4, "f32", sched)

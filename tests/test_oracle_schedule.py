@@ -156,7 +156,7 @@ def _check_program(kind, p, m, progs):
             pytest.fail("F and B of the same (mb, vs) in one action")
 
 
-@pytest.mark.parametrize("kind", [sc.STP, sc.STP_NOSEP, sc.ONEF1B_I, sc.ZB, sc.ONEF1B])
+@pytest.mark.parametrize("kind", [sc.STP, sc.STP_NOSEP, sc.ONEF1B_I, sc.ZB, sc.ONEF1B, sc.STP_MEM])
 @pytest.mark.parametrize("p", [1, 2, 3, 4, 5, 8])
 def test_program_invariants_and_no_deadlock(kind, p):
     for m in range(1, 4 * p + 5):
@@ -189,7 +189,7 @@ def test_rstp_phase_claims(p):
     assert sc.action_str(first) == "FBS1 f2 b1"
 
 
-@pytest.mark.parametrize("kind", [sc.STP, sc.STP_NOBRAID, sc.ONEF1B_I, sc.ONEF1B_I_NAIVE, sc.ZB])
+@pytest.mark.parametrize("kind", [sc.STP, sc.STP_NOBRAID, sc.ONEF1B_I, sc.ONEF1B_I_NAIVE, sc.ZB, sc.STP_MEM])
 @pytest.mark.parametrize("p,lay", [(1, [2, 1]), (2, [1, 1, 1, 1]), (2, [2, 1, 2, 1]), (3, [1] * 6)])
 def test_unit_expansion_invariants(kind, p, lay):
     m = 2 * p
@@ -265,7 +265,7 @@ def test_simulated_8gpu_rows_from_measured_units():
 # ---------------------------------------------------------------------------
 # simulate_durations / program_order_peak pins (VERDICT r1 "unpinned oracle parts")
 
-ALL_KINDS = [sc.STP, sc.ONEF1B_I, sc.ZB, sc.STP_NOBRAID, sc.STP_NOSEP, sc.ONEF1B_I_NAIVE]
+ALL_KINDS = [sc.STP, sc.ONEF1B_I, sc.ZB, sc.STP_NOBRAID, sc.STP_NOSEP, sc.ONEF1B_I_NAIVE, sc.STP_MEM]
 
 
 @pytest.mark.parametrize("kind", ALL_KINDS)
@@ -363,3 +363,37 @@ def test_simulate_durations_pp_latency_plain_1f1b(p):
     base = sm.simulate_durations(sc.ONEF1B, p, progs, durs)
     assert base == pytest.approx(m * (F + B) + (p - 1) * (F + B))
     assert sm.simulate_durations(sc.ONEF1B, p, progs, durs, pp_latency=c) >= base + 2 * (p - 1) * c - 1e-9
+
+
+# ---------------------------------------------------------------------------
+# Ours^ (STP-MEM, reading R3): the paper's claims about schedule (d)
+
+
+@pytest.mark.parametrize("p", [1, 2, 3, 4, 8])
+def test_stp_mem_app_a_braids_and_separation(p):
+    """App. A: every overlapped F&B pairs a forward microbatch index
+    greater than the backward one, the backward is decoupled from W (FBS, no FB
+    / BFULL), and each chunk's first action on a device is a lone forward (the
+    'additional forward pass ... before the overlapped F&B execution')."""
+    m = 4 * p
+    for d, acts in enumerate(sc.build_program(sc.STP_MEM, p, m)):
+        assert not [a for a in acts if a[0] in (sc.A_FB, sc.A_BFULL)]
+        assert all(a[2] > a[3] for a in acts if a[0] == sc.A_FBS)
+        for c in (0, 1):
+            first = next(a for a in acts if a[1] == c and a[0] != sc.A_W)
+            assert first[0] in (sc.A_F, sc.A_FW) and first[2] == 1
+
+
+@pytest.mark.parametrize("p,m", [(2, 8), (2, 16), (4, 12), (4, 16), (4, 32), (8, 32)])
+def test_stp_mem_app_b_memory_and_bubbles(p, m):
+    """App. B: schedule (d) 'has a lower peak memory footprint
+    compared to our standard schedule (c)' -- at most ZB-V's 2p (Table 1) vs
+    Ours' 3p -- 'it introduces additional PP bubbles' (longer makespan than
+    (c) under the Table 1 cost model) and it still hides part of the TP
+    communication ('large TP overheads'): less exposed than ZB-V's 4m T_AR."""
+    costs = (10.0, 12.0, 8.0, 4.0)
+    mem = sm.simulate(sc.STP_MEM, p, sc.build_program(sc.STP_MEM, p, m), *costs)
+    ours = sm.simulate(sc.STP, p, sc.build_program(sc.STP, p, m), *costs)
+    assert max(mem["peak"]) <= 2 * p < max(ours["peak"]) == 3 * p
+    assert mem["makespan"] > ours["makespan"]
+    assert max(mem["exposed"]) < 4 * m * costs[3]

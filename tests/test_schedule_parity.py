@@ -8,7 +8,8 @@ import pytest
 
 from oracle import schedule as sc
 
-GRID = [(k, p, m) for k in (sc.STP, sc.STP_NOSEP, sc.STP_NOBRAID, sc.ZB, sc.ONEF1B_I, sc.ONEF1B_I_NAIVE, sc.ONEF1B)
+GRID = [(k, p, m) for k in (sc.STP, sc.STP_NOSEP, sc.STP_NOBRAID, sc.ZB, sc.ONEF1B_I, sc.ONEF1B_I_NAIVE, sc.ONEF1B,
+                            sc.STP_MEM)
         for p in (1, 2, 3, 4, 8) for m in (1, 2, 3, 4, 5, 8, 12, 16, 4 * p + 3)
         if not (k in (sc.ONEF1B_I, sc.ONEF1B_I_NAIVE) and m % p)]
 
@@ -96,7 +97,7 @@ def _cpp_text_mllm(kind, p, m, t, lay):
         L.lib.stp_free_schedule(h)
 
 
-MLLM_GRID = [(k, p, m) for k in (sc.STP, sc.STP_NOSEP, sc.STP_NOBRAID, sc.ZB, sc.ONEF1B_I)
+MLLM_GRID = [(k, p, m) for k in (sc.STP, sc.STP_NOSEP, sc.STP_NOBRAID, sc.ZB, sc.ONEF1B_I, sc.STP_MEM)
              for p in (1, 2, 4) for m in (1, 4, 8, 16) if not (k == sc.ONEF1B_I and m % p)]
 
 

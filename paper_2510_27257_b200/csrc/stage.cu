@@ -132,6 +132,18 @@ struct SlotLayer {
   void *xn = nullptr, *qkv = nullptr, *o = nullptr, *x1 = nullptr, *xn2 = nullptr, *gu = nullptr, *hh = nullptr,
        *xres = nullptr, *dy_attn = nullptr, *dqkv = nullptr, *dy_mlp = nullptr;
   float *lse = nullptr, *rstd1 = nullptr, *rstd2 = nullptr;
+  // activation offloading (§4.3): [gu | hh] of an offloaded layer lives in a
+  // pool block from F_MLP until its D2H copy, in host memory until the reload
+  // before the backward, and in a pool block again until W_MLP
+  int blk = -1;
+  void* host = nullptr;
+  cudaEvent_t ev_d2h = nullptr, ev_h2d = nullptr;
+};
+
+struct OffBlock {
+  void* dev = nullptr;
+  cudaEvent_t ev = nullptr;  // the last reader / writer of the previous occupant
+  bool ev_valid = false, busy = false;
 };
 
 struct Slot {
@@ -188,6 +200,17 @@ struct stp_stage {
   const void* patches = nullptr;
   void *vrtmp = nullptr, *vntmp = nullptr, *vdtmp_h = nullptr, *vdtmp_o = nullptr, *vdtmp_m = nullptr,
        *vattn_ws = nullptr;
+  // activation offloading (§4.3, STP_OFFLOAD_ALPHA): the MLP
+  // activations [gu | hh] of the first off_n layers of chunk 0 go to pinned
+  // host memory after their forward and come back before their backward
+  float off_alpha = 0.f;
+  int off_n = 0;
+  size_t off_bytes = 0;
+  std::vector<stp::OffBlock> off_pool;
+  cudaStream_t s_d2h = nullptr, s_h2d = nullptr;
+  std::vector<void*> host_allocs;
+  std::map<std::pair<int, int>, bool> off_reloaded;  // (chunk, mb) -> reload issued this pass
+  int64_t off_d2h_bytes = 0, off_h2d_bytes = 0;
   // chunks
   std::vector<stp::Chunk> chunks;
   // streams / comms
@@ -343,8 +366,12 @@ void carve_slot(stp_stage* S, const Chunk& C, Slot& sl, Carver& cv) {
     L.rstd2 = (float*)cv.take(S->sl * 4);
     L.x1 = cv.take(shard * es);
     L.xn2 = cv.take(s * h * es);
-    L.gu = cv.take(s * 2 * S->fi * es);  // backward overwrites it with dGU
-    L.hh = cv.take(s * S->fi * es);
+    if (C.c == 0 && !C.vit && j < S->off_n) {
+      L.gu = L.hh = nullptr;  // pool block while on the device (offloaded layer)
+    } else {
+      L.gu = cv.take(s * 2 * S->fi * es);  // backward overwrites it with dGU
+      L.hh = cv.take(s * S->fi * es);
+    }
     L.xres = cv.take(shard * es);
     L.dy_attn = cv.take(s * h * es);
     L.dqkv = cv.take(s * S->qkv_w * es);
@@ -884,6 +911,75 @@ stp_status vit_cb(stp_stage* S, const Chunk& C, const stp_unit& u, Slot* sl) {
   return STP_OK;
 }
 
+// ------------------------------------------------------ activation offload
+// PAPER.md §4.3: "the saved activations required for the weight
+// gradients are offloaded to the CPU in parallel with the computation streams
+// and reloaded when necessary"; chunk-0 activations, whose lifespan is long,
+// are the target, chunk 1 is never offloaded.  Reading R4:
+// alpha = the fraction of chunk 0's layers whose MLP activations [gu | hh]
+// (60% of a layer's stash) are offloaded, the earliest layers first (their
+// backward comes last); D2H right after the layer's F_MLP, H2D for all of a
+// microbatch's offloaded layers when its backward lane opens (CB 0), each
+// B_MLP waits for its own reload.  Separate copy streams per direction (PCIe
+// is full duplex); device memory of the offloaded tensors comes from a pool
+// sized by a dry run of the unit list.
+bool off_layer(const stp_stage* S, const Chunk& C, int j) { return S->off_n > 0 && C.c == 0 && !C.vit && j < S->off_n; }
+
+stp_status off_acquire(stp_stage* S, cudaStream_t st, int* out) {
+  for (size_t i = 0; i < S->off_pool.size(); ++i) {
+    OffBlock& b = S->off_pool[i];
+    if (b.busy) continue;
+    b.busy = true;
+    if (b.ev_valid) STP_CUDA_TRY(cudaStreamWaitEvent(st, b.ev, 0));
+    *out = (int)i;
+    return STP_OK;
+  }
+  return fail(STP_ESTATE, "offload pool exhausted (pool sizing / schedule mismatch)");
+}
+
+stp_status off_release(stp_stage* S, int blk, cudaStream_t st) {
+  OffBlock& b = S->off_pool[blk];
+  STP_CUDA_TRY(cudaEventRecord(b.ev, st));
+  b.ev_valid = true;
+  b.busy = false;
+  return STP_OK;
+}
+
+void off_bind(stp_stage* S, SlotLayer& L, int blk) {
+  L.blk = blk;
+  L.gu = S->off_pool[blk].dev;
+  L.hh = (uint8_t*)L.gu + S->s * 2 * S->fi * S->es;
+}
+
+// after F_MLP(j) of an offloaded layer: D2H of [gu | hh], block back to the pool
+stp_status off_store(stp_stage* S, Slot* sl, int j, cudaEvent_t fwd_done) {
+  SlotLayer& L = sl->L[j];
+  STP_CUDA_TRY(cudaStreamWaitEvent(S->s_d2h, fwd_done, 0));
+  STP_CUDA_TRY(cudaMemcpyAsync(L.host, L.gu, S->off_bytes, cudaMemcpyDeviceToHost, S->s_d2h));
+  STP_CUDA_TRY(cudaEventRecord(L.ev_d2h, S->s_d2h));
+  STP_TRY(off_release(S, L.blk, S->s_d2h));
+  L.blk = -1;
+  L.gu = L.hh = nullptr;
+  S->off_d2h_bytes += (int64_t)S->off_bytes;
+  return STP_OK;
+}
+
+// the backward lane of (chunk 0, mb) opens: reload every offloaded layer, the
+// last layer (first needed) first
+stp_status off_reload(stp_stage* S, Chunk& C, Slot* sl) {
+  for (int j = std::min(S->off_n, C.nl) - 1; j >= 0; --j) {
+    SlotLayer& L = sl->L[j];
+    int blk = -1;
+    STP_TRY(off_acquire(S, S->s_h2d, &blk));
+    off_bind(S, L, blk);
+    STP_CUDA_TRY(cudaStreamWaitEvent(S->s_h2d, L.ev_d2h, 0));
+    STP_CUDA_TRY(cudaMemcpyAsync(L.gu, L.host, S->off_bytes, cudaMemcpyHostToDevice, S->s_h2d));
+    STP_CUDA_TRY(cudaEventRecord(L.ev_h2d, S->s_h2d));
+    S->off_h2d_bytes += (int64_t)S->off_bytes;
+  }
+  return STP_OK;
+}
+
 // ------------------------------------------------------------ units
 stp_status vit_compute(stp_stage* S, const stp_unit& u, Slot* sl);
 stp_status unit_compute(stp_stage* S, const stp_unit& u) {
@@ -936,6 +1032,11 @@ stp_status unit_compute(stp_stage* S, const stp_unit& u) {
     case STP_U_F_MLP: {
       SlotLayer& L = sl->L[j];
       const LayerIdx& I = LI(S, u.layer);
+      if (off_layer(S, C, j)) {
+        int blk = -1;
+        STP_TRY(off_acquire(S, st, &blk));
+        off_bind(S, L, blk);
+      }
       STP_TRY(gemm_dispatch(dt, STP_GEMM_NT, STP_EPI_STORE, s, 2 * S->fi, h, L.xn2, h, P(S, I.wgu), h, L.gu,
                             2 * S->fi, nullptr, nullptr, 0, mc, st));
       STP_TRY(swiglu_fwd(dt, s, S->fi, L.gu, L.hh, st));
@@ -965,6 +1066,10 @@ stp_status unit_compute(stp_stage* S, const stp_unit& u) {
       // (STP_EPI_SWIGLU_BWD would fuse the SwiGLU backward into this GEMM's
       // epilogue; measured slower: the epilogue's [G | U] reads stall the 2-SM
       // kernel, GEMM average 1321 -> 1187 TFLOP/s.  Separate kernel kept.)
+      if (off_layer(S, C, j)) {
+        if (L.blk < 0) return fail(STP_ESTATE, "offloaded layer not reloaded before its backward");
+        STP_CUDA_TRY(cudaStreamWaitEvent(st, L.ev_h2d, 0));
+      }
       STP_TRY(gemm_dispatch(dt, STP_GEMM_NN, STP_EPI_STORE, s, S->fi, h, L.dy_mlp, h, P(S, I.wd), S->fi, S->dtmp_h,
                             S->fi, nullptr, nullptr, 0, mc, st));
       STP_TRY(swiglu_bwd(dt, s, S->fi, S->dtmp_h, L.gu, L.gu, st));  // dGU overwrites GU
@@ -1285,6 +1390,8 @@ stp_status run_step(stp_stage* S, float* h_loss, stp_step_stats* stats) {
   S->pf = S->pfb[0];
   S->pb = S->pbb[0];
   for (int i = 0; i < 2; ++i) S->pfb_pending[i] = S->pbb_pending[i] = false;
+  S->off_reloaded.clear();
+  S->off_d2h_bytes = S->off_h2d_bytes = 0;
   for (auto& C : S->chunks) {
     C.mb2slot.clear();
     for (auto& sl : C.slots) {
@@ -1312,6 +1419,15 @@ stp_status run_step(stp_stage* S, float* h_loss, stp_step_stats* stats) {
     cudaStream_t st = stream_of(S, i, u);
     if (u.dep0 >= 0) STP_CUDA_TRY(cudaStreamWaitEvent(st, S->ev_done[u.dep0], 0));
     if (u.dep1 >= 0) STP_CUDA_TRY(cudaStreamWaitEvent(st, S->ev_done[u.dep1], 0));
+    if (S->off_n > 0 && u.op == STP_U_CB && u.layer == 0 && u.chunk == 0 && !S->chunks[0].vit) {
+      auto key = std::make_pair(u.chunk, u.mb);
+      if (!S->off_reloaded[key]) {
+        Slot* osl = find_slot(S, u.chunk, u.mb);
+        if (!osl) return fail(STP_ESTATE, "reload without stash");
+        STP_TRY(off_reload(S, S->chunks[0], osl));
+        S->off_reloaded[key] = true;
+      }
+    }
     if (S->timing) STP_CUDA_TRY(cudaEventRecord(S->ev_t0[i], st));
     stp_status r = STP_OK;
     switch (u.op) {
@@ -1326,6 +1442,22 @@ stp_status run_step(stp_stage* S, float* h_loss, stp_step_stats* stats) {
       return r;
     }
     STP_CUDA_TRY(cudaEventRecord(S->ev_done[i], st));
+    if (S->off_n > 0 && u.chunk == 0 && (u.op == STP_U_F_MLP || u.op == STP_U_W_MLP)) {
+      Chunk& C0 = S->chunks[0];
+      const int j = u.layer - C0.l0;
+      if (off_layer(S, C0, j)) {
+        Slot* osl = find_slot(S, u.chunk, u.mb);
+        if (!osl) return fail(STP_ESTATE, "offload without stash");
+        if (u.op == STP_U_F_MLP) {
+          STP_TRY(off_store(S, osl, j, S->ev_done[i]));
+          S->off_reloaded[{u.chunk, u.mb}] = false;
+        } else {
+          STP_TRY(off_release(S, osl->L[j].blk, st));
+          osl->L[j].blk = -1;
+          osl->L[j].gu = osl->L[j].hh = nullptr;
+        }
+      }
+    }
     if (S->debug) {  // STP_DEBUG=1: log every unit and run it to completion
       fprintf(stderr, "[stp pp%d tp%d] unit %d/%d a%d s%d op%d l%d c%d mb%d dep%d\n", S->pp_rank, S->tp_rank, i, n,
               u.action, u.stream, u.op, u.layer, u.chunk, u.mb, u.dep0);
@@ -1366,6 +1498,11 @@ stp_status run_step(stp_stage* S, float* h_loss, stp_step_stats* stats) {
   }
   for (auto& kv : S->s_send) {
     STP_CUDA_TRY(cudaEventRecord(S->ev_end, kv.second));
+    STP_CUDA_TRY(cudaStreamWaitEvent(S->s_comm, S->ev_end, 0));
+  }
+  for (cudaStream_t cs : {S->s_d2h, S->s_h2d}) {
+    if (!cs) continue;
+    STP_CUDA_TRY(cudaEventRecord(S->ev_end, cs));
     STP_CUDA_TRY(cudaStreamWaitEvent(S->s_comm, S->ev_end, 0));
   }
   for (auto& kv : S->s_recv) {
@@ -1788,6 +1925,11 @@ static stp_status init_stage_impl(const stp_model_cfg* mc, const stp_vit_cfg* vc
     S->chunks.push_back(C);
   }
   STP_TRY(build_params(S.get()));
+  if (const char* e = getenv("STP_OFFLOAD_ALPHA")) {
+    S->off_alpha = (float)atof(e);
+    STP_CHECK_ARG(S->off_alpha >= 0.f && S->off_alpha <= 1.f, "STP_OFFLOAD_ALPHA in [0, 1]");
+    if (!S->chunks[0].vit && S->chunks.size() == 2) S->off_n = (int)std::lround(S->off_alpha * S->chunks[0].nl);
+  }
   // stash slots per chunk: program-order peak of live chunk-microbatches
   std::vector<int> cur(nchunks, 0), best(nchunks, 0);
   for (const auto& a : S->sched.ranks[S->pp_rank]) {
@@ -1809,6 +1951,45 @@ static stp_status init_stage_impl(const stp_model_cfg* mc, const stp_vit_cfg* vc
       carve_slot(S.get(), C, sl, cv);
     }
     S->peak_bytes += (int64_t)C.slot_bytes * best[C.c];
+  }
+  if (S->off_n > 0) {
+    // pool size: dry run of the unit list (acquire at F_MLP, release at the
+    // D2H issue; n_off acquires at the reload, one release per W_MLP) + 2
+    // blocks of slack so a forward does not wait for the previous D2H
+    S->off_bytes = (size_t)(S->s * 3 * S->fi) * S->es;
+    const Chunk& C0 = S->chunks[0];
+    int cur = 0, peak = 0;
+    std::map<int, bool> reloaded;
+    for (const auto& u : S->units) {
+      if (u.chunk != 0) continue;
+      const int j = u.layer - C0.l0;
+      if (u.op == STP_U_F_MLP && off_layer(S.get(), C0, j)) {
+        peak = std::max(peak, ++cur);
+        --cur;
+        reloaded[u.mb] = false;
+      } else if (u.op == STP_U_CB && u.layer == 0 && !reloaded[u.mb]) {
+        cur += std::min(S->off_n, C0.nl);
+        peak = std::max(peak, cur);
+        reloaded[u.mb] = true;
+      } else if (u.op == STP_U_W_MLP && off_layer(S.get(), C0, j)) {
+        --cur;
+      }
+    }
+    S->off_pool.resize(peak + 2);
+    for (auto& b : S->off_pool) {
+      STP_TRY(dalloc(S.get(), &b.dev, S->off_bytes));
+      STP_CUDA_TRY(cudaEventCreateWithFlags(&b.ev, cudaEventDisableTiming));
+    }
+    S->peak_bytes += (int64_t)S->off_bytes * (int64_t)S->off_pool.size();
+    for (auto& sl : S->chunks[0].slots)
+      for (int j = 0; j < std::min(S->off_n, C0.nl); ++j) {
+        void* hp = nullptr;
+        STP_CUDA_TRY(cudaHostAlloc(&hp, S->off_bytes, cudaHostAllocDefault));
+        S->host_allocs.push_back(hp);
+        sl.L[j].host = hp;
+        STP_CUDA_TRY(cudaEventCreateWithFlags(&sl.L[j].ev_d2h, cudaEventDisableTiming));
+        STP_CUDA_TRY(cudaEventCreateWithFlags(&sl.L[j].ev_h2d, cudaEventDisableTiming));
+      }
   }
   const size_t es = S->es;
   {
@@ -1868,6 +2049,10 @@ static stp_status init_stage_impl(const stp_model_cfg* mc, const stp_vit_cfg* vc
   STP_CUDA_TRY(cudaDeviceGetStreamPriorityRange(&lo, &hi));
   STP_CUDA_TRY(cudaStreamCreateWithFlags(&S->s_comp, cudaStreamNonBlocking));
   STP_CUDA_TRY(cudaStreamCreateWithPriority(&S->s_comm, cudaStreamNonBlocking, hi));
+  if (S->off_n > 0) {
+    STP_CUDA_TRY(cudaStreamCreateWithFlags(&S->s_d2h, cudaStreamNonBlocking));
+    STP_CUDA_TRY(cudaStreamCreateWithFlags(&S->s_h2d, cudaStreamNonBlocking));
+  }
   // events
   const int n = (int)S->units.size();
   S->ev_done.resize(n);
@@ -2079,6 +2264,17 @@ void stp_destroy_stage(stp_stage* st) {
     if (st->ev_pfb[i]) cudaEventDestroy(st->ev_pfb[i]);
     if (st->ev_pbb[i]) cudaEventDestroy(st->ev_pbb[i]);
   }
+  for (auto& b : st->off_pool)
+    if (b.ev) cudaEventDestroy(b.ev);
+  for (auto& C : st->chunks)
+    for (auto& sl : C.slots)
+      for (auto& L : sl.L) {
+        if (L.ev_d2h) cudaEventDestroy(L.ev_d2h);
+        if (L.ev_h2d) cudaEventDestroy(L.ev_h2d);
+      }
+  for (void* hp : st->host_allocs) cudaFreeHost(hp);
+  if (st->s_d2h) cudaStreamDestroy(st->s_d2h);
+  if (st->s_h2d) cudaStreamDestroy(st->s_h2d);
   for (auto& kv : st->s_send) cudaStreamDestroy(kv.second);
   for (auto& kv : st->s_recv) cudaStreamDestroy(kv.second);
   if (st->s_comp) cudaStreamDestroy(st->s_comp);

@@ -98,9 +98,16 @@ def pack_rank_param(name: str, P: Dict[str, np.ndarray], cfg, tp: int, r: int) -
 class Stage:
     def __init__(self, cfg, tp: int = 1, pp: int = 1, n_micro: int = 1, tp_rank: int = 0, pp_rank: int = 0,
                  dtype: str = "bf16", sched: str = "stp", layers_per_vstage: Optional[Sequence[int]] = None,
-                 device: int = 0, world_nccl_id: Optional[bytes] = None, vit=None):
+                 device: int = 0, world_nccl_id: Optional[bytes] = None, vit=None,
+                 offload_alpha: Optional[float] = None):
         """vit (stp_inputs.VitShape): MLLM stage, virtual stage 0 = ViT + merger
-        (stp_init_stage_mllm); bind the patches with bind_images()."""
+        (stp_init_stage_mllm); bind the patches with bind_images().
+        offload_alpha: activation offloading (§4.3; the library reads
+        STP_OFFLOAD_ALPHA at init): fraction of chunk 0's layers whose MLP
+        activations go to pinned host memory between forward and backward."""
+        import os
+        if offload_alpha is not None:
+            os.environ["STP_OFFLOAD_ALPHA"] = str(offload_alpha)
         self.cfg, self.tp, self.pp, self.m = cfg, tp, pp, n_micro
         self.vit = vit
         self.tp_rank, self.pp_rank, self.device = tp_rank, pp_rank, device
@@ -124,6 +131,8 @@ class Stage:
             vc = L.VitCfg(vit.hidden, vit.n_layers, vit.n_heads, vit.head_dim, vit.mlp, vit.patch_dim, vit.grid_h,
                           vit.grid_w, vit.ln_eps, vit.rope_theta)
             L.call("stp_init_stage_mllm", C.byref(mc), C.byref(vc), C.byref(pc), idbuf, device, C.byref(self.h))
+        if offload_alpha is not None:
+            del os.environ["STP_OFFLOAD_ALPHA"]
         n = C.c_int32()
         L.call("stp_stage_param_count", self.h, C.byref(n))
         self.names: List[str] = []

@@ -1,0 +1,58 @@
+"""Activation offloading (§4.3; reading R4): chunk 0's
+MLP activations of the first alpha * L_c layers go to pinned host memory after
+their forward and come back before their backward.  The arithmetic is
+untouched, so the step must be BIT-identical to the same step without
+offloading (loss and every gradient), for schedules with full, separated and
+deferred weight gradients; and it must also match the oracle.  The stash
+accounting shrinks by the offloaded bytes (minus the pool)."""
+import dataclasses
+
+import numpy as np
+import pytest
+import torch
+
+import stp_inputs as si
+from tests.stage_parity import compare, oracle_reference, rank_grads_ref
+
+pytestmark = pytest.mark.gpu
+
+
+def _step(cfg, m, dtype, sched, alpha, P, toks, tgts, lay):
+    from paper_2510_27257_b200.stage import Stage
+    st = Stage(cfg, n_micro=m, dtype=dtype, sched=sched, layers_per_vstage=lay, offload_alpha=alpha)
+    st.load_params(P)
+    loss, stats = st.step(torch.from_numpy(toks).cuda(), torch.from_numpy(tgts).cuda())
+    g = st.grads_numpy()
+    loss2, _ = st.step(torch.from_numpy(toks).cuda(), torch.from_numpy(tgts).cuda())  # pool reuse across steps
+    st.close()
+    return loss, loss2, g, stats.peak_act_bytes
+
+
+@pytest.mark.parametrize("sched", ["stp", "1f1b-i", "zb", "stp-mem"])
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+def test_offload_is_bit_identical(sched, dtype):
+    cfg = dataclasses.replace(si.TINY, n_layers=6, seq=64)
+    lay = [4, 2]
+    m = 4
+    P, toks, tgts, ref_loss, G = oracle_reference(cfg, m)
+    l0, l0b, g0, peak0 = _step(cfg, m, dtype, sched, 0.0, P, toks, tgts, lay)
+    l1, l1b, g1, peak1 = _step(cfg, m, dtype, sched, 1.0, P, toks, tgts, lay)
+    assert l0 == l1 and l0b == l1b
+    for k in g0:
+        assert np.array_equal(g0[k], g1[k]), k
+    assert peak1 < peak0
+    bad = compare(cfg, g1, rank_grads_ref(cfg, G, 1, 0), l1, ref_loss, dtype)
+    assert not bad, bad
+
+
+def test_offload_partial_alpha_qwen_shaped():
+    """alpha = 0.5 on Qwen2-7B layer shapes (bf16, tcgen05 path): identical to
+    no offloading."""
+    cfg = dataclasses.replace(si.QWEN2_7B, n_layers=4, seq=512, vocab=4096)
+    P = si.make_params(cfg, seed=4, std=0.02)
+    toks, tgts = si.make_tokens(cfg, 2, seed=9)
+    r0 = _step(cfg, 2, "bf16", "stp", 0.0, P, toks, tgts, [2, 2])
+    r1 = _step(cfg, 2, "bf16", "stp", 0.5, P, toks, tgts, [2, 2])
+    assert r0[0] == r1[0]
+    for k in r0[2]:
+        assert np.array_equal(r0[2][k], r1[2][k]), k

@@ -474,8 +474,6 @@ def ours(args):
         for sched in args.compare_scheds.split(","):
             if sched.startswith("1f1b-i") and args.m % p:
                 continue
-            if sched.startswith("zb") and args.config in MLLM_CONFIGS and False:
-                continue
             progress(f"compare: {sched}")
             stc = make_stage(sched)
             for _ in range(args.warmup):

@@ -51,7 +51,9 @@ extern "C" {
  * kernels can run beside the GEMM. */
 typedef enum { STP_GEMM_NT = 0, STP_GEMM_NN = 1, STP_GEMM_TN = 2 } stp_gemm_layout;
 typedef enum { STP_EPI_STORE = 0, STP_EPI_BIAS = 1, STP_EPI_ACCUM_F32 = 2, STP_EPI_RESID = 3,
-               STP_EPI_SWIGLU_BWD = 4 } stp_epilogue;
+               STP_EPI_SWIGLU_BWD = 4,
+               STP_EPI_STORE_CE = 5  /* internal: LM head store + fp32 CE row statistics (stp_op_lm_head_ce) */
+} stp_epilogue;
 
 stp_status stp_op_gemm(int32_t dtype, int32_t layout, int32_t epilogue,
                        int64_t M, int64_t N, int64_t K,
@@ -175,6 +177,14 @@ stp_status stp_op_ce_stats(int32_t dtype, int64_t s, int64_t Vl, const void* log
  * loss_acc (fp32 scalar) += loss_scale * sum_i (lse_i - target_logit_i). */
 stp_status stp_op_ce_combine(int64_t s, int32_t t, const float* stats_all, float* lse,
                              float* loss_acc, float loss_scale, void* stream);
+/* LM head fused with the local CE statistics (F_HEAD unit; reading Q18, fp32
+ * statistics): logits[s, Vl] = xf[s, h] W[Vl, h]^T stored in dtype (for the
+ * backward), and stats fp32 [s, 3] computed from the fp32 accumulators in the
+ * GEMM epilogue (bf16) before rounding: (row max, sum exp(z - max), target
+ * logit or 0).  ws: stp_op_lm_head_ce_ws_bytes(s, Vl) bytes of device scratch. */
+int64_t stp_op_lm_head_ce_ws_bytes(int64_t s, int64_t Vl);
+stp_status stp_op_lm_head_ce(int32_t dtype, int64_t s, int64_t Vl, int64_t h, const void* xf, const void* W,
+                             void* logits, const int32_t* tgt, int64_t v0, void* ws, float* stats, void* stream);
 /* dlogits = grad_scale * (softmax - onehot) written in place over logits. */
 stp_status stp_op_ce_grad(int32_t dtype, int64_t s, int64_t Vl, void* logits, int64_t ld,
                           const int32_t* tgt, int64_t v0, const float* lse, float grad_scale,

@@ -111,6 +111,8 @@ _SIGS = {
     "stp_op_embed_fwd": (i32, [i32, i64, i64, vp, i64, i64, vp, vp, vp]),
     "stp_op_embed_bwd": (i32, [i32, i64, i64, vp, i64, i64, vp, vp, vp]),
     "stp_op_ce_stats": (i32, [i32, i64, i64, vp, i64, vp, i64, vp, vp]),
+    "stp_op_lm_head_ce_ws_bytes": (i64, [i64, i64]),
+    "stp_op_lm_head_ce": (i32, [i32, i64, i64, i64, vp, vp, vp, vp, i64, vp, vp, vp]),
     "stp_op_ce_combine": (i32, [i64, i32, vp, vp, vp, f32, vp]),
     "stp_op_ce_grad": (i32, [i32, i64, i64, vp, i64, vp, i64, vp, f32, vp]),
     "stp_op_colsum_acc": (i32, [i32, i64, i64, vp, i64, vp, vp]),

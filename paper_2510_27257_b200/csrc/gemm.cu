@@ -43,7 +43,41 @@ struct GemmArgs {
   const void* bias;
   const void* R;
   int64_t ldr;
+  // STP_EPI_STORE_CE (LM head): fp32 cross-entropy row statistics of the
+  // accumulator before rounding, per 128-column block (ce_part [M][ce_nblk]
+  // x (max, sum exp(z - max))) and the target logit (ce_tl [M])
+  const int32_t* ce_tgt;
+  int64_t ce_v0;
+  float* ce_part;
+  float* ce_tl;
+  int ce_nblk;
 };
+
+// Running (max, sum exp) of one row over 32 fp32 accumulator columns; the
+// target logit is written by the one thread whose chunk holds it.
+__device__ __forceinline__ void ce_update(const GemmArgs& p, int row, int col, const uint32_t* v, float& m, float& l) {
+  const int nv = min(32, p.N - col);
+  float mx = -INFINITY;
+#pragma unroll
+  for (int j = 0; j < 32; ++j)
+    if (j < nv) mx = fmaxf(mx, __uint_as_float(v[j]));
+  const float mn = fmaxf(m, mx);
+  float acc = (m == -INFINITY) ? 0.f : l * __expf(m - mn);
+#pragma unroll
+  for (int j = 0; j < 32; ++j)
+    if (j < nv) acc += __expf(__uint_as_float(v[j]) - mn);
+  m = mn;
+  l = acc;
+  const int64_t tl = (int64_t)p.ce_tgt[row] - p.ce_v0 - col;
+  if (tl >= 0 && tl < nv) p.ce_tl[row] = __uint_as_float(v[tl]);
+}
+__device__ __forceinline__ void ce_flush(const GemmArgs& p, int row, int col, float& m, float& l) {
+  float* q = p.ce_part + ((int64_t)row * p.ce_nblk + col / 128) * 2;
+  q[0] = m;
+  q[1] = l;
+  m = -INFINITY;
+  l = 0.f;
+}
 
 template <int BN>
 struct Cfg {
@@ -290,13 +324,20 @@ __global__ void __launch_bounds__(256, 1)
       mbar_wait_wd(tfull + acc, acc_phase, 7, p.M, p.N, p.K);
       tc_fence_after();
       const int row = mb * BM + ew * 32 + lane;
+      float ce_m = -INFINITY, ce_l = 0.f;
 #pragma unroll 1
       for (int c0 = 0; c0 < BN; c0 += 32) {
         uint32_t v[32];
         tmem_ld_32x32b_x32(tmem_base + ((uint32_t)(ew * 32) << 16) + acc * BN + c0, v);
         tmem_wait_ld();
         const int col = nb * BN + c0;
-        if (row < p.M && col < p.N) epilogue_row32(p, row, col, v);
+        if (row < p.M && col < p.N) {
+          epilogue_row32(p, row, col, v);
+          if (p.epilogue == STP_EPI_STORE_CE) {
+            ce_update(p, row, col, v, ce_m, ce_l);
+            if ((c0 & 127) == 96 || col + 32 >= p.N) ce_flush(p, row, col, ce_m, ce_l);
+          }
+        }
       }
       tc_fence_before();
       __syncwarp();
@@ -485,13 +526,20 @@ __global__ void __launch_bounds__(256, 1)
       mbar_wait_wd(tfull + acc, acc_phase, 15, p.M, p.N, p.K);
       tc_fence_after();
       const int row = mb * BM + ew * 32 + lane;
+      float ce_m = -INFINITY, ce_l = 0.f;
 #pragma unroll 1
       for (int c0 = 0; c0 < BN; c0 += 32) {
         uint32_t v[32];
         tmem_ld_32x32b_x32(tmem_base + ((uint32_t)(ew * 32) << 16) + acc * BN + c0, v);
         tmem_wait_ld();
         const int col = nb * BN + c0;
-        if (row < p.M && col < p.N) epilogue_row32(p, row, col, v);
+        if (row < p.M && col < p.N) {
+          epilogue_row32(p, row, col, v);
+          if (p.epilogue == STP_EPI_STORE_CE) {
+            ce_update(p, row, col, v, ce_m, ce_l);
+            if ((c0 & 127) == 96 || col + 32 >= p.N) ce_flush(p, row, col, ce_m, ce_l);
+          }
+        }
       }
       tc_fence_before();
       __syncwarp();
@@ -684,13 +732,20 @@ __global__ void __launch_bounds__(256, 1)
       tc_fence_after();
       const int row = (p.n_fast ? tile / num_n2 : tile % num_m2) * 256 + (int)rank * 128 + ew * 32 + lane;
       const int nb0 = (p.n_fast ? tile % num_n2 : tile / num_m2) * 256;
+      float ce_m = -INFINITY, ce_l = 0.f;
 #pragma unroll 1
       for (int c0 = 0; c0 < 256; c0 += 32) {
         uint32_t v[32];
         tmem_ld_32x32b_x32(tmem_base + ((uint32_t)(ew * 32) << 16) + acc * 256 + c0, v);
         tmem_wait_ld();
         const int col = nb0 + c0;
-        if (row < p.M && col < p.N) epilogue_row32(p, row, col, v);
+        if (row < p.M && col < p.N) {
+          epilogue_row32(p, row, col, v);
+          if (p.epilogue == STP_EPI_STORE_CE) {
+            ce_update(p, row, col, v, ce_m, ce_l);
+            if ((c0 & 127) == 96 || col + 32 >= p.N) ce_flush(p, row, col, ce_m, ce_l);
+          }
+        }
       }
       tc_fence_before();
       __syncwarp();
@@ -915,6 +970,38 @@ stp_status launch_bf16_2sm(const GemmArgs& a, const CUtensorMap& ta, const CUten
   return STP_OK;
 }
 
+// Extra operands of the STORE_CE epilogue (set by lm_head_ce for one call).
+struct CeExtra {
+  const int32_t* tgt = nullptr;
+  int64_t v0 = 0;
+  float* part = nullptr;
+  float* tl = nullptr;
+};
+thread_local CeExtra g_ce;
+
+// stats[row] = (M, sum_b l_b exp(m_b - M), target logit) over the 128-column
+// blocks of the STORE_CE epilogue (the layout ce_stats produces).
+__global__ void ce_part_reduce(int64_t rows, int nblk, const float* __restrict__ part, const float* __restrict__ tl,
+                               float* stats) {
+  const int lane = threadIdx.x & 31;
+  const int64_t w = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (w >= rows) return;
+  const float* q = part + w * nblk * 2;
+  float m = -INFINITY;
+  for (int b = lane; b < nblk; b += 32) m = fmaxf(m, q[2 * b]);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+  float l = 0.f;
+  for (int b = lane; b < nblk; b += 32) l += q[2 * b + 1] * __expf(q[2 * b] - m);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) l += __shfl_xor_sync(0xffffffffu, l, o);
+  if (lane == 0) {
+    stats[w * 3 + 0] = m;
+    stats[w * 3 + 1] = l;
+    stats[w * 3 + 2] = tl[w];
+  }
+}
+
 stp_status gemm_bf16(int layout, int epi, int64_t M, int64_t N, int64_t K, const void* A, int64_t lda,
                      const void* B, int64_t ldb, void* Cp, int64_t ldc, const void* bias, const void* R,
                      int64_t ldr, int max_ctas, cudaStream_t st) {
@@ -961,6 +1048,18 @@ stp_status gemm_bf16(int layout, int epi, int64_t M, int64_t N, int64_t K, const
   g.bias = bias;
   g.R = R;
   g.ldr = ldr;
+  g.ce_tgt = nullptr;
+  g.ce_v0 = 0;
+  g.ce_part = nullptr;
+  g.ce_tl = nullptr;
+  g.ce_nblk = (int)((N + 127) / 128);
+  if (epi == STP_EPI_STORE_CE) {
+    if (!g_ce.tgt || !g_ce.part || !g_ce.tl) return fail(STP_EINVAL, "STORE_CE epilogue needs targets and outputs");
+    g.ce_tgt = g_ce.tgt;
+    g.ce_v0 = g_ce.v0;
+    g.ce_part = g_ce.part;
+    g.ce_tl = g_ce.tl;
+  }
   CUtensorMap ta, tb;
   stp_status s;
   if (!a_mn) s = tensor_map(&ta, A, K, M, lda, BK, BM);  // A [M, K]
@@ -1102,12 +1201,51 @@ stp_status tensor_map_heads(CUtensorMap* out, const void* ptr, int dh, int heads
   return tensor_map_heads_impl(out, ptr, dh, heads, rows, ld, box_rows);
 }
 
+stp_status ce_stats(int dtype, int64_t s, int64_t Vl, const void* logits, int64_t ld, const int32_t* tgt, int64_t v0,
+                    float* stats, cudaStream_t st);
+
+stp_status gemm_dispatch(int dtype, int layout, int epi, int64_t M, int64_t N, int64_t K, const void* A,
+                         int64_t lda, const void* B, int64_t ldb, void* C, int64_t ldc, const void* bias,
+                         const void* R, int64_t ldr, int max_ctas, cudaStream_t st);
+
+int64_t lm_head_ce_ws_bytes(int64_t s, int64_t Vl) { return (s * ((Vl + 127) / 128) * 2 + s) * 4 + 256; }
+
+// LM head with the vocab-parallel CE statistics of its fp32 accumulators
+// (reading Q18: fp32 softmax statistics): logits[s, Vl] = xf W^T (stored in
+// the model dtype for the backward) and stats[s, 3] = (row max, sum exp(z -
+// max), target logit or 0) of this rank's vocabulary rows [v0, v0 + Vl).
+stp_status lm_head_ce(int dtype, int64_t s, int64_t Vl, int64_t h, const void* xf, const void* W, void* logits,
+                      const int32_t* tgt, int64_t v0, void* ws, float* stats, int max_ctas, cudaStream_t st) {
+  if (s == 0) return STP_OK;
+  if (dtype != STP_DTYPE_BF16) {  // fp32 logits are the accumulator: plain store + stats pass
+    STP_TRY(gemm_dispatch(dtype, STP_GEMM_NT, STP_EPI_STORE, s, Vl, h, xf, h, W, h, logits, Vl, nullptr, nullptr, 0,
+                          max_ctas, st));
+    return ce_stats(dtype, s, Vl, logits, Vl, tgt, v0, stats, st);
+  }
+  const int nblk = (int)((Vl + 127) / 128);
+  float* part = (float*)ws;
+  float* tl = part + s * nblk * 2;
+  STP_CUDA_TRY(cudaMemsetAsync(tl, 0, s * 4, st));
+  g_ce.tgt = tgt;
+  g_ce.v0 = v0;
+  g_ce.part = part;
+  g_ce.tl = tl;
+  const stp_status r = gemm_dispatch(dtype, STP_GEMM_NT, STP_EPI_STORE_CE, s, Vl, h, xf, h, W, h, logits, Vl, nullptr,
+                                     nullptr, 0, max_ctas, st);
+  g_ce = CeExtra{};
+  STP_TRY(r);
+  ce_part_reduce<<<(unsigned)((s + 7) / 8), 256, 0, st>>>(s, nblk, part, tl, stats);
+  count_launch();
+  STP_LAUNCH_CHECK();
+  return STP_OK;
+}
+
 stp_status gemm_dispatch(int dtype, int layout, int epi, int64_t M, int64_t N, int64_t K, const void* A,
                          int64_t lda, const void* B, int64_t ldb, void* C, int64_t ldc, const void* bias,
                          const void* R, int64_t ldr, int max_ctas, cudaStream_t st) {
   STP_CHECK_ARG(M >= 0 && N >= 0 && K >= 0, "negative GEMM size");
   STP_CHECK_ARG(layout >= 0 && layout <= 2, "layout");
-  STP_CHECK_ARG(epi >= 0 && epi <= 4, "epilogue");
+  STP_CHECK_ARG(epi >= 0 && epi <= 5, "epilogue");
   STP_CHECK_ARG(epi != STP_EPI_SWIGLU_BWD || ldc >= 2 * N, "SWIGLU_BWD epilogue needs ldc >= 2N ([G | U] rows)");
   if (M == 0 || N == 0) return STP_OK;
   const double es = dtype == STP_DTYPE_BF16 ? 2.0 : 4.0;
@@ -1124,6 +1262,14 @@ stp_status gemm_dispatch(int dtype, int layout, int epi, int64_t M, int64_t N, i
 }
 
 }  // namespace stp
+
+extern "C" int64_t stp_op_lm_head_ce_ws_bytes(int64_t s, int64_t Vl) { return stp::lm_head_ce_ws_bytes(s, Vl); }
+
+extern "C" stp_status stp_op_lm_head_ce(int32_t dtype, int64_t s, int64_t Vl, int64_t h, const void* xf, const void* W,
+                                        void* logits, const int32_t* tgt, int64_t v0, void* ws, float* stats,
+                                        void* stream) {
+  return stp::lm_head_ce(dtype, s, Vl, h, xf, W, logits, tgt, v0, ws, stats, 0, (cudaStream_t)stream);
+}
 
 extern "C" stp_status stp_op_gemm(int32_t dtype, int32_t layout, int32_t epilogue, int64_t M, int64_t N, int64_t K,
                                   const void* A, int64_t lda, const void* B, int64_t ldb, void* C, int64_t ldc,

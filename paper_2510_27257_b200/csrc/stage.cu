@@ -79,6 +79,9 @@ stp_status tp_fused_bwd(int dtype, int64_t rows, int64_t h, const void* const* p
 stp_status rmsnorm_dgamma(int dtype, int64_t rows, int64_t h, const void* dy, const void* x, const float* rstd,
                           float* dgamma, cudaStream_t st);
 stp_status convert(int sd, int dd, int64_t n, const void* src, void* dst, cudaStream_t st);
+int64_t lm_head_ce_ws_bytes(int64_t s, int64_t Vl);
+stp_status lm_head_ce(int dtype, int64_t s, int64_t Vl, int64_t h, const void* xf, const void* W, void* logits,
+                      const int32_t* tgt, int64_t v0, void* ws, float* stats, int max_ctas, cudaStream_t st);
 // ViT first chunk (vit.cu)
 stp_status layernorm_fwd(int dtype, int64_t rows, int64_t h, const void* x, const void* resid, void* x_out,
                          const void* g, const void* b, float eps, void* y, float* mean, float* rstd, cudaStream_t st);
@@ -231,6 +234,7 @@ struct stp_stage {
   void *rtmp = nullptr, *ntmp = nullptr;           // comm-stream temps [sl, h]
   void *dtmp_h = nullptr, *dtmp_o = nullptr;       // compute temps dH [s, fi], dO [s, o_w]
   void* attn_ws = nullptr;
+  void* ce_ws = nullptr;                           // LM-head CE statistics partials
   float* dgamma = nullptr;                         // internal gamma grads (per layer ln1, ln2, + final)
   std::map<int, int> dgamma_off;                   // param index -> offset into dgamma
   int64_t dgamma_n = 0;
@@ -1044,10 +1048,10 @@ stp_status unit_compute(stp_stage* S, const stp_unit& u) {
                            nullptr, nullptr, 0, mc, st);
     }
     case STP_U_F_HEAD: {
-      STP_TRY(gemm_dispatch(dt, STP_GEMM_NT, STP_EPI_STORE, s, S->Vl, h, sl->xf, h, P(S, S->p_lm), h, sl->logits,
-                            S->Vl, nullptr, nullptr, 0, mc, st));
+      // LM head + local CE statistics from the fp32 accumulators (GEMM epilogue)
       const int32_t* tgt = S->targets + (int64_t)(u.mb - 1) * s;
-      return ce_stats(dt, s, S->Vl, sl->logits, S->Vl, tgt, vocab0(S), sl->stats, st);
+      return lm_head_ce(dt, s, S->Vl, h, sl->xf, P(S, S->p_lm), sl->logits, tgt, vocab0(S), S->ce_ws, sl->stats, mc,
+                        st);
     }
     case STP_U_B_HEAD: {
       const float scale = 1.f / ((float)s * (float)S->m);
@@ -2027,6 +2031,7 @@ static stp_status init_stage_impl(const stp_model_cfg* mc, const stp_vit_cfg* vc
   STP_TRY(dalloc(S.get(), &S->dtmp_h, S->s * S->fi * es));
   STP_TRY(dalloc(S.get(), &S->dtmp_o, S->s * S->o_w * es));
   STP_TRY(dalloc(S.get(), &S->attn_ws, attn_bwd_ws_bytes(S->s, (int)S->qh, (int)S->kh, (int)S->d)));
+  STP_TRY(dalloc(S.get(), &S->ce_ws, lm_head_ce_ws_bytes(S->s, S->Vl)));
   if (S->mllm) {
     STP_TRY(dalloc(S.get(), &S->vrtmp, S->svl * S->hv * es));
     STP_TRY(dalloc(S.get(), &S->vntmp, S->svl * S->hv * es));

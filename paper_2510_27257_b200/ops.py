@@ -141,6 +141,15 @@ def ce_stats(logits, tgt, v0, stats):
     call("stp_op_ce_stats", dt(logits), s, Vl, ptr(logits), logits.stride(0), ptr(tgt), v0, ptr(stats), stream())
 
 
+def lm_head_ce(xf, W, logits, tgt, v0, stats):
+    """logits = xf W^T (stored) + fp32 CE statistics of the accumulators -> stats [s, 3]."""
+    s_, h = xf.shape
+    Vl = W.shape[0]
+    ws = torch.empty(max(1, lib.stp_op_lm_head_ce_ws_bytes(s_, Vl)), dtype=torch.uint8, device=xf.device)
+    call("stp_op_lm_head_ce", dt(xf), s_, Vl, h, ptr(xf), ptr(W), ptr(logits), ptr(tgt), v0, ptr(ws), ptr(stats),
+         stream())
+
+
 def ce_combine(stats_all, lse, loss_acc, loss_scale):
     t, s, _ = stats_all.shape
     call("stp_op_ce_combine", s, t, ptr(stats_all), ptr(lse), ptr(loss_acc), loss_scale, stream())

@@ -238,3 +238,32 @@ def test_attention_bwd_repeatable():
     for x in outs[1:]:
         diff = (x - outs[0]).abs()
         assert (diff <= 2 ** -6 * outs[0].abs() + 1e-6).all()
+
+
+@pytest.mark.parametrize("dt", ["f32", "bf16"])
+@pytest.mark.parametrize("s,h,Vl", [(5, 64, 200), (300, 256, 1000), (1024, 3584, 4096)])
+def test_lm_head_ce_statistics_fp32(dt, s, h, Vl):
+    """F_HEAD: logits = xf W^T stored in the model dtype, and the local CE
+    statistics (row max, sum exp(z - max), target logit) from the fp32
+    accumulators (GEMM epilogue for bf16; reading Q18) -- compared with the
+    exact statistics of the fp64 product of the same (rounded) inputs, so the
+    bf16 rounding of the logits does not enter the statistics."""
+    ops = _ops()
+    x, dx_ = _in((s, h), 21, dt)
+    w, dw_ = _in((Vl, h), 22, dt, 0.05)
+    v0 = 3 * Vl
+    tgt = np.random.default_rng(23).integers(0, 4 * Vl, s).astype(np.int32)
+    z = x @ w.T
+    logits = torch.empty(s, Vl, dtype=DT[dt], device="cuda")
+    stats = torch.empty(s, 3, dtype=torch.float32, device="cuda")
+    ops.lm_head_ce(dx_, dw_, logits, torch.from_numpy(tgt).cuda(), v0, stats)
+    torch.cuda.synchronize()
+    st = _np(stats)
+    mx = z.max(axis=1)
+    se = np.exp(z - mx[:, None]).sum(axis=1)
+    own = (tgt >= v0) & (tgt < v0 + Vl)
+    tl = np.where(own, z[np.arange(s), np.clip(tgt - v0, 0, Vl - 1)], 0.0)
+    assert np.abs(st[:, 0] - mx).max() <= 1e-4 * (1 + np.abs(mx).max())
+    assert np.abs(st[:, 1] / se - 1).max() <= 1e-4
+    assert np.abs(st[:, 2] - tl).max() <= 1e-4 * (1 + np.abs(tl).max())
+    assert _rel(_np(logits), z) <= (1e-5 if dt == "f32" else 1e-2)

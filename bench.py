@@ -467,6 +467,10 @@ def ours(args):
                                     "sample": sample_desc(scfg, args.model) + f" ({dt:.1f} s), scaled by "
                                               "algorithmic FLOPs to the full workload"}
     st.close()
+    del st
+    import gc
+    gc.collect()
+    torch.cuda.empty_cache()  # the comparison stages need the memory (N = 1: ~150 GB per stage)
     if args.compare:
         # the paper's comparison (§5, Table 1) on the same kernels: every schedule,
         # same model / inputs / grid, W warm-up + K device-timed steps each
@@ -483,6 +487,9 @@ def ours(args):
             stc.set_timing(True)
             _, ts = stc.step(d_tok, d_tgt)
             stc.close()
+            del stc
+            gc.collect()
+            torch.cuda.empty_cache()
             v = torch.tensor([float(np.mean(cms)), ts.exposed_tp_ms / max(ts.step_ms, 1e-9),
                               ts.pp_bubble_ms / max(ts.step_ms, 1e-9), float(ts.peak_act_bytes)],
                              dtype=torch.float64, device="cuda")

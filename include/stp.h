@@ -63,7 +63,7 @@ typedef enum {
   STP_SCHED_STP_NOSEP = 4,
   STP_SCHED_1F1B_I_NAIVE = 5,
   STP_SCHED_1F1B = 6,
-  STP_SCHED_STP_MEM = 7   /* Ours^: memory-efficient warm-up (App. A Fig. 8b, App. B (d); reading R3) */
+  STP_SCHED_STP_MEM = 7   /* Ours^: memory-efficient warm-up (App. A Fig. 8b, App. B (d); reading R4) */
 } stp_sched_kind;
 
 /* Action kinds (Fig. 5 caption P:L112 and §4.2: F, B, W, F&B, F&W). */

@@ -29,7 +29,7 @@ Readings:
   1F1B-I-NAIVE  1F1B-I actions; every backward W unit waits for the TP
           communication of its own B unit (all TP comm synchronous).
   STP-MEM Ours^, the schedule with the memory-efficient warm-up (App. A
-          Fig. 8b, App. B schedule (d); reading R3): V-shape,
+          Fig. 8b, App. B schedule (d); reading R4): V-shape,
           list-scheduled under unit costs with ZB-V's memory budget of 2p
           chunk-microbatches; each decision prefers, in order, a braided
           F(f)&B(b) of one chunk with f > b (App. A: "the microbatch index in
@@ -254,7 +254,7 @@ def build_zb_greedy(p: int, m: int) -> List[List[Action]]:
 
 
 def build_stp_mem(p: int, m: int) -> List[List[Action]]:
-    """Ours^ (reading R3, see module doc): unit costs F = B = W = 1 (FBS and
+    """Ours^ (reading R4, see module doc): unit costs F = B = W = 1 (FBS and
     FW take 2); at every time step each idle device takes the first feasible
     choice in the order FBS > B > FW / F > W."""
     V = 2 * p

@@ -230,7 +230,7 @@ bool zb_greedy(int p, int m, std::vector<std::vector<stp_action>>& progs) {
 }
 
 // Ours^ (STP_SCHED_STP_MEM; memory-efficient warm-up, App. A Fig. 8b and
-// App. B schedule (d); reading R3): V-shape list
+// App. B schedule (d); reading R4): V-shape list
 // schedule under unit costs (F = B = W = 1, FBS / FW = 2) with ZB-V's memory
 // budget of 2p chunk-microbatches; each idle device takes the first feasible
 // of: braided F(f)&B(b) of one chunk with f > b and W deferred (FBS), lone B,

@@ -919,7 +919,7 @@ stp_status vit_cb(stp_stage* S, const Chunk& C, const stp_unit& u, Slot* sl) {
 // PAPER.md §4.3: "the saved activations required for the weight
 // gradients are offloaded to the CPU in parallel with the computation streams
 // and reloaded when necessary"; chunk-0 activations, whose lifespan is long,
-// are the target, chunk 1 is never offloaded.  Reading R4:
+// are the target, chunk 1 is never offloaded.  reading R5:
 // alpha = the fraction of chunk 0's layers whose MLP activations [gu | hh]
 // (60% of a layer's stash) are offloaded, the earliest layers first (their
 // backward comes last); D2H right after the layer's F_MLP, H2D for all of a

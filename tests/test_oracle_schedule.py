@@ -366,7 +366,7 @@ def test_simulate_durations_pp_latency_plain_1f1b(p):
 
 
 # ---------------------------------------------------------------------------
-# Ours^ (STP-MEM, reading R3): the paper's claims about schedule (d)
+# Ours^ (STP-MEM, reading R4): the paper's claims about schedule (d)
 
 
 @pytest.mark.parametrize("p", [1, 2, 3, 4, 8])

@@ -51,6 +51,12 @@ struct GemmArgs {
   float* ce_part;
   float* ce_tl;
   int ce_nblk;
+  // push mode (STORE / BIAS epilogues): row m goes to push[m / push_rows] at
+  // row push_off + m % push_rows -- the reduce-scatter of a row-parallel
+  // GEMM's partial done by the epilogue's NVLink stores into each TP peer's
+  // receive buffer (stp_gemm_push_targets)
+  void* push[8];
+  int64_t push_rows, push_off;
 };
 
 // Running (max, sum exp) of one row over 32 fp32 accumulator columns; the
@@ -166,7 +172,9 @@ __device__ __forceinline__ void epilogue_row32(const GemmArgs& p, int row, int c
       for (int j = 0; j < 32 && col + j < p.N; ++j) f[j] += __bfloat162float(r[j]);
     }
   }
-  bf16* c = reinterpret_cast<bf16*>(p.C) + (int64_t)row * p.ldc + col;
+  bf16* c = p.push_rows > 0 ? reinterpret_cast<bf16*>(p.push[row / p.push_rows]) +
+                                  (p.push_off + row % p.push_rows) * p.ldc + col
+                            : reinterpret_cast<bf16*>(p.C) + (int64_t)row * p.ldc + col;
   if (full) {
 #pragma unroll
     for (int j = 0; j < 32; j += 8) {
@@ -970,6 +978,14 @@ stp_status launch_bf16_2sm(const GemmArgs& a, const CUtensorMap& ta, const CUten
   return STP_OK;
 }
 
+// Push targets of the next bf16 GEMM on this thread (stp_gemm_push_targets).
+struct PushExtra {
+  void* ptr[8] = {};
+  int n = 0;
+  int64_t rows = 0, off = 0;
+};
+thread_local PushExtra g_push;
+
 // Extra operands of the STORE_CE epilogue (set by lm_head_ce for one call).
 struct CeExtra {
   const int32_t* tgt = nullptr;
@@ -1053,6 +1069,16 @@ stp_status gemm_bf16(int layout, int epi, int64_t M, int64_t N, int64_t K, const
   g.ce_part = nullptr;
   g.ce_tl = nullptr;
   g.ce_nblk = (int)((N + 127) / 128);
+  g.push_rows = 0;
+  g.push_off = 0;
+  if (g_push.n > 0) {
+    if (epi != STP_EPI_STORE && epi != STP_EPI_BIAS) return fail(STP_EINVAL, "push targets need a STORE/BIAS epilogue");
+    if (M != g_push.rows * g_push.n) return fail(STP_EINVAL, "push targets: M != rows * ranks");
+    for (int i = 0; i < g_push.n; ++i) g.push[i] = g_push.ptr[i];
+    g.push_rows = g_push.rows;
+    g.push_off = g_push.off;
+    g_push = PushExtra{};
+  }
   if (epi == STP_EPI_STORE_CE) {
     if (!g_ce.tgt || !g_ce.part || !g_ce.tl) return fail(STP_EINVAL, "STORE_CE epilogue needs targets and outputs");
     g.ce_tgt = g_ce.tgt;
@@ -1207,6 +1233,18 @@ stp_status ce_stats(int dtype, int64_t s, int64_t Vl, const void* logits, int64_
 stp_status gemm_dispatch(int dtype, int layout, int epi, int64_t M, int64_t N, int64_t K, const void* A,
                          int64_t lda, const void* B, int64_t ldb, void* C, int64_t ldc, const void* bias,
                          const void* R, int64_t ldr, int max_ctas, cudaStream_t st);
+
+// The next bf16 GEMM on this thread stores row m of C into
+// ptrs[m / rows] + (off + m % rows) * ldc (n <= 8 targets, C unused): the
+// row-parallel GEMM writes its partial directly into the TP peers' receive
+// buffers over NVLink (the reduce-scatter's transfer fused into the epilogue).
+void gemm_push_targets(void* const* ptrs, int n, int64_t rows, int64_t off) {
+  g_push = PushExtra{};
+  for (int i = 0; i < n && i < 8; ++i) g_push.ptr[i] = ptrs[i];
+  g_push.n = n;
+  g_push.rows = rows;
+  g_push.off = off;
+}
 
 int64_t lm_head_ce_ws_bytes(int64_t s, int64_t Vl) { return (s * ((Vl + 127) / 128) * 2 + s) * 4 + 256; }
 

@@ -80,6 +80,7 @@ stp_status rmsnorm_dgamma(int dtype, int64_t rows, int64_t h, const void* dy, co
                           float* dgamma, cudaStream_t st);
 stp_status convert(int sd, int dd, int64_t n, const void* src, void* dst, cudaStream_t st);
 int64_t lm_head_ce_ws_bytes(int64_t s, int64_t Vl);
+void gemm_push_targets(void* const* ptrs, int n, int64_t rows, int64_t off);
 stp_status lm_head_ce(int dtype, int64_t s, int64_t Vl, int64_t h, const void* xf, const void* W, void* logits,
                       const int32_t* tgt, int64_t v0, void* ws, float* stats, int max_ctas, cudaStream_t st);
 // ViT first chunk (vit.cu)
@@ -254,6 +255,12 @@ struct stp_stage {
   cudaEvent_t ev_pfb[2] = {nullptr, nullptr}, ev_pbb[2] = {nullptr, nullptr};
   bool pfb_pending[2] = {false, false}, pbb_pending[2] = {false, false};
   bool pf_pending = false, pb_pending = false;  // the current comm phase read pf / pb
+  // p2p push mode (STP_P2P_PUSH): the row-parallel GEMM of a unit writes row
+  // block q of its partial into TP peer q's partial buffer at this rank's slice
+  // (the reduce-scatter's NVLink transfer in the GEMM epilogue); pf_push /
+  // pb_push: the current partial was pushed (the comm phase then reads t local
+  // slices instead of pulling the peers' rows)
+  bool p2p_push = false, pf_push = false, pb_push = false;
   // copy-engine TP transport (STP_TP_TRANSPORT=ce; tpcomm.cu)
   bool ce = false, ce_spin = false;
   bool p2p = false;              // STP_TP_TRANSPORT=p2p: fused NVLink load/store kernels instead of copy engines
@@ -524,6 +531,10 @@ stp_status ce_ag_shard(stp_stage* S, const void* shard, void* dst) {
 // free), B(c) after it (every peer's rows have landed here).
 int p2p_pieces(stp_stage* S, const void* partial, const void** pieces) {
   const size_t bytes = (size_t)(S->sl * S->h) * S->es;
+  if ((partial == S->pf && S->pf_push) || (partial == S->pb && S->pb_push)) {
+    for (int q = 0; q < S->t; ++q) pieces[q] = (const uint8_t*)partial + q * bytes;  // slice q: rank q's rows
+    return S->t;
+  }
   for (int q = 0; q < S->t; ++q) {
     const uint8_t* b = q == S->tp_rank ? (const uint8_t*)partial : sym_peer_ptr(S, q, partial);
     pieces[q] = b ? b + S->tp_rank * bytes : nullptr;
@@ -985,6 +996,26 @@ stp_status off_reload(stp_stage* S, Chunk& C, Slot* sl) {
 }
 
 // ------------------------------------------------------------ units
+
+// Before a unit's row-parallel GEMM: in push mode, target every TP rank's copy
+// of the partial buffer (row block q -> rank q, at this rank's slice).
+stp_status push_partial(stp_stage* S, void* partial, bool* pushed) {
+  *pushed = false;
+  if (!S->p2p_push) return STP_OK;
+  void* ptrs[8];
+  for (int q = 0; q < S->t; ++q) {
+    ptrs[q] = q == S->tp_rank ? partial : sym_peer_ptr(S, q, partial);
+    if (!ptrs[q]) return fail(STP_ESTATE, "push target not in the symmetric set");
+  }
+  gemm_push_targets(ptrs, S->t, S->sl, (int64_t)S->tp_rank * S->sl);
+  *pushed = true;
+  return STP_OK;
+}
+stp_status push_done(stp_stage* S, stp_status r) {
+  if (S->p2p_push) gemm_push_targets(nullptr, 0, 0, 0);  // never leak targets into a later GEMM
+  return r;
+}
+
 stp_status vit_compute(stp_stage* S, const stp_unit& u, Slot* sl);
 stp_status unit_compute(stp_stage* S, const stp_unit& u) {
   Chunk& C = chunk_of(S, u.chunk);
@@ -1017,6 +1048,7 @@ stp_status unit_compute(stp_stage* S, const stp_unit& u) {
   const int j = u.layer - C.l0;
   switch (u.op) {
     case STP_U_F_EMB: {
+      S->pf_push = false;
       const int32_t* tok = S->tokens + (int64_t)(u.mb - 1) * s;
       return embed_fwd(dt, s, h, tok, vocab0(S), S->Vl, P(S, S->p_embed), S->pf, st);
     }
@@ -1030,8 +1062,9 @@ stp_status unit_compute(stp_stage* S, const stp_unit& u) {
       const uint8_t* q = (const uint8_t*)L.qkv;
       STP_TRY(attn_fwd(dt, s, (int)S->qh, (int)S->kh, (int)S->d, 1, q, q + S->qh * S->d * S->es,
                        q + (S->qh + S->kh) * S->d * S->es, S->qkv_w, L.o, S->o_w, L.lse, st));
-      return gemm_dispatch(dt, STP_GEMM_NT, STP_EPI_STORE, s, h, S->o_w, L.o, S->o_w, P(S, I.wo), S->o_w, S->pf, h,
-                           nullptr, nullptr, 0, mc, st);
+      STP_TRY(push_partial(S, S->pf, &S->pf_push));
+      return push_done(S, gemm_dispatch(dt, STP_GEMM_NT, STP_EPI_STORE, s, h, S->o_w, L.o, S->o_w, P(S, I.wo), S->o_w, S->pf, h,
+                           nullptr, nullptr, 0, mc, st));
     }
     case STP_U_F_MLP: {
       SlotLayer& L = sl->L[j];
@@ -1044,8 +1077,9 @@ stp_status unit_compute(stp_stage* S, const stp_unit& u) {
       STP_TRY(gemm_dispatch(dt, STP_GEMM_NT, STP_EPI_STORE, s, 2 * S->fi, h, L.xn2, h, P(S, I.wgu), h, L.gu,
                             2 * S->fi, nullptr, nullptr, 0, mc, st));
       STP_TRY(swiglu_fwd(dt, s, S->fi, L.gu, L.hh, st));
-      return gemm_dispatch(dt, STP_GEMM_NT, STP_EPI_STORE, s, h, S->fi, L.hh, S->fi, P(S, I.wd), S->fi, S->pf, h,
-                           nullptr, nullptr, 0, mc, st);
+      STP_TRY(push_partial(S, S->pf, &S->pf_push));
+      return push_done(S, gemm_dispatch(dt, STP_GEMM_NT, STP_EPI_STORE, s, h, S->fi, L.hh, S->fi, P(S, I.wd), S->fi, S->pf, h,
+                           nullptr, nullptr, 0, mc, st));
     }
     case STP_U_F_HEAD: {
       // LM head + local CE statistics from the fp32 accumulators (GEMM epilogue)
@@ -1058,8 +1092,9 @@ stp_status unit_compute(stp_stage* S, const stp_unit& u) {
       const int32_t* tgt = S->targets + (int64_t)(u.mb - 1) * s;
       STP_TRY(ce_combine(s, S->t, sl->stats_all, sl->lse_ce, S->loss_acc, scale, st));
       STP_TRY(ce_grad(dt, s, S->Vl, sl->logits, S->Vl, tgt, vocab0(S), sl->lse_ce, scale, st));
-      return gemm_dispatch(dt, STP_GEMM_NN, STP_EPI_STORE, s, h, S->Vl, sl->logits, S->Vl, P(S, S->p_lm), h, S->pb,
-                           h, nullptr, nullptr, 0, mc, st);
+      STP_TRY(push_partial(S, S->pb, &S->pb_push));
+      return push_done(S, gemm_dispatch(dt, STP_GEMM_NN, STP_EPI_STORE, s, h, S->Vl, sl->logits, S->Vl, P(S, S->p_lm), h, S->pb,
+                           h, nullptr, nullptr, 0, mc, st));
     }
     case STP_U_W_HEAD:
       return gemm_dispatch(dt, STP_GEMM_TN, STP_EPI_ACCUM_F32, S->Vl, h, s, sl->logits, S->Vl, sl->xf, h,
@@ -1077,8 +1112,9 @@ stp_status unit_compute(stp_stage* S, const stp_unit& u) {
       STP_TRY(gemm_dispatch(dt, STP_GEMM_NN, STP_EPI_STORE, s, S->fi, h, L.dy_mlp, h, P(S, I.wd), S->fi, S->dtmp_h,
                             S->fi, nullptr, nullptr, 0, mc, st));
       STP_TRY(swiglu_bwd(dt, s, S->fi, S->dtmp_h, L.gu, L.gu, st));  // dGU overwrites GU
-      return gemm_dispatch(dt, STP_GEMM_NN, STP_EPI_STORE, s, h, 2 * S->fi, L.gu, 2 * S->fi, P(S, I.wgu), h, S->pb,
-                           h, nullptr, nullptr, 0, mc, st);
+      STP_TRY(push_partial(S, S->pb, &S->pb_push));
+      return push_done(S, gemm_dispatch(dt, STP_GEMM_NN, STP_EPI_STORE, s, h, 2 * S->fi, L.gu, 2 * S->fi, P(S, I.wgu), h, S->pb,
+                           h, nullptr, nullptr, 0, mc, st));
     }
     case STP_U_W_MLP: {
       SlotLayer& L = sl->L[j];
@@ -1099,8 +1135,9 @@ stp_status unit_compute(stp_stage* S, const stp_unit& u) {
       STP_TRY(attn_bwd(dt, s, (int)S->qh, (int)S->kh, (int)S->d, 1, q, q + ko, q + vo, S->qkv_w, L.o, S->o_w,
                        S->dtmp_o, L.lse, dq, dq + ko, dq + vo, S->qkv_w, S->attn_ws, st));
       STP_TRY(rope(dt, 1, s, S->qkv_w, 0, (int)(S->qh + S->kh), (int)S->d, S->mc.rope_theta, 0, L.dqkv, st));
-      return gemm_dispatch(dt, STP_GEMM_NN, STP_EPI_STORE, s, h, S->qkv_w, L.dqkv, S->qkv_w, P(S, I.wqkv), h, S->pb,
-                           h, nullptr, nullptr, 0, mc, st);
+      STP_TRY(push_partial(S, S->pb, &S->pb_push));
+      return push_done(S, gemm_dispatch(dt, STP_GEMM_NN, STP_EPI_STORE, s, h, S->qkv_w, L.dqkv, S->qkv_w, P(S, I.wqkv), h, S->pb,
+                           h, nullptr, nullptr, 0, mc, st));
     }
     case STP_U_W_ATTN: {
       SlotLayer& L = sl->L[j];
@@ -2006,6 +2043,8 @@ static stp_status init_stage_impl(const stp_model_cfg* mc, const stp_vit_cfg* vc
     S->p2p = S->ce && tr == "p2p";
     if (S->mllm && S->ce)
       return fail(STP_EUNSUPPORTED, "MLLM stages with tp > 1 need STP_TP_TRANSPORT=nccl (ViT phases use NCCL RS/AG)");
+    const char* pu = getenv("STP_P2P_PUSH");
+    S->p2p_push = S->p2p && S->dtype == STP_DTYPE_BF16 && S->t <= 8 && pu && atoi(pu) > 0;
     const char* w = getenv("STP_CE_WAIT");
     S->ce_spin = w && std::string(w) == "spin";
   }

@@ -87,3 +87,22 @@ def test_multi_rank_mllm_parity(tp, pp, sched, dtype):
                            env={"STP_TP_TRANSPORT": "nccl"})
     assert rc == 0, out[-4000:]
     assert out.count("PASS") == n, out[-4000:]
+
+
+# p2p transport with the reduce-scatter's transfer fused into the row-parallel
+# GEMMs' epilogues (STP_P2P_PUSH=1: each rank's O / FC2 / dgrad GEMM stores row
+# block q of its partial into TP peer q's partial buffer over NVLink).
+PUSH_CASES = [(2, 1, "stp", "bf16"), (2, 2, "stp", "bf16"), (4, 1, "stp", "bf16"), (4, 1, "1f1b-i", "bf16"),
+              (2, 2, "zb", "bf16")]
+
+
+@pytest.mark.parametrize("tp,pp,sched,dtype", PUSH_CASES)
+def test_multi_rank_parity_gemm_push(tp, pp, sched, dtype):
+    n = tp * pp
+    if torch.cuda.device_count() < n:
+        pytest.skip(f"needs {n} GPUs")
+    args = ["--tp", str(tp), "--pp", str(pp), "--sched", sched, "--dtype", dtype, "--seq", "64",
+            "--n-micro", str(2 * pp if sched != "stp" else 4)]
+    rc, out = run_torchrun(n, args, 30100 + 7 * tp + 3 * pp + len(sched), env={"STP_P2P_PUSH": "1"})
+    assert rc == 0, out[-4000:]
+    assert out.count("PASS") == n, out[-4000:]

@@ -26,6 +26,7 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <array>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -245,7 +246,13 @@ struct stp_stage {
   // events
   std::vector<cudaEvent_t> ev_done;
   std::vector<cudaEvent_t> ev_t0, ev_t1;  // timing
-  cudaEvent_t ev_base = nullptr, ev_end = nullptr, ev_caller = nullptr;
+  cudaEvent_t ev_base = nullptr, ev_end = nullptr, ev_caller = nullptr, ev_join = nullptr;
+  float* h_loss_pin = nullptr;  // pinned: the step's loss read-back (a fixed address for graph replay)
+  // CUDA-graph replay of the step (STP_GRAPH=1)
+  bool use_graph = false;
+  cudaGraphExec_t graph_exec = nullptr;
+  std::array<const void*, 3> graph_key{};
+  int64_t graph_launches = 0, steps_done = 0;
   // partial buffers: one per lane with NCCL (the collective copies it out
   // before it completes), two per lane with the copy-engine transport (peers
   // pull from them; see ce_* below).  ev_*b[i]: the comm phase that last read
@@ -1419,11 +1426,7 @@ bool is_last_w(stp_stage* S, const stp_unit& u) {
   return u.op == STP_U_W_ATTN && u.layer == C.l0;
 }
 
-stp_status run_step(stp_stage* S, float* h_loss, stp_step_stats* stats) {
-  if (S->poisoned) return fail(STP_ESTATE, "stage poisoned by an earlier CUDA/NCCL error");
-  if (!S->bound) return fail(STP_ESTATE, "stp_bind_params not called");
-  STP_CUDA_TRY(cudaSetDevice(S->dev));
-  const int64_t launches0 = g_kernel_launches;
+void reset_step_state(stp_stage* S) {
   S->ev_pool_next = 0;
   S->trace.clear();
   S->pf_pending = S->pb_pending = false;
@@ -1438,8 +1441,15 @@ stp_status run_step(stp_stage* S, float* h_loss, stp_step_stats* stats) {
     for (auto& sl : C.slots) {
       sl.busy = false;
       sl.mb = -1;
+      sl.free_events.clear();  // the previous step has completed (run_step synchronises)
     }
   }
+  for (auto& b : S->off_pool) b.ev_valid = false;
+}
+
+// Enqueue one whole step on the stage's streams (everything joins back into
+// s_comp at the end), eagerly or inside a CUDA-graph capture of s_comp.
+stp_status enqueue_step(stp_stage* S) {
   // start: everything after whatever the caller enqueued before
   STP_CUDA_TRY(cudaEventRecord(S->ev_base, S->s_comp));
   STP_CUDA_TRY(cudaStreamWaitEvent(S->s_comm, S->ev_base, 0));
@@ -1551,16 +1561,60 @@ stp_status run_step(stp_stage* S, float* h_loss, stp_step_stats* stats) {
     STP_CUDA_TRY(cudaStreamWaitEvent(S->s_comm, S->ev_end, 0));
   }
   STP_CUDA_TRY(cudaEventRecord(S->ev_end, S->s_comm));
-  float loss = 0.f;
-  STP_CUDA_TRY(cudaMemcpyAsync(&loss, S->loss_acc, sizeof(float), cudaMemcpyDeviceToHost, S->s_comm));
-  cudaError_t e = cudaStreamSynchronize(S->s_comm);
+  STP_CUDA_TRY(cudaMemcpyAsync(S->h_loss_pin, S->loss_acc, sizeof(float), cudaMemcpyDeviceToHost, S->s_comm));
+  STP_CUDA_TRY(cudaEventRecord(S->ev_join, S->s_comm));
+  STP_CUDA_TRY(cudaStreamWaitEvent(S->s_comp, S->ev_join, 0));
+  return STP_OK;
+}
+
+// One step: eager enqueue, or (STP_GRAPH=1, not in timing / debug mode) the
+// step captured once as a CUDA graph over all of the stage's streams and
+// replayed while the device inputs (tokens, targets, patches) stay the same.
+stp_status run_step(stp_stage* S, float* h_loss, stp_step_stats* stats) {
+  if (S->poisoned) return fail(STP_ESTATE, "stage poisoned by an earlier CUDA/NCCL error");
+  if (!S->bound) return fail(STP_ESTATE, "stp_bind_params not called");
+  STP_CUDA_TRY(cudaSetDevice(S->dev));
+  const int64_t launches0 = g_kernel_launches;
+  const int n = (int)S->units.size();
+  const bool graph = S->use_graph && !S->timing && !S->debug;
+  const std::array<const void*, 3> key{S->tokens, S->targets, S->patches};
+  if (graph && S->graph_exec && S->graph_key == key) {
+    STP_CUDA_TRY(cudaGraphLaunch(S->graph_exec, S->s_comp));
+    g_kernel_launches += S->graph_launches;
+  } else if (graph && S->steps_done > 0) {  // first step eager: lazily created tables / counters exist
+    if (S->graph_exec) {
+      cudaGraphExecDestroy(S->graph_exec);
+      S->graph_exec = nullptr;
+    }
+    reset_step_state(S);
+    STP_CUDA_TRY(cudaStreamBeginCapture(S->s_comp, cudaStreamCaptureModeRelaxed));
+    const stp_status r = enqueue_step(S);
+    cudaGraph_t g = nullptr;
+    const cudaError_t ec = cudaStreamEndCapture(S->s_comp, &g);
+    if (r != STP_OK || ec != cudaSuccess || !g) {
+      if (g) cudaGraphDestroy(g);
+      cudaGetLastError();
+      return r != STP_OK ? r : fail(STP_ECUDA, std::string("step capture: ") + cudaGetErrorString(ec));
+    }
+    const cudaError_t ei = cudaGraphInstantiate(&S->graph_exec, g, 0);
+    cudaGraphDestroy(g);
+    if (ei != cudaSuccess) return fail(STP_ECUDA, std::string("graph instantiate: ") + cudaGetErrorString(ei));
+    S->graph_key = key;
+    S->graph_launches = g_kernel_launches - launches0;
+    STP_CUDA_TRY(cudaGraphLaunch(S->graph_exec, S->s_comp));
+  } else {
+    reset_step_state(S);
+    STP_TRY(enqueue_step(S));
+  }
+  ++S->steps_done;
+  cudaError_t e = cudaStreamSynchronize(S->s_comp);
   if (e != cudaSuccess) {
     S->poisoned = true;
     return fail(STP_ECUDA, std::string("step failed: ") + cudaGetErrorString(e));
   }
   STP_CUDA_TRY(cudaDeviceSynchronize());
   const bool holds_loss = S->chunks.back().last || S->chunks.front().last;
-  if (h_loss) *h_loss = holds_loss ? loss : 0.f;
+  if (h_loss) *h_loss = holds_loss ? *S->h_loss_pin : 0.f;
   S->launches_step = g_kernel_launches - launches0;
   if (stats) {
     memset(stats, 0, sizeof(*stats));
@@ -2110,6 +2164,13 @@ static stp_status init_stage_impl(const stp_model_cfg* mc, const stp_vit_cfg* vc
   STP_CUDA_TRY(cudaEventCreate(&S->ev_base));
   STP_CUDA_TRY(cudaEventCreateWithFlags(&S->ev_caller, cudaEventDisableTiming));
   STP_CUDA_TRY(cudaEventCreate(&S->ev_end));
+  STP_CUDA_TRY(cudaEventCreateWithFlags(&S->ev_join, cudaEventDisableTiming));
+  STP_CUDA_TRY(cudaHostAlloc((void**)&S->h_loss_pin, sizeof(float), cudaHostAllocDefault));
+  *S->h_loss_pin = 0.f;
+  // Graph replay needs replay-invariant synchronisation: the p2p / ce
+  // transports' flag handshakes compare against phase numbers that grow every
+  // step, so graphs are used with TP = 1 or the NCCL transport only.
+  if (const char* e = getenv("STP_GRAPH")) S->use_graph = atoi(e) > 0 && !S->ce;
   for (int i = 0; i < 2; ++i) {
     STP_CUDA_TRY(cudaEventCreateWithFlags(&S->ev_pfb[i], cudaEventDisableTiming));
     STP_CUDA_TRY(cudaEventCreateWithFlags(&S->ev_pbb[i], cudaEventDisableTiming));
@@ -2304,6 +2365,9 @@ void stp_destroy_stage(stp_stage* st) {
   if (st->ev_base) cudaEventDestroy(st->ev_base);
   if (st->ev_caller) cudaEventDestroy(st->ev_caller);
   if (st->ev_end) cudaEventDestroy(st->ev_end);
+  if (st->ev_join) cudaEventDestroy(st->ev_join);
+  if (st->graph_exec) cudaGraphExecDestroy(st->graph_exec);
+  if (st->h_loss_pin) cudaFreeHost(st->h_loss_pin);
   for (int i = 0; i < 2; ++i) {
     if (st->ev_pfb[i]) cudaEventDestroy(st->ev_pfb[i]);
     if (st->ev_pbb[i]) cudaEventDestroy(st->ev_pbb[i]);

@@ -98,3 +98,27 @@ def test_timing_stats():
     assert len(t0) == stats.n_units and all(b >= a for a, b in zip(t0, t1))
     assert stats.step_ms > 0 and stats.compute_busy_ms > 0
     st.close()
+
+
+@pytest.mark.parametrize("sched", ["stp", "1f1b-i", "zb"])
+def test_cuda_graph_replay_matches_eager(sched, monkeypatch):
+    """STP_GRAPH=1: the first step runs eagerly, the second is captured as one
+    CUDA graph over every stream of the stage and launched, later steps replay
+    it.  Three steps accumulate the same loss and gradients as three eager
+    steps (to 1e-6: fp32-atomic accumulations are order-nondeterministic)."""
+    from paper_2510_27257_b200.stage import Stage
+    cfg = dataclasses.replace(si.TINY, seq=64)
+    P, toks, tgts, ref_loss, G = oracle_reference(cfg, 4)
+    dt, dg = torch.from_numpy(toks).cuda(), torch.from_numpy(tgts).cuda()
+    out = []
+    for graph in ("0", "1"):
+        monkeypatch.setenv("STP_GRAPH", graph)
+        st = Stage(cfg, n_micro=4, dtype="bf16", sched=sched)
+        st.load_params(P)
+        losses = [st.step(dt, dg)[0] for _ in range(3)]
+        out.append((losses, st.grads_numpy()))
+        st.close()
+    (l0, g0), (l1, g1) = out
+    assert np.allclose(l0, l1, rtol=1e-6, atol=0)
+    for k in g0:
+        assert np.linalg.norm(g0[k] - g1[k]) <= 1e-6 * max(np.linalg.norm(g0[k]), 1e-30), k

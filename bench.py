@@ -265,6 +265,7 @@ def workload_config(args, cfg, tp_pp):
             + ", random init",
             "global_batch": args.m, "seq_len": cfg.seq, "parallelism": f"tp{t}pp{p}vpp2",
             "schedule": args.sched,
+            "cuda_graph": os.environ.get("STP_GRAPH", "0") == "1",
             "tp_transport": (os.environ.get("STP_TP_TRANSPORT", "p2p") if t > 1 else "none"),
             "l2": "no flush: weights (15.2 GB / tp*pp) and stash (tens of GB) exceed the 126 MB L2"}
 
@@ -293,6 +294,8 @@ def start_watchdog(limit_s: float):
 
 
 def ours(args):
+    if args.graph >= 0:
+        os.environ["STP_GRAPH"] = str(args.graph)
     import torch
     import torch.distributed as dist
 
@@ -523,6 +526,9 @@ def main():
     ap.add_argument("--layers", type=int, default=0, help="override layer count (debug only)")
     ap.add_argument("--sched", default="stp")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--graph", type=int, default=-1,
+                    help="1: replay each step as one CUDA graph (STP_GRAPH; TP = 1 or the NCCL transport), "
+                         "0: eager enqueue; default: the STP_GRAPH environment")
     ap.add_argument("--offload", type=float, default=0.0,
                     help="activation offloading alpha (PAPER.md §4.3): fraction of chunk 0's layers whose MLP "
                          "activations go to pinned host memory between forward and backward")

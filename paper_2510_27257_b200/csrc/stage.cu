@@ -572,7 +572,10 @@ stp_status p2p_rs(stp_stage* S, const void* partial, const void* resid, void* x_
   STP_TRY(ce_handshake(S, 0, c));
   STP_TRY(tp_fused_fwd(S->dtype, S->sl, S->h, pieces, np, resid, x_out, g, S->mc.rms_eps, rstd, dsts, nd,
                        S->s_comm));
-  if (nd) STP_TRY(ce_handshake(S, 1, c));
+  // nd == 0 (no all-gather): peers' reuse of this partial buffer is ordered by
+  // the alternate-buffer argument (§8c); STP_DEBUG=1 adds the B handshake anyway
+  // (every TP rank takes the same branch: same unit list, same environment)
+  if (nd || S->debug) STP_TRY(ce_handshake(S, 1, c));
   return STP_OK;
 }
 // all-gather of a local shard (optionally RMSNorm-ed on the way)
@@ -597,7 +600,7 @@ stp_status p2p_bwd(stp_stage* S, const void* x, const void* g, const float* rstd
   if (np < 0 || nd < 0) return fail(STP_ESTATE, "buffer not in the symmetric set");
   STP_TRY(ce_handshake(S, 0, c));
   STP_TRY(tp_fused_bwd(S->dtype, S->sl, S->h, pieces, np, x, g, rstd, dres, dx, S->rtmp, dsts, nd, S->s_comm));
-  if (nd) STP_TRY(ce_handshake(S, 1, c));
+  if (nd || S->debug) STP_TRY(ce_handshake(S, 1, c));
   return rmsnorm_dgamma(S->dtype, S->sl, S->h, S->rtmp, x, rstd, dgamma, S->s_comm);
 }
 

@@ -226,6 +226,20 @@ int fused_grid(int64_t rows) {
   return (int)std::max<int64_t>(1, std::min<int64_t>(blocks, cap));
 }
 
+// Optional SM partitioning (STP_COMM_SMEM = bytes): the fused comm kernels
+// request that much (unused) dynamic shared memory, so their CTAs cannot
+// co-reside with a persistent GEMM CTA (~197 KB) and run only on the SMs the
+// GEMM leaves free (STP_GEMM_MAX_CTAS < SMs): compute and communication on
+// disjoint SMs instead of sharing issue slots (the overlap contention of
+// PAPER.md App. F).  0 (default) = no partitioning.
+int comm_smem() {
+  static const int v = [] {
+    const char* e = getenv("STP_COMM_SMEM");
+    return e ? std::max(0, atoi(e)) : 0;
+  }();
+  return v;
+}
+
 typedef CUresult (*PFN_waitValue32)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
 
 PFN_waitValue32 get_wait() {
@@ -288,8 +302,11 @@ stp_status tp_fused_fwd(int dtype, int64_t rows, int64_t h, const void* const* p
   for (int i = 0; i < nd; ++i) ds.p[i] = dsts[i];
   ds.n = nd;
   return STP_DISPATCH_DTYPE(dtype, [&] {
-    tp_fused_fwd_kernel<T><<<fused_grid(rows), 32 * kWarps, 0, st>>>(rows, (int)h, pc, (const T*)resid, (T*)x_out,
-                                                                    (const T*)g, eps, rstd, ds);
+    const int sm = comm_smem();
+    if (sm > 48 * 1024)
+      STP_CUDA_TRY(cudaFuncSetAttribute(tp_fused_fwd_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
+    tp_fused_fwd_kernel<T><<<fused_grid(rows), 32 * kWarps, sm, st>>>(rows, (int)h, pc, (const T*)resid, (T*)x_out,
+                                                                     (const T*)g, eps, rstd, ds);
     count_launch();
     STP_LAUNCH_CHECK();
     return STP_OK;
@@ -309,8 +326,11 @@ stp_status tp_fused_bwd(int dtype, int64_t rows, int64_t h, const void* const* p
   for (int i = 0; i < nd; ++i) ds.p[i] = dsts[i];
   ds.n = nd;
   return STP_DISPATCH_DTYPE(dtype, [&] {
-    tp_fused_bwd_kernel<T><<<fused_grid(rows), 32 * kWarps, 0, st>>>(rows, (int)h, pc, (const T*)x, (const T*)g, rstd,
-                                                                    (const T*)dres, (T*)dx, (T*)dy_out, ds);
+    const int sm = comm_smem();
+    if (sm > 48 * 1024)
+      STP_CUDA_TRY(cudaFuncSetAttribute(tp_fused_bwd_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
+    tp_fused_bwd_kernel<T><<<fused_grid(rows), 32 * kWarps, sm, st>>>(rows, (int)h, pc, (const T*)x, (const T*)g,
+                                                                     rstd, (const T*)dres, (T*)dx, (T*)dy_out, ds);
     count_launch();
     STP_LAUNCH_CHECK();
     return STP_OK;

@@ -6,7 +6,11 @@ each checked against the CPU fp64 oracle:
      8 q / 2 kv heads, I 2816, s 512, V 4096), which runs the default tcgen05
      kernels (2-SM / 1-SM GEMMs, tcgen05 attention forward and fused
      backward): loss rel 2e-2, grad norms 5e-2, per-tensor difference 3e-2
-     against the oracle on the same bf16-rounded parameters (N(0, 0.02^2)).
+     against the oracle on the same bf16-rounded parameters (N(0, 0.02^2));
+  3. one bf16 MLLM step (ViT with d = 80 heads + 2x2 merger on virtual stage
+     0, small LM on virtual stage 1): the ViT kernels (LayerNorm, QuickGELU /
+     GELU, 2-D RoPE, bidirectional tcgen05 attention) against the oracle's
+     MLLM step (oracle/vit.py), same gates.
 """
 import dataclasses
 
@@ -39,3 +43,24 @@ def run():
     qcfg = dataclasses.replace(si.QWEN2_7B, hidden=1024, n_layers=2, n_q_heads=8, n_kv_heads=2, head_dim=128,
                                ffn=2816, seq=512, vocab=4096)
     _one(qcfg, 2, "bf16", lay=[1, 1], std=0.02, bf16_inputs=True)
+    _mllm()
+
+
+def _mllm():
+    from paper_2510_27257_b200.stage import Stage
+    from tests import mllm_parity as mp
+    from tests.stage_parity import compare
+    cfg, vit, m = mp.LM_BF16, mp.VIT_BF16, 2
+    P, PV, patches, full, tgts, ref_loss, G, GV = mp.mllm_reference(cfg, vit, m, bf16_inputs=True)
+    st = Stage(cfg, n_micro=m, dtype="bf16", sched="stp", device=0, layers_per_vstage=[vit.n_layers, cfg.n_layers],
+               vit=vit)
+    st.load_params(P, PV)
+    st.bind_images(torch.from_numpy(patches).to(torch.bfloat16).cuda().contiguous())
+    loss, stats = st.step(torch.from_numpy(full).cuda(), torch.from_numpy(tgts).cuda())
+    bad = compare(cfg, st.grads_numpy(), mp.rank_reference(cfg, vit, G, GV, 1, 0), loss, ref_loss, "bf16",
+                  elementwise=True)
+    st.close()
+    if bad:
+        raise AssertionError("smoke MLLM parity failed: " + "; ".join(bad[:5]))
+    print(f"smoke ok (bf16 MLLM, ViT d=80): loss {loss:.6f} (oracle {ref_loss:.6f}), {stats.n_units} units, "
+          f"{stats.n_kernels} kernels")

@@ -1,4 +1,4 @@
-"""smoke(): two small STP train steps on cuda:0 through the C-ABI library,
+"""smoke(): three small STP train steps on cuda:0 through the C-ABI library,
 each checked against the CPU fp64 oracle:
   1. TINY fp32 (TP=1, PP=1, two virtual stages, R-STP braided schedule):
      loss and every gradient, rel 1e-4;

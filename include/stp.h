@@ -187,7 +187,19 @@ stp_status stp_nccl_get_id(void* buf);
  * one fused NVLink kernel; "ce" uses copy-engine pulls; "nccl" uses NCCL
  * reduce-scatter / all-gather.  An IPC or peer-access failure returns
  * STP_ECUDA with the CUDA error text.  Multi-rank stages require
- * CUDA_DEVICE_MAX_CONNECTIONS >= 16 (STP_EUNSUPPORTED otherwise). */
+ * CUDA_DEVICE_MAX_CONNECTIONS >= 16 (STP_EUNSUPPORTED otherwise).
+ * Other environment knobs read here (all optional):
+ *   STP_OFFLOAD_ALPHA  activation offloading (§4.3, R5):
+ *                      fraction in [0, 1] of chunk 0's layers whose MLP
+ *                      activations live in pinned host memory between their
+ *                      forward and backward; needs page-locked host memory
+ *   STP_GRAPH=1        replay each step as one CUDA graph once the device
+ *                      inputs repeat (TP = 1 or STP_TP_TRANSPORT=nccl)
+ *   STP_P2P_PUSH=1     p2p transport, bf16: the row-parallel GEMMs store
+ *                      their partial rows straight into the TP peers' buffers
+ *   STP_P2P_CTAS, STP_COMM_SMEM, STP_GEMM_MAX_CTAS   CTA caps / SM
+ *                      partitioning between the comm kernels and the GEMMs
+ *   STP_DEBUG=1        synchronise and log every unit */
 stp_status stp_init_stage(const stp_model_cfg* model, const stp_parallel_cfg* par,
                           const void* world_nccl_id, int32_t cuda_device,
                           stp_stage** out);

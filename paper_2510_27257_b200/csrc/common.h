@@ -27,6 +27,8 @@ inline stp_status fail(stp_status st, const std::string& msg) {
     if (e_ != cudaSuccess) {                                                   \
       ::stp::set_error("%s:%d %s: %s", __FILE__, __LINE__, #expr,              \
                        cudaGetErrorString(e_));                                \
+      cudaGetLastError(); /* clear a non-sticky error so a later launch check  \
+                             does not report it again */                       \
       return STP_ECUDA;                                                        \
     }                                                                          \
   } while (0)

@@ -91,7 +91,7 @@ struct Cfg {
   static constexpr int B_BYTES = BN * BK * 2;
   static constexpr int STAGES = kSmemBudget / (A_BYTES + B_BYTES);
   static constexpr int SMEM = STAGES * (A_BYTES + B_BYTES) + 1024 + 512;
-  static constexpr int TMEM_COLS = 2 * BN;
+  static constexpr int TMEM_COLS = BN == 192 ? 512 : 2 * BN;  // tcgen05.alloc takes powers of two
 };
 
 __device__ __forceinline__ uint32_t pack_bf16x2(float a, float b) {
@@ -1037,10 +1037,17 @@ stp_status gemm_bf16(int layout, int epi, int64_t M, int64_t N, int64_t K, const
     const int64_t waves = (tiles + slots - 1) / slots;
     return (double)tiles / (double)(waves * slots);
   };
+  // useful fraction of the padded N extent (the last n-block of a skinny
+  // TP-sharded GEMM can be mostly padding: N = 1152 in 256-wide tiles wastes 10%)
+  auto npad = [&](int bn) { return (double)N / (double)(((N + bn - 1) / bn) * bn); };
   auto score1 = [&](int bn) {
-    return eff(((M + BM - 1) / BM) * ((N + bn - 1) / bn), sms) * (bn == 128 ? 0.60 : 0.80);
+    const double tile_eff = bn == 128 ? 0.60 : bn == 192 ? 0.72 : 0.80;
+    return eff(((M + BM - 1) / BM) * ((N + bn - 1) / bn), sms) * tile_eff * npad(bn);
   };
-  const int BNsel = (N <= 128 || score1(128) > score1(256)) ? 128 : 256;
+  int BNsel = (N <= 128 || score1(128) > score1(256)) ? 128 : 256;
+  // 128 x 192 tiles (1-SM) for N a multiple of 192 but not of 256 (not with the
+  // CE-statistics epilogue, whose 128-column blocks need 128-aligned tiles)
+  if (N % 192 == 0 && N % 256 != 0 && epi != STP_EPI_STORE_CE && score1(192) > score1(BNsel)) BNsel = 192;
   GemmArgs g;
   STP_TRY(tile_counter(st, &g.tile_ctr));
   g.M = (int)M;
@@ -1094,7 +1101,7 @@ stp_status gemm_bf16(int layout, int epi, int64_t M, int64_t N, int64_t K, const
   bool use_2sm = gemm_mc_mode() == 3 && M > 128;
   if (gemm_mc_mode() == 1 && M > 128) {
     const int64_t t2 = ((M + 255) / 256) * ((N + 255) / 256);
-    use_2sm = eff(t2, sms / 2) * 0.90 >= score1(BNsel);
+    use_2sm = eff(t2, sms / 2) * 0.90 * npad(256) >= score1(BNsel);
   }
   if (use_2sm) {
     // 2-SM: per-CTA boxes of 128 rows (K-major) / 2 x 64 columns (MN-major)
@@ -1109,7 +1116,7 @@ stp_status gemm_bf16(int layout, int epi, int64_t M, int64_t N, int64_t K, const
     if (!a_mn && b_mn) return launch_bf16_2sm<false, true>(g, ta2, tb2, max_ctas, st);
     if (a_mn && b_mn) return launch_bf16_2sm<true, true>(g, ta2, tb2, max_ctas, st);
   }
-  const bool mc2 = gemm_mc_mode() == 2 && g.num_m_blk >= 2;
+  const bool mc2 = gemm_mc_mode() == 2 && g.num_m_blk >= 2 && BNsel != 192;
   // multicast variant: each CTA loads half of the B tile (K-major: BN/2 rows)
   if (!b_mn) s = tensor_map(&tb, B, K, N, ldb, BK, mc2 ? BNsel / 2 : BNsel);  // B [N, K]
   else s = tensor_map(&tb, B, N, K, ldb, 64, BK);                              // B [K, N]
@@ -1133,6 +1140,9 @@ stp_status gemm_bf16(int layout, int epi, int64_t M, int64_t N, int64_t K, const
   STP_GEMM_CASE(256, false, true)
   STP_GEMM_CASE(128, true, true)
   STP_GEMM_CASE(256, true, true)
+  STP_GEMM_CASE(192, false, false)
+  STP_GEMM_CASE(192, false, true)
+  STP_GEMM_CASE(192, true, true)
 #undef STP_GEMM_CASE
   return fail(STP_EUNSUPPORTED, "gemm layout");
 }

@@ -247,6 +247,7 @@ struct stp_stage {
   std::vector<cudaEvent_t> ev_done;
   std::vector<cudaEvent_t> ev_t0, ev_t1;  // timing
   cudaEvent_t ev_base = nullptr, ev_end = nullptr, ev_caller = nullptr, ev_join = nullptr;
+  cudaEvent_t ev_gstart = nullptr, ev_gend = nullptr;  // timing of a graph launch
   float* h_loss_pin = nullptr;  // pinned: the step's loss read-back (a fixed address for graph replay)
   // CUDA-graph replay of the step (STP_GRAPH=1)
   bool use_graph = false;
@@ -1581,8 +1582,14 @@ stp_status run_step(stp_stage* S, float* h_loss, stp_step_stats* stats) {
   const int n = (int)S->units.size();
   const bool graph = S->use_graph && !S->timing && !S->debug;
   const std::array<const void*, 3> key{S->tokens, S->targets, S->patches};
+  // events recorded inside a graph carry no timestamps: a graph step is timed
+  // by an event pair around the launch on s_comp (where the graph starts and joins)
+  bool timed_launch = false;
   if (graph && S->graph_exec && S->graph_key == key) {
+    STP_CUDA_TRY(cudaEventRecord(S->ev_gstart, S->s_comp));
     STP_CUDA_TRY(cudaGraphLaunch(S->graph_exec, S->s_comp));
+    STP_CUDA_TRY(cudaEventRecord(S->ev_gend, S->s_comp));
+    timed_launch = true;
     g_kernel_launches += S->graph_launches;
   } else if (graph && S->steps_done > 0) {  // first step eager: lazily created tables / counters exist
     if (S->graph_exec) {
@@ -1604,7 +1611,10 @@ stp_status run_step(stp_stage* S, float* h_loss, stp_step_stats* stats) {
     if (ei != cudaSuccess) return fail(STP_ECUDA, std::string("graph instantiate: ") + cudaGetErrorString(ei));
     S->graph_key = key;
     S->graph_launches = g_kernel_launches - launches0;
+    STP_CUDA_TRY(cudaEventRecord(S->ev_gstart, S->s_comp));
     STP_CUDA_TRY(cudaGraphLaunch(S->graph_exec, S->s_comp));
+    STP_CUDA_TRY(cudaEventRecord(S->ev_gend, S->s_comp));
+    timed_launch = true;
   } else {
     reset_step_state(S);
     STP_TRY(enqueue_step(S));
@@ -1622,7 +1632,8 @@ stp_status run_step(stp_stage* S, float* h_loss, stp_step_stats* stats) {
   if (stats) {
     memset(stats, 0, sizeof(*stats));
     float ms = 0.f;
-    STP_CUDA_TRY(cudaEventElapsedTime(&ms, S->ev_base, S->ev_end));
+    if (timed_launch) STP_CUDA_TRY(cudaEventElapsedTime(&ms, S->ev_gstart, S->ev_gend));
+    else STP_CUDA_TRY(cudaEventElapsedTime(&ms, S->ev_base, S->ev_end));
     stats->step_ms = ms;
     stats->n_units = n;
     stats->n_kernels = (int32_t)S->launches_step;
@@ -2168,6 +2179,8 @@ static stp_status init_stage_impl(const stp_model_cfg* mc, const stp_vit_cfg* vc
   STP_CUDA_TRY(cudaEventCreateWithFlags(&S->ev_caller, cudaEventDisableTiming));
   STP_CUDA_TRY(cudaEventCreate(&S->ev_end));
   STP_CUDA_TRY(cudaEventCreateWithFlags(&S->ev_join, cudaEventDisableTiming));
+  STP_CUDA_TRY(cudaEventCreate(&S->ev_gstart));
+  STP_CUDA_TRY(cudaEventCreate(&S->ev_gend));
   STP_CUDA_TRY(cudaHostAlloc((void**)&S->h_loss_pin, sizeof(float), cudaHostAllocDefault));
   *S->h_loss_pin = 0.f;
   // Graph replay needs replay-invariant synchronisation: the p2p / ce
@@ -2369,6 +2382,8 @@ void stp_destroy_stage(stp_stage* st) {
   if (st->ev_caller) cudaEventDestroy(st->ev_caller);
   if (st->ev_end) cudaEventDestroy(st->ev_end);
   if (st->ev_join) cudaEventDestroy(st->ev_join);
+  if (st->ev_gstart) cudaEventDestroy(st->ev_gstart);
+  if (st->ev_gend) cudaEventDestroy(st->ev_gend);
   if (st->graph_exec) cudaGraphExecDestroy(st->graph_exec);
   if (st->h_loss_pin) cudaFreeHost(st->h_loss_pin);
   for (int i = 0; i < 2; ++i) {

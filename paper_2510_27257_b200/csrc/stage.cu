@@ -248,6 +248,7 @@ struct stp_stage {
   std::vector<cudaEvent_t> ev_t0, ev_t1;  // timing
   cudaEvent_t ev_base = nullptr, ev_end = nullptr, ev_caller = nullptr, ev_join = nullptr;
   cudaEvent_t ev_gstart = nullptr, ev_gend = nullptr;  // timing of a graph launch
+  cudaEvent_t ev_last = nullptr;  // the step's last event the caller's stream waits on (ev_end / ev_gend)
   float* h_loss_pin = nullptr;  // pinned: the step's loss read-back (a fixed address for graph replay)
   // CUDA-graph replay of the step (STP_GRAPH=1)
   bool use_graph = false;
@@ -1585,11 +1586,13 @@ stp_status run_step(stp_stage* S, float* h_loss, stp_step_stats* stats) {
   // events recorded inside a graph carry no timestamps: a graph step is timed
   // by an event pair around the launch on s_comp (where the graph starts and joins)
   bool timed_launch = false;
+  S->ev_last = S->ev_end;
   if (graph && S->graph_exec && S->graph_key == key) {
     STP_CUDA_TRY(cudaEventRecord(S->ev_gstart, S->s_comp));
     STP_CUDA_TRY(cudaGraphLaunch(S->graph_exec, S->s_comp));
     STP_CUDA_TRY(cudaEventRecord(S->ev_gend, S->s_comp));
     timed_launch = true;
+    S->ev_last = S->ev_gend;
     g_kernel_launches += S->graph_launches;
   } else if (graph && S->steps_done > 0) {  // first step eager: lazily created tables / counters exist
     if (S->graph_exec) {
@@ -1615,6 +1618,7 @@ stp_status run_step(stp_stage* S, float* h_loss, stp_step_stats* stats) {
     STP_CUDA_TRY(cudaGraphLaunch(S->graph_exec, S->s_comp));
     STP_CUDA_TRY(cudaEventRecord(S->ev_gend, S->s_comp));
     timed_launch = true;
+    S->ev_last = S->ev_gend;
   } else {
     reset_step_state(S);
     STP_TRY(enqueue_step(S));
@@ -2315,7 +2319,7 @@ stp_status stp_train_step(stp_stage* st, const int32_t* d_tokens, const int32_t*
   st->tokens = d_tokens;
   st->targets = d_targets;
   STP_TRY(run_step(st, h_loss, stats));
-  STP_CUDA_TRY(cudaStreamWaitEvent((cudaStream_t)stream, st->ev_end, 0));
+  STP_CUDA_TRY(cudaStreamWaitEvent((cudaStream_t)stream, st->ev_last ? st->ev_last : st->ev_end, 0));
   return STP_OK;
 }
 

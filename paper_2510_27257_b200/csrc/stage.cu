@@ -2109,7 +2109,13 @@ static stp_status init_stage_impl(const stp_model_cfg* mc, const stp_vit_cfg* vc
     // TP transport: p2p (default; fused NVLink kernels), ce (copy engines),
     // nccl (NCCL reduce-scatter / all-gather: the baseline)
     const char* e = getenv("STP_TP_TRANSPORT");
-    const std::string tr = e ? e : "p2p";
+    // Default per schedule (round-2 contention sweep): braided
+    // schedules overlap every comm phase with the other microbatch's GEMMs, so
+    // they take the copy-engine transport (no SM-resident transfer kernel next
+    // to the GEMMs); schedules whose forward comm is exposed take the fused p2p
+    // kernel (the shortest phase).
+    const bool braided = S->kind == STP_SCHED_STP || S->kind == STP_SCHED_STP_NOSEP || S->kind == STP_SCHED_STP_MEM;
+    const std::string tr = e ? e : (S->mllm ? "nccl" : braided ? "ce" : "p2p");
     if (tr != "p2p" && tr != "ce" && tr != "nccl") return fail(STP_EINVAL, "STP_TP_TRANSPORT must be p2p, ce or nccl");
     S->ce = S->t > 1 && (tr == "ce" || tr == "p2p");
     S->p2p = S->ce && tr == "p2p";

@@ -47,16 +47,17 @@ def test_multi_rank_parity(tp, pp, sched, dtype):
     assert out.count("PASS") == n, out[-4000:]
 
 
-# The non-default TP transports (CASES above run the default "p2p": one fused
-# kernel per comm phase, NVLink loads of the peers' partials, residual +
-# RMSNorm (bwd), NVLink stores of the all-gather): "ce" = copy-engine NVLink
-# pulls + fused RS-sum / residual / RMSNorm kernel; "nccl" = NCCL
-# reduce-scatter / all-gather (the baseline transport).
+# Every TP transport explicitly (CASES above run each schedule's default: "ce"
+# for the braided STP family, "p2p" otherwise): "p2p" = one fused kernel per
+# comm phase, NVLink loads of the peers' partials, residual + RMSNorm (bwd),
+# NVLink stores of the all-gather; "ce" = copy-engine NVLink pulls + fused
+# RS-sum / residual / RMSNorm kernel; "nccl" = NCCL reduce-scatter /
+# all-gather (the baseline transport).
 CE_CASES = [(2, 1, "stp", "f32"), (2, 1, "stp", "bf16"), (4, 1, "stp", "f32"), (4, 1, "1f1b-i", "bf16"),
             (2, 2, "stp", "f32"), (2, 2, "1f1b-i", "f32")]
 
 
-@pytest.mark.parametrize("transport", ["ce", "nccl"])
+@pytest.mark.parametrize("transport", ["p2p", "ce", "nccl"])
 @pytest.mark.parametrize("tp,pp,sched,dtype", CE_CASES)
 def test_multi_rank_parity_symmetric(tp, pp, sched, dtype, transport):
     n = tp * pp
@@ -65,7 +66,8 @@ def test_multi_rank_parity_symmetric(tp, pp, sched, dtype, transport):
     seq = 64 if dtype == "bf16" else 32
     args = ["--tp", str(tp), "--pp", str(pp), "--sched", sched, "--dtype", dtype, "--seq", str(seq),
             "--n-micro", str(2 * pp if sched != "stp" else 4)]
-    rc, out = run_torchrun(n, args, 29700 + 7 * tp + 3 * pp + len(sched) + len(dtype) + 50 * (transport == "nccl"),
+    rc, out = run_torchrun(n, args, 29700 + 7 * tp + 3 * pp + len(sched) + len(dtype) + 50 * (transport == "nccl")
+                           + 100 * (transport == "p2p"),
                            env={"STP_TP_TRANSPORT": transport})
     assert rc == 0, out[-4000:]
     assert out.count("PASS") == n, out[-4000:]
@@ -103,6 +105,7 @@ def test_multi_rank_parity_gemm_push(tp, pp, sched, dtype):
         pytest.skip(f"needs {n} GPUs")
     args = ["--tp", str(tp), "--pp", str(pp), "--sched", sched, "--dtype", dtype, "--seq", "64",
             "--n-micro", str(2 * pp if sched != "stp" else 4)]
-    rc, out = run_torchrun(n, args, 30100 + 7 * tp + 3 * pp + len(sched), env={"STP_P2P_PUSH": "1"})
+    rc, out = run_torchrun(n, args, 30100 + 7 * tp + 3 * pp + len(sched),
+                           env={"STP_P2P_PUSH": "1", "STP_TP_TRANSPORT": "p2p"})
     assert rc == 0, out[-4000:]
     assert out.count("PASS") == n, out[-4000:]

@@ -99,6 +99,23 @@ __device__ __forceinline__ uint32_t pack_bf16x2(float a, float b) {
   return *reinterpret_cast<uint32_t*>(&h);
 }
 
+// 256-bit global accesses (sm_100 STG.256 / LDG.256): one thread writes a whole
+// 32-byte sector per instruction.  The epilogue's threads each own one row, so
+// a warp's 16-byte stores wrote half sectors (ncu: 2x the sectors of the
+// bytes) -- the drain of a short-K GEMM's tiles was store-bound.
+__device__ __forceinline__ void st256(void* p, uint32_t a, uint32_t b, uint32_t c, uint32_t d, uint32_t e, uint32_t f,
+                                      uint32_t g, uint32_t h) {
+  asm volatile("st.global.v8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(p), "r"(a), "r"(b), "r"(c), "r"(d),
+               "r"(e), "r"(f), "r"(g), "r"(h)
+               : "memory");
+}
+__device__ __forceinline__ void ld256(const void* p, float* o) {
+  asm volatile("ld.global.v8.f32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+               : "=f"(o[0]), "=f"(o[1]), "=f"(o[2]), "=f"(o[3]), "=f"(o[4]), "=f"(o[5]), "=f"(o[6]), "=f"(o[7])
+               : "l"(p));
+}
+__device__ __forceinline__ bool aligned32(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 31) == 0; }
+
 // Epilogue for 32 consecutive columns of one row.
 __device__ __forceinline__ void epilogue_row32(const GemmArgs& p, int row, int col, const uint32_t* v) {
   float f[32];
@@ -107,7 +124,16 @@ __device__ __forceinline__ void epilogue_row32(const GemmArgs& p, int row, int c
   const bool full = (col + 32 <= p.N);
   if (p.epilogue == STP_EPI_ACCUM_F32) {
     float* c = reinterpret_cast<float*>(p.C) + (int64_t)row * p.ldc + col;
-    if (full) {
+    if (full && aligned32(c)) {
+#pragma unroll
+      for (int j = 0; j < 32; j += 8) {
+        float o[8];
+        ld256(c + j, o);
+        st256(c + j, __float_as_uint(o[0] + f[j]), __float_as_uint(o[1] + f[j + 1]), __float_as_uint(o[2] + f[j + 2]),
+              __float_as_uint(o[3] + f[j + 3]), __float_as_uint(o[4] + f[j + 4]), __float_as_uint(o[5] + f[j + 5]),
+              __float_as_uint(o[6] + f[j + 6]), __float_as_uint(o[7] + f[j + 7]));
+      }
+    } else if (full) {
 #pragma unroll
       for (int j = 0; j < 32; j += 4) {
         float4 o = *reinterpret_cast<float4*>(c + j);
@@ -175,7 +201,13 @@ __device__ __forceinline__ void epilogue_row32(const GemmArgs& p, int row, int c
   bf16* c = p.push_rows > 0 ? reinterpret_cast<bf16*>(p.push[row / p.push_rows]) +
                                   (p.push_off + row % p.push_rows) * p.ldc + col
                             : reinterpret_cast<bf16*>(p.C) + (int64_t)row * p.ldc + col;
-  if (full) {
+  if (full && aligned32(c)) {
+#pragma unroll
+    for (int j = 0; j < 32; j += 16)
+      st256(c + j, pack_bf16x2(f[j], f[j + 1]), pack_bf16x2(f[j + 2], f[j + 3]), pack_bf16x2(f[j + 4], f[j + 5]),
+            pack_bf16x2(f[j + 6], f[j + 7]), pack_bf16x2(f[j + 8], f[j + 9]), pack_bf16x2(f[j + 10], f[j + 11]),
+            pack_bf16x2(f[j + 12], f[j + 13]), pack_bf16x2(f[j + 14], f[j + 15]));
+  } else if (full) {
 #pragma unroll
     for (int j = 0; j < 32; j += 8) {
       uint4 u;

@@ -62,3 +62,28 @@ def test_config_resolution():
     assert a.grid == "2x2"
     cfg = bench.model_cfg(res("cfg2", 8))
     assert cfg.n_q_heads == 32 and cfg.n_kv_heads == 8 and cfg.seq == 6144
+
+
+def test_config_resolution():
+    """--config maps N to the TP x PP grid, model, sequence and microbatches of
+    BASELINE.json's configs (cfg2: N=8 -> TP8 with the 32/8-head variant; cfg5
+    MLLM: m = 8 at N = 1, NCCL transport at TP > 1)."""
+    import argparse
+    sys.path.insert(0, ROOT)
+    import bench
+
+    def res(cfg, n):
+        a = argparse.Namespace(config=cfg, gpus=n, model="", seq=0, m=0, grid="", layers=0)
+        return bench.resolve(a)
+    a = res("cfg2", 8)
+    assert (a.grid, a.model, a.seq, a.m) == ("8x1", "qwen2-7b-tp8", 6144, 8)
+    a = res("cfg3", 4)
+    assert (a.grid, a.seq, a.m) == ("2x2", 4096, 16)
+    a = res("cfg4", 4)
+    assert (a.grid, a.model, a.m) == ("2x2", "qwen2.5-14b", 32)
+    a = res("cfg5", 1)
+    assert (a.grid, a.seq, a.m) == ("1x1", 8192, 8)
+    os.environ.pop("STP_TP_TRANSPORT", None)
+    a = res("cfg5", 4)
+    assert (a.grid, a.m) == ("2x2", 16) and os.environ.get("STP_TP_TRANSPORT") == "nccl"
+    os.environ.pop("STP_TP_TRANSPORT", None)

@@ -266,8 +266,8 @@ def workload_config(args, cfg, tp_pp):
             "global_batch": args.m, "seq_len": cfg.seq, "parallelism": f"tp{t}pp{p}vpp2",
             "schedule": args.sched,
             "cuda_graph": os.environ.get("STP_GRAPH", "0") == "1",
-            "tp_transport": (os.environ.get("STP_TP_TRANSPORT", "ce" if args.sched.startswith("stp") and
-                                            args.sched != "stp-nobraid" else "p2p") if t > 1 else "none"),
+            "tp_transport": (os.environ.get("STP_TP_TRANSPORT", "ce" if args.sched in ("stp", "stp-nosep")
+                                            else "p2p") if t > 1 else "none"),
             "l2": "no flush: weights (15.2 GB / tp*pp) and stash (tens of GB) exceed the 126 MB L2"}
 
 
@@ -500,7 +500,7 @@ def ours(args):
             if world > 1:
                 dist.all_reduce(v, op=dist.ReduceOp.MAX)
             cm, ce, cb, cpk = v.tolist()
-            braided = sched.split("@")[0] in ("stp", "stp-nosep", "stp-mem")
+            braided = sched.split("@")[0] in ("stp", "stp-nosep")
             comp[sched] = {"tokens_per_s": tokens / (cm / 1e3), "ms_per_step": cm, "exposed_tp_pct": 100 * ce,
                            "tp_transport": (os.environ.get("STP_TP_TRANSPORT", "ce" if braided else "p2p")
                                             if t > 1 else "none"),

@@ -606,6 +606,33 @@ stp_status p2p_bwd(stp_stage* S, const void* x, const void* g, const float* rstd
   return rmsnorm_dgamma(S->dtype, S->sl, S->h, S->rtmp, x, rstd, dgamma, S->s_comm);
 }
 
+// Copy-engine variant of p2p_bwd: pull this rank's rows of every peer's
+// backward partial (copy engines), one fused kernel for the sum + RMSNorm-bwd +
+// residual grad writing this rank's rows of dst, then the all-gather pulls.
+// (Round 2: the separate RS-sum / RMSNorm-bwd / shard-copy kernels of the
+// generic path made the copy-engine CB phase 1.7x the CF phase.)
+stp_status ce_bwd(stp_stage* S, const void* x, const void* g, const float* rstd, const void* dres, void* dx,
+                  float* dgamma, void* dst) {
+  const uint32_t c = ++S->phase;
+  STP_TRY(ce_handshake(S, 0, c));
+  STP_TRY(ce_pull(S, true, S->pb, nullptr));
+  const size_t bytes = (size_t)(S->sl * S->h) * S->es;
+  const void* pieces[16];
+  for (int q = 0; q < S->t; ++q)
+    pieces[q] = q == S->tp_rank ? (const uint8_t*)S->pb + q * bytes : (const uint8_t*)S->stage_buf + q * bytes;
+  void* y = dst ? (uint8_t*)dst + S->tp_rank * bytes : nullptr;
+  STP_TRY(tp_fused_bwd(S->dtype, S->sl, S->h, pieces, S->t, x, g, rstd, dres, dx, S->rtmp, &y, y ? 1 : 0,
+                       S->s_comm));
+  S->open_phase = c;
+  if (dst) STP_TRY(ce_ag(S, dst));
+  return rmsnorm_dgamma(S->dtype, S->sl, S->h, S->rtmp, x, rstd, dgamma, S->s_comm);
+}
+stp_status fused_bwd(stp_stage* S, const void* x, const void* g, const float* rstd, const void* dres, void* dx,
+                     float* dgamma, void* dst) {
+  if (S->p2p) return p2p_bwd(S, x, g, rstd, dres, dx, dgamma, dst);
+  return ce_bwd(S, x, g, rstd, dres, dx, dgamma, dst);
+}
+
 stp_status ag_dx(stp_stage* S, const void* shard_src, void* dst, size_t count) {
   if (S->p2p) return p2p_ag(S, shard_src, nullptr, nullptr, dst);
   if (S->ce) return ce_ag_shard(S, shard_src, dst);
@@ -1306,19 +1333,19 @@ stp_status unit_cb(stp_stage* S, const stp_unit& u) {
     return ag_dx(S, sl->dx_in, sl->L[C.nl - 1].dy_mlp, (size_t)shard);
   }
   int idx = k - 1;
-  if (S->p2p) {  // fused RS + RMSNorm-bwd + residual grad + AG kernel per phase
+  if (S->ce) {  // fused RS + RMSNorm-bwd + residual grad (+ AG) per phase: p2p kernel or copy-engine pulls
     S->pb_pending = true;
     if (C.last && idx == 0)
-      return p2p_bwd(S, sl->L[C.nl - 1].xres, P(S, S->p_final), sl->rstdf, nullptr, sl->dx_in, DG(S, S->p_final),
+      return fused_bwd(S, sl->L[C.nl - 1].xres, P(S, S->p_final), sl->rstdf, nullptr, sl->dx_in, DG(S, S->p_final),
                      sl->L[C.nl - 1].dy_mlp);
     const int id2 = C.last ? idx - 1 : idx;
     const int j = C.nl - 1 - id2 / 2;
     SlotLayer& L = sl->L[j];
     const LayerIdx& I = LI(S, C.l0 + j);
-    if (id2 % 2 == 0) return p2p_bwd(S, L.x1, P(S, I.ln2), L.rstd2, sl->dx_in, sl->dx_in, DG(S, I.ln2), L.dy_attn);
+    if (id2 % 2 == 0) return fused_bwd(S, L.x1, P(S, I.ln2), L.rstd2, sl->dx_in, sl->dx_in, DG(S, I.ln2), L.dy_attn);
     const void* xprev = j == 0 ? sl->x_in : sl->L[j - 1].xres;
     void* dst = j > 0 ? sl->L[j - 1].dy_mlp : (C.first ? sl->dx0 : nullptr);
-    STP_TRY(p2p_bwd(S, xprev, P(S, I.ln1), L.rstd1, sl->dx_in, sl->dx_in, DG(S, I.ln1), dst));
+    STP_TRY(fused_bwd(S, xprev, P(S, I.ln1), L.rstd1, sl->dx_in, sl->dx_in, DG(S, I.ln1), dst));
     if (j > 0 || C.first) return STP_OK;
     return cb_handoff(S, C, u, sl);
   }

@@ -203,8 +203,7 @@ int64_t stp_kernel_launches(void);
 
 /* Runtime tuning knobs (process-wide; STP_EINVAL for unknown keys / values):
  *   "gemm_mc"  0 = 1-SM tcgen05 GEMM, 1 = automatic 1-SM / 2-SM choice per
- *              shape (default), 2 = 2-CTA cluster with B-tile TMA multicast,
- *              3 = always the 2-SM (cta_group::2) kernel */
+ *              shape (default), 3 = always the 2-SM (cta_group::2) kernel */
 stp_status stp_set_option(const char* key, int64_t value);
 
 /* ------------------------------------------------------------ profiling

@@ -393,208 +393,6 @@ __global__ void __launch_bounds__(256, 1)
 }
 
 
-// 2-CTA cluster variant: the two CTAs of a cluster compute vertically
-// adjacent 128 x BN tiles (m-blocks 2mp, 2mp+1) of the same n-block; each CTA
-// loads its own A block and HALF of the shared B tile, multicast to both
-// CTAs, so per-SM L2->SMEM operand traffic drops from (128+BN) to
-// (128+BN/2) rows per k-block.  The MMA itself is the 1-CTA path above
-// (cta_group::1, M=128); only the loads and the "stage free" signal are
-// cluster-wide (each MMA's commit arrives on both CTAs' empty barriers).
-// Cluster tiles are handed out dynamically: rank 0's producer fetches the id
-// and writes it into both CTAs' tile rings (DSMEM + remote mbarrier arrive).
-template <int BN, bool A_MN, bool B_MN>
-__global__ void __launch_bounds__(256, 1)
-    gemm_bf16_sm100_mc2(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                        const GemmArgs p) {
-  using C = Cfg<BN>;
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t* sA = smem;
-  uint8_t* sB = smem + C::STAGES * C::A_BYTES;
-  uint64_t* full = reinterpret_cast<uint64_t*>(sB + C::STAGES * C::B_BYTES);
-  uint64_t* empty = full + C::STAGES;
-  uint64_t* tfull = empty + C::STAGES;
-  uint64_t* tempty = tfull + 2;
-  uint64_t* ring_full = tempty + 2;   // [4]
-  uint64_t* ring_empty = ring_full + 4;
-  int* ring = reinterpret_cast<int*>(ring_empty + 4);
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(ring + 4);
-
-  const int warp = threadIdx.x >> 5;
-  const int lane = threadIdx.x & 31;
-  const uint32_t rank = cluster_ctarank();
-  const uint32_t peer = rank ^ 1u;
-
-  if (threadIdx.x == 0) {
-    for (int s = 0; s < C::STAGES; ++s) {
-      mbar_init(full + s, 1);
-      mbar_init(empty + s, 2);  // both CTAs' MMAs must have consumed the stage
-    }
-    for (int a = 0; a < 2; ++a) {
-      mbar_init(tfull + a, 1);
-      mbar_init(tempty + a, 4);
-    }
-    for (int r = 0; r < 4; ++r) {
-      mbar_init(ring_full + r, 1);
-      mbar_init(ring_empty + r, 11);  // rank 0: own MMA + 4 epi; rank 1: producer + MMA + 4 epi
-    }
-    fence_barrier_init();
-    tma_prefetch_desc(&tmA);
-    tma_prefetch_desc(&tmB);
-  }
-  if (warp == 2) tmem_alloc<C::TMEM_COLS>(tmem_slot);
-  tc_fence_before();
-  cluster_sync();  // peer barriers initialised before any remote arrive / multicast
-  tc_fence_after();
-  const uint32_t tmem_base = *tmem_slot;
-
-  const int n_mp = (p.num_m_blk + 1) / 2;
-  const int num_ct = n_mp * p.num_n_blk;
-  const int n_clusters = gridDim.x / 2;
-  // remote addresses (rank 0 owns ring_empty accounting; ring entries pushed to both)
-  const uint32_t ring_empty0 = mapa(smem_u32(ring_empty), 0);
-  constexpr uint32_t kBHalf = C::B_BYTES / 2;
-
-  auto release_slot = [&](int rs) {  // a consumer is done reading ring[rs]
-    if (rank == 0) mbar_arrive(ring_empty + rs);
-    else mbar_arrive_cluster(ring_empty0 + rs * 8);
-  };
-
-  if (warp == 0) {
-    if (lane == 0) {
-      int stage = 0;
-      uint32_t phase = 0;
-      for (int it = 0;; ++it) {
-        const int rs = it & 3;
-        int tile;
-        if (rank == 0) {
-          mbar_wait_cluster_wd(ring_empty + rs, ((it >> 2) & 1) ^ 1, 8, p.M, p.N, p.K);
-          const int got = atomicAdd(p.tile_ctr, 1);
-          if (got == num_ct + n_clusters - 1) atomicExch(p.tile_ctr, 0);
-          tile = got < num_ct ? got : -1;
-          ring[rs] = tile;
-          st_cluster_u32(mapa(smem_u32(ring + rs), 1), (uint32_t)tile);
-          mbar_arrive(ring_full + rs);
-          mbar_arrive_cluster(mapa(smem_u32(ring_full + rs), 1));
-        } else {
-          mbar_wait_cluster_wd(ring_full + rs, (it >> 2) & 1, 9, p.M, p.N, p.K);
-          tile = ring[rs];
-          release_slot(rs);
-        }
-        if (tile < 0) break;
-        const int mb = 2 * (p.n_fast ? tile / p.num_n_blk : tile % n_mp) + (int)rank;
-        const int nb = p.n_fast ? tile % p.num_n_blk : tile / n_mp;
-        for (int kb = 0; kb < p.num_k_blk; ++kb) {
-          mbar_wait_cluster_wd(empty + stage, phase ^ 1, 10, p.M, p.N, p.K);
-          mbar_arrive_expect_tx(full + stage, C::A_BYTES + C::B_BYTES);
-          uint8_t* a = sA + stage * C::A_BYTES;
-          uint8_t* b = sB + stage * C::B_BYTES;
-          if (!A_MN) {
-            tma_load_2d(a, &tmA, full + stage, kb * BK, mb * BM);
-          } else {
-#pragma unroll
-            for (int c = 0; c < BM / 64; ++c) tma_load_2d(a + c * 64 * BK * 2, &tmA, full + stage, mb * BM + c * 64, kb * BK);
-          }
-          // this CTA's half of B, multicast to both CTAs of the cluster
-          if (!B_MN) {
-            tma_load_2d_mc(b + rank * kBHalf, &tmB, full + stage, kb * BK, nb * BN + (int)rank * (BN / 2), 0x3);
-          } else {
-#pragma unroll
-            for (int c = 0; c < BN / 128; ++c) {
-              const int ch = (int)rank * (BN / 128) + c;
-              tma_load_2d_mc(b + ch * 64 * BK * 2, &tmB, full + stage, nb * BN + ch * 64, kb * BK, 0x3);
-            }
-          }
-          if (++stage == C::STAGES) {
-            stage = 0;
-            phase ^= 1;
-          }
-        }
-      }
-    }
-  } else if (warp == 1) {
-    if (lane == 0) {
-      constexpr uint32_t idesc = make_idesc_bf16(BM, BN, A_MN, B_MN);
-      int stage = 0;
-      uint32_t phase = 0;
-      for (int local = 0;; ++local) {
-        const int rs = local & 3;
-        mbar_wait_cluster_wd(ring_full + rs, (local >> 2) & 1, 11, p.M, p.N, p.K);
-        const int tile = ring[rs];
-        release_slot(rs);
-        if (tile < 0) break;
-        const int acc = local & 1;
-        const uint32_t acc_phase = (local >> 1) & 1;
-        mbar_wait_wd(tempty + acc, acc_phase ^ 1, 12, p.M, p.N, p.K);
-        tc_fence_after();
-        const uint32_t d_tmem = tmem_base + acc * BN;
-        for (int kb = 0; kb < p.num_k_blk; ++kb) {
-          mbar_wait_wd(full + stage, phase, 13, p.M, p.N, p.K);
-          tc_fence_after();
-          const uint32_t a_addr = smem_u32(sA + stage * C::A_BYTES);
-          const uint32_t b_addr = smem_u32(sB + stage * C::B_BYTES);
-#pragma unroll
-          for (int k = 0; k < BK / 16; ++k) {
-            const uint64_t ad = A_MN ? make_sw128_desc(a_addr + k * 2048, 64 * BK * 2, 1024)
-                                     : make_sw128_desc(a_addr + k * 32, 16, 1024);
-            const uint64_t bd = B_MN ? make_sw128_desc(b_addr + k * 2048, 64 * BK * 2, 1024)
-                                     : make_sw128_desc(b_addr + k * 32, 16, 1024);
-            mma_f16_ss(d_tmem, ad, bd, idesc, (kb | k) != 0);
-          }
-          mma_commit_mc(empty + stage, 0x3);  // stage free in both CTAs once both MMAs read it
-          if (++stage == C::STAGES) {
-            stage = 0;
-            phase ^= 1;
-          }
-        }
-        mma_commit(tfull + acc);
-      }
-    }
-  } else if (warp >= 4) {
-    const int ew = warp & 3;
-    for (int local = 0;; ++local) {
-      const int rs = local & 3;
-      mbar_wait_cluster_wd(ring_full + rs, (local >> 2) & 1, 14, p.M, p.N, p.K);
-      const int tile = ring[rs];
-      __syncwarp();
-      if (lane == 0) release_slot(rs);
-      if (tile < 0) break;
-      const int mb = 2 * (p.n_fast ? tile / p.num_n_blk : tile % n_mp) + (int)rank;
-      const int nb = p.n_fast ? tile % p.num_n_blk : tile / n_mp;
-      const int acc = local & 1;
-      const uint32_t acc_phase = (local >> 1) & 1;
-      mbar_wait_wd(tfull + acc, acc_phase, 15, p.M, p.N, p.K);
-      tc_fence_after();
-      const int row = mb * BM + ew * 32 + lane;
-      float ce_m = -INFINITY, ce_l = 0.f;
-#pragma unroll 1
-      for (int c0 = 0; c0 < BN; c0 += 32) {
-        uint32_t v[32];
-        tmem_ld_32x32b_x32(tmem_base + ((uint32_t)(ew * 32) << 16) + acc * BN + c0, v);
-        tmem_wait_ld();
-        const int col = nb * BN + c0;
-        if (row < p.M && col < p.N) {
-          epilogue_row32(p, row, col, v);
-          if (p.epilogue == STP_EPI_STORE_CE) {
-            ce_update(p, row, col, v, ce_m, ce_l);
-            if ((c0 & 127) == 96 || col + 32 >= p.N) ce_flush(p, row, col, ce_m, ce_l);
-          }
-        }
-      }
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(tempty + acc);
-    }
-  }
-  tc_fence_before();
-  cluster_sync();  // no CTA exits while its peer may still signal / write its smem
-  if (warp == 2) {
-    tc_fence_after();
-    tmem_dealloc<C::TMEM_COLS>(tmem_base);
-  }
-}
-
-
 // 2-SM variant (tcgen05.mma.cta_group::2): a CTA pair computes a 256 x 256
 // tile; each SM stages 128 rows of A and 128 of the 256 B columns, and one
 // thread of the even CTA issues M=256 MMAs reading both SMs' shared memory,
@@ -937,40 +735,13 @@ stp_status launch_bf16(const GemmArgs& a, const CUtensorMap& ta, const CUtensorM
   return STP_OK;
 }
 
-template <int BN, bool A_MN, bool B_MN>
-stp_status launch_bf16_mc2(const GemmArgs& a, const CUtensorMap& ta, const CUtensorMap& tb, int max_ctas,
-                           cudaStream_t st) {
-  using C = Cfg<BN>;
-  auto kern = gemm_bf16_sm100_mc2<BN, A_MN, B_MN>;
-  static unsigned long long attr_mask = 0;  // per instantiation, one bit per device
-  STP_TRY(set_max_smem_once((const void*)kern, C::SMEM, &attr_mask));
-  const int n_ct = ((a.num_m_blk + 1) / 2) * a.num_n_blk;
-  int clusters = num_sms() / 2;
-  if (max_ctas > 0 && max_ctas / 2 < clusters) clusters = std::max(1, max_ctas / 2);
-  if (n_ct < clusters) clusters = n_ct;
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(2 * clusters);
-  cfg.blockDim = dim3(256);
-  cfg.dynamicSmemBytes = C::SMEM;
-  cfg.stream = st;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = 2;
-  attr[0].val.clusterDim.y = 1;
-  attr[0].val.clusterDim.z = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  STP_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, ta, tb, a));
-  count_launch();
-  return STP_OK;
-}
-
 }  // namespace
 
 // Tuning knob (stp_set_option "gemm_mc"): 1 = auto (default: 2-SM kernel unless
 // its 256x256 wave quantisation is clearly worse than the 1-SM 128xBN one),
-// 0 = 1-SM kernel, 3 = 2-SM kernel, 2 = 1-SM cluster with B multicast
-// (measured slower; kept for comparison).  Env STP_GEMM_MC sets the default.
+// 0 = 1-SM kernel, 3 = 2-SM kernel.  (Round 1's 1-SM cluster variant with B
+// multicast, measured slower than the 2-SM kernel, was removed in round 2.)
+// Env STP_GEMM_MC sets the default.
 int& gemm_mc_mode_ref() {
   static int mode = [] {
     const char* e = getenv("STP_GEMM_MC");
@@ -1148,22 +919,9 @@ stp_status gemm_bf16(int layout, int epi, int64_t M, int64_t N, int64_t K, const
     if (!a_mn && b_mn) return launch_bf16_2sm<false, true>(g, ta2, tb2, max_ctas, st);
     if (a_mn && b_mn) return launch_bf16_2sm<true, true>(g, ta2, tb2, max_ctas, st);
   }
-  const bool mc2 = gemm_mc_mode() == 2 && g.num_m_blk >= 2 && BNsel != 192;
-  // multicast variant: each CTA loads half of the B tile (K-major: BN/2 rows)
-  if (!b_mn) s = tensor_map(&tb, B, K, N, ldb, BK, mc2 ? BNsel / 2 : BNsel);  // B [N, K]
+  if (!b_mn) s = tensor_map(&tb, B, K, N, ldb, BK, BNsel);  // B [N, K]
   else s = tensor_map(&tb, B, N, K, ldb, 64, BK);                              // B [K, N]
   if (s != STP_OK) return s;
-  if (mc2) {
-#define STP_GEMM_MC_CASE(bn, amn, bmn) \
-  if (BNsel == bn && a_mn == amn && b_mn == bmn) return launch_bf16_mc2<bn, amn, bmn>(g, ta, tb, max_ctas, st);
-    STP_GEMM_MC_CASE(128, false, false)
-    STP_GEMM_MC_CASE(256, false, false)
-    STP_GEMM_MC_CASE(128, false, true)
-    STP_GEMM_MC_CASE(256, false, true)
-    STP_GEMM_MC_CASE(128, true, true)
-    STP_GEMM_MC_CASE(256, true, true)
-#undef STP_GEMM_MC_CASE
-  }
 #define STP_GEMM_CASE(bn, amn, bmn) \
   if (BNsel == bn && a_mn == amn && b_mn == bmn) return launch_bf16<bn, amn, bmn>(g, ta, tb, max_ctas, st);
   STP_GEMM_CASE(128, false, false)

@@ -85,7 +85,7 @@ stp_status stp_set_option(const char* key, int64_t value) {
   if (!key) return stp::fail(STP_EINVAL, "key is NULL");
   const std::string k(key);
   if (k == "gemm_mc") {
-    if (value < 0 || value > 3) return stp::fail(STP_EINVAL, "gemm_mc must be 0 (1-SM), 1 (auto), 2 or 3 (2-SM)");
+    if (value < 0 || value > 3 || value == 2) return stp::fail(STP_EINVAL, "gemm_mc must be 0 (1-SM), 1 (auto) or 3 (2-SM)");
     stp::gemm_mc_mode_ref() = (int)value;
     return STP_OK;
   }

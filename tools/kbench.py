@@ -37,7 +37,7 @@ def main():
     ap.add_argument("--tp", type=int, default=1)
     ap.add_argument("--seq", type=int, default=6144)
     ap.add_argument("--iters", type=int, default=10)
-    ap.add_argument("--gemm-mc", default="0,2")
+    ap.add_argument("--gemm-mc", default="1")
     ap.add_argument("--skip-gemm", action="store_true")
     ap.add_argument("--only", default="", help="comma list of GEMM names (e.g. fc1_wgrad); skips attention")
     a = ap.parse_args()

@@ -3,7 +3,7 @@ seq 6144): every GEMM of the unit set (forward NT, dgrad NN, wgrad TN with
 fp32 accumulation) and causal GQA attention fwd / bwd, timed with CUDA events
 (warm-up 3, mean of N), for each tuning-knob variant.  One JSON line per case.
 
-  python tools/kbench.py [--tp 1] [--iters 10] [--gemm-mc 0,2] [--skip-gemm]
+  python tools/kbench.py [--tp 1] [--iters 10] [--gemm-mc 0,1,3] [--skip-gemm]
 """
 import argparse
 import json

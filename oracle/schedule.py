@@ -21,9 +21,14 @@ Readings:
           pairs, then the remaining BFULL.
   1F1B    v = 1 (PipeDream): warm-up min(p-d-1, m) forwards.
   ZB      ZB-V-style greedy (V-shape, every backward split into B and W,
-          memory cap 2p chunk-microbatches, unit costs; priority B > F > W).
-          The exact ZB-V order of Qi et al. is not in the paper: PARITY
-          UNPINNED beyond Table 1's closed forms (exposure 4m*T_AR, peak 2p).
+          memory cap 2p chunk-microbatches; priority B > F > W), list-
+          scheduled under representative costs (F, B, W) = (12, 15, 9): the
+          B200 per-layer unit times at TP4 (F : B : W = 1 : 1.28 : 0.86, plus
+          the exposed TP phase of a lone F / B), so its order suits the
+          kernels it runs on (round 1 used unit costs; under real costs that
+          order left bubbles growing with m).  The exact ZB-V order of Qi et
+          al. is not in the paper: PARITY UNPINNED beyond Table 1's closed
+          forms (exposure 4m*T_AR, peak 2p).
   NOBRAID R-STP actions, braided actions expanded un-interleaved.
   NOSEP   R-STP slot grid without steps 2-4 (no W separation).
   1F1B-I-NAIVE  1F1B-I actions; every backward W unit waits for the TP
@@ -185,8 +190,12 @@ def build_1f1b(p: int, m: int, d: int) -> List[Action]:
     return out
 
 
+ZB_COSTS = (12, 15, 9)   # (F, B, W) durations of the ZB list schedule (module doc)
+
+
 def build_zb_greedy(p: int, m: int) -> List[List[Action]]:
-    """ZB-V-style greedy list schedule under unit costs (see module doc)."""
+    """ZB-V-style greedy list schedule under ZB_COSTS (see module doc)."""
+    cF, cB, cW = ZB_COSTS
     V = 2 * p
     cap = 2 * p
     fdone: Dict[Tuple[int, int], int] = {}     # (mb, vs) -> end time
@@ -195,14 +204,17 @@ def build_zb_greedy(p: int, m: int) -> List[List[Action]]:
     nextb = [[1, 1] for _ in range(p)]
     wq: List[List[Tuple[int, int]]] = [[] for _ in range(p)]
     live = [0] * p
+    free = [0] * p
     progs: List[List[Action]] = [[] for _ in range(p)]
     total = 3 * 2 * m * p
     t = 0
     n = 0
     while n < total:
-        if t > 100 * (total + 10):
+        if t > 100 * max(cF, cB, cW) * (total + 10):
             raise RuntimeError("ZB greedy did not terminate")
         for d in range(p):
+            if free[d] > t:
+                continue
             # B candidates
             choice = None
             for c in (1, 0):
@@ -218,7 +230,7 @@ def build_zb_greedy(p: int, m: int) -> List[List[Action]]:
             if choice is not None:
                 c, b = choice
                 vs = vstage(ZB, p, d, c)
-                bdone[(b, vs)] = t + 1
+                bdone[(b, vs)] = free[d] = t + cB
                 nextb[d][c] += 1
                 wq[d].append((c, b))
                 progs[d].append(act(A_B, c, b=b))
@@ -238,7 +250,7 @@ def build_zb_greedy(p: int, m: int) -> List[List[Action]]:
             if choice is not None:
                 c, f = choice
                 vs = vstage(ZB, p, d, c)
-                fdone[(f, vs)] = t + 1
+                fdone[(f, vs)] = free[d] = t + cF
                 nextf[d][c] += 1
                 live[d] += 1
                 progs[d].append(act(A_F, c, f))
@@ -247,6 +259,7 @@ def build_zb_greedy(p: int, m: int) -> List[List[Action]]:
             if wq[d]:
                 c, b = wq[d].pop(0)
                 live[d] -= 1
+                free[d] = t + cW
                 progs[d].append(act(A_W, c, w=b, wc=c))
                 n += 1
         t += 1

@@ -157,12 +157,18 @@ std::vector<stp_action> one_f_one_b(int p, int m, int d) {
 // device takes (in priority) a ready B (smallest mb, chunk 1 first), else a
 // ready F if fewer than 2p chunk-microbatches are live (chunk 1 first), else
 // the oldest deferred W.
+// Durations (F, B, W) of the ZB list schedule: B200's per-layer unit times at
+// TP4 (F : B : W = 1 : 1.28 : 0.86, plus a lone F / B's exposed TP phase), the
+// same constants as oracle/schedule.py ZB_COSTS.
+constexpr long kZbF = 12, kZbB = 15, kZbW = 9;
+
 bool zb_greedy(int p, int m, std::vector<std::vector<stp_action>>& progs) {
   const int V = 2 * p, cap = 2 * p;
   std::map<std::pair<int, int>, long> fdone, bdone;
   std::vector<std::array<int, 2>> nextf(p, {1, 1}), nextb(p, {1, 1});
   std::vector<std::deque<std::pair<int, int>>> wq(p);
   std::vector<int> live(p, 0);
+  std::vector<long> busy(p, 0);
   progs.assign(p, {});
   const long total = 3L * 2 * m * p;
   long n = 0, t = 0;
@@ -171,8 +177,9 @@ bool zb_greedy(int p, int m, std::vector<std::vector<stp_action>>& progs) {
     return it != mp.end() && it->second <= t;
   };
   while (n < total) {
-    if (t > 100 * (total + 10)) return false;
+    if (t > 100 * kZbB * (total + 10)) return false;
     for (int d = 0; d < p; ++d) {
+      if (busy[d] > t) continue;
       int bc = -1, bb = 0;
       for (int c : {1, 0}) {
         const int b = nextb[d][c];
@@ -187,7 +194,7 @@ bool zb_greedy(int p, int m, std::vector<std::vector<stp_action>>& progs) {
       }
       if (bc >= 0) {
         const int vs = sched_vstage(STP_SCHED_ZB, p, d, bc);
-        bdone[{bb, vs}] = t + 1;
+        bdone[{bb, vs}] = busy[d] = t + kZbB;
         nextb[d][bc]++;
         wq[d].push_back({bc, bb});
         progs[d].push_back(mk(STP_A_B, bc, -1, bb));
@@ -209,7 +216,7 @@ bool zb_greedy(int p, int m, std::vector<std::vector<stp_action>>& progs) {
       }
       if (fc >= 0) {
         const int vs = sched_vstage(STP_SCHED_ZB, p, d, fc);
-        fdone[{ff, vs}] = t + 1;
+        fdone[{ff, vs}] = busy[d] = t + kZbF;
         nextf[d][fc]++;
         live[d]++;
         progs[d].push_back(mk(STP_A_F, fc, ff));
@@ -220,6 +227,7 @@ bool zb_greedy(int p, int m, std::vector<std::vector<stp_action>>& progs) {
         auto w = wq[d].front();
         wq[d].pop_front();
         live[d]--;
+        busy[d] = t + kZbW;
         progs[d].push_back(mk(STP_A_W, w.first, -1, -1, w.second, w.first));
         ++n;
       }

@@ -69,8 +69,7 @@ struct FusedArgs {
   int causal;          // 1: causal (LM), 0: bidirectional (ViT)
   const float* nl2;    // [nq, sp]: -lse * log2(e); -inf beyond s (masks the ragged tail)
   const float* Dp;     // [nq, sp]: rowsum(dO * O); 0 beyond s
-  float* accq;         // fp32 [nq][128][sp] (d-major): dQ^T per head, zeroed (TMEM lane = d drains a contiguous row)
-  float* acc;          // fp32 [2 nkv][s][128] (row-major): dk | dv kv heads, zeroed
+  float* acc;          // fp32 [nq + 2 nkv][s][128] (head-major): dq heads | dk | dv kv heads, zeroed
   float scale_log2;    // log2(e) / sqrt(d)
 };
 
@@ -320,22 +319,25 @@ __global__ void __launch_bounds__(384, 1)
       tmem_wait_ld();
       tc_fence_before();
       mbar_arrive(dq_free + gi);
-      // d-major accumulator: this thread's 64 query values of column d are
-      // contiguous, 16 vector reductions (red.global.add.v4.f32) instead of 64
-      // scalar ones.  Query rows past s (the padded tail up to sp) receive
-      // exact zeros (P = 0 there), so no tail test is needed.
-      if (r < a.dh) {
-        float* dst = a.accq + ((int64_t)h * D + r) * a.sp + qbase;
+      // head-major accumulator: row stride 128 floats, so the 64 query rows of
+      // this thread's column d are compile-time offsets of one pointer
+      float* dst = a.acc + ((int64_t)h * a.s + qbase) * D + r;
+      if (r >= a.dh) {
+        // zero-padded d rows of dQ^T: nothing to add
+      } else if (qbase + QT <= a.s) {
 #pragma unroll
-        for (int j = 0; j < QT; j += 4)
-          red_add_v4_f32(dst + j, __uint_as_float(qv[j]), __uint_as_float(qv[j + 1]), __uint_as_float(qv[j + 2]),
-                         __uint_as_float(qv[j + 3]));
+        for (int j = 0; j < QT; ++j) red_add_f32(dst + j * D, __uint_as_float(qv[j]));
+      } else {
+        const int nv = a.s - qbase;
+#pragma unroll
+        for (int j = 0; j < QT; ++j)
+          if (j < nv) red_add_f32(dst + j * D, __uint_as_float(qv[j]));
       }
     }
     // dK / dV of the key tile: group gi adds d columns [64 gi, 64 gi + 64)
     mbar_wait_wd(done, 0, 311, a.s, h, kt);
     tc_fence_after();
-    float* kr = a.acc + ((int64_t)g * a.s + (vrow ? krow : 0)) * D + gi * 64;
+    float* kr = a.acc + ((int64_t)(a.nq + g) * a.s + (vrow ? krow : 0)) * D + gi * 64;
     float* vr = kr + (int64_t)a.nkv * a.s * D;
 #pragma unroll 1
     for (int c = 0; c < 2; ++c) {
@@ -404,27 +406,9 @@ __global__ void attn_bwd_prep(int s, int sp, int nq, int dh, const bf16* __restr
   }
 }
 
-// dq columns of dqkv (bf16 [s, ldd]) = accq (d-major [nq][128][sp]) / sqrt(d):
-// 32 x 32 tiles transposed through shared memory (coalesced on both sides).
-__global__ void attn_bwd_finalize_dq(int s, int sp, int nq, int dh, const float* __restrict__ accq, bf16* dst,
-                                     int64_t ldd, float scale) {
-  __shared__ float tile[32][33];
-  const int h = blockIdx.z, d0 = blockIdx.y * 32, r0 = blockIdx.x * 32;
-  const int tx = threadIdx.x, ty = threadIdx.y;  // 32 x 8
-  for (int i = ty; i < 32; i += 8) {
-    const int d = d0 + i, row = r0 + tx;
-    tile[i][tx] = (d < dh && row < s) ? accq[((int64_t)h * D + d) * sp + row] : 0.f;
-  }
-  __syncthreads();
-  for (int i = ty; i < 32; i += 8) {
-    const int row = r0 + i, d = d0 + tx;
-    if (row < s && d < dh) dst[(int64_t)row * ldd + (int64_t)h * dh + d] = __float2bfloat16_rn(tile[tx][i] * scale);
-  }
-}
-
-// dk | dv columns of dqkv (bf16, [s, ldd], starting at column col0) = acc
-// (row-major [C][s][128]) x (scale for the first qk_heads heads, 1 after).
-// One float4 per thread; a warp reads one 512-byte head row.
+// dqkv (bf16, [s, ldd], columns dq | dk | dv) = acc (head-major [C][s][128])
+// x (1/sqrt(d) for the dq and dk heads, 1 for dv).  One float4 per thread;
+// a warp reads one 512-byte head row.
 __global__ void attn_bwd_finalize(int s, int C, int qk_heads, int dh, const float* __restrict__ acc, bf16* dst,
                                   int64_t ldd, float scale) {
   const int nd4 = dh / 4;
@@ -443,11 +427,10 @@ __global__ void attn_bwd_finalize(int s, int C, int qk_heads, int dh, const floa
 
 }  // namespace
 
-// Workspace of the fused path: nl2 [nq, sp], Dp [nq, sp], accq [nq][128][sp],
-// acc [2 nkv][s][128] (fp32).
+// Workspace of the fused path: nl2 [nq, sp], Dp [nq, sp], acc [nq + 2 nkv][s][128] (fp32).
 int64_t attn_bwd_fused_ws_bytes(int64_t s, int nq, int nkv) {
   const int64_t sp = (s + QT - 1) / QT * QT;
-  return 2 * (int64_t)nq * sp * 4 + 512 + (int64_t)nq * D * sp * 4 + s * (int64_t)(2 * nkv) * D * 4;
+  return 2 * (int64_t)nq * sp * 4 + 256 + s * (int64_t)(nq + 2 * nkv) * D * 4;
 }
 
 // d = 128 or 80 bf16, fused [q | k | v] layout of qkv and dqkv (row strides ld,
@@ -460,9 +443,9 @@ stp_status attn_bwd_fused_launch(int s, int nq, int nkv, int dh, int causal, con
   const int sp = (s + QT - 1) / QT * QT;
   float* nl2 = reinterpret_cast<float*>(ws);
   float* Dp = nl2 + (int64_t)nq * sp;
-  float* accq = reinterpret_cast<float*>((reinterpret_cast<uintptr_t>(Dp + (int64_t)nq * sp) + 255) & ~uintptr_t(255));
-  float* acc = accq + (int64_t)nq * D * sp;  // sp % 64 == 0: stays 256-byte aligned
-  STP_CUDA_TRY(cudaMemsetAsync(accq, 0, ((size_t)nq * D * sp + (size_t)s * 2 * nkv * D) * 4, st));
+  float* acc = reinterpret_cast<float*>((reinterpret_cast<uintptr_t>(Dp + (int64_t)nq * sp) + 255) & ~uintptr_t(255));
+  const int C = nq + 2 * nkv;
+  STP_CUDA_TRY(cudaMemsetAsync(acc, 0, (size_t)s * C * D * 4, st));
   {
     const int64_t warps = (int64_t)sp * nq;
     attn_bwd_prep<<<(unsigned)((warps + 7) / 8), 256, 0, st>>>(s, sp, nq, dh, (const bf16*)o, (const bf16*)dout, ldo, lse,
@@ -481,7 +464,6 @@ stp_status attn_bwd_fused_launch(int s, int nq, int nkv, int dh, int causal, con
   a.sp = sp;
   a.nl2 = nl2;
   a.Dp = Dp;
-  a.accq = accq;
   a.acc = acc;
   a.dh = dh;
   a.causal = causal;
@@ -490,18 +472,10 @@ stp_status attn_bwd_fused_launch(int s, int nq, int nkv, int dh, int causal, con
   attn_bwd_fused_sm100<<<dim3(nq, nt), 384, FB_SMEM, st>>>(tkv, tq64, td64, a);
   count_launch();
   STP_LAUNCH_CHECK();
-  const float rs = 1.f / sqrtf((float)dh);
   {
-    dim3 grid((unsigned)((s + 31) / 32), (unsigned)((dh + 31) / 32), (unsigned)nq);
-    attn_bwd_finalize_dq<<<grid, dim3(32, 8), 0, st>>>(s, sp, nq, dh, accq, (bf16*)dqkv, ldd, rs);
-    count_launch();
-    STP_LAUNCH_CHECK();
-  }
-  {
-    const int C = 2 * nkv;
     const int64_t total = (int64_t)s * C * (dh / 4);
     const int grid = (int)std::min<int64_t>((total + 255) / 256, 16 * num_sms());
-    attn_bwd_finalize<<<grid, 256, 0, st>>>(s, C, nkv, dh, acc, (bf16*)dqkv + (int64_t)nq * dh, ldd, rs);
+    attn_bwd_finalize<<<grid, 256, 0, st>>>(s, C, nq + nkv, dh, acc, (bf16*)dqkv, ldd, 1.f / sqrtf((float)dh));
     count_launch();
     STP_LAUNCH_CHECK();
   }

@@ -39,6 +39,7 @@ def main():
     ap.add_argument("--iters", type=int, default=10)
     ap.add_argument("--gemm-mc", default="1")
     ap.add_argument("--skip-gemm", action="store_true")
+    ap.add_argument("--skip-elementwise", action="store_true")
     ap.add_argument("--only", default="", help="comma list of GEMM names (e.g. fc1_wgrad); skips attention")
     a = ap.parse_args()
     t, s = a.tp, a.seq
@@ -75,6 +76,35 @@ def main():
                 del A, B, C
     if a.only:
         return
+    if not a.skip_elementwise:
+        # HBM-bound kernels of the units at the per-rank shapes (bytes = what a
+        # kernel must read + write once; GB/s vs the measured 6456 GB/s copy bandwidth)
+        rows = s // t
+        xs = torch.randn(rows, h, device=dev, dtype=bf)
+        rs_ = torch.randn(rows, h, device=dev, dtype=bf)
+        g = torch.ones(h, device=dev, dtype=bf)
+        y = torch.empty_like(xs)
+        xo = torch.empty_like(xs)
+        rstd = torch.empty(rows, device=dev, dtype=torch.float32)
+        ms = timed(lambda: ops.rmsnorm_fwd(xs, g, 1e-6, y, rstd, resid=rs_, x_out=xo), a.iters)
+        print(json.dumps({"kernel": "rmsnorm_fwd_resid", "rows": rows, "h": h, "ms": ms,
+                          "gbps": 4 * rows * h * 2 / ms / 1e6}), flush=True)
+        dxo = torch.empty_like(xs)
+        dg = torch.zeros(h, device=dev, dtype=torch.float32)
+        ms = timed(lambda: ops.rmsnorm_bwd(y, xo, g, rstd, dxo, None, dres=rs_), a.iters)
+        print(json.dumps({"kernel": "rmsnorm_bwd_resid", "rows": rows, "h": h, "ms": ms,
+                          "gbps": 4 * rows * h * 2 / ms / 1e6}), flush=True)
+        gu = torch.randn(s, 2 * I, device=dev, dtype=bf)
+        H = torch.empty(s, I, device=dev, dtype=bf)
+        ms = timed(lambda: ops.swiglu_fwd(gu, H), a.iters)
+        print(json.dumps({"kernel": "swiglu_fwd", "s": s, "I": I, "ms": ms, "gbps": 3 * s * I * 2 / ms / 1e6}),
+              flush=True)
+        dH = torch.randn(s, I, device=dev, dtype=bf)
+        dgu = torch.empty_like(gu)
+        ms = timed(lambda: ops.swiglu_bwd(dH, gu, dgu), a.iters)
+        print(json.dumps({"kernel": "swiglu_bwd", "s": s, "I": I, "ms": ms, "gbps": 5 * s * I * 2 / ms / 1e6}),
+              flush=True)
+        del gu, H, dH, dgu
     x = torch.randn(s, qkv, device=dev, dtype=bf)
     o = torch.empty(s, nq * d, device=dev, dtype=bf)
     lse = torch.empty(nq, s, device=dev, dtype=torch.float32)

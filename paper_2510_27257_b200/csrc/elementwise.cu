@@ -7,6 +7,7 @@
 // All are HBM-bound: 16-byte vectorised, coalesced row access (one warp per
 // row for the [s, h] row kernels), warp-shuffle reductions, fp32 arithmetic,
 // grids sized in multiples of the SM count.
+#include <algorithm>
 #include <cmath>
 #include <map>
 #include <mutex>
@@ -145,6 +146,123 @@ __global__ void __launch_bounds__(256) rmsnorm_fwd_cached_kernel(int64_t rows, i
 #pragma unroll
         for (int i = 0; i < VN; ++i) o.set(i, a[v].f(i) * rs * gg.f(i));
         o.store(y + r * h + c);
+      }
+    }
+  }
+}
+
+// Row-per-CTA variants (round 2): 128 threads share a row, each holding
+// RB_STEPS vectors of 4 elements in registers, a block-level reduction through
+// shared memory.  The warp-per-row cached kernels above held a whole 3584-wide
+// row per warp (175-200 registers per thread: one CTA of 8 warps per SM) and
+// ran latency-bound at 2.1-2.2 TB/s (kbench, profiles/r02_kbench_elementwise.jsonl).
+constexpr int RB_THREADS = 128;
+constexpr int RB_STEPS = 8;  // h <= 128 * 4 * 8 = 4096
+
+template <typename T>
+struct V4 {  // 4 elements: 8 bytes (bf16) or 16 bytes (fp32)
+  T v[4];
+  __device__ __forceinline__ void load(const T* p) {
+    if constexpr (sizeof(T) == 2) *reinterpret_cast<uint2*>(v) = *reinterpret_cast<const uint2*>(p);
+    else *reinterpret_cast<uint4*>(v) = *reinterpret_cast<const uint4*>(p);
+  }
+  __device__ __forceinline__ void store(T* p) const {
+    if constexpr (sizeof(T) == 2) *reinterpret_cast<uint2*>(p) = *reinterpret_cast<const uint2*>(v);
+    else *reinterpret_cast<uint4*>(p) = *reinterpret_cast<const uint4*>(v);
+  }
+  __device__ __forceinline__ float f(int i) const { return to_f<T>(v[i]); }
+  __device__ __forceinline__ void set(int i, float x) { v[i] = from_f<T>(x); }
+};
+
+__device__ __forceinline__ float block_sum_128(float v, float* red) {
+  v = warp_sum(v);
+  const int w = threadIdx.x >> 5;
+  if ((threadIdx.x & 31) == 0) red[w] = v;
+  __syncthreads();
+  const float t = red[0] + red[1] + red[2] + red[3];
+  __syncthreads();  // red is reused by the next row
+  return t;
+}
+
+template <typename T>
+__global__ void __launch_bounds__(RB_THREADS) rmsnorm_fwd_rowblock_kernel(int64_t rows, int h, const T* __restrict__ x,
+                                                                         const T* __restrict__ resid, T* x_out,
+                                                                         const T* __restrict__ g, float eps, T* y,
+                                                                         float* rstd_out) {
+  __shared__ float red[4];
+  for (int64_t r = blockIdx.x; r < rows; r += gridDim.x) {
+    V4<T> a[RB_STEPS];
+    float ss = 0.f;
+#pragma unroll
+    for (int k = 0; k < RB_STEPS; ++k) {
+      const int c = (k * RB_THREADS + threadIdx.x) * 4;
+      if (c < h) {
+        a[k].load(x + r * h + c);
+        if (resid) {
+          V4<T> b;
+          b.load(resid + r * h + c);
+#pragma unroll
+          for (int i = 0; i < 4; ++i) a[k].set(i, a[k].f(i) + b.f(i));
+          a[k].store(x_out + r * h + c);
+        }
+#pragma unroll
+        for (int i = 0; i < 4; ++i) ss += a[k].f(i) * a[k].f(i);
+      }
+    }
+    const float rs = rsqrtf(block_sum_128(ss, red) / (float)h + eps);
+    if (rstd_out && threadIdx.x == 0) rstd_out[r] = rs;
+#pragma unroll
+    for (int k = 0; k < RB_STEPS; ++k) {
+      const int c = (k * RB_THREADS + threadIdx.x) * 4;
+      if (c < h) {
+        V4<T> gg, o;
+        gg.load(g + c);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) o.set(i, a[k].f(i) * rs * gg.f(i));
+        o.store(y + r * h + c);
+      }
+    }
+  }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(RB_THREADS) rmsnorm_bwd_rowblock_kernel(int64_t rows, int h, const T* __restrict__ dy,
+                                                                         const T* __restrict__ x,
+                                                                         const T* __restrict__ g,
+                                                                         const float* __restrict__ rstd,
+                                                                         const T* dres, T* dx) {
+  __shared__ float red[4];
+  for (int64_t r = blockIdx.x; r < rows; r += gridDim.x) {
+    const float rs = rstd[r];
+    V4<T> a[RB_STEPS], d[RB_STEPS];
+    float dot = 0.f;
+#pragma unroll
+    for (int k = 0; k < RB_STEPS; ++k) {
+      const int c = (k * RB_THREADS + threadIdx.x) * 4;
+      if (c < h) {
+        a[k].load(x + r * h + c);
+        d[k].load(dy + r * h + c);
+        V4<T> gg;
+        gg.load(g + c);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) dot += gg.f(i) * d[k].f(i) * a[k].f(i);
+      }
+    }
+    const float kk = rs * rs * rs * block_sum_128(dot, red) / (float)h;
+#pragma unroll
+    for (int k = 0; k < RB_STEPS; ++k) {
+      const int c = (k * RB_THREADS + threadIdx.x) * 4;
+      if (c < h) {
+        V4<T> gg, o, q;
+        gg.load(g + c);
+        if (dres) q.load(dres + r * h + c);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          float v = rs * gg.f(i) * d[k].f(i) - a[k].f(i) * kk;
+          if (dres) v += q.f(i);
+          o.set(i, v);
+        }
+        o.store(dx + r * h + c);
       }
     }
   }
@@ -639,7 +757,10 @@ stp_status rmsnorm_fwd(int dtype, int64_t rows, int64_t h, const void* x, const 
   if (rows == 0) return STP_OK;
   return STP_DISPATCH_DTYPE(dtype, [&] {
     constexpr int VN = Vec<T>::N;
-    if (h <= 32 * VN * 16)
+    if (h <= RB_THREADS * 4 * RB_STEPS && h % 4 == 0)
+      rmsnorm_fwd_rowblock_kernel<T><<<(unsigned)std::min<int64_t>(rows, (int64_t)num_sms() * 16), RB_THREADS, 0, st>>>(
+          rows, (int)h, (const T*)x, (const T*)resid, (T*)x_out, (const T*)g, eps, (T*)y, rstd);
+    else if (h <= 32 * VN * 16)
       rmsnorm_fwd_cached_kernel<T, 16><<<grid_for(rows, kWarpsPerBlock), 32 * kWarpsPerBlock, 0, st>>>(
           rows, (int)h, (const T*)x, (const T*)resid, (T*)x_out, (const T*)g, eps, (T*)y, rstd);
     else
@@ -660,7 +781,10 @@ stp_status rmsnorm_bwd(int dtype, int64_t rows, int64_t h, const void* dy, const
       STP_TRY(launch_dgamma<T>(rows, h, (const T*)dy, (const T*)x, rstd, dgamma, st));
     }
     constexpr int VN = Vec<T>::N;
-    if (h <= 32 * VN * 16)
+    if (h <= RB_THREADS * 4 * RB_STEPS && h % 4 == 0)
+      rmsnorm_bwd_rowblock_kernel<T><<<(unsigned)std::min<int64_t>(rows, (int64_t)num_sms() * 16), RB_THREADS, 0, st>>>(
+          rows, (int)h, (const T*)dy, (const T*)x, (const T*)g, rstd, (const T*)dres, (T*)dx);
+    else if (h <= 32 * VN * 16)
       rmsnorm_bwd_cached_kernel<T, 16><<<grid_for(rows, kWarpsPerBlock), 32 * kWarpsPerBlock, 0, st>>>(
           rows, (int)h, (const T*)dy, (const T*)x, (const T*)g, rstd, (const T*)dres, (T*)dx);
     else

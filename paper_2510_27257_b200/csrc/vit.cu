@@ -12,7 +12,9 @@
 //     elementwise.cu.
 // Row kernels: one warp per row, the row cached in registers (h <= 32 * VN *
 // 16), 16-byte vectors, warp-shuffle reductions, fp32 statistics.
+#include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <map>
 #include <mutex>
 #include <tuple>
@@ -159,6 +161,152 @@ __global__ void __launch_bounds__(256) ln_bwd_kernel(int64_t rows, int h, const 
   }
 }
 
+// Row-per-CTA variants (128 threads per row, 4 elements per thread and step;
+// the warp-per-row kernels above keep a whole row per warp in registers, which
+// costs occupancy -- see elementwise.cu's RMSNorm row kernels, round 2).
+constexpr int LB_THREADS = 128;
+constexpr int LB_STEPS = 8;  // h <= 4096
+
+// STP_LN_ROWBLOCK=0 keeps the warp-per-row kernels (A/B in tools/kbench.py).
+bool ln_rowblock(int64_t h) {
+  static const bool off = [] {
+    const char* e = getenv("STP_LN_ROWBLOCK");
+    return e && e[0] == '0';
+  }();
+  return !off && h % 4 == 0 && h <= LB_THREADS * 4 * LB_STEPS;
+}
+
+template <typename T>
+struct W4 {
+  T v[4];
+  __device__ __forceinline__ void load(const T* p) {
+    if constexpr (sizeof(T) == 2) *reinterpret_cast<uint2*>(v) = *reinterpret_cast<const uint2*>(p);
+    else *reinterpret_cast<uint4*>(v) = *reinterpret_cast<const uint4*>(p);
+  }
+  __device__ __forceinline__ void store(T* p) const {
+    if constexpr (sizeof(T) == 2) *reinterpret_cast<uint2*>(p) = *reinterpret_cast<const uint2*>(v);
+    else *reinterpret_cast<uint4*>(p) = *reinterpret_cast<const uint4*>(v);
+  }
+  __device__ __forceinline__ float f(int i) const { return to_f<T>(v[i]); }
+  __device__ __forceinline__ void set(int i, float x) { v[i] = from_f<T>(x); }
+};
+
+__device__ __forceinline__ float bsum128(float v, float* red) {
+  v = wsum(v);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+  __syncthreads();
+  const float t = red[0] + red[1] + red[2] + red[3];
+  __syncthreads();
+  return t;
+}
+
+template <typename T>
+__global__ void __launch_bounds__(LB_THREADS) ln_fwd_rowblock_kernel(int64_t rows, int h, const T* __restrict__ x,
+                                                                     const T* __restrict__ resid, T* x_out,
+                                                                     const T* __restrict__ g, const T* __restrict__ b,
+                                                                     float eps, T* y, float* mean_out,
+                                                                     float* rstd_out) {
+  __shared__ float red[4];
+  for (int64_t r = blockIdx.x; r < rows; r += gridDim.x) {
+    W4<T> a[LB_STEPS];
+    float s1 = 0.f;
+#pragma unroll
+    for (int k = 0; k < LB_STEPS; ++k) {
+      const int c = (k * LB_THREADS + threadIdx.x) * 4;
+      if (c < h) {
+        a[k].load(x + r * h + c);
+        if (resid) {
+          W4<T> q;
+          q.load(resid + r * h + c);
+#pragma unroll
+          for (int i = 0; i < 4; ++i) a[k].set(i, a[k].f(i) + q.f(i));
+          a[k].store(x_out + r * h + c);
+        }
+#pragma unroll
+        for (int i = 0; i < 4; ++i) s1 += a[k].f(i);
+      }
+    }
+    const float mu = bsum128(s1, red) / (float)h;
+    float s2 = 0.f;
+#pragma unroll
+    for (int k = 0; k < LB_STEPS; ++k) {
+      const int c = (k * LB_THREADS + threadIdx.x) * 4;
+      if (c < h) {
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const float d = a[k].f(i) - mu;
+          s2 += d * d;
+        }
+      }
+    }
+    const float rs = rsqrtf(bsum128(s2, red) / (float)h + eps);
+    if (threadIdx.x == 0) {
+      if (mean_out) mean_out[r] = mu;
+      if (rstd_out) rstd_out[r] = rs;
+    }
+#pragma unroll
+    for (int k = 0; k < LB_STEPS; ++k) {
+      const int c = (k * LB_THREADS + threadIdx.x) * 4;
+      if (c < h) {
+        W4<T> gg, bb, o;
+        gg.load(g + c);
+        bb.load(b + c);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) o.set(i, (a[k].f(i) - mu) * rs * gg.f(i) + bb.f(i));
+        o.store(y + r * h + c);
+      }
+    }
+  }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(LB_THREADS) ln_bwd_rowblock_kernel(int64_t rows, int h, const T* __restrict__ dy,
+                                                                     const T* __restrict__ x, const T* __restrict__ g,
+                                                                     const float* __restrict__ mean,
+                                                                     const float* __restrict__ rstd, const T* dres,
+                                                                     T* dx) {
+  __shared__ float red[4];
+  for (int64_t r = blockIdx.x; r < rows; r += gridDim.x) {
+    const float mu = mean[r], rs = rstd[r];
+    W4<T> a[LB_STEPS], d[LB_STEPS];
+    float sg = 0.f, sgx = 0.f;
+#pragma unroll
+    for (int k = 0; k < LB_STEPS; ++k) {
+      const int c = (k * LB_THREADS + threadIdx.x) * 4;
+      if (c < h) {
+        a[k].load(x + r * h + c);
+        d[k].load(dy + r * h + c);
+        W4<T> gg;
+        gg.load(g + c);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const float gd = gg.f(i) * d[k].f(i);
+          sg += gd;
+          sgx += gd * (a[k].f(i) - mu) * rs;
+        }
+      }
+    }
+    const float mg = bsum128(sg, red) / (float)h, mgx = bsum128(sgx, red) / (float)h;
+#pragma unroll
+    for (int k = 0; k < LB_STEPS; ++k) {
+      const int c = (k * LB_THREADS + threadIdx.x) * 4;
+      if (c < h) {
+        W4<T> gg, o, q;
+        gg.load(g + c);
+        if (dres) q.load(dres + r * h + c);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const float xh = (a[k].f(i) - mu) * rs;
+          float val = rs * (gg.f(i) * d[k].f(i) - mg - xh * mgx);
+          if (dres) val += q.f(i);
+          o.set(i, val);
+        }
+        o.store(dx + r * h + c);
+      }
+    }
+  }
+}
+
 // dg[c] += sum_rows dy xhat, db[c] += sum_rows dy: one thread per column,
 // a block of rows per blockIdx.y, one fp32 atomic per column and block.
 template <typename T>
@@ -261,9 +409,13 @@ stp_status layernorm_fwd(int dtype, int64_t rows, int64_t h, const void* x, cons
   if (rows == 0) return STP_OK;
   return STP_DISPATCH_DTYPE(dtype, [&] {
     if (h > 32 * V16<T>::N * kNV) return fail(STP_EUNSUPPORTED, "layernorm hidden too large for the row-cached kernel");
-    ln_fwd_kernel<T><<<blocks_for(rows, kWarps), 32 * kWarps, 0, st>>>(rows, (int)h, (const T*)x, (const T*)resid,
-                                                                       (T*)x_out, (const T*)g, (const T*)b, eps, (T*)y,
-                                                                       mean, rstd);
+    if (ln_rowblock(h))
+      ln_fwd_rowblock_kernel<T><<<(unsigned)std::min<int64_t>(rows, (int64_t)num_sms() * 16), LB_THREADS, 0, st>>>(
+          rows, (int)h, (const T*)x, (const T*)resid, (T*)x_out, (const T*)g, (const T*)b, eps, (T*)y, mean, rstd);
+    else
+      ln_fwd_kernel<T><<<blocks_for(rows, kWarps), 32 * kWarps, 0, st>>>(rows, (int)h, (const T*)x, (const T*)resid,
+                                                                         (T*)x_out, (const T*)g, (const T*)b, eps,
+                                                                         (T*)y, mean, rstd);
     count_launch();
     STP_LAUNCH_CHECK();
     return STP_OK;
@@ -285,9 +437,13 @@ stp_status layernorm_bwd(int dtype, int64_t rows, int64_t h, const void* dy, con
       count_launch();
       STP_LAUNCH_CHECK();
     }
-    ln_bwd_kernel<T><<<blocks_for(rows, kWarps), 32 * kWarps, 0, st>>>(rows, (int)h, (const T*)dy, (const T*)x,
-                                                                       (const T*)g, mean, rstd, (const T*)dres,
-                                                                       (T*)dx);
+    if (ln_rowblock(h))
+      ln_bwd_rowblock_kernel<T><<<(unsigned)std::min<int64_t>(rows, (int64_t)num_sms() * 16), LB_THREADS, 0, st>>>(
+          rows, (int)h, (const T*)dy, (const T*)x, (const T*)g, mean, rstd, (const T*)dres, (T*)dx);
+    else
+      ln_bwd_kernel<T><<<blocks_for(rows, kWarps), 32 * kWarps, 0, st>>>(rows, (int)h, (const T*)dy, (const T*)x,
+                                                                         (const T*)g, mean, rstd, (const T*)dres,
+                                                                         (T*)dx);
     count_launch();
     STP_LAUNCH_CHECK();
     return STP_OK;

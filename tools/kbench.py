@@ -94,6 +94,23 @@ def main():
         ms = timed(lambda: ops.rmsnorm_bwd(y, xo, g, rstd, dxo, None, dres=rs_), a.iters)
         print(json.dumps({"kernel": "rmsnorm_bwd_resid", "rows": rows, "h": h, "ms": ms,
                           "gbps": 4 * rows * h * 2 / ms / 1e6}), flush=True)
+        # ViT LayerNorm (+ residual) at the MLLM shape: cfg5's image rows per
+        # rank (4 images x 1024 patches ... here s rows) x hv 1280
+        hv = 1280
+        xv = torch.randn(s, hv, device=dev, dtype=bf)
+        rv = torch.randn(s, hv, device=dev, dtype=bf)
+        gv = torch.ones(hv, device=dev, dtype=bf)
+        bv = torch.zeros(hv, device=dev, dtype=bf)
+        yv, xov, dxv = torch.empty_like(xv), torch.empty_like(xv), torch.empty_like(xv)
+        mv = torch.empty(s, device=dev, dtype=torch.float32)
+        rsv = torch.empty(s, device=dev, dtype=torch.float32)
+        ms = timed(lambda: ops.layernorm_fwd(xv, gv, bv, 1e-6, yv, mv, rsv, resid=rv, x_out=xov), a.iters)
+        print(json.dumps({"kernel": "layernorm_fwd_resid", "rows": s, "h": hv, "ms": ms,
+                          "gbps": 4 * s * hv * 2 / ms / 1e6}), flush=True)
+        ms = timed(lambda: ops.layernorm_bwd(yv, xov, gv, mv, rsv, dxv, dres=rv), a.iters)
+        print(json.dumps({"kernel": "layernorm_bwd_resid", "rows": s, "h": hv, "ms": ms,
+                          "gbps": 4 * s * hv * 2 / ms / 1e6}), flush=True)
+        del xv, rv, yv, xov, dxv
         gu = torch.randn(s, 2 * I, device=dev, dtype=bf)
         H = torch.empty(s, I, device=dev, dtype=bf)
         ms = timed(lambda: ops.swiglu_fwd(gu, H), a.iters)

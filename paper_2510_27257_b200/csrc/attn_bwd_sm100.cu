@@ -5,8 +5,8 @@
 //   P = exp(S - lse), dV = P^T dO, dP = dO V^T, dS = P (dP - D),
 //   dQ = dS K / sqrt(d), dK = dS^T Q / sqrt(d), D = rowsum(dO O)).
 //
-// One CTA per (128-row key tile kt, query head h); heavy key tiles first
-// (blockIdx.y = kt: kt = 0 sees every query tile).  Loop over the 64-row query
+// One CTA per (128-row key tile kt, query head h); grouped by kv head, heavy key
+// tiles first within a group (kt = 0 sees every query tile).  Loop over the 64-row query
 // tiles i >= 2 kt (causal), five GEMMs per (key tile, query tile):
 //   S^T  = K Q_i^T              (TMEM, M = 128 keys, N = 64 queries)
 //   dP^T = V dO_i^T             (TMEM)
@@ -14,9 +14,11 @@
 //   dK  += dS^T Q_i             (A = dS^T from TMEM, beside P^T)
 //   dQ_i^T = K^T dS_i^T         (M = d, N = 64; A = K^T and B = dS^T from smem,
 //                                both MN-major; D written over dP^T)
-// dQ_i^T is drained from TMEM by the warp group that converted tile i and
-// added into a head-major fp32 [nq + 2 nkv][s][128] accumulator with red.global.add
-// (L2-side reductions, no read-back); dK / dV are accumulated over the query
+// dQ_i^T is drained from TMEM by the warp group that converted tile i, staged
+// in shared memory as fp32 [64 queries][128 d] (in the tile's dS^T buffer,
+// free once dQ_i has read it, plus a 16 KB buffer) and added into a head-major
+// fp32 [nq + 2 nkv][s][128] accumulator by two bulk (TMA engine) reductions of
+// contiguous rows (d = 80: per-element red.global.add); dK / dV are accumulated over the query
 // loop in TMEM and added into the same accumulator once per CTA (the GQA sum
 // over a kv head's query heads happens there: no per-head partials and no
 // reduce pass).  attn_bwd_finalize converts the accumulator to bf16 (x 1/sqrt(d)
@@ -30,7 +32,7 @@
 // i % 2 == g; one key row per thread, 64 query columns).  TMEM: dV [0,128),
 // dK [128,256), buffer b (= g) at 256 + 128 b: S^T [0,64) -> P^T [0,32) +
 // dS^T [32,64); dP^T [64,128) -> dQ^T.  The MMA order per tile,
-//   S(i+1), dV(i), dP(i+1), dK(i), dQ(i),
+//   S(i+1), dV(i), dP(i+1), dQ(i), dK(i)   (dQ first: drained while dK runs),
 // lets the tensor pipe compute tile i+1's S^T while group (i % 2) converts
 // tile i; tcgen05.mma executes in issue order, so S(i+2) cannot overwrite
 // P^T / dS^T(i) before dV(i) / dK(i) have read them, and dP(i+2) waits for
@@ -39,6 +41,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 
 #include "attn_sm100_common.h"
 #include "common.h"
@@ -60,7 +63,8 @@ constexpr int QT_BYTES = QT * D * 2;      // 16 KB
 constexpr int QATOM = QT * 64 * 2;        // 8 KB
 constexpr int ST = 3;                     // Q_i / dO_i / (nl2, D) ring stages
 constexpr int DS_BYTES = T * QT * 2;      // dS^T tile [128 keys][64 queries] bf16, 16 KB
-constexpr int FB_SMEM = 1024 + 2 * TILE_BYTES + 2 * ST * QT_BYTES + 2 * DS_BYTES + 2 * ST * QT * 4 + 256;
+constexpr int STG_BYTES = 32 * D * 4;     // dQ staging: query rows [32, 64) of a tile, fp32 [32][128]
+constexpr int FB_SMEM = 1024 + 2 * TILE_BYTES + 2 * ST * QT_BYTES + 2 * DS_BYTES + 2 * STG_BYTES + 2 * ST * QT * 4 + 256;
 static_assert(FB_SMEM <= 232448, "shared memory");
 
 struct FusedArgs {
@@ -71,19 +75,25 @@ struct FusedArgs {
   const float* Dp;     // [nq, sp]: rowsum(dO * O); 0 beyond s
   float* acc;          // fp32 [nq + 2 nkv][s][128] (head-major): dq heads | dk | dv kv heads, zeroed
   float scale_log2;    // log2(e) / sqrt(d)
+  int nt;              // key tiles
+  int kv_major;        // 1: CTAs ordered by kv head, then key tile (heavy first), then query head
+  int dq_bulk;         // 1: dQ tiles staged in smem and added by bulk (TMA) reductions; 0: red.add per element
 };
 
 __global__ void __launch_bounds__(384, 1)
     attn_bwd_fused_sm100(const __grid_constant__ CUtensorMap tm_kv, const __grid_constant__ CUtensorMap tm_q64,
                          const __grid_constant__ CUtensorMap tm_do64, const FusedArgs a) {
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // 1024-byte aligned by a pointer offset (not an integer round trip), so every
+  // pointer derived from it keeps the shared state space: LDS / STS, not generic LD / ST
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t* sK = smem;
   uint8_t* sV = smem + TILE_BYTES;
   uint8_t* sQ = smem + 2 * TILE_BYTES;  // [ST]
   uint8_t* sdO = sQ + ST * QT_BYTES;    // [ST]
   uint8_t* sdS = sdO + ST * QT_BYTES;   // [2]
-  float* s_nl = reinterpret_cast<float*>(sdS + 2 * DS_BYTES);  // [ST][QT]
+  float* s_stg = reinterpret_cast<float*>(sdS + 2 * DS_BYTES);  // [2][32][128] fp32
+  float* s_nl = s_stg + 2 * 32 * D;                              // [ST][QT]
   float* s_D = s_nl + ST * QT;                                 // [ST][QT]
   uint64_t* bar = reinterpret_cast<uint64_t*>(s_D + ST * QT);
   uint64_t* kv_full = bar;
@@ -99,8 +109,20 @@ __global__ void __launch_bounds__(384, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(done + 1);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int h = blockIdx.x, kt = blockIdx.y;
-  const int grp = a.nq / a.nkv, g = h / grp;
+  const int grp = a.nq / a.nkv;
+  int h, kt;
+  if (a.kv_major) {
+    // One GQA group (a kv head and its grp query heads) at a time: the CTAs in
+    // flight then red.add into ~grp + 2 heads' rows of the accumulator (28 MB at
+    // TP1, s 6144), which stay in L2; ordered by key tile within the group.
+    const int b = blockIdx.x, per_g = grp * a.nt;
+    kt = (b % per_g) / grp;
+    h = (b / per_g) * grp + b % grp;
+  } else {
+    h = blockIdx.x % a.nq;
+    kt = blockIdx.x / a.nq;
+  }
+  const int g = h / grp;
   const int nq64 = (a.s + QT - 1) / QT;
   const int q0 = a.causal ? 2 * kt : 0;  // first query tile that sees key tile kt
   const int n_q = nq64 - q0;
@@ -215,14 +237,15 @@ __global__ void __launch_bounds__(384, 1)
       if (it + 1 < n_q) issue_dp(it + 1);
       mbar_wait_wd(ds_full + b, ph, 306, a.s, h, kt);
       tc_fence_after();
-#pragma unroll
-      for (int kk = 0; kk < QT / 16; ++kk)  // dK += dS^T Q_i
-        mma_f16_ts_el(tdK, tS + 32 + kk * 8, qmn + (uint64_t)(kk * 128), idMN, (it > 0 || kk > 0) ? 1u : 0u);
+      // dQ first: the group drains it while the tensor pipe runs dK
       const uint64_t dsd = ddS0_mn + (uint64_t)((b * DS_BYTES) >> 4);
 #pragma unroll
       for (int kk = 0; kk < T / 16; ++kk)  // dQ_i^T = K^T dS_i^T (K = 128 keys)
         mma_f16_ss_el(tP, dK_mn + (uint64_t)(kk * 128), dsd + (uint64_t)(kk * 128), idQ, kk > 0 ? 1u : 0u);
       mma_commit_el(dq_full + b);
+#pragma unroll
+      for (int kk = 0; kk < QT / 16; ++kk)  // dK += dS^T Q_i
+        mma_f16_ts_el(tdK, tS + 32 + kk * 8, qmn + (uint64_t)(kk * 128), idMN, (it > 0 || kk > 0) ? 1u : 0u);
       mma_commit_el(qdo_empty + st);
     }
     mma_commit_el(done);
@@ -235,6 +258,9 @@ __global__ void __launch_bounds__(384, 1)
     const uint32_t tS = tB + 128 * gi, tP = tS + 64;  // group gi always uses buffer gi (tiles it % 2 == gi)
     uint8_t* dsrow = sdS + gi * DS_BYTES + (r >> 3) * 1024 + (r & 7) * 128;
     const uint64_t sc2 = pk2f(a.scale_log2, a.scale_log2);
+    const bool leader = quad == 0 && lane == 0;
+    float* stg0 = reinterpret_cast<float*>(sdS + gi * DS_BYTES);  // dQ rows [0, 32): dS^T(i) is consumed once dQ(i) is
+    float* stg1 = s_stg + gi * 32 * D;                            // dQ rows [32, 64)
     for (int it = gi; it < n_q; it += 2) {
       const int st = it % ST;
       const uint32_t ph = (it >> 1) & 1;
@@ -278,6 +304,10 @@ __global__ void __launch_bounds__(384, 1)
       mbar_arrive(p_full + gi);
       mbar_wait_wd(dp_full + gi, ph, 309, a.s, h, kt);
       tc_fence_after();
+      if (a.dq_bulk && it >= 2) {  // the previous tile's bulk reductions have read sdS / the staging buffer
+        if (leader) bulk_wait_read_all();
+        named_bar_sync(1 + gi, 128);
+      }
 #pragma unroll
       for (int ch = 0; ch < 2; ++ch) {
         uint32_t dv[32];
@@ -321,6 +351,25 @@ __global__ void __launch_bounds__(384, 1)
       mbar_arrive(dq_free + gi);
       // head-major accumulator: row stride 128 floats, so the 64 query rows of
       // this thread's column d are compile-time offsets of one pointer
+      if (a.dq_bulk) {
+        // stage the tile as fp32 [64 q][128 d] (rows of dQ^T's lane d = this
+        // thread's column; d >= dh hold zeros) and add it with two bulk reductions
+        // into the contiguous accumulator rows
+#pragma unroll
+        for (int j = 0; j < 32; ++j) stg0[j * D + r] = __uint_as_float(qv[j]);
+#pragma unroll
+        for (int j = 0; j < 32; ++j) stg1[j * D + r] = __uint_as_float(qv[32 + j]);
+        fence_proxy_async();
+        named_bar_sync(1 + gi, 128);
+        if (leader) {
+          const int nv = min(QT, a.s - qbase);
+          float* dst0 = a.acc + ((int64_t)h * a.s + qbase) * D;
+          bulk_reduce_add_f32(dst0, stg0, (uint32_t)min(nv, 32) * D * 4);
+          if (nv > 32) bulk_reduce_add_f32(dst0 + 32 * D, stg1, (uint32_t)(nv - 32) * D * 4);
+          bulk_commit();
+        }
+        continue;
+      }
       float* dst = a.acc + ((int64_t)h * a.s + qbase) * D + r;
       if (r >= a.dh) {
         // zero-padded d rows of dQ^T: nothing to add
@@ -334,6 +383,7 @@ __global__ void __launch_bounds__(384, 1)
           if (j < nv) red_add_f32(dst + j * D, __uint_as_float(qv[j]));
       }
     }
+    if (a.dq_bulk && leader) bulk_wait_all();
     // dK / dV of the key tile: group gi adds d columns [64 gi, 64 gi + 64)
     mbar_wait_wd(done, 0, 311, a.s, h, kt);
     tc_fence_after();
@@ -469,7 +519,20 @@ stp_status attn_bwd_fused_launch(int s, int nq, int nkv, int dh, int causal, con
   a.causal = causal;
   a.scale_log2 = LOG2E / sqrtf((float)dh);
   const int nt = (s + T - 1) / T;
-  attn_bwd_fused_sm100<<<dim3(nq, nt), 384, FB_SMEM, st>>>(tkv, tq64, td64, a);
+  a.nt = nt;
+  static const int kv_major = [] {
+    const char* e = getenv("STP_ATTN_BWD_ORDER");  // "0": key tile major over all heads (round-2 order)
+    return e && e[0] == '0' ? 0 : 1;
+  }();
+  a.kv_major = kv_major;
+  static const int dq_bulk = [] {
+    const char* e = getenv("STP_ATTN_DQ_BULK");  // "0": per-element red.add drain of dQ
+    return e && e[0] == '0' ? 0 : 1;
+  }();
+  // d = 80 (ViT): the staged tile would carry 48 zero columns per row through
+  // the bulk reductions (kbench 393 -> 363 TFLOP/s); per-element red.add there
+  a.dq_bulk = dq_bulk && dh == D;
+  attn_bwd_fused_sm100<<<(unsigned)(nq * nt), 384, FB_SMEM, st>>>(tkv, tq64, td64, a);
   count_launch();
   STP_LAUNCH_CHECK();
   {

@@ -71,7 +71,9 @@ constexpr int FWD_SMEM = 1024 + 5 * TILE_BYTES + 4 * T * 4 + 256;  // Q, K[2], V
 __global__ void __launch_bounds__(FWD_THREADS, 1)
     attn_fwd_sm100(const __grid_constant__ CUtensorMap tm_qkv, const FwdArgs a) {
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // 1024-byte aligned by a pointer offset (not an integer round trip), so every
+  // pointer derived from it keeps the shared state space: LDS / STS, not generic LD / ST
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t* sQ = smem;
   uint8_t* sK = smem + TILE_BYTES;      // [2]
   uint8_t* sV = smem + 3 * TILE_BYTES;  // [2]

@@ -59,11 +59,6 @@ __device__ __forceinline__ float fmax3(float a, float b, float c) {
   asm("max.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
   return r;
 }
-__device__ __forceinline__ uint64_t fadd2(uint64_t a, uint64_t b) {
-  uint64_t r;
-  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
-  return r;
-}
 
 constexpr int FWD_THREADS = 384;
 constexpr int FWD_SMEM = 1024 + 5 * TILE_BYTES + 4 * T * 4 + 256;  // Q, K[2], V[2], (m, l) x 2 halves, barriers
@@ -205,10 +200,17 @@ __global__ void __launch_bounds__(FWD_THREADS, 1)
         for (int i = 0; i < 64; ++i)
           if (cbase + i >= lim) sv[i] = -INFINITY;
       }
-      float mx = fmax3(sv[0], sv[1], sv[2]);
+      // row max as a 3-ary tree (depth 4) instead of a 31-deep dependent chain:
+      // the softmax warps are latency-bound (two per scheduler)
+      float m1[22];
 #pragma unroll
-      for (int i = 3; i < 63; i += 2) mx = fmax3(mx, sv[i], sv[i + 1]);
-      mx = fmaxf(mx, sv[63]) * sl2;
+      for (int i = 0; i < 21; ++i) m1[i] = fmax3(sv[3 * i], sv[3 * i + 1], sv[3 * i + 2]);
+      m1[21] = sv[63];
+      float m2[8];
+#pragma unroll
+      for (int i = 0; i < 7; ++i) m2[i] = fmax3(m1[3 * i], m1[3 * i + 1], m1[3 * i + 2]);
+      m2[7] = m1[21];
+      float mx = fmaxf(fmax3(m2[0], m2[1], m2[2]), fmax3(m2[3], m2[4], fmax3(m2[5], m2[6], m2[7]))) * sl2;
       const bool need = mx > m + 8.f;
       if (__any_sync(0xffffffffu, need)) {
         float alpha = 1.f;
@@ -236,19 +238,19 @@ __global__ void __launch_bounds__(FWD_THREADS, 1)
       // m == -inf (every key of this half masked so far): exponent -inf -> P = 0
       const float nm = (m == -INFINITY) ? -INFINITY : -m;
       const uint64_t sc2 = pk2f(sl2, sl2), nm2 = pk2f(nm, nm);
-      uint64_t lacc = pk2f(0.f, 0.f);
+      uint64_t lacc[4] = {pk2f(0.f, 0.f), pk2f(0.f, 0.f), pk2f(0.f, 0.f), pk2f(0.f, 0.f)};  // 4 chains of 8
       uint32_t pk[32];
 #pragma unroll
       for (int i = 0; i < 64; i += 2) {
         float t0, t1;
         up2f(ffma2(pk2f(sv[i], sv[i + 1]), sc2, nm2), t0, t1);
         const float p0 = ex2(t0), p1 = ex2(t1);
-        lacc = fadd2(lacc, pk2f(p0, p1));
+        lacc[(i >> 1) & 3] = fadd2(lacc[(i >> 1) & 3], pk2f(p0, p1));
         pk[i >> 1] = pack2(p0, p1);
       }
       {
         float l0, l1;
-        up2f(lacc, l0, l1);
+        up2f(fadd2(fadd2(lacc[0], lacc[1]), fadd2(lacc[2], lacc[3])), l0, l1);
         l += l0 + l1;
       }
       // P_half over the first 32 of this half's 64 S columns (already read above)

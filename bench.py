@@ -209,6 +209,22 @@ def cpu_sample(big: bool = False):
 _sample_model = ["qwen2-7b"]
 
 
+def cpu_cfg1_full():
+    """SURVEY §8d.4's un-extrapolated CPU timing: the oracle on cfg1 (the tiny
+    config: L 4, h 64, s 32, V 256) for a whole step of m = 4 microbatches."""
+    import stp_inputs as si
+    from oracle import model as om
+    cfg, m = si.TINY, 4
+    P = si.make_params(cfg, seed=1)
+    toks, tgts = si.make_tokens(cfg, m, seed=2)
+    t0 = time.perf_counter()
+    om.forward_backward(P, cfg, toks, tgts)
+    dt = time.perf_counter() - t0
+    return {"value": m * cfg.seq / dt, "unit": "tokens/s", "seconds": dt,
+            "sample": f"cfg1 (L {cfg.n_layers}, h {cfg.hidden}, s {cfg.seq}, V {cfg.vocab}), m {m}, fwd+bwd fp64, "
+                      "timed in full (no extrapolation)"}
+
+
 def sample_desc(cfg, model):
     return (f"{cfg.n_layers} {model}-shaped decoder layer(s) + LM head (V={cfg.vocab}), 1 x {cfg.seq} tokens, "
             f"fwd+bwd fp64")
@@ -247,7 +263,8 @@ def reference_arm(args, full_cfg):
         "config": workload_config(args, full_cfg, tuple(int(x) for x in args.grid.split("x"))),
         "cpu_baseline": {"value": tok_s, "unit": "tokens/s", "cores": cpu_cores(), "kind": "oracle",
                          "sample": sample_desc(cfg, args.model) + f" ({mean:.1f} s/sample), scaled by algorithmic "
-                                   "FLOPs to the full workload"},
+                                   "FLOPs to the full workload",
+                         "cfg1_full": cpu_cfg1_full()},
         "e2e": {"value": tok_s, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -469,7 +486,8 @@ def ours(args):
             cpu_tok = (fl / dt) / gemm_flops_per_token(cfg)
             line["cpu_baseline"] = {"value": cpu_tok, "unit": "tokens/s", "cores": cpu_cores(), "kind": "oracle",
                                     "sample": sample_desc(scfg, args.model) + f" ({dt:.1f} s), scaled by "
-                                              "algorithmic FLOPs to the full workload"}
+                                              "algorithmic FLOPs to the full workload",
+                                    "cfg1_full": cpu_cfg1_full()}
     st.close()
     del st
     import gc

@@ -75,7 +75,10 @@ __device__ __forceinline__ void ce_update(const GemmArgs& p, int row, int col, c
   m = mn;
   l = acc;
   const int64_t tl = (int64_t)p.ce_tgt[row] - p.ce_v0 - col;
-  if (tl >= 0 && tl < nv) p.ce_tl[row] = __uint_as_float(v[tl]);
+  // compile-time indices only: a runtime v[tl] would put the accumulator chunk in local memory
+#pragma unroll
+  for (int j = 0; j < 32; ++j)
+    if (j == tl && j < nv) p.ce_tl[row] = __uint_as_float(v[j]);
 }
 __device__ __forceinline__ void ce_flush(const GemmArgs& p, int row, int col, float& m, float& l) {
   float* q = p.ce_part + ((int64_t)row * p.ce_nblk + col / 128) * 2;
@@ -144,7 +147,9 @@ __device__ __forceinline__ void epilogue_row32(const GemmArgs& p, int row, int c
         *reinterpret_cast<float4*>(c + j) = o;
       }
     } else {
-      for (int j = 0; j < 32 && col + j < p.N; ++j) c[j] += f[j];
+#pragma unroll
+      for (int j = 0; j < 32; ++j)
+        if (col + j < p.N) c[j] += f[j];
     }
     return;
   }
@@ -170,7 +175,9 @@ __device__ __forceinline__ void epilogue_row32(const GemmArgs& p, int row, int c
                                                        pack_bf16x2(du[4], du[5]), pack_bf16x2(du[6], du[7]));
       }
     } else {
-      for (int j = 0; j < 32 && col + j < p.N; ++j) {
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        if (col + j >= p.N) continue;
         const float z = __bfloat162float(gp[j]), sg = 1.f / (1.f + __expf(-z)), dh = f[j];
         const float u = __bfloat162float(up[j]);
         up[j] = __float2bfloat16_rn(dh * z * sg);
@@ -195,7 +202,9 @@ __device__ __forceinline__ void epilogue_row32(const GemmArgs& p, int row, int c
         for (int q = 0; q < 8; ++q) f[j + q] += __bfloat162float(h[q]);
       }
     } else {
-      for (int j = 0; j < 32 && col + j < p.N; ++j) f[j] += __bfloat162float(r[j]);
+#pragma unroll
+      for (int j = 0; j < 32; ++j)
+        if (col + j < p.N) f[j] += __bfloat162float(r[j]);
     }
   }
   bf16* c = p.push_rows > 0 ? reinterpret_cast<bf16*>(p.push[row / p.push_rows]) +
@@ -218,7 +227,9 @@ __device__ __forceinline__ void epilogue_row32(const GemmArgs& p, int row, int c
       *reinterpret_cast<uint4*>(c + j) = u;
     }
   } else {
-    for (int j = 0; j < 32 && col + j < p.N; ++j) c[j] = __float2bfloat16_rn(f[j]);
+#pragma unroll
+    for (int j = 0; j < 32; ++j)
+      if (col + j < p.N) c[j] = __float2bfloat16_rn(f[j]);
   }
 }
 

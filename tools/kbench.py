@@ -41,6 +41,8 @@ def main():
     ap.add_argument("--skip-gemm", action="store_true")
     ap.add_argument("--skip-elementwise", action="store_true")
     ap.add_argument("--only", default="", help="comma list of GEMM names (e.g. fc1_wgrad); skips attention")
+    ap.add_argument("--cublas", action="store_true",
+                    help="also time torch.matmul (cuBLAS) on each GEMM shape and layout (bf16 output)")
     a = ap.parse_args()
     t, s = a.tp, a.seq
     h, I, V = 3584, 18944 // t, 152064 // t
@@ -70,9 +72,25 @@ def main():
                     A = torch.randn(K, M, device=dev, dtype=bf)
                     B = torch.randn(K, N, device=dev, dtype=bf)
                 C = torch.zeros(M, N, device=dev, dtype=torch.float32 if epi == 2 else bf)
-                ms = timed(lambda: ops.gemm(lay, A, B, C, M, N, K, epi=epi, dtype=1), a.iters)
-                print(json.dumps({"kernel": "gemm", "name": name, "gemm_mc": mc, "M": M, "N": N, "K": K,
-                                  "ms": ms, "tflops": 2 * M * N * K / ms / 1e9}), flush=True)
+                ours = lambda: ops.gemm(lay, A, B, C, M, N, K, epi=epi, dtype=1)  # noqa: E731
+                ms = timed(ours, a.iters)
+                if not a.cublas:
+                    print(json.dumps({"kernel": "gemm", "name": name, "gemm_mc": mc, "M": M, "N": N, "K": K,
+                                      "ms": ms, "tflops": 2 * M * N * K / ms / 1e9}), flush=True)
+                if a.cublas:  # same operands and layout; bf16 output (no fp32 accumulate epilogue)
+                    Ct = torch.empty(M, N, device=dev, dtype=bf)
+                    mm = {0: lambda: torch.matmul(A, B.t(), out=Ct), 1: lambda: torch.matmul(A, B, out=Ct),
+                          2: lambda: torch.matmul(A.t(), B, out=Ct)}[lay]
+                    ms_c = timed(mm, a.iters)
+                    for _ in range(2):  # alternate (same power / clock state), best of three each
+                        ms = min(ms, timed(ours, a.iters))
+                        ms_c = min(ms_c, timed(mm, a.iters))
+                    print(json.dumps({"kernel": "gemm", "name": name, "gemm_mc": mc, "M": M, "N": N, "K": K,
+                                      "ms": ms, "tflops": 2 * M * N * K / ms / 1e9}), flush=True)
+                    print(json.dumps({"kernel": "gemm_cublas", "name": name, "M": M, "N": N, "K": K, "ms": ms_c,
+                                      "tflops": 2 * M * N * K / ms_c / 1e9, "speed_ours_vs_cublas": ms_c / ms}),
+                          flush=True)
+                    del Ct
                 del A, B, C
     if a.only:
         return

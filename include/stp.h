@@ -181,11 +181,13 @@ stp_status stp_nccl_get_id(void* buf);
  * caller, e.g. with torch.distributed); NULL allowed only when tp*pp == 1.
  * The library derives the TP and PP communicators with ncclCommSplit.
  * Streams are created internally.  Parameters are bound separately.
- * TP transport (env STP_TP_TRANSPORT, read here): "p2p" (default) maps the TP
- * peers' stash slots / partial buffers / flag words with CUDA IPC (all TP
- * ranks on one node, peer access over NVLink) and runs each comm phase as
- * one fused NVLink kernel; "ce" uses copy-engine pulls; "nccl" uses NCCL
- * reduce-scatter / all-gather.  An IPC or peer-access failure returns
+ * TP transport (env STP_TP_TRANSPORT, read here): "p2p" maps the TP peers'
+ * stash slots / partial buffers / flag words with CUDA IPC (all TP ranks on
+ * one node, peer access over NVLink) and runs each comm phase as one fused
+ * NVLink kernel; "ce" pulls the rows with the copy engines over the same
+ * mappings and reduces / normalises in one local kernel; "nccl" uses NCCL
+ * reduce-scatter / all-gather.  Default: "ce" for the braided schedules (STP,
+ * STP-NOSEP), "p2p" for the others, "nccl" for MLLM stages.  An IPC or peer-access failure returns
  * STP_ECUDA with the CUDA error text.  Multi-rank stages require
  * CUDA_DEVICE_MAX_CONNECTIONS >= 16 (STP_EUNSUPPORTED otherwise).
  * Other environment knobs read here (all optional):
@@ -199,6 +201,11 @@ stp_status stp_nccl_get_id(void* buf);
  *                      their partial rows straight into the TP peers' buffers
  *   STP_P2P_CTAS, STP_COMM_SMEM, STP_GEMM_MAX_CTAS   CTA caps / SM
  *                      partitioning between the comm kernels and the GEMMs
+ *   STP_NCCL_TP_CTAS, STP_NCCL_PP_CTAS   NCCL maxCTAs of the TP (16) and PP
+ *                      (4) communicators; STP_NCCL_REGISTER=1 registers the
+ *                      stash with the TP communicator (NCCL transport)
+ *   STP_CE_WAIT=spin   ce transport: spin-wait kernels instead of
+ *                      cuStreamWaitValue32 for the peer flags
  *   STP_DEBUG=1        synchronise and log every unit */
 stp_status stp_init_stage(const stp_model_cfg* model, const stp_parallel_cfg* par,
                           const void* world_nccl_id, int32_t cuda_device,

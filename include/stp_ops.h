@@ -203,7 +203,21 @@ int64_t stp_kernel_launches(void);
 
 /* Runtime tuning knobs (process-wide; STP_EINVAL for unknown keys / values):
  *   "gemm_mc"  0 = 1-SM tcgen05 GEMM, 1 = automatic 1-SM / 2-SM choice per
- *              shape (default), 3 = always the 2-SM (cta_group::2) kernel */
+ *              shape (default), 3 = always the 2-SM (cta_group::2) kernel
+ * Kernel-variant environment switches (read once per process; the defaults
+ * are the measured-faster variants, the alternatives exist for A/B runs,
+ * DESIGN.md §7c):
+ *   STP_GEMM_RASTER=0       m-block-fastest GEMM tile order
+ *   STP_ATTN_BWD_ORDER=0    attention backward CTAs key-tile major over all heads
+ *                           (default: grouped by kv head)
+ *   STP_ATTN_DQ_BULK=0      attention backward dQ drained with per-element
+ *                           red.add (default for d = 128: smem + bulk reductions)
+ *   STP_LN_ROWBLOCK=0       warp-per-row LayerNorm kernels (default: a row per
+ *                           128-thread CTA for h <= 4096)
+ *   STP_DGAMMA_VEC=1        vectorised RMSNorm dgamma column reduction
+ *   STP_ATTN_MMA_SYNC=1     d = 128 attention on the mma.sync kernels instead
+ *                           of tcgen05 (the recompiled-baseline comparison)
+ *   STP_GEMM_MC=n           initial value of "gemm_mc" */
 stp_status stp_set_option(const char* key, int64_t value);
 
 /* ------------------------------------------------------------ profiling

@@ -1143,7 +1143,9 @@ stp_status unit_compute(stp_stage* S, const stp_unit& u) {
       const LayerIdx& I = LI(S, u.layer);
       // (STP_EPI_SWIGLU_BWD would fuse the SwiGLU backward into this GEMM's
       // epilogue; measured slower: the epilogue's [G | U] reads stall the 2-SM
-      // kernel, GEMM average 1321 -> 1187 TFLOP/s.  Separate kernel kept.)
+      // kernel, GEMM average 1321 -> 1187 TFLOP/s in round 1; re-measured after
+      // the epilogue stopped spilling: GEMM 1576 -> 1688 ms per N = 1 step for
+      // the ~40 ms the separate kernel costs, profiles/r02x_*.  Kept separate.)
       if (off_layer(S, C, j)) {
         if (L.blk < 0) return fail(STP_ESTATE, "offloaded layer not reloaded before its backward");
         STP_CUDA_TRY(cudaStreamWaitEvent(st, L.ev_h2d, 0));

@@ -1,4 +1,5 @@
 #!/usr/bin/env bash
+# (historical: STP_ATTN_EXP_EMU was removed after this measurement -- DESIGN.md §7c)
 # attention forward with part of the exponentials on the FMA pipe (STP_ATTN_EXP_EMU
 # pairs of 8): parity at the default, kbench sweep 0..4, N=1 headline.
 mkdir -p gpurun_out

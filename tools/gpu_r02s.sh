@@ -1,4 +1,5 @@
 #!/usr/bin/env bash
+# (historical: STP_ATTN_DP_EARLY was removed after this measurement -- DESIGN.md §7c)
 # attention backward MMA issue order A/B: dP(i+1) after dV(i) (default) or right after S(i+1).
 mkdir -p gpurun_out
 for e in 0 1; do

@@ -1,4 +1,5 @@
 #!/usr/bin/env bash
+# (historical: STP_SWIGLU_EPI was removed after this measurement -- DESIGN.md §7c)
 # SwiGLU backward fused into the FC2 dgrad epilogue (STP_SWIGLU_EPI=1; re-measured now that the
 # epilogue keeps its registers): whole-step bf16 parity with it on, N=1 A/B.
 mkdir -p gpurun_out

@@ -58,12 +58,27 @@ def run(stp_units, ref_units, p=2, layers=28, ms=(8, 16, 32)):
     return out
 
 
+def load_units(path):
+    """tools/comm_phase_times.py output: one JSON document, possibly after
+    NCCL's version banner (round 2) or pretty-printed (round 1)."""
+    text = open(path).read()
+    return json.loads(text[text.index("{"):])
+
+
 def main():
+    """python tests/simulate_8gpu.py [OUT.json [STP_UNITS.json REF_UNITS.json]]
+    (default: the round-1 unit times)."""
     prof = os.path.join(ROOT, "profiles")
-    stp = json.load(open(os.path.join(prof, "r01_unit_times_tp4_stp.json")))["units"]
-    ref = json.load(open(os.path.join(prof, "r01_unit_times_tp4_1f1b-i.json")))["units"]
-    res = run(stp, ref)
+    if len(sys.argv) > 3:
+        stp_path, ref_path = sys.argv[2], sys.argv[3]
+    else:
+        stp_path = os.path.join(prof, "r01_unit_times_tp4_stp.json")
+        ref_path = os.path.join(prof, "r01_unit_times_tp4_1f1b-i.json")
+    stp, ref = load_units(stp_path), load_units(ref_path)
+    res = run(stp["units"], ref["units"])
     res["label"] = "SIMULATED (oracle simulator, measured TP=4 unit times) - not a measurement"
+    res["unit_times"] = {"stp": os.path.relpath(stp_path, ROOT) + f" ({stp.get('sched')}, {stp.get('transport')})",
+                         "reference": os.path.relpath(ref_path, ROOT) + f" ({ref.get('sched')}, {ref.get('transport')})"}
     print(json.dumps(res, indent=1))
     if len(sys.argv) > 1:
         json.dump(res, open(sys.argv[1], "w"), indent=1)

@@ -67,7 +67,9 @@ def main():
     if rank == 0:
         bytes_coll = (a.tp - 1) / a.tp * a.seq * cfg.hidden * 2
         out = {"tp": a.tp, "pp": a.pp, "sched": a.sched, "seq": a.seq, "layers": a.layers,
-               "transport": os.environ.get("STP_TP_TRANSPORT", "p2p"), "step_ms": stats.step_ms,
+               # the stage's default rule (stage.cu init): ce for the braided schedules
+               "transport": os.environ.get("STP_TP_TRANSPORT", "ce" if a.sched in ("stp", "stp-nosep") else "p2p"),
+               "step_ms": stats.step_ms,
                "exposed_tp_ms": stats.exposed_tp_ms, "pp_bubble_ms": stats.pp_bubble_ms,
                "nvlink_bound_ms_per_collective": bytes_coll / 900e9 * 1e3,
                "units": {k: {"n": len(v), "mean_ms": statistics.mean(v), "median_ms": statistics.median(v)}

@@ -4,11 +4,14 @@
 // bf16: persistent warp-specialised tcgen05 kernel.  One CTA per SM, 256
 // threads: warp 0 = TMA producer, warp 1 = MMA issuer (one elected lane),
 // warp 2 = TMEM allocator, warps 4-7 = epilogue (TMEM -> registers ->
-// global).  Tile 128 x BN x 64, BN in {128, 256}, a ring of smem stages
+// global).  Tile 128 x BN x 64, BN in {128, 192, 256}, a ring of smem stages
 // (128-byte swizzle, filled by TMA, released by tcgen05.commit), two TMEM
-// accumulators so the epilogue of tile i overlaps the main loop of tile i+1.
+// accumulators so the epilogue of tile i overlaps the main loop of tile i+1;
+// a 2-SM variant (cta_group::2, 256 x 256 tiles) for the large shapes.
 // Operands may be K-major or MN-major (descriptor transpose bits) so forward
 // (X W^T), dgrad (dY W) and wgrad (dY^T X) all run without transposes.
+// The epilogue indexes the accumulator registers with compile-time indices
+// only (a runtime index puts the chunk in local memory: DESIGN.md §7c).
 //
 // fp32: true-fp32 SIMT FMA GEMM (no TF32) for the fp32 parity mode.
 #include <cudaTypedefs.h>
